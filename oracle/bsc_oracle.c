@@ -1,0 +1,1006 @@
+/* TEST INFRASTRUCTURE ONLY — the parity oracle, never the product.
+ *
+ * Plain-C restatement of the reference BSC truncated-EM step. Each function
+ * cites the reference lines it follows (paths relative to
+ * /root/reference/proj/src). Summation orders follow the reference compiled
+ * against oracle/eigen_shim; tests/test_oracle.py checks this file bit for
+ * bit against oracle/_ref/libprsp_ref.so (the reference sources themselves)
+ * and against the SPEC.md known answers.
+ */
+#define _GNU_SOURCE
+#include "bsc_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { OK = 0, E_CONFIG = 2, E_DATA = 3, E_NUMERIC = 4, E_INTERNAL = 5 };
+
+static _Thread_local char g_err[512];
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+const char* bsc_last_error(void) { return g_err; }
+
+#define K_LOG_2PI 1.8378770664093454836 /* linear_discrete.cpp:24 */
+#define K_MIN_SIGMA2 1e-12              /* model.hpp:32 */
+#define K_MIN_PI 1e-6                   /* model.hpp:33 */
+
+static double dmax(double a, double b) { return (a < b) ? b : a; } /* std::max */
+static double dmin(double a, double b) { return (b < a) ? b : a; } /* std::min */
+
+/* ------------------------------------------------------------------ RNG */
+/* std::mt19937_64 (the engine pinned by core.hpp:129-150). */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} rng_t;
+
+static void rng_seed(rng_t* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    r->mt[i] = 6364136223846793005ULL * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) +
+               (uint64_t)i;
+  r->idx = 312;
+}
+
+static uint64_t rng_next(rng_t* r) {
+  if (r->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      uint64_t x = (r->mt[i] & 0xFFFFFFFF80000000ULL) |
+                   (r->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+      r->mt[i] = r->mt[(i + 156) % 312] ^ xa;
+    }
+    r->idx = 0;
+  }
+  uint64_t y = r->mt[r->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+/* splitmix64 mix, core.cpp:50-57; RngStream::derived core.cpp:59-61. */
+static uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+static void rng_derived(rng_t* r, uint64_t base, uint64_t index) {
+  rng_seed(r, mix64(mix64(base) ^ mix64(index + 1)));
+}
+
+/* core.cpp:63-66 */
+static double rng_uniform01(rng_t* r) {
+  return (double)(rng_next(r) >> 11) * 0x1.0p-53;
+}
+
+/* core.cpp:68-76 (Box-Muller on the stream's own uniforms). */
+static double rng_normal(rng_t* r) {
+  double u1 = rng_uniform01(r);
+  while (u1 <= 0.0) u1 = rng_uniform01(r);
+  const double u2 = rng_uniform01(r);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+/* core.cpp:78 */
+static int rng_bernoulli(rng_t* r, double p) { return rng_uniform01(r) < p; }
+
+int bsc_rng_normals(uint64_t base_seed, uint64_t index, int derived, uint64_t n,
+                    double* out) {
+  rng_t r;
+  if (derived)
+    rng_derived(&r, base_seed, index);
+  else
+    rng_seed(&r, base_seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = rng_normal(&r);
+  return OK;
+}
+
+int bsc_rng_uniforms(uint64_t seed, uint64_t n, double* out) {
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint64_t i = 0; i < n; ++i) out[i] = rng_uniform01(&r);
+  return OK;
+}
+
+/* ------------------------------------------------------------- fixtures */
+/* bars.cpp:20-31 (dictionary) and :33-65 (draw order: 2R Bernoullis, then
+ * one normal per pixel). */
+int bsc_make_bars(uint32_t size, uint64_t n, double prob, double amplitude,
+                  double noise, int max_mode, uint64_t seed, double* y_out,
+                  double* truth_out) {
+  if (size == 0) return fail(E_CONFIG, "bars: size must be >= 1");
+  if (n == 0) return fail(E_CONFIG, "bars: need at least one data point");
+  if (amplitude <= 0.0) return fail(E_CONFIG, "bars: amplitude must be > 0");
+  if (noise < 0.0) return fail(E_CONFIG, "bars: noise must be >= 0");
+  const uint32_t nb = 2 * size;
+  const double p = prob > 0.0 ? prob : 2.0 / (double)nb;
+  if (p >= 1.0) return fail(E_CONFIG, "bars: prob must lie in (0,1)");
+  const size_t d = (size_t)size * size;
+  double* w = calloc(d * nb, sizeof(double));
+  uint32_t* act = malloc(nb * sizeof(uint32_t));
+  for (uint32_t k = 0; k < size; ++k)
+    for (uint32_t j = 0; j < size; ++j) {
+      w[((size_t)k * size + j) * nb + k] = amplitude;
+      w[((size_t)j * size + k) * nb + size + k] = amplitude;
+    }
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t na = 0;
+    for (uint32_t b = 0; b < nb; ++b)
+      if (rng_bernoulli(&r, p)) act[na++] = b;
+    for (size_t px = 0; px < d; ++px) {
+      double v = 0.0;
+      for (uint32_t a = 0; a < na; ++a) {
+        const double wv = w[px * nb + act[a]];
+        v = max_mode ? dmax(v, wv) : v + wv;
+      }
+      y_out[i * d + px] = v + noise * rng_normal(&r);
+    }
+  }
+  if (truth_out) memcpy(truth_out, w, d * nb * sizeof(double));
+  free(w);
+  free(act);
+  return OK;
+}
+
+static int validate_params(uint32_t d, uint32_t h, const double* w, double pi,
+                           double sigma2) {
+  for (size_t i = 0; i < (size_t)d * h; ++i)
+    if (!isfinite(w[i])) return fail(E_NUMERIC, "bsc: non-finite dictionary");
+  if (!(sigma2 > 0.0) || !isfinite(sigma2))
+    return fail(E_CONFIG, "bsc: sigma2 must be positive");
+  if (!(pi > 0.0 && pi < 1.0)) return fail(E_CONFIG, "bsc: pi must lie in (0,1)");
+  return OK;
+}
+
+/* LinearDiscreteModel::generate, linear_discrete.cpp:452-479 (BSC): H
+ * Bernoullis, mean = W s (left-to-right; s_j = 0 terms add an exact zero and
+ * are skipped, s_j = 1 terms add W exactly), then D normals. */
+int bsc_generate(uint32_t d, uint32_t h, const double* w, double pi,
+                 double sigma2, uint64_t n, uint64_t seed, double* y_out) {
+  int rc = validate_params(d, h, w, pi, sigma2);
+  if (rc) return rc;
+  const double noise_std = sqrt(sigma2);
+  uint32_t* act = malloc(h * sizeof(uint32_t));
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t na = 0;
+    for (uint32_t j = 0; j < h; ++j)
+      if (rng_bernoulli(&r, pi)) act[na++] = j;
+    for (uint32_t di = 0; di < d; ++di) {
+      double acc = 0.0;
+      const double* row = w + (size_t)di * h;
+      for (uint32_t a = 0; a < na; ++a) acc += row[act[a]];
+      y_out[i * d + di] = acc + noise_std * rng_normal(&r);
+    }
+  }
+  free(act);
+  return OK;
+}
+
+/* Ground-truth dictionary for BASELINE configs c2-c4:
+ * W_dh ~ N(0,1) from RngStream::derived(seed, 0x77747275 "wtru") in
+ * row-major order, each column scaled to unit L2 norm, then times `scale`. */
+int bsc_random_dictionary(uint32_t d, uint32_t h, uint64_t seed, double scale,
+                          double* w_out) {
+  rng_t r;
+  rng_derived(&r, seed, 0x77747275ULL);
+  for (size_t i = 0; i < (size_t)d * h; ++i) w_out[i] = rng_normal(&r);
+  for (uint32_t j = 0; j < h; ++j) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < d; ++i) acc += w_out[(size_t)i * h + j] * w_out[(size_t)i * h + j];
+    const double nrm = sqrt(acc);
+    for (uint32_t i = 0; i < d; ++i)
+      w_out[(size_t)i * h + j] = w_out[(size_t)i * h + j] / nrm * scale;
+  }
+  return OK;
+}
+
+/* model.cpp:187-199 (data_column_means, data_mean_variance). */
+static void column_means(const double* y, uint64_t n, uint32_t d, double* means) {
+  for (uint32_t j = 0; j < d; ++j) means[j] = 0.0;
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < d; ++j) means[j] += y[i * d + j];
+  for (uint32_t j = 0; j < d; ++j) means[j] /= (double)n;
+}
+
+static double mean_variance(const double* y, uint64_t n, uint32_t d,
+                            const double* means) {
+  double acc = 0.0;
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < d; ++j) {
+      const double c = y[i * d + j] - means[j];
+      acc += c * c;
+    }
+  return acc / (double)(n * d);
+}
+
+int bsc_data_mean_variance(const double* y, uint64_t n, uint32_t d, double* out) {
+  double* m = malloc(d * sizeof(double));
+  column_means(y, n, d, m);
+  *out = mean_variance(y, n, d, m);
+  free(m);
+  return OK;
+}
+
+/* BASELINE.json init recipe as pinned in SURVEY.md §8(d):
+ * W0[d,h] = mean_d + 0.25*std_d*z (z: RngStream::derived(seed, 0x696e6974),
+ * row-major (d,h)); std_d the per-pixel population std; pi0 = 1/H;
+ * sigma2_0 = data_mean_variance (model.cpp:187-199). */
+int bsc_baseline_init(uint32_t d, uint32_t h, const double* y, uint64_t n,
+                      uint64_t seed, double* w_out, double* pi_out,
+                      double* sigma2_out) {
+  if (n < 2) return fail(E_DATA, "init requires at least two data points");
+  double* m = malloc(d * sizeof(double));
+  double* sd = malloc(d * sizeof(double));
+  column_means(y, n, d, m);
+  for (uint32_t j = 0; j < d; ++j) sd[j] = 0.0;
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < d; ++j) {
+      const double c = y[i * d + j] - m[j];
+      sd[j] += c * c;
+    }
+  for (uint32_t j = 0; j < d; ++j) sd[j] = sqrt(sd[j] / (double)n);
+  rng_t r;
+  rng_derived(&r, seed, 0x696e6974ULL);
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j)
+      w_out[(size_t)i * h + j] = m[i] + 0.25 * sd[i] * rng_normal(&r);
+  *pi_out = 1.0 / (double)h;
+  *sigma2_out = dmax(mean_variance(y, n, d, m), K_MIN_SIGMA2);
+  free(m);
+  free(sd);
+  return OK;
+}
+
+/* LinearDiscreteModel::standard_init, linear_discrete.cpp:129-148 with
+ * detail::init_weights, model.cpp:201-220 (RngStream(seed)). */
+int bsc_standard_init(uint32_t d, uint32_t h, uint32_t hprime, const double* y,
+                      uint64_t n, uint64_t seed, double* w_out, double* pi_out,
+                      double* sigma2_out) {
+  if (n < 2) return fail(E_DATA, "standard_init requires at least two data points");
+  double* m = malloc(d * sizeof(double));
+  column_means(y, n, d, m);
+  const double var = mean_variance(y, n, d, m);
+  const double sd = var > 0.0 ? sqrt(var / h) : 0.0;
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j) w_out[(size_t)i * h + j] = m[i] + sd * rng_normal(&r);
+  *sigma2_out = dmax(var, K_MIN_SIGMA2);
+  const double hp = (double)(hprime < h ? hprime : h);
+  *pi_out = hp / (2.0 * (double)h);
+  free(m);
+  return OK;
+}
+
+/* ----------------------------------------------------------- truncation */
+/* core.cpp:36-45 */
+static int lse(const double* v, size_t n, double* out) {
+  if (n == 0) return fail(E_NUMERIC, "log_sum_exp: empty support");
+  double m = -INFINITY;
+  for (size_t i = 0; i < n; ++i) m = dmax(m, v[i]);
+  if (isinf(m) && m < 0) return fail(E_NUMERIC, "log_sum_exp: empty support");
+  if (n == 1) {
+    *out = v[0];
+    return OK;
+  }
+  double acc = 0.0;
+  for (size_t i = 0; i < n; ++i) acc += exp(v[i] - m);
+  *out = m + log(acc);
+  return OK;
+}
+
+int bsc_log_sum_exp(const double* v, uint64_t n, double* out) {
+  return lse(v, (size_t)n, out);
+}
+
+typedef struct {
+  const double* s;
+  uint32_t i;
+} keyed_t;
+
+/* Descending score, equal scores keep the lower index (stable_sort semantics
+ * of truncation.cpp:48-53 with `>` as the strict order). */
+static int cmp_desc(const void* a, const void* b) {
+  const keyed_t* x = a;
+  const keyed_t* y = b;
+  const double sx = x->s[x->i], sy = y->s[y->i];
+  if (sx > sy) return -1;
+  if (sy > sx) return 1;
+  return (x->i < y->i) ? -1 : (x->i > y->i);
+}
+
+static int cmp_u32(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x < y) ? -1 : (x > y);
+}
+
+/* truncation.cpp:38-57, with a caller-provided scratch of h entries. */
+static int select_cands(const double* scores, uint32_t h, uint32_t hprime,
+                        uint32_t* out, keyed_t* scratch) {
+  if (hprime == 0 || hprime > h)
+    return fail(E_CONFIG, "select_candidates: hprime out of range");
+  for (uint32_t i = 0; i < h; ++i)
+    if (!isfinite(scores[i]))
+      return fail(E_CONFIG, "select_candidates: scores must be finite");
+  for (uint32_t i = 0; i < h; ++i) scratch[i] = (keyed_t){scores, i};
+  qsort(scratch, h, sizeof(keyed_t), cmp_desc);
+  for (uint32_t i = 0; i < hprime; ++i) out[i] = scratch[i].i;
+  qsort(out, hprime, sizeof(uint32_t), cmp_u32);
+  return OK;
+}
+
+int bsc_select_candidates(const double* scores, uint32_t h, uint32_t hprime,
+                          uint32_t* out) {
+  keyed_t* k = malloc((h ? h : 1) * sizeof(keyed_t));
+  int rc = select_cands(scores, h, hprime, out, k);
+  free(k);
+  return rc;
+}
+
+/* truncation.cpp:23-30 */
+static int validate_trunc(uint32_t h, uint32_t hprime, uint32_t gamma) {
+  if (h == 0) return fail(E_CONFIG, "truncation: latents must be >= 1");
+  if (hprime == 0 || hprime > h)
+    return fail(E_CONFIG, "truncation: hprime must satisfy 1 <= hprime <= latents");
+  if (gamma == 0 || gamma > hprime)
+    return fail(E_CONFIG, "truncation: gamma must satisfy 1 <= gamma <= hprime");
+  return OK;
+}
+
+/* truncation.cpp:61-93 (V = 1), saturating. */
+static uint64_t sat_mul(uint64_t a, uint64_t b) {
+  if (a != 0 && b > UINT64_MAX / a) return UINT64_MAX;
+  return a * b;
+}
+static uint64_t sat_add(uint64_t a, uint64_t b) {
+  return (UINT64_MAX - a < b) ? UINT64_MAX : a + b;
+}
+static uint64_t binom(uint64_t n, uint64_t k) {
+  if (k > n) return 0;
+  if (n - k < k) k = n - k;
+  uint64_t r = 1;
+  for (uint64_t i = 1; i <= k; ++i) {
+    r = sat_mul(r, n - k + i);
+    r /= i;
+  }
+  return r;
+}
+static uint64_t state_count(uint32_t h, uint32_t hprime, uint32_t gamma) {
+  uint64_t total = sat_add(1, h);
+  for (uint32_t k = 2; k <= gamma; ++k) total = sat_add(total, binom(hprime, k));
+  return total;
+}
+
+int bsc_state_count(uint32_t h, uint32_t hprime, uint32_t gamma, uint64_t* out) {
+  int rc = validate_trunc(h, hprime, gamma);
+  if (rc) return rc;
+  *out = state_count(h, hprime, gamma);
+  return OK;
+}
+
+/* StateTemplate multi-active patterns, truncation.cpp:116-147: depth-first
+ * over candidate positions, supports of size 2..gamma in lexicographic order
+ * with prefixes first. Patterns are stored as position lists. */
+typedef struct {
+  uint32_t hprime, gamma;
+  size_t count;
+  uint8_t* len;  /* [count] */
+  uint8_t* pos;  /* [count * gamma] */
+} tmpl_t;
+
+static void dfs(tmpl_t* t, uint8_t* support, uint32_t depth, uint32_t next) {
+  if (depth >= 2) {
+    t->len[t->count] = (uint8_t)depth;
+    memcpy(t->pos + t->count * t->gamma, support, depth);
+    t->count++;
+  }
+  if (depth == t->gamma) return;
+  for (uint32_t p = next; p < t->hprime; ++p) {
+    support[depth] = (uint8_t)p;
+    dfs(t, support, depth + 1, p + 1);
+  }
+}
+
+static int tmpl_build(tmpl_t* t, uint32_t h, uint32_t hprime, uint32_t gamma,
+                      uint64_t cap) {
+  int rc = validate_trunc(h, hprime, gamma);
+  if (rc) return rc;
+  const uint64_t total = state_count(h, hprime, gamma);
+  if (total > cap)
+    return fail(E_CONFIG, "state explosion: %llu states per data point exceeds cap of %llu",
+                (unsigned long long)total, (unsigned long long)cap);
+  if (hprime > 255) return fail(E_CONFIG, "oracle: hprime > 255 unsupported");
+  t->hprime = hprime;
+  t->gamma = gamma;
+  t->count = 0;
+  const size_t np = (size_t)(total - 1 - h);
+  t->len = malloc(np ? np : 1);
+  t->pos = malloc((np ? np : 1) * gamma);
+  uint8_t support[256];
+  if (gamma >= 2) dfs(t, support, 0, 0);
+  return OK;
+}
+
+static void tmpl_free(tmpl_t* t) {
+  free(t->len);
+  free(t->pos);
+}
+
+/* StateTemplate::instantiate, truncation.cpp:153-169, as (count, units) lists:
+ * zero state, H singletons, then patterns mapped through the candidates. */
+typedef struct {
+  size_t n;
+  uint8_t* len;   /* [n] */
+  uint32_t* act;  /* [n * gamma_max] ascending unit indices */
+  uint32_t stride;
+} states_t;
+
+static void instantiate(const tmpl_t* t, uint32_t h, const uint32_t* cand,
+                        states_t* s) {
+  size_t k = 0;
+  s->len[k++] = 0;
+  for (uint32_t u = 0; u < h; ++u) {
+    s->len[k] = 1;
+    s->act[k * s->stride] = u;
+    ++k;
+  }
+  for (size_t p = 0; p < t->count; ++p) {
+    s->len[k] = t->len[p];
+    for (uint32_t a = 0; a < t->len[p]; ++a)
+      s->act[k * s->stride + a] = cand[t->pos[p * t->gamma + a]];
+    ++k;
+  }
+  s->n = k;
+}
+
+int bsc_enumerate_binary(const uint32_t* cand, uint32_t hprime, uint32_t h,
+                         uint32_t gamma, double* out, uint64_t* count) {
+  for (uint32_t i = 1; i < hprime; ++i)
+    if (cand[i] <= cand[i - 1])
+      return fail(E_CONFIG, "enumerate states: candidate set must be ascending");
+  for (uint32_t i = 0; i < hprime; ++i)
+    if (cand[i] >= h)
+      return fail(E_CONFIG, "enumerate states: candidate index out of range");
+  tmpl_t t;
+  int rc = tmpl_build(&t, h, hprime, gamma, 1000000);
+  if (rc) return rc;
+  states_t s;
+  const size_t total = 1 + h + t.count;
+  s.stride = gamma;
+  s.len = malloc(total);
+  s.act = malloc(total * gamma * sizeof(uint32_t));
+  instantiate(&t, h, cand, &s);
+  *count = s.n;
+  if (out) {
+    memset(out, 0, s.n * h * sizeof(double));
+    for (size_t i = 0; i < s.n; ++i)
+      for (uint32_t a = 0; a < s.len[i]; ++a) out[i * h + s.act[i * s.stride + a]] = 1.0;
+  }
+  free(s.len);
+  free(s.act);
+  tmpl_free(&t);
+  return OK;
+}
+
+/* ---------------------------------------------------------------- model */
+static double gauss_log_norm(size_t dim, double sigma2) { /* :26-28 */
+  return -0.5 * (double)dim * (K_LOG_2PI + log(sigma2));
+}
+
+/* log_prior :150-166 + log_joint :168-178 (BSC). */
+int bsc_log_joint(uint32_t d, uint32_t h, const double* w, double pi,
+                  double sigma2, const double* y, const double* s, double* out) {
+  const double lp1 = log(pi), lp0 = log(1.0 - pi);
+  double prior = 0.0;
+  for (uint32_t j = 0; j < h; ++j) {
+    if (s[j] == 0.0) {
+      prior += lp0;
+      continue;
+    }
+    if (s[j] != 1.0) return fail(E_CONFIG, "bsc: latent value outside the alphabet");
+    prior += lp1;
+  }
+  double resid = 0.0;
+  for (uint32_t i = 0; i < d; ++i) {
+    double acc = 0.0;
+    for (uint32_t j = 0; j < h; ++j) acc += w[(size_t)i * h + j] * s[j];
+    const double r = y[i] - acc;
+    resid += r * r;
+  }
+  *out = prior + gauss_log_norm(d, sigma2) - resid / (2.0 * sigma2);
+  return OK;
+}
+
+/* Per-shard accumulators in the field order of linear_discrete.cpp:211-217. */
+typedef struct {
+  double *sum_s, *sum_ssT, *sum_y_sT;
+  double counts, sum_y2, log_partition;
+  uint64_t points;
+} stats_t;
+
+typedef struct {
+  uint32_t d, h, hprime, gamma;
+  const double* w;
+  double pi, sigma2, temperature;
+  const double* y;
+  const double* gram; /* W^T W, left-to-right over d (linear_discrete.cpp:220) */
+  const double* wt;   /* W^T, H x D */
+  const tmpl_t* tmpl;
+} ctx_t;
+
+static void stats_alloc(stats_t* s, uint32_t d, uint32_t h) {
+  s->sum_s = calloc(h, sizeof(double));
+  s->sum_ssT = calloc((size_t)h * h, sizeof(double));
+  s->sum_y_sT = calloc((size_t)d * h, sizeof(double));
+  s->counts = s->sum_y2 = s->log_partition = 0.0;
+  s->points = 0;
+}
+
+static void stats_free(stats_t* s) {
+  free(s->sum_s);
+  free(s->sum_ssT);
+  free(s->sum_y_sT);
+}
+
+static void gram_of(const double* w, uint32_t d, uint32_t h, double* wt, double* gram) {
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j) wt[(size_t)j * d + i] = w[(size_t)i * h + j];
+  for (uint32_t i = 0; i < h; ++i)
+    for (uint32_t j = 0; j < h; ++j) {
+      double acc = 0.0;
+      for (uint32_t t = 0; t < d; ++t) acc += wt[(size_t)i * d + t] * w[(size_t)t * h + j];
+      gram[(size_t)i * h + j] = acc;
+    }
+}
+
+/* LinearDiscreteModel::estep_impl, linear_discrete.cpp:202-325, BSC value
+ * table {1} (:75-79). If `map_states` is non-NULL the inference readout of
+ * :313-322 is written too. */
+static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
+                      stats_t* st, double* map_states, double* map_mass,
+                      double* expected) {
+  const uint32_t d = c->d, h = c->h;
+  const double inv2s = 1.0 / (2.0 * c->sigma2);
+  const double norm_const = gauss_log_norm(d, c->sigma2);
+  const double log_p1 = log(c->pi), log_p0 = log(1.0 - c->pi);
+  const double dlp = log_p1 - log_p0;
+  const double zero_prior = (double)h * log_p0;
+
+  const size_t total = 1 + h + c->tmpl->count;
+  states_t s;
+  s.stride = c->gamma;
+  s.len = malloc(total);
+  s.act = malloc(total * c->gamma * sizeof(uint32_t));
+  double* b = malloc(h * sizeof(double));
+  double* scores = malloc(h * sizeof(double));
+  double* es = malloc(h * sizeof(double));
+  double* lj = malloc(total * sizeof(double));
+  double* q = malloc(total * sizeof(double));
+  uint32_t* cand = malloc(c->hprime * sizeof(uint32_t));
+  keyed_t* scratch = malloc(h * sizeof(keyed_t));
+  int rc = OK;
+
+  for (uint64_t n = row_begin; n < row_end; ++n) {
+    const double* y = c->y + n * d;
+    for (uint32_t u = 0; u < h; ++u) { /* :241, b = W^T y */
+      double acc = 0.0;
+      for (uint32_t t = 0; t < d; ++t) acc += c->wt[(size_t)u * d + t] * y[t];
+      b[u] = acc;
+    }
+    double y2 = 0.0; /* :242 */
+    for (uint32_t t = 0; t < d; ++t) y2 += y[t] * y[t];
+    for (uint32_t u = 0; u < h; ++u) { /* :244-252 */
+      const double v = 1.0;
+      double best = -INFINITY;
+      best = dmax(best, log_p1 + (2.0 * v * b[u] - v * v * c->gram[(size_t)u * h + u]) * inv2s);
+      scores[u] = best;
+    }
+    rc = select_cands(scores, h, c->hprime, cand, scratch); /* :253 */
+    if (rc) break;
+    instantiate(c->tmpl, h, cand, &s); /* :254 */
+
+    const double base = zero_prior + norm_const - y2 * inv2s; /* :256 */
+    for (size_t i = 0; i < s.n; ++i) {                      /* :257-270 */
+      const uint32_t* act = s.act + i * s.stride;
+      double prior = 0.0, lin = 0.0, quad = 0.0;
+      for (uint32_t a = 0; a < s.len[i]; ++a) {
+        const uint32_t ha = act[a];
+        const double va = 1.0;
+        prior += dlp;
+        lin += va * b[ha];
+        quad += va * va * c->gram[(size_t)ha * h + ha];
+        for (uint32_t cc = a + 1; cc < s.len[i]; ++cc)
+          quad += 2.0 * va * 1.0 * c->gram[(size_t)ha * h + act[cc]];
+      }
+      lj[i] = base + prior + (2.0 * lin - quad) * inv2s;
+    }
+
+    double lse1;
+    rc = lse(lj, s.n, &lse1); /* :272 */
+    if (rc) break;
+    if (c->temperature == 1.0) { /* :273-276 */
+      for (size_t i = 0; i < s.n; ++i) q[i] = exp(lj[i] - lse1);
+    } else { /* :277-286 */
+      double m = lj[0];
+      for (size_t i = 0; i < s.n; ++i) m = dmax(m, lj[i]);
+      double acc = 0.0;
+      for (size_t i = 0; i < s.n; ++i) {
+        q[i] = exp((lj[i] - m) / c->temperature);
+        acc += q[i];
+      }
+      for (size_t i = 0; i < s.n; ++i) q[i] /= acc;
+    }
+
+    for (uint32_t j = 0; j < h; ++j) es[j] = 0.0; /* :288-303 */
+    for (size_t i = 0; i < s.n; ++i) {
+      const double qi = q[i];
+      const uint32_t* act = s.act + i * s.stride;
+      for (uint32_t a = 0; a < s.len[i]; ++a) {
+        const uint32_t ha = act[a];
+        const double va = 1.0;
+        es[ha] += qi * va;
+        st->counts += qi;
+        st->sum_ssT[(size_t)ha * h + ha] += qi * va * va;
+        for (uint32_t cc = a + 1; cc < s.len[i]; ++cc) {
+          const double cross = qi * va * 1.0;
+          st->sum_ssT[(size_t)ha * h + act[cc]] += cross;
+          st->sum_ssT[(size_t)act[cc] * h + ha] += cross;
+        }
+      }
+    }
+    for (uint32_t j = 0; j < h; ++j) st->sum_s[j] += es[j]; /* :304 */
+    for (uint32_t i = 0; i < d; ++i) {                       /* :305-308 */
+      const double yi = y[i];
+      double* row = st->sum_y_sT + (size_t)i * h;
+      for (uint32_t j = 0; j < h; ++j) row[j] += yi * es[j];
+    }
+    st->sum_y2 += y2; /* :309-311 */
+    st->log_partition += lse1;
+    st->points++;
+
+    if (map_states) { /* :313-322 */
+      size_t best = 0;
+      for (size_t i = 1; i < s.n; ++i)
+        if (q[i] > q[best]) best = i;
+      map_mass[n] = q[best];
+      for (uint32_t a = 0; a < s.len[best]; ++a)
+        map_states[n * h + s.act[best * s.stride + a]] = 1.0;
+      for (uint32_t j = 0; j < h; ++j) expected[n * h + j] = es[j];
+    }
+  }
+  free(s.len);
+  free(s.act);
+  free(b);
+  free(scores);
+  free(es);
+  free(lj);
+  free(q);
+  free(cand);
+  free(scratch);
+  return rc;
+}
+
+static int ctx_init(ctx_t* c, tmpl_t* t, uint32_t d, uint32_t h, uint32_t hprime,
+                    uint32_t gamma, const double* w, double pi, double sigma2,
+                    double temperature, const double* y) {
+  int rc = validate_params(d, h, w, pi, sigma2);
+  if (rc) return rc;
+  rc = tmpl_build(t, h, hprime, gamma, 1000000);
+  if (rc) return rc;
+  double* wt = malloc((size_t)d * h * sizeof(double));
+  double* gram = malloc((size_t)h * h * sizeof(double));
+  gram_of(w, d, h, wt, gram);
+  *c = (ctx_t){d, h, hprime, gamma, w, pi, sigma2, temperature, y, gram, wt, t};
+  return OK;
+}
+
+static void ctx_free(ctx_t* c, tmpl_t* t) {
+  free((void*)c->gram);
+  free((void*)c->wt);
+  tmpl_free(t);
+}
+
+static void stats_out(const stats_t* st, uint32_t d, uint32_t h, double* sum_s,
+                      double* sum_ssT, double* sum_y_sT, double* value_counts,
+                      double* scalars) {
+  if (sum_s) memcpy(sum_s, st->sum_s, h * sizeof(double));
+  if (sum_ssT) memcpy(sum_ssT, st->sum_ssT, (size_t)h * h * sizeof(double));
+  if (sum_y_sT) memcpy(sum_y_sT, st->sum_y_sT, (size_t)d * h * sizeof(double));
+  if (value_counts) value_counts[0] = st->counts;
+  if (scalars) {
+    scalars[0] = st->sum_y2;
+    scalars[1] = st->log_partition;
+    scalars[2] = (double)st->points;
+  }
+}
+
+/* estep_stats, linear_discrete.cpp:327-334 */
+int bsc_estep_stats(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                    const double* w, double pi, double sigma2,
+                    double temperature, const double* y, uint64_t n,
+                    uint64_t row_begin, uint64_t row_end, double* sum_s,
+                    double* sum_ssT, double* sum_y_sT, double* value_counts,
+                    double* scalars) {
+  if (row_end < row_begin || row_end > n) return fail(E_CONFIG, "bad row range");
+  ctx_t c;
+  tmpl_t t;
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
+  if (rc) return rc;
+  stats_t st;
+  stats_alloc(&st, d, h);
+  rc = estep_rows(&c, row_begin, row_end, &st, NULL, NULL, NULL);
+  if (!rc) stats_out(&st, d, h, sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
+  stats_free(&st);
+  ctx_free(&c, &t);
+  return rc;
+}
+
+/* Left-looking Cholesky + per-column substitution, the order fixed by
+ * oracle/eigen_shim (Eigen::LLT usage at linear_discrete.cpp:354-357). */
+static int cholesky(const double* a, size_t n, double* l) {
+  memset(l, 0, n * n * sizeof(double));
+  for (size_t j = 0; j < n; ++j) {
+    double s = a[j * n + j];
+    for (size_t k = 0; k < j; ++k) s -= l[j * n + k] * l[j * n + k];
+    if (!(s > 0.0) || !isfinite(s)) return 1;
+    const double dd = sqrt(s);
+    l[j * n + j] = dd;
+    for (size_t i = j + 1; i < n; ++i) {
+      double t = a[i * n + j];
+      for (size_t k = 0; k < j; ++k) t -= l[i * n + k] * l[j * n + k];
+      l[i * n + j] = t / dd;
+    }
+  }
+  return 0;
+}
+
+static void chol_solve(const double* l, size_t n, double* v) {
+  for (size_t i = 0; i < n; ++i) {
+    double s = v[i];
+    for (size_t k = 0; k < i; ++k) s -= l[i * n + k] * v[k];
+    v[i] = s / l[i * n + i];
+  }
+  for (size_t ii = n; ii-- > 0;) {
+    double s = v[ii];
+    for (size_t k = ii + 1; k < n; ++k) s -= l[k * n + ii] * v[k];
+    v[ii] = s / l[ii * n + ii];
+  }
+}
+
+/* LinearDiscreteModel::mstep, linear_discrete.cpp:336-408 (BSC branch :373-376). */
+int bsc_mstep(uint32_t d, uint32_t h, const double* w_prev, double pi_prev,
+              double sigma2_prev, const double* sum_s, const double* sum_ssT,
+              const double* sum_y_sT, const double* value_counts,
+              const double* scalars, double* w_out, double* pi_out,
+              double* sigma2_out) {
+  (void)sum_s;
+  (void)pi_prev;
+  (void)sigma2_prev;
+  const uint64_t points = (uint64_t)scalars[2];
+  const double n = (double)points, dd = (double)d, nh = n * (double)h;
+  if (points == 0) return fail(E_CONFIG, "bsc: mstep without data");
+  if (w_out != w_prev) memcpy(w_out, w_prev, (size_t)d * h * sizeof(double));
+
+  double trace = 0.0; /* :349 */
+  for (uint32_t i = 0; i < h; ++i) trace += sum_ssT[(size_t)i * h + i];
+  if (trace > 0.0) {
+    double* bm = malloc((size_t)h * h * sizeof(double));
+    double* l = malloc((size_t)h * h * sizeof(double));
+    memcpy(bm, sum_ssT, (size_t)h * h * sizeof(double));
+    const double ridge = 1e-9 * trace / (double)h; /* :352-353 */
+    for (uint32_t i = 0; i < h; ++i) bm[(size_t)i * h + i] += ridge;
+    if (cholesky(bm, h, l) == 0) { /* :354-360 */
+      double* col = malloc(h * sizeof(double));
+      for (uint32_t c = 0; c < d; ++c) {
+        for (uint32_t i = 0; i < h; ++i) col[i] = sum_y_sT[(size_t)c * h + i];
+        chol_solve(l, h, col);
+        for (uint32_t i = 0; i < h; ++i) w_out[(size_t)c * h + i] = col[i];
+      }
+      free(col);
+    }
+    free(bm);
+    free(l);
+  }
+
+  const double t1 = scalars[0]; /* :366-369 */
+  double t2 = 0.0;
+  for (size_t i = 0; i < (size_t)d * h; ++i) t2 += w_out[i] * sum_y_sT[i];
+  double t3 = 0.0;
+  for (uint32_t i = 0; i < h; ++i)
+    for (uint32_t j = 0; j < h; ++j) {
+      double acc = 0.0;
+      for (uint32_t t = 0; t < d; ++t) acc += w_out[(size_t)t * h + i] * w_out[(size_t)t * h + j];
+      t3 += acc * sum_ssT[(size_t)i * h + j];
+    }
+  *sigma2_out = dmax((t1 - 2.0 * t2 + t3) / (n * dd), K_MIN_SIGMA2);
+  *pi_out = dmin(dmax(value_counts[0] / nh, K_MIN_PI), 1.0 - K_MIN_PI);
+  return OK;
+}
+
+/* ------------------------------------------------- map_reduce over shards */
+typedef struct {
+  const ctx_t* c;
+  uint64_t n, shards;
+  stats_t* partial;
+  int* rc;
+  char (*err)[512];
+  uint64_t next;
+  pthread_mutex_t mu;
+} pool_t;
+
+static void shard_range(uint64_t n, uint64_t shards, uint64_t i, uint64_t* b,
+                        uint64_t* e) { /* ShardPlan::with_shards, parallel.cpp:27-43 */
+  const uint64_t base = n / shards, extra = n % shards;
+  *b = i * base + (i < extra ? i : extra);
+  *e = *b + base + (i < extra ? 1 : 0);
+}
+
+static void* pool_worker(void* arg) {
+  pool_t* p = arg;
+  for (;;) {
+    pthread_mutex_lock(&p->mu);
+    const uint64_t i = p->next++;
+    pthread_mutex_unlock(&p->mu);
+    if (i >= p->shards) return NULL;
+    uint64_t b, e;
+    shard_range(p->n, p->shards, i, &b, &e);
+    p->rc[i] = estep_rows(p->c, b, e, &p->partial[i], NULL, NULL, NULL);
+    if (p->rc[i]) snprintf(p->err[i], 512, "shard %llu: %s", (unsigned long long)i, g_err);
+  }
+}
+
+/* LinearDiscreteModel::step (:410-427) via map_reduce (parallel.cpp:109-158):
+ * per-shard stats, ordered fold (SuffStats::combine, :89-107), then mstep. */
+int bsc_step(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+             const double* w, double pi, double sigma2, double temperature,
+             const double* y, uint64_t n, uint32_t shards, uint32_t workers,
+             double* w_out, double* pi_out, double* sigma2_out,
+             double* free_energy) {
+  if (shards == 0 || workers == 0) return fail(E_CONFIG, "shard plan: shards and workers must be >= 1");
+  ctx_t c;
+  tmpl_t t;
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
+  if (rc) return rc;
+  pool_t p;
+  p.c = &c;
+  p.n = n;
+  p.shards = shards;
+  p.partial = malloc(shards * sizeof(stats_t));
+  p.rc = calloc(shards, sizeof(int));
+  p.err = calloc(shards, 512);
+  p.next = 0;
+  pthread_mutex_init(&p.mu, NULL);
+  for (uint32_t i = 0; i < shards; ++i) stats_alloc(&p.partial[i], d, h);
+  const uint32_t threads = workers < shards ? workers : shards;
+  if (threads <= 1) {
+    pool_worker(&p);
+  } else {
+    pthread_t* th = malloc(threads * sizeof(pthread_t));
+    for (uint32_t i = 0; i < threads; ++i) pthread_create(&th[i], NULL, pool_worker, &p);
+    for (uint32_t i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+  }
+  for (uint32_t i = 0; i < shards && !rc; ++i)
+    if (p.rc[i]) rc = fail(p.rc[i], "%s", p.err[i]);
+  if (!rc) {
+    stats_t* tot = &p.partial[0];
+    for (uint32_t i = 1; i < shards; ++i) {
+      const stats_t* o = &p.partial[i];
+      for (uint32_t j = 0; j < h; ++j) tot->sum_s[j] += o->sum_s[j];
+      for (size_t j = 0; j < (size_t)h * h; ++j) tot->sum_ssT[j] += o->sum_ssT[j];
+      for (size_t j = 0; j < (size_t)d * h; ++j) tot->sum_y_sT[j] += o->sum_y_sT[j];
+      tot->counts += o->counts;
+      tot->sum_y2 += o->sum_y2;
+      tot->log_partition += o->log_partition;
+      tot->points += o->points;
+    }
+    double scal[3] = {tot->sum_y2, tot->log_partition, (double)tot->points};
+    double vc = tot->counts;
+    rc = bsc_mstep(d, h, w, pi, sigma2, tot->sum_s, tot->sum_ssT, tot->sum_y_sT,
+                   &vc, scal, w_out, pi_out, sigma2_out);
+    *free_energy = tot->log_partition;
+  }
+  for (uint32_t i = 0; i < shards; ++i) stats_free(&p.partial[i]);
+  free(p.partial);
+  free(p.rc);
+  free(p.err);
+  pthread_mutex_destroy(&p.mu);
+  ctx_free(&c, &t);
+  return rc;
+}
+
+/* Per-point candidate sets exactly as estep_impl selects them (:240-253). */
+int bsc_candidates(uint32_t d, uint32_t h, uint32_t hprime, const double* w,
+                   double pi, double sigma2, const double* y, uint64_t n,
+                   uint32_t* out) {
+  int rc = validate_params(d, h, w, pi, sigma2);
+  if (rc) return rc;
+  double* wt = malloc((size_t)d * h * sizeof(double));
+  double* gram = malloc((size_t)h * h * sizeof(double));
+  double* scores = malloc(h * sizeof(double));
+  keyed_t* scratch = malloc(h * sizeof(keyed_t));
+  gram_of(w, d, h, wt, gram);
+  const double inv2s = 1.0 / (2.0 * sigma2), lp = log(pi);
+  for (uint64_t i = 0; i < n && !rc; ++i) {
+    const double* yy = y + i * d;
+    for (uint32_t u = 0; u < h; ++u) {
+      double acc = 0.0;
+      for (uint32_t t = 0; t < d; ++t) acc += wt[(size_t)u * d + t] * yy[t];
+      scores[u] = dmax(-INFINITY, lp + (2.0 * 1.0 * acc - 1.0 * 1.0 * gram[(size_t)u * h + u]) * inv2s);
+    }
+    rc = select_cands(scores, h, hprime, out + i * hprime, scratch);
+  }
+  free(wt);
+  free(gram);
+  free(scores);
+  free(scratch);
+  return rc;
+}
+
+/* LinearDiscreteModel::inference, linear_discrete.cpp:429-450 (T = 1). */
+int bsc_inference(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                  const double* w, double pi, double sigma2, const double* y,
+                  uint64_t n, double* map_states, double* map_mass,
+                  double* expected) {
+  ctx_t c;
+  tmpl_t t;
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, 1.0, y);
+  if (rc) return rc;
+  memset(map_states, 0, n * h * sizeof(double));
+  stats_t st;
+  stats_alloc(&st, d, h);
+  rc = estep_rows(&c, 0, n, &st, map_states, map_mass, expected);
+  stats_free(&st);
+  ctx_free(&c, &t);
+  return rc;
+}
+
+/* exact_log_likelihood, linear_discrete.cpp:481-508. */
+int bsc_exact_log_likelihood(uint32_t d, uint32_t h, const double* w, double pi,
+                             double sigma2, const double* y, uint64_t n,
+                             double* out) {
+  int rc = validate_params(d, h, w, pi, sigma2);
+  if (rc) return rc;
+  const uint64_t count = state_count(h, h, h);
+  if (count > (1u << 22))
+    return fail(E_CONFIG, "bsc: state space too large for exact evaluation");
+  uint32_t* all = malloc(h * sizeof(uint32_t));
+  for (uint32_t i = 0; i < h; ++i) all[i] = i;
+  double* dense = malloc(count * h * sizeof(double));
+  uint64_t got;
+  rc = bsc_enumerate_binary(all, h, h, h, dense, &got);
+  double* lj = malloc(count * sizeof(double));
+  double total = 0.0;
+  for (uint64_t i = 0; i < n && !rc; ++i) {
+    for (uint64_t s = 0; s < got && !rc; ++s)
+      rc = bsc_log_joint(d, h, w, pi, sigma2, y + i * d, dense + s * h, &lj[s]);
+    double l;
+    if (!rc) rc = lse(lj, got, &l);
+    if (!rc) total += l;
+  }
+  *out = total;
+  free(all);
+  free(dense);
+  free(lj);
+  return rc;
+}

@@ -1,0 +1,262 @@
+"""TEST INFRASTRUCTURE ONLY — the parity oracle, never the product.
+
+ctypes front end over the two CPU oracles of the BSC truncated-EM path:
+
+* ``port`` — ``oracle/_build/libbsc_oracle.so``, the plain-C restatement
+  (``oracle/bsc_oracle.c``), built everywhere (here and travelling to the GPU
+  box as a prebuilt ``.so``);
+* ``ref``  — ``oracle/_ref/libprsp_ref.so``, the reference's own sources
+  (``/root/reference/proj/src``) compiled against ``oracle/eigen_shim``.
+  Built only where ``/root/reference`` exists; the prebuilt ``.so`` travels.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs may
+import this module. Functions raise :class:`OracleError` carrying the
+prsp status code (prsp.h:39-45).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_LIB = os.path.join(HERE, "_build", "libbsc_oracle.so")
+REF_LIB = os.path.join(HERE, "_ref", "libprsp_ref.so")
+REF_SRC = "/root/reference/proj/src"
+
+_u32, _u64, _dbl, _int, _ptr = C.c_uint32, C.c_uint64, C.c_double, C.c_int, C.c_void_p
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the C restatement (and the reference, when its sources exist)."""
+    out = subprocess.run(["make", "-C", HERE, "all"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_ptr)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Oracle:
+    """One CPU oracle library (``kind`` = "port" or "ref")."""
+
+    def __init__(self, kind: str = "port"):
+        path = PORT_LIB if kind == "port" else REF_LIB
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"oracle library missing: {path} (run oracle.build())")
+        self.kind = kind
+        self.lib = C.CDLL(path)
+        self.pre = "bsc_" if kind == "port" else "ref_"
+        self.lib[self.pre + "last_error"].restype = C.c_char_p
+
+    @staticmethod
+    def available(kind: str) -> bool:
+        return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
+
+    def _call(self, name, *args):
+        fn = self.lib[self.pre + name]
+        fn.restype = _int
+        rc = fn(*args)
+        if rc != 0:
+            msg = self.lib[self.pre + "last_error"]().decode()
+            raise OracleError(rc, msg)
+
+    # ------------------------------------------------------------ fixtures
+    def rng_normals(self, base_seed, index, derived, n):
+        out = np.empty(n)
+        self._call("rng_normals", _u64(base_seed), _u64(index), _int(derived), _u64(n), _p(out))
+        return out
+
+    def make_bars(self, size, n, prob=0.0, amplitude=10.0, noise=2.0, max_mode=False, seed=0):
+        d, hb = size * size, 2 * size
+        y = np.empty((n, d))
+        truth = np.empty((d, hb))
+        self._call("make_bars", _u32(size), _u64(n), _dbl(prob), _dbl(amplitude), _dbl(noise),
+                   _int(int(max_mode)), _u64(seed), _p(y), _p(truth))
+        return y, truth
+
+    def generate(self, w, pi, sigma2, n, seed):
+        w = _f64(w)
+        d, h = w.shape
+        y = np.empty((n, d))
+        self._call("generate", _u32(d), _u32(h), _p(w), _dbl(pi), _dbl(sigma2), _u64(n), _u64(seed), _p(y))
+        return y
+
+    def random_dictionary(self, d, h, seed, scale=5.0):
+        w = np.empty((d, h))
+        self._call("random_dictionary", _u32(d), _u32(h), _u64(seed), _dbl(scale), _p(w))
+        return w
+
+    def baseline_init(self, y, h, seed):
+        y = _f64(y)
+        n, d = y.shape
+        w = np.empty((d, h))
+        pi, s2 = _dbl(), _dbl()
+        self._call("baseline_init", _u32(d), _u32(h), _p(y), _u64(n), _u64(seed), _p(w), C.byref(pi), C.byref(s2))
+        return w, pi.value, s2.value
+
+    def standard_init(self, y, h, hprime, gamma, seed):
+        y = _f64(y)
+        n, d = y.shape
+        w = np.empty((d, h))
+        pi, s2 = _dbl(), _dbl()
+        if self.kind == "port":
+            self._call("standard_init", _u32(d), _u32(h), _u32(hprime), _p(y), _u64(n), _u64(seed),
+                       _p(w), C.byref(pi), C.byref(s2))
+        else:
+            self._call("standard_init", _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(y), _u64(n),
+                       _u64(seed), _p(w), C.byref(pi), C.byref(s2))
+        return w, pi.value, s2.value
+
+    def data_mean_variance(self, y):
+        y = _f64(y)
+        out = _dbl()
+        self._call("data_mean_variance", _p(y), _u64(y.shape[0]), _u32(y.shape[1]), C.byref(out))
+        return out.value
+
+    # ---------------------------------------------------------- truncation
+    def select_candidates(self, scores, hprime):
+        s = _f64(scores)
+        out = np.empty(hprime, np.uint32)
+        self._call("select_candidates", _p(s), _u32(len(s)), _u32(hprime), _p(out))
+        return out
+
+    def state_count(self, h, hprime, gamma):
+        out = _u64()
+        self._call("state_count", _u32(h), _u32(hprime), _u32(gamma), C.byref(out))
+        return out.value
+
+    def enumerate_binary(self, cand, h, gamma):
+        cand = np.ascontiguousarray(cand, dtype=np.uint32)
+        cnt = _u64()
+        self._call("enumerate_binary", _p(cand), _u32(len(cand)), _u32(h), _u32(gamma), None, C.byref(cnt))
+        out = np.empty((cnt.value, h))
+        self._call("enumerate_binary", _p(cand), _u32(len(cand)), _u32(h), _u32(gamma), _p(out), C.byref(cnt))
+        return out
+
+    def log_sum_exp(self, v):
+        v = _f64(v)
+        out = _dbl()
+        self._call("log_sum_exp", _p(v), _u64(len(v)), C.byref(out))
+        return out.value
+
+    # --------------------------------------------------------------- model
+    def log_joint(self, w, pi, sigma2, y, s):
+        w, y, s = _f64(w), _f64(y), _f64(s)
+        out = _dbl()
+        self._call("log_joint", _u32(w.shape[0]), _u32(w.shape[1]), _p(w), _dbl(pi), _dbl(sigma2), _p(y), _p(s),
+                   C.byref(out))
+        return out.value
+
+    def estep_stats(self, w, pi, sigma2, y, hprime, gamma, temperature=1.0, rows=None):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        b, e = (0, n) if rows is None else rows
+        st = dict(sum_s=np.empty(h), sum_ssT=np.empty((h, h)), sum_y_sT=np.empty((d, h)),
+                  value_counts=np.empty(1), scalars=np.empty(3))
+        self._call("estep_stats", _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(pi), _dbl(sigma2),
+                   _dbl(temperature), _p(y), _u64(n), _u64(b), _u64(e), _p(st["sum_s"]), _p(st["sum_ssT"]),
+                   _p(st["sum_y_sT"]), _p(st["value_counts"]), _p(st["scalars"]))
+        sc = st.pop("scalars")
+        st.update(sum_y2=sc[0], log_partition=sc[1], points=int(sc[2]))
+        return st
+
+    def mstep(self, stats, w_prev, pi_prev, sigma2_prev, hprime=1, gamma=1):
+        w_prev = _f64(w_prev)
+        d, h = w_prev.shape
+        w = np.empty((d, h))
+        pi, s2 = _dbl(), _dbl()
+        sc = np.array([stats["sum_y2"], stats["log_partition"], float(stats["points"])])
+        vc = _f64(np.atleast_1d(stats["value_counts"]))
+        args = [_p(w_prev), _dbl(pi_prev), _dbl(sigma2_prev), _p(_f64(stats["sum_s"])), _p(_f64(stats["sum_ssT"])),
+                _p(_f64(stats["sum_y_sT"])), _p(vc), _p(sc), _p(w), C.byref(pi), C.byref(s2)]
+        if self.kind == "port":
+            self._call("mstep", _u32(d), _u32(h), *args)
+        else:
+            self._call("mstep", _u32(d), _u32(h), _u32(hprime), _u32(gamma), *args)
+        return w, pi.value, s2.value
+
+    def step(self, w, pi, sigma2, y, hprime, gamma, temperature=1.0, shards=1, workers=1):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        wo = np.empty((d, h))
+        pio, s2o, f = _dbl(), _dbl(), _dbl()
+        self._call("step", _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(pi), _dbl(sigma2),
+                   _dbl(temperature), _p(y), _u64(y.shape[0]), _u32(shards), _u32(workers), _p(wo),
+                   C.byref(pio), C.byref(s2o), C.byref(f))
+        return wo, pio.value, s2o.value, f.value
+
+    def candidates(self, w, pi, sigma2, y, hprime):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        out = np.empty((y.shape[0], hprime), np.uint32)
+        self._call("candidates", _u32(d), _u32(h), _u32(hprime), _p(w), _dbl(pi), _dbl(sigma2), _p(y),
+                   _u64(y.shape[0]), _p(out))
+        return out
+
+    def inference(self, w, pi, sigma2, y, hprime, gamma):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        ms, mm, ex = np.empty((n, h)), np.empty(n), np.empty((n, h))
+        if self.kind == "port":
+            self._call("inference", _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(pi), _dbl(sigma2),
+                       _p(y), _u64(n), _p(ms), _p(mm), _p(ex))
+        else:
+            self._call("inference", _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(pi), _dbl(sigma2),
+                       _p(y), _u64(n), _u32(1), _p(ms), _p(mm), _p(ex))
+        return ms, mm, ex
+
+    def exact_log_likelihood(self, w, pi, sigma2, y):
+        w, y = _f64(w), _f64(y)
+        out = _dbl()
+        self._call("exact_log_likelihood", _u32(w.shape[0]), _u32(w.shape[1]), _p(w), _dbl(pi), _dbl(sigma2),
+                   _p(y), _u64(y.shape[0]), C.byref(out))
+        return out.value
+
+
+class RefSession:
+    """The reference's ``LinearDiscreteModel::step`` over a resident dataset,
+    for timing (bench.py ``--impl reference``)."""
+
+    def __init__(self, y, h, hprime, gamma):
+        self.lib = C.CDLL(REF_LIB)
+        self.lib.ref_last_error.restype = C.c_char_p
+        y = _f64(y)
+        self.d, self.h, self.n = y.shape[1], h, y.shape[0]
+        self.handle = _ptr()
+        rc = self.lib.ref_session_create(_u32(self.d), _u32(h), _u32(hprime), _u32(gamma), _p(y), _u64(self.n),
+                                         C.byref(self.handle))
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def step(self, w, pi, sigma2, shards, workers):
+        w = _f64(w)
+        wo = np.empty_like(w)
+        pio, s2o, f = _dbl(), _dbl(), _dbl()
+        rc = self.lib.ref_session_step(self.handle, _p(w), _dbl(pi), _dbl(sigma2), _u32(shards), _u32(workers),
+                                       _p(wo), C.byref(pio), C.byref(s2o), C.byref(f))
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+        return wo, pio.value, s2o.value, f.value
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self.lib.ref_session_free(self.handle)
+            self.handle = None
