@@ -1,0 +1,108 @@
+/* prsp_bsc_gpu — B200 (sm_100a) drop-in for the BSC truncated-EM step of prsp.
+ *
+ * C ABI over the CUDA engine (paper_1908_06843_b200/csrc). Plain pointers
+ * and sizes only. Conventions follow the reference C API
+ * (/root/reference/proj/include/prsp.h:23-26, :39-45):
+ *   - functions return PRSP_OK (0) or a prsp_status code
+ *     (2 config, 3 data, 4 numeric, 5 internal);
+ *   - the message of the last failure on this thread is prsp_bsc_gpu_last_error();
+ *   - outputs are written only on success; the caller owns host buffers,
+ *     the context owns all device memory;
+ *   - one host thread per context (not re-entrant).
+ * Matrices are row-major fp64: Y is N×D (one data point per row), W is D×H.
+ * "scalars" arrays are {sum_y2, log_partition, points}.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/src):
+ *   prsp_bsc_gpu_create        LinearDiscreteModel ctor (linear_discrete.cpp:32-62)
+ *                              + TruncationConfig::validate (truncation.cpp:23-30)
+ *   prsp_bsc_gpu_step          LinearDiscreteModel::step (linear_discrete.cpp:410-427)
+ *   prsp_bsc_gpu_estep         LinearDiscreteModel::estep_stats (:327-334) over the resident shard
+ *   prsp_bsc_gpu_mstep         LinearDiscreteModel::mstep (:336-408)
+ *   prsp_bsc_gpu_inference     LinearDiscreteModel::inference (:429-450)
+ *   prsp_bsc_gpu_candidates    select_candidates per point as in estep_impl (:240-253)
+ *   prsp_bsc_gpu_step_host     Model::step with host DataSet + params in, params + F out
+ *                              (the call em.cpp:39 makes every iteration)
+ *   prsp_bsc_generate          LinearDiscreteModel::generate (:452-479)
+ *   prsp_bsc_bars_generate     make_bars (bars.cpp:33-65) / prsp_bars_generate (prsp.h:76-80)
+ *   prsp_bsc_standard_init     LinearDiscreteModel::standard_init (:129-148)
+ */
+#ifndef PRSP_BSC_GPU_H
+#define PRSP_BSC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct prsp_bsc_gpu prsp_bsc_gpu; /* one device's engine + resident shard */
+
+const char* prsp_bsc_gpu_version(void);
+const char* prsp_bsc_gpu_last_error(void);
+int prsp_bsc_gpu_device_count(void);
+
+/* ---- context ----------------------------------------------------------- */
+int prsp_bsc_gpu_create(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
+                        int device, prsp_bsc_gpu** out);
+void prsp_bsc_gpu_free(prsp_bsc_gpu* ctx);
+/* Run on an existing cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+int prsp_bsc_gpu_set_stream(prsp_bsc_gpu* ctx, void* cuda_stream);
+int prsp_bsc_gpu_sync(prsp_bsc_gpu* ctx);
+int prsp_bsc_gpu_states_per_point(const prsp_bsc_gpu* ctx, uint64_t* out);
+
+/* ---- resident data shard and parameters -------------------------------- */
+int prsp_bsc_gpu_load_data(prsp_bsc_gpu* ctx, const double* y_host, uint64_t n);
+int prsp_bsc_gpu_load_data_device(prsp_bsc_gpu* ctx, const double* y_device, uint64_t n);
+int prsp_bsc_gpu_set_params(prsp_bsc_gpu* ctx, const double* w, double pi, double sigma2);
+int prsp_bsc_gpu_get_params(prsp_bsc_gpu* ctx, double* w, double* pi, double* sigma2);
+
+/* ---- the hot path ------------------------------------------------------- */
+/* E-step over the resident shard into the device statistics buffer. */
+int prsp_bsc_gpu_estep(prsp_bsc_gpu* ctx, double temperature);
+/* Device statistics buffer (fp64, packed [sum_y_sT D·H | sum_s H | sum_ssT H·H |
+ * value_counts | sum_y2 | log_partition | points]) for an in-place all-reduce
+ * across ranks between estep and mstep. */
+int prsp_bsc_gpu_stats_buffer(prsp_bsc_gpu* ctx, double** device_ptr, uint64_t* count);
+int prsp_bsc_gpu_get_stats(prsp_bsc_gpu* ctx, double* sum_s, double* sum_ssT, double* sum_y_sT,
+                           double* value_counts, double* scalars);
+int prsp_bsc_gpu_set_stats(prsp_bsc_gpu* ctx, const double* sum_s, const double* sum_ssT, const double* sum_y_sT,
+                           const double* value_counts, const double* scalars);
+/* M-step from the device statistics buffer; the new params stay resident. */
+int prsp_bsc_gpu_mstep(prsp_bsc_gpu* ctx);
+/* estep + mstep on the resident shard; *free_energy = Σ_n log Z_n at the incoming params. */
+int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy);
+/* Reference-facing step: host Y and params in, host params and F out
+ * (copies inside; Y may be pinned for full PCIe rate). */
+int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y_host, uint64_t n, const double* w, double pi,
+                           double sigma2, double temperature, double* w_out, double* pi_out, double* sigma2_out,
+                           double* free_energy);
+
+/* ---- parity hooks and inference ----------------------------------------- */
+/* Candidate sets (N×H', ascending) of the resident shard at the current params. */
+int prsp_bsc_gpu_candidates(prsp_bsc_gpu* ctx, uint32_t* out);
+/* map_states N×H (0/1), map_mass N, expected N×H (⟨s_n⟩). */
+int prsp_bsc_gpu_inference(prsp_bsc_gpu* ctx, double* map_states, double* map_mass, double* expected);
+/* Device timings of the last step (ms): gram, gemm Y·W, enumerate, gemm Yᵀ⟨S⟩, finalize, mstep. */
+int prsp_bsc_gpu_set_timing(prsp_bsc_gpu* ctx, int on);
+int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6);
+int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out);
+
+/* ---- fixtures (CPU; the reference's generators, same draw order) -------- */
+int prsp_bsc_bars_generate(uint32_t size, uint64_t n, double prob, double amplitude, double noise, int max_mode,
+                           uint64_t seed, double* y_out, double* truth_out);
+int prsp_bsc_generate(uint32_t dim, uint32_t latents, const double* w, double pi, double sigma2, uint64_t n,
+                      uint64_t seed, double* y_out);
+/* Unit-norm columns × scale, N(0,1) from RngStream::derived(seed, "wtru"). */
+int prsp_bsc_random_dictionary(uint32_t dim, uint32_t latents, uint64_t seed, double scale, double* w_out);
+/* BASELINE.json init: W = mean_d + 0.25·std_d·z, π = 1/H, σ² = mean data variance. */
+int prsp_bsc_baseline_init(uint32_t dim, uint32_t latents, const double* y, uint64_t n, uint64_t seed,
+                           double* w_out, double* pi_out, double* sigma2_out);
+int prsp_bsc_standard_init(uint32_t dim, uint32_t latents, uint32_t hprime, const double* y, uint64_t n,
+                           uint64_t seed, double* w_out, double* pi_out, double* sigma2_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRSP_BSC_GPU_H */

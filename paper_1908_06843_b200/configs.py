@@ -1,0 +1,70 @@
+"""BASELINE.json workloads c0–c4 (synthetic, seeded; SURVEY.md §8(d) pins the recipes).
+
+c0/c1 are the reference bars generator (bars.cpp:33-65); c2–c4 draw a
+unit-norm×5 random dictionary from RngStream::derived(seed, "wtru") and sample
+data with LinearDiscreteModel::generate (linear_discrete.cpp:452-479). The
+initial parameters follow BASELINE.json's recipe (W = mean_d + 0.25·std_d·z,
+π = 1/H, σ² = mean data variance) and are identical for the oracle and the GPU.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import bsc
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    D: int
+    H: int
+    hprime: int
+    gamma: int
+    N: int
+    iters: int
+    seed: int
+    kind: str  # "bars" or "random"
+    bars_size: int = 0
+    pi_true: float = 0.0
+    sigma2_true: float = 0.0
+    dict_seed: int = 0
+
+    def describe(self) -> dict:
+        return dict(workload=self.name, D=self.D, H=self.H, hprime=self.hprime, gamma=self.gamma, N=self.N,
+                    seed=self.seed)
+
+
+CONFIGS = {
+    "c0": Workload("c0_bars5x5_exact", 25, 10, 10, 10, 1_000, 50, 0, "bars", bars_size=5),
+    "c1": Workload("c1_bars10x10", 100, 20, 10, 4, 10_000, 50, 1, "bars", bars_size=10),
+    "c2": Workload("c2_random_D256_H300", 256, 300, 12, 4, 200_000, 20, 2, "random", pi_true=5 / 300,
+                   sigma2_true=0.25, dict_seed=2),
+    "c3": Workload("c3_random_D576_H1000", 576, 1000, 14, 5, 1_000_000, 10, 3, "random", pi_true=8 / 1000,
+                   sigma2_true=0.25, dict_seed=3),
+    "c4": Workload("c4_strong_D576_H1000_N4M", 576, 1000, 14, 5, 4_000_000, 10, 4, "random", pi_true=8 / 1000,
+                   sigma2_true=0.25, dict_seed=3),
+}
+
+
+def truth(w: Workload) -> np.ndarray:
+    if w.kind == "bars":
+        _, t = bsc.bars_generate(w.bars_size, 1, seed=w.seed)
+        return t
+    return bsc.random_dictionary(w.D, w.H, w.dict_seed, 5.0)
+
+
+def data(w: Workload, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
+    """The workload's data points (first ``n`` of the seeded stream for bars;
+    an independent seeded sample of size ``n`` for the random dictionaries)."""
+    n = w.N if n is None else int(n)
+    if w.kind == "bars":
+        y, _ = bsc.bars_generate(w.bars_size, n, seed=w.seed + seed_offset)
+        return y
+    wt = truth(w)
+    return bsc.generate(bsc.BscParams(wt, w.pi_true, w.sigma2_true), n, w.seed + seed_offset)
+
+
+def init(w: Workload, y: np.ndarray) -> bsc.BscParams:
+    return bsc.baseline_init(y, w.H, w.seed)

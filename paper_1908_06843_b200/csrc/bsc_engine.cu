@@ -1,0 +1,657 @@
+// BscEngine implementation: buffers, state template, kernel orchestration.
+// See bsc_engine.hpp; the reference path is LinearDiscreteModel::step
+// (/root/reference/proj/src/linear_discrete.cpp:410-427).
+#include "bsc_engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <unordered_map>
+
+#include "bsc_kernels.cuh"
+#include "dgemm.cuh"
+#include "mstep_kernels.cuh"
+
+namespace bscgpu {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(kInternal, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t count, const char* what) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), what);
+  ck(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), what);
+  return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Register-resident unit slots per lane (H ≤ 32·MAXJ).
+int maxj_for(uint32_t h) {
+  const int need = static_cast<int>((h + 31) / 32);
+  for (int m : {1, 2, 4, 6, 8, 10, 12, 16, 24, 32})
+    if (need <= m) return m;
+  return 32;
+}
+const void* enum_fn(int maxj) {
+  switch (maxj) {
+    case 1: return (const void*)enumerate_kernel<1>;
+    case 2: return (const void*)enumerate_kernel<2>;
+    case 4: return (const void*)enumerate_kernel<4>;
+    case 6: return (const void*)enumerate_kernel<6>;
+    case 8: return (const void*)enumerate_kernel<8>;
+    case 10: return (const void*)enumerate_kernel<10>;
+    case 12: return (const void*)enumerate_kernel<12>;
+    case 16: return (const void*)enumerate_kernel<16>;
+    case 24: return (const void*)enumerate_kernel<24>;
+    default: return (const void*)enumerate_kernel<32>;
+  }
+}
+
+constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
+
+// Tile configurations (see dgemm.cuh).
+// GEMM1  B = Y·W:     M = points, N = Hp, K = Dp.
+#define GEMM1_CFG 128, 64, 16, 32, 32, true, true, 3
+// GEMM2  Yᵀ·⟨S⟩:      M = Dp, N = Hp, K = points (split-K).
+#define GEMM2_CFG 64, 64, 16, 32, 32, false, true, 3
+// M-step products (C −= A·Bᵀ and C −= A·B).
+#define SYRK_CFG 64, 64, 16, 32, 32, true, false, 3
+#define SOLVE_CFG 64, 64, 16, 32, 32, true, true, 3
+
+}  // namespace
+
+BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
+                     int device)
+    : D_(dim), H_(latents), hprime_(hprime), gamma_(gamma), cap_(state_cap), device_(device) {
+  if (D_ == 0 || H_ == 0) throw Error(kConfig, "linear model: dim and latents must be >= 1");
+  // TruncationConfig::validate, truncation.cpp:23-30
+  if (hprime_ == 0 || hprime_ > H_) throw Error(kConfig, "truncation: hprime must satisfy 1 <= hprime <= latents");
+  if (gamma_ == 0 || gamma_ > hprime_) throw Error(kConfig, "truncation: gamma must satisfy 1 <= gamma <= hprime");
+  if (cap_ == 0) throw Error(kConfig, "truncation: state cap must be >= 1");
+  if (hprime_ > static_cast<uint32_t>(kMaxHprime))
+    throw Error(kConfig, "gpu: hprime > 64 is not supported by the sm_100a enumerator");
+  if (H_ > 1024) throw Error(kConfig, "gpu: latents > 1024 is not supported by the sm_100a enumerator");
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "device count");
+  if (device_ < 0 || device_ >= ndev) throw Error(kConfig, "gpu: device index out of range");
+  ck(cudaSetDevice(device_), "set device");
+  cudaStream_t s;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  stream_ = s;
+  own_stream_ = true;
+  Dp_ = round_up(static_cast<int>(D_), 8);
+  Hp_ = round_up(static_cast<int>(H_), 8);
+  lay_ = StatsLayout{static_cast<long long>(D_), static_cast<long long>(H_)};
+  build_template();
+
+  d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
+  d_g_ = dalloc<double>((size_t)H_ * H_, "G");
+  d_wnorm_ = dalloc<double>(H_, "wnorm");
+  d_gdiag_ = dalloc<double>(H_, "gdiag");
+  d_stats_ = dalloc<double>(lay_.count(), "stats");
+  d_smulti_ = dalloc<double>(H_, "s_multi");
+  d_err_ = dalloc<int>(1, "err");
+  d_bm_ = dalloc<double>((size_t)H_ * Hp_, "Bm");
+  d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
+  d_msc_ = dalloc<MstepScalars>(1, "mstep scalars");
+  // row-wise triangular solves stage 128 rows × (64+1) doubles dynamically
+  ck(cudaFuncSetAttribute(trsm_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 65 * 8),
+     "trsm smem");
+  ck(cudaFuncSetAttribute(trsm_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 65 * 8),
+     "trsm smem");
+  for (auto& e : ev_) {
+    cudaEvent_t ev;
+    ck(cudaEventCreate(&ev), "event");
+    e = ev;
+  }
+}
+
+BscEngine::~BscEngine() {
+  cudaSetDevice(device_);
+  for (void* p : {(void*)d_desc_, (void*)d_child_, (void*)d_level_off_, (void*)d_gather_, (void*)d_item_off_, (void*)d_out_off_, (void*)d_y_,
+                  (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
+                  (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
+                  (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, d_msc_})
+    dfree(p);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  if (own_stream_ && stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+void BscEngine::set_stream(void* stream) {
+  if (own_stream_ && stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+  stream_ = stream;
+  own_stream_ = false;
+}
+
+void BscEngine::sync() { ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)), "sync"); }
+
+// StateTemplate (truncation.cpp:95-151): multi-active supports of size
+// 2..γ over candidate positions, depth-first, prefixes first. The gather
+// tables invert it: for every candidate position p and pair (p<q) the list of
+// states containing it, cut into work items of similar length.
+void BscEngine::build_template() {
+  // truncated_state_count (truncation.cpp:83-93), saturating, V = 1
+  auto sat_add = [](uint64_t a, uint64_t b) { return UINT64_MAX - a < b ? UINT64_MAX : a + b; };
+  auto binom = [](uint64_t n, uint64_t k) -> uint64_t {
+    if (k > n) return 0;
+    k = std::min(k, n - k);
+    unsigned __int128 r = 1;
+    for (uint64_t i = 1; i <= k; ++i) {
+      r = r * (n - k + i) / i;
+      if (r > UINT64_MAX) return UINT64_MAX;
+    }
+    return static_cast<uint64_t>(r);
+  };
+  uint64_t total = sat_add(1, H_);
+  for (uint32_t k = 2; k <= gamma_; ++k) total = sat_add(total, binom(hprime_, k));
+  if (total > cap_)
+    throw Error(kConfig, "state explosion: " + std::to_string(total) + " states per data point exceeds cap of " +
+                             std::to_string(cap_));
+
+  // reference DFS order (truncation.cpp:116-147) → dfs index of each support
+  std::vector<uint64_t> masks;
+  masks.reserve(total - 1 - H_);
+  std::vector<int> support;
+  auto dfs = [&](auto&& self, uint32_t next) -> void {
+    if (support.size() >= 2) {
+      uint64_t m = 0;
+      for (int p : support) m |= 1ull << p;
+      masks.push_back(m);
+    }
+    if (support.size() == gamma_) return;
+    for (uint32_t p = next; p < hprime_; ++p) {
+      support.push_back(static_cast<int>(p));
+      self(self, p + 1);
+      support.pop_back();
+    }
+  };
+  if (gamma_ >= 2) dfs(dfs, 0);
+  n_multi_ = static_cast<int>(masks.size());
+  dfs_masks_ = masks;
+
+  // level-lexicographic table: level 1 = {p}, then combinations of size k
+  const int hp = static_cast<int>(hprime_);
+  std::vector<std::vector<int>> sets;  // sorted member lists
+  std::vector<int> level_off{0};
+  for (int p = 0; p < hp; ++p) sets.push_back({p});
+  level_off.push_back(hp);
+  std::vector<int> comb;
+  for (uint32_t k = 2; k <= gamma_; ++k) {
+    comb.assign(k, 0);
+    for (uint32_t i = 0; i < k; ++i) comb[i] = static_cast<int>(i);
+    for (;;) {
+      sets.push_back(comb);
+      int i = static_cast<int>(k) - 1;
+      while (i >= 0 && comb[i] == hp - static_cast<int>(k) + i) --i;
+      if (i < 0) break;
+      ++comb[i];
+      for (uint32_t j = i + 1; j < k; ++j) comb[j] = comb[j - 1] + 1;
+    }
+    level_off.push_back(static_cast<int>(sets.size()));
+  }
+  const int n_tab = static_cast<int>(sets.size());
+  if (n_tab != hp + n_multi_) throw Error(kInternal, "state template size mismatch");
+  auto key = [](const std::vector<int>& v) {
+    uint64_t m = 0;
+    for (int p : v) m |= 1ull << p;
+    return m;
+  };
+  std::unordered_map<uint64_t, int> index_of, dfs_of;
+  for (int i = 0; i < n_tab; ++i) index_of[key(sets[i])] = i;
+  for (int i = 0; i < n_multi_; ++i) dfs_of[masks[i]] = i;
+  const int n_coup = gamma_ >= 3 ? level_off[gamma_ - 1] - hp : 0;
+  std::vector<StateDesc> desc(n_tab, StateDesc{0, 0, 0, -1});
+  std::vector<int2> child(hp + n_coup, int2{0, 0});
+  for (int i = hp; i < n_tab; ++i) {
+    const auto& S = sets[i];
+    const int z = S.back();
+    std::vector<int> A(S.begin(), S.end() - 1);
+    const int x = A.back();
+    std::vector<int> sib(A.begin(), A.end() - 1);
+    sib.push_back(z);
+    desc[i] = StateDesc{index_of.at(key(A)), index_of.at(key(sib)), x | (z << 8), dfs_of.at(key(S))};
+  }
+  for (int i = 0; i < hp + n_coup; ++i) {
+    const auto& A = sets[i];
+    const int nc = hp - 1 - A.back();
+    if (nc > 0 && A.size() < gamma_) {
+      std::vector<int> c0 = A;
+      c0.push_back(A.back() + 1);
+      const int fc = index_of.at(key(c0));
+      for (int c = 0; c < nc; ++c) {  // children contiguous in the next level
+        std::vector<int> cc = A;
+        cc.push_back(A.back() + 1 + c);
+        if (index_of.at(key(cc)) != fc + c) throw Error(kInternal, "state template: children not contiguous");
+      }
+      child[i] = int2{fc, nc};
+    }
+  }
+  n_tab_ = n_tab;
+  n_coup_ = n_coup;
+
+  // gather lists: ⟨s_p⟩ ← nodes with max p; ⟨s_p s_q⟩ ← nodes with max q containing p
+  n_out_ = hp + hp * (hp - 1) / 2;
+  auto pair_index = [hp](int p, int q) {  // row-major p < q
+    return hp + p * (2 * hp - p - 1) / 2 + (q - p - 1);
+  };
+  std::vector<std::vector<int>> lists(n_out_);
+  for (int i = 0; i < n_tab; ++i) {
+    const auto& S = sets[i];
+    const int q = S.back();
+    lists[q].push_back(i);
+    for (size_t a = 0; a + 1 < S.size(); ++a) lists[pair_index(S[a], q)].push_back(i);
+  }
+  size_t tot = 0;
+  for (auto& l : lists) tot += l.size();
+  const size_t chunk = std::max<size_t>(8, (tot + 95) / 96);
+  std::vector<int> gather, item_off{0}, out_off{0};
+  for (auto& l : lists) {
+    for (size_t s = 0; s < l.size(); s += chunk) {
+      const size_t e = std::min(l.size(), s + chunk);
+      gather.insert(gather.end(), l.begin() + s, l.begin() + e);
+      item_off.push_back(static_cast<int>(gather.size()));
+    }
+    out_off.push_back(static_cast<int>(item_off.size() - 1));
+  }
+  n_items_ = static_cast<int>(item_off.size() - 1);
+  d_desc_ = dalloc<StateDesc>(desc.size(), "desc");
+  d_child_ = dalloc<int2>(child.size(), "child");
+  d_level_off_ = dalloc<int>(level_off.size(), "level_off");
+  d_gather_ = dalloc<int>(gather.size(), "gather");
+  d_item_off_ = dalloc<int>(item_off.size(), "item_off");
+  d_out_off_ = dalloc<int>(out_off.size(), "out_off");
+  ck(cudaMemcpy(d_desc_, desc.data(), desc.size() * sizeof(StateDesc), cudaMemcpyHostToDevice), "desc");
+  if (!child.empty()) ck(cudaMemcpy(d_child_, child.data(), child.size() * sizeof(int2), cudaMemcpyHostToDevice), "child");
+  ck(cudaMemcpy(d_level_off_, level_off.data(), level_off.size() * 4, cudaMemcpyHostToDevice), "level_off");
+  if (!gather.empty()) ck(cudaMemcpy(d_gather_, gather.data(), gather.size() * 4, cudaMemcpyHostToDevice), "gather");
+  ck(cudaMemcpy(d_item_off_, item_off.data(), item_off.size() * 4, cudaMemcpyHostToDevice), "item_off");
+  ck(cudaMemcpy(d_out_off_, out_off.data(), out_off.size() * 4, cudaMemcpyHostToDevice), "out_off");
+}
+
+void BscEngine::ensure_work(uint64_t n) {
+  if (n <= cap_n_ && d_y_) return;
+  for (void* p : {(void*)d_y_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_, (void*)d_map_mass_,
+                  (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_})
+    dfree(p);
+  const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
+  d_y_ = dalloc<double>(rows * Dp_, "Y");
+  d_b_ = dalloc<double>(rows * Hp_, "B");
+  d_es_ = dalloc<double>(rows * Hp_, "ES");
+  d_cand_ = dalloc<uint32_t>(rows * hprime_, "cand");
+  d_map_state_ = dalloc<int>(rows, "map_state");
+  d_map_mass_ = dalloc<double>(rows, "map_mass");
+  cap_n_ = n;
+
+  // split-K for Yᵀ⟨S⟩: ≈4 waves of 148 SMs over the output tiles
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, device_), "props");
+  const int tiles = ((Dp_ + 63) / 64) * ((Hp_ + 63) / 64);
+  splits_ = std::max(1, std::min<int>((4 * prop.multiProcessorCount + tiles - 1) / tiles,
+                                      static_cast<int>(std::max<uint64_t>(1, rows / 512))));
+  part_stride_ = (long long)Dp_ * Hp_;
+  d_part_ = dalloc<double>((size_t)splits_ * part_stride_, "splitK partials");
+
+  // enumerator launch shape: per-warp shared region, as many warps as fit
+  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_items_, n_out_);
+  const int per_warp = L.total * 8;
+  int warps = 8;
+  while (warps > 1 && warps * per_warp > 200 * 1024) warps /= 2;
+  if (per_warp > 200 * 1024)
+    throw Error(kConfig, "gpu: state template too large for shared memory (" + std::to_string(n_multi_) + " states)");
+  enum_block_ = warps * 32;
+  enum_smem_ = warps * per_warp;
+  const int maxj = maxj_for(H_);
+  const void* fn = enum_fn(maxj);
+  ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "enum smem attr");
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, enum_block_, enum_smem_), "occupancy");
+  per_sm = std::max(per_sm, 1);
+  enum_ctas_ = per_sm * prop.multiProcessorCount;
+  const uint64_t need = (n + warps - 1) / warps;
+  enum_ctas_ = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(enum_ctas_, need)));
+  enum_warps_total_ = enum_ctas_ * warps;
+  d_warp_es_ = dalloc<double>((size_t)enum_warps_total_ * H_, "warp_es");
+  d_warp_sc_ = dalloc<double>((size_t)enum_warps_total_ * 2, "warp_scalars");
+}
+
+void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
+  if (n == 0) throw Error(kData, "run: empty dataset");
+  ck(cudaSetDevice(device_), "set device");
+  const uint64_t prev_cap = cap_n_;
+  ensure_work(n);
+  auto s = static_cast<cudaStream_t>(stream_);
+  if (n < prev_cap && n_ > n) {
+    // shrinking inside an existing allocation: clear stale rows past n
+    ck(cudaMemsetAsync(d_y_ + n * Dp_, 0, (cap_n_ - n) * Dp_ * sizeof(double), s), "clear Y");
+  }
+  ck(cudaMemcpy2DAsync(d_y_, (size_t)Dp_ * 8, y, (size_t)D_ * 8, (size_t)D_ * 8, n,
+                       device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
+     "upload Y");
+  n_ = n;
+}
+
+void BscEngine::set_params(const double* w, double pi, double sigma2) {
+  // LinearDiscreteModel::validate, linear_discrete.cpp:99-127 (BSC)
+  for (size_t i = 0; i < (size_t)D_ * H_; ++i)
+    if (!std::isfinite(w[i])) throw Error(kNumeric, "bsc: non-finite dictionary");
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) throw Error(kConfig, "bsc: sigma2 must be positive");
+  if (!(pi > 0.0 && pi < 1.0)) throw Error(kConfig, "bsc: pi must lie in (0,1)");
+  ck(cudaSetDevice(device_), "set device");
+  ck(cudaMemcpy2DAsync(d_w_, (size_t)Hp_ * 8, w, (size_t)H_ * 8, (size_t)H_ * 8, D_, cudaMemcpyHostToDevice,
+                       static_cast<cudaStream_t>(stream_)),
+     "upload W");
+  pi_ = pi;
+  sigma2_ = sigma2;
+  have_params_ = true;
+  gram_fresh_ = false;
+}
+
+void BscEngine::get_params(double* w, double* pi, double* sigma2) {
+  if (w)
+    ck(cudaMemcpy2DAsync(w, (size_t)H_ * 8, d_w_, (size_t)Hp_ * 8, (size_t)H_ * 8, D_, cudaMemcpyDeviceToHost,
+                         static_cast<cudaStream_t>(stream_)),
+       "download W");
+  sync();
+  if (pi) *pi = pi_;
+  if (sigma2) *sigma2 = sigma2_;
+}
+
+void BscEngine::refresh_gram() {
+  auto s = static_cast<cudaStream_t>(stream_);
+  dim3 grid((H_ + 127) / 128, H_);
+  gram_exact_kernel<<<grid, 128, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, d_wnorm_, d_gdiag_);
+  ck(cudaGetLastError(), "gram");
+  ++launches_;
+  gram_fresh_ = true;
+}
+
+void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
+  auto s = static_cast<cudaStream_t>(stream_);
+  // value_table (:71-97, BSC :75-79) and the per-shard constants (:219-227),
+  // computed on the host with the same libm as the reference.
+  const double log_p1 = std::log(pi_), log_p0 = std::log(1.0 - pi_);
+  const double inv2s = 1.0 / (2.0 * sigma2_);
+  const double norm_const = -0.5 * static_cast<double>(D_) * (kLog2Pi + std::log(sigma2_));
+  const double zero_prior = static_cast<double>(H_) * log_p0;
+
+  EnumArgs a{};
+  a.N = static_cast<int>(n_);
+  a.D = D_;
+  a.H = H_;
+  a.Dp = Dp_;
+  a.Hp = Hp_;
+  a.hprime = hprime_;
+  a.gamma = gamma_;
+  a.Y = d_y_;
+  a.W = d_w_;
+  a.B = d_b_;
+  a.G = d_g_;
+  a.wnorm = d_wnorm_;
+  a.gdiag = d_gdiag_;
+  a.ES = d_es_;
+  a.ssT = d_stats_ + lay_.off_ssT();
+  a.s_multi = d_smulti_;
+  a.warp_es = d_warp_es_;
+  a.warp_scalars = d_warp_sc_;
+  a.cand_out = cands ? d_cand_ : nullptr;
+  a.map_mass = infer ? d_map_mass_ : nullptr;
+  a.map_state = infer ? d_map_state_ : nullptr;
+  a.err = d_err_;
+  a.desc = static_cast<const StateDesc*>(d_desc_);
+  a.child = static_cast<const int2*>(d_child_);
+  a.level_off = d_level_off_;
+  a.n_multi = n_multi_;
+  a.n_tab = n_tab_;
+  a.n_coup = n_coup_;
+  a.gather_idx = d_gather_;
+  a.item_off = d_item_off_;
+  a.out_item_off = d_out_off_;
+  a.n_items = n_items_;
+  a.n_out = n_out_;
+  a.log_pi = log_p1;
+  a.dlp = log_p1 - log_p0;
+  a.inv2s = inv2s;
+  a.base0 = zero_prior + norm_const;
+  a.inv_T = 1.0 / temperature;
+  a.eps_dot = 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
+
+  const int maxj = maxj_for(H_);
+  void* args[] = {&a};
+  ck(cudaLaunchKernel(enum_fn(maxj), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s), "enumerate launch");
+  ck(cudaGetLastError(), "enumerate");
+  ++launches_;
+}
+
+void BscEngine::estep(double temperature, bool want_candidates) {
+  if (!have_params_) throw Error(kConfig, "bsc: parameters not set");
+  if (n_ == 0) throw Error(kData, "run: empty dataset");
+  if (!(temperature >= 1.0) || !std::isfinite(temperature))
+    throw Error(kConfig, "temperature must be finite and >= 1");
+  ck(cudaSetDevice(device_), "set device");
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto ev = [&](int i) {
+    if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[i]), s), "event");
+  };
+  launches_ = 0;
+  ev(0);
+  if (!gram_fresh_) refresh_gram();
+  ev(1);
+  {  // K1: B = Y·W
+    GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, d_w_, Hp_, d_b_, Hp_, 1.0, 0.0, Dp_, 0};
+    ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
+    ++launches_;
+  }
+  ev(2);
+  ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
+  ck(cudaMemsetAsync(d_smulti_, 0, (size_t)H_ * 8, s), "zero s_multi");
+  ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
+  launch_enumerate(temperature, want_candidates, false);
+  ev(3);
+  {  // K4: Σ y⟨s⟩ᵀ = Yᵀ·ES, split-K over points, reduced in fixed order
+    const int rows = static_cast<int>((n_ + 1) & ~1ull);
+    int kchunk = (rows + splits_ - 1) / splits_;
+    kchunk = (kchunk + 1) & ~1;
+    const int splits = (rows + kchunk - 1) / kchunk;
+    GemmArgs g{Dp_, Hp_, rows, d_y_, Dp_, d_es_, Hp_, d_part_, Hp_, 1.0, 0.0, kchunk, part_stride_};
+    ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
+    const long long DH = (long long)D_ * H_;
+    reduce_ysT_kernel<<<(DH + 255) / 256, 256, 0, s>>>(d_part_, splits, part_stride_, D_, H_, Hp_,
+                                                        d_stats_ + lay_.off_ysT());
+    ck(cudaGetLastError(), "reduce ysT");
+    launches_ += 2;
+  }
+  ev(4);
+  finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
+      d_warp_es_, enum_warps_total_, d_warp_sc_, d_smulti_, H_, static_cast<long long>(n_), d_stats_,
+      lay_.off_s(), lay_.off_ssT(), lay_.off_tail());
+  counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
+  ck(cudaGetLastError(), "finalize");
+  launches_ += 2;
+  ev(5);
+}
+
+void BscEngine::check_err() {
+  int err = 0;
+  ck(cudaMemcpyAsync(&err, d_err_, sizeof(int), cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream_)),
+     "err");
+  sync();
+  if (err & kErrNonFiniteScore) throw Error(kConfig, "select_candidates: scores must be finite");
+  if (err & kErrNonFiniteLogJoint) throw Error(kNumeric, "log_sum_exp: empty support");
+}
+
+void BscEngine::mstep() {
+  ck(cudaSetDevice(device_), "set device");
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto* sc = static_cast<MstepScalars*>(d_msc_);
+  const int H = static_cast<int>(H_), D = static_cast<int>(D_);
+  mstep_prepare_kernel<<<64, 256, 0, s>>>(d_stats_, lay_.off_ssT(), D, H, Hp_, d_bm_, d_x_, Hp_, sc);
+  ck(cudaGetLastError(), "mstep prepare");
+  ++launches_;
+  // blocked right-looking Cholesky, lower: L overwrites Bm
+  for (int k0 = 0; k0 < H; k0 += kCholNb) {
+    const int kb = std::min(kCholNb, H - k0), k1 = k0 + kb;
+    potrf_diag_kernel<<<1, 256, 0, s>>>(d_bm_, Hp_, k0, kb, sc);
+    ++launches_;
+    if (k1 < H) {
+      const int rows = H - k1, tpb = 128;
+      trsm_rows_kernel<true><<<(rows + tpb - 1) / tpb, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, k0, kb, d_bm_, Hp_,
+                                                                                   k1, rows, k0);
+      GemmArgs g{rows, rows, kb, d_bm_ + (long long)k1 * Hp_ + k0, Hp_, d_bm_ + (long long)k1 * Hp_ + k0, Hp_,
+                 d_bm_ + (long long)k1 * Hp_ + k1, Hp_, -1.0, 1.0, kb, 0};
+      ck(launch_dgemm<SYRK_CFG>(g, 1, s), "syrk");
+      launches_ += 2;
+    }
+  }
+  ck(cudaGetLastError(), "cholesky");
+  // X·L·Lᵀ = Σy⟨s⟩ᵀ: forward (Z·Lᵀ = R) then backward (X·L = Z), column blocks
+  const int tpb = 128, nblk = (D + tpb - 1) / tpb;
+  for (int j0 = 0; j0 < H; j0 += kCholNb) {
+    const int kb = std::min(kCholNb, H - j0);
+    if (j0 > 0) {
+      GemmArgs g{D, kb, j0, d_x_, Hp_, d_bm_ + (long long)j0 * Hp_, Hp_, d_x_ + j0, Hp_, -1.0, 1.0, j0, 0};
+      ck(launch_dgemm<SYRK_CFG>(g, 1, s), "solve fwd gemm");
+      ++launches_;
+    }
+    trsm_rows_kernel<true><<<nblk, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
+    ++launches_;
+  }
+  const int last0 = (H - 1) / kCholNb * kCholNb;
+  for (int j0 = last0; j0 >= 0; j0 -= kCholNb) {
+    const int kb = std::min(kCholNb, H - j0), j1 = j0 + kb;
+    if (j1 < H) {
+      GemmArgs g{D, kb, H - j1, d_x_ + j1, Hp_, d_bm_ + (long long)j1 * Hp_ + j0, Hp_, d_x_ + j0, Hp_, -1.0, 1.0,
+                 H - j1, 0};
+      ck(launch_dgemm<SOLVE_CFG>(g, 1, s), "solve bwd gemm");
+      ++launches_;
+    }
+    trsm_rows_kernel<false><<<nblk, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "solve");
+  commit_w_kernel<<<64, 256, 0, s>>>(d_x_, Hp_, d_w_, Hp_, D, H, sc);
+  refresh_gram();  // Gram of W' (next E-step's G, exact order) also feeds t3
+  mstep_traces_kernel<<<1, 1024, 0, s>>>(d_w_, Hp_, d_g_, d_stats_, lay_.off_ssT(), D, H, sc);
+  mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, sc);
+  ck(cudaGetLastError(), "mstep scalars");
+  launches_ += 3;
+  if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[6]), s), "event");
+  MstepScalars h{};
+  ck(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s), "mstep scalars D2H");
+  sync();
+  pi_ = h.pi;
+  sigma2_ = h.sigma2;
+}
+
+double BscEngine::step(double temperature) {
+  estep(temperature);
+  double F = 0.0;
+  ck(cudaMemcpyAsync(&F, d_stats_ + lay_.off_tail() + 2, sizeof(double), cudaMemcpyDeviceToHost,
+                     static_cast<cudaStream_t>(stream_)),
+     "F");
+  check_err();
+  mstep();
+  if (timing_) {
+    auto el = [&](int a, int b) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(ev_[a]), static_cast<cudaEvent_t>(ev_[b]));
+      return ms;
+    };
+    t_.gram_ms = el(0, 1);
+    t_.gemm1_ms = el(1, 2);
+    t_.enum_ms = el(2, 3);
+    t_.gemm2_ms = el(3, 4);
+    t_.finalize_ms = el(4, 5);
+    t_.mstep_ms = el(5, 6);
+  }
+  return F;
+}
+
+void BscEngine::get_stats(double* sum_s, double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars) {
+  std::vector<double> h(lay_.count());
+  ck(cudaMemcpyAsync(h.data(), d_stats_, h.size() * 8, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream_)),
+     "stats D2H");
+  sync();
+  if (sum_y_sT) std::memcpy(sum_y_sT, h.data() + lay_.off_ysT(), (size_t)D_ * H_ * 8);
+  if (sum_s) std::memcpy(sum_s, h.data() + lay_.off_s(), (size_t)H_ * 8);
+  if (sum_ssT) std::memcpy(sum_ssT, h.data() + lay_.off_ssT(), (size_t)H_ * H_ * 8);
+  const double* t = h.data() + lay_.off_tail();
+  if (value_counts) value_counts[0] = t[0];
+  if (scalars) {
+    scalars[0] = t[1];
+    scalars[1] = t[2];
+    scalars[2] = t[3];
+  }
+}
+
+void BscEngine::set_stats(const double* sum_s, const double* sum_ssT, const double* sum_y_sT,
+                          const double* value_counts, const double* scalars) {
+  std::vector<double> h(lay_.count(), 0.0);
+  std::memcpy(h.data() + lay_.off_ysT(), sum_y_sT, (size_t)D_ * H_ * 8);
+  std::memcpy(h.data() + lay_.off_s(), sum_s, (size_t)H_ * 8);
+  std::memcpy(h.data() + lay_.off_ssT(), sum_ssT, (size_t)H_ * H_ * 8);
+  double* t = h.data() + lay_.off_tail();
+  t[0] = value_counts[0];
+  t[1] = scalars[0];
+  t[2] = scalars[1];
+  t[3] = scalars[2];
+  if (!(t[3] >= 1.0)) throw Error(kConfig, "bsc: mstep without data");
+  ck(cudaMemcpyAsync(d_stats_, h.data(), h.size() * 8, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream_)),
+     "stats H2D");
+  sync();
+}
+
+void BscEngine::get_candidates(uint32_t* out) {
+  ck(cudaMemcpyAsync(out, d_cand_, n_ * hprime_ * 4, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream_)),
+     "cand D2H");
+  sync();
+}
+
+// LinearDiscreteModel::inference (linear_discrete.cpp:429-450): T = 1, MAP
+// state (first maximum in reference order), its mass, and ⟨s_n⟩.
+void BscEngine::inference(double* map_states, double* map_mass, double* expected) {
+  if (!have_params_) throw Error(kConfig, "bsc: parameters not set");
+  ck(cudaSetDevice(device_), "set device");
+  auto s = static_cast<cudaStream_t>(stream_);
+  if (!gram_fresh_) refresh_gram();
+  GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, d_w_, Hp_, d_b_, Hp_, 1.0, 0.0, Dp_, 0};
+  ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
+  ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
+  ck(cudaMemsetAsync(d_smulti_, 0, (size_t)H_ * 8, s), "zero s_multi");
+  ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
+  launch_enumerate(1.0, true, true);
+  std::vector<int> st(n_);
+  std::vector<uint32_t> cand(n_ * hprime_);
+  ck(cudaMemcpyAsync(st.data(), d_map_state_, n_ * 4, cudaMemcpyDeviceToHost, s), "map D2H");
+  ck(cudaMemcpyAsync(cand.data(), d_cand_, cand.size() * 4, cudaMemcpyDeviceToHost, s), "cand D2H");
+  ck(cudaMemcpyAsync(map_mass, d_map_mass_, n_ * 8, cudaMemcpyDeviceToHost, s), "mass D2H");
+  ck(cudaMemcpy2DAsync(expected, (size_t)H_ * 8, d_es_, (size_t)Hp_ * 8, (size_t)H_ * 8, n_, cudaMemcpyDeviceToHost,
+                       s),
+     "ES D2H");
+  check_err();
+  const std::vector<uint64_t>& masks = dfs_masks_;
+  std::memset(map_states, 0, n_ * H_ * 8);
+  for (uint64_t n = 0; n < n_; ++n) {
+    const int i = st[n];
+    double* row = map_states + n * H_;
+    if (i == 0) continue;
+    if (i <= static_cast<int>(H_)) {
+      row[i - 1] = 1.0;
+      continue;
+    }
+    const uint64_t m = masks[i - 1 - H_];
+    for (uint32_t p = 0; p < hprime_; ++p)
+      if ((m >> p) & 1) row[cand[n * hprime_ + p]] = 1.0;
+  }
+}
+
+}  // namespace bscgpu

@@ -1,0 +1,128 @@
+// BscEngine: one device's share of the BSC truncated-EM step.
+//
+// Owns the resident data shard, the dictionary and the device statistics,
+// and launches the sm_100a kernels of bsc_kernels.cuh / mstep_kernels.cuh /
+// dgemm.cuh. One host thread per engine; not re-entrant.
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace bscgpu {
+
+// Error taxonomy mirroring prsp (core.hpp:32-43); codes are prsp_status.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline constexpr int kConfig = 2, kData = 3, kNumeric = 4, kInternal = 5;
+
+struct StatsLayout {
+  long long D, H;
+  long long off_ysT() const { return 0; }
+  long long off_s() const { return D * H; }
+  long long off_ssT() const { return D * H + H; }
+  long long off_tail() const { return D * H + H + H * H; }  // counts, y2, logZ, points
+  long long count() const { return off_tail() + 4; }
+};
+
+struct EngineTimings {
+  float gram_ms, gemm1_ms, enum_ms, gemm2_ms, finalize_ms, mstep_ms;
+};
+
+class BscEngine {
+ public:
+  BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap, int device);
+  ~BscEngine();
+  BscEngine(const BscEngine&) = delete;
+  BscEngine& operator=(const BscEngine&) = delete;
+
+  void set_stream(void* stream);
+  void* stream() const { return stream_; }
+
+  // Data shard (row-major N×D, host or device pointer); stays resident.
+  void load_data(const double* y, uint64_t n, bool device_ptr);
+  uint64_t points() const { return n_; }
+
+  void set_params(const double* w_host, double pi, double sigma2);
+  void get_params(double* w_host, double* pi, double* sigma2);
+
+  // E-step over the resident shard at temperature T → device stats buffer.
+  void estep(double temperature, bool want_candidates = false);
+  // M-step from the device stats buffer → device params (W, π, σ²).
+  void mstep();
+  // estep + mstep; returns F = Σ_n log Z_n at the incoming params.
+  double step(double temperature);
+
+  double* stats_device() { return d_stats_; }
+  const StatsLayout& layout() const { return lay_; }
+  void get_stats(double* sum_s, double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars);
+  void set_stats(const double* sum_s, const double* sum_ssT, const double* sum_y_sT, const double* value_counts,
+                 const double* scalars);
+  void get_candidates(uint32_t* out);  // N×H' from the last estep(…, true)
+  void inference(double* map_states, double* map_mass, double* expected);
+
+  uint32_t dim() const { return D_; }
+  uint32_t latents() const { return H_; }
+  uint32_t hprime() const { return hprime_; }
+  uint32_t gamma() const { return gamma_; }
+  uint64_t states_per_point() const { return 1 + H_ + n_multi_; }
+  int enum_launch_ctas() const { return enum_ctas_; }
+  int enum_warps() const { return enum_warps_total_; }
+  const EngineTimings& timings() const { return t_; }
+  void set_timing(bool on) { timing_ = on; }
+  int kernel_launches_last_step() const { return launches_; }
+  void sync();
+
+ private:
+  void build_template();
+  void ensure_work(uint64_t n);
+  void refresh_gram();
+  void launch_enumerate(double temperature, bool cands, bool infer);
+  void check_err();
+
+  uint32_t D_, H_, hprime_, gamma_;
+  uint64_t cap_;
+  int device_;
+  int Dp_, Hp_;
+  void* stream_ = nullptr;
+  bool own_stream_ = false;
+  StatsLayout lay_{};
+
+  // params (host mirror of the scalars; W lives on the device)
+  double pi_ = 0.5, sigma2_ = 1.0;
+  bool have_params_ = false, gram_fresh_ = false;
+
+  // template tables
+  int n_multi_ = 0, n_tab_ = 0, n_coup_ = 0, n_items_ = 0, n_out_ = 0;
+  std::vector<uint64_t> dfs_masks_;  // multi-active supports in reference order
+  void* d_desc_ = nullptr;
+  void* d_child_ = nullptr;
+  int* d_level_off_ = nullptr;
+  int *d_gather_ = nullptr, *d_item_off_ = nullptr, *d_out_off_ = nullptr;
+
+  uint64_t n_ = 0, cap_n_ = 0;
+  double *d_y_ = nullptr, *d_w_ = nullptr, *d_g_ = nullptr, *d_wnorm_ = nullptr, *d_gdiag_ = nullptr;
+  double *d_b_ = nullptr, *d_es_ = nullptr;
+  double *d_stats_ = nullptr, *d_smulti_ = nullptr;
+  double *d_warp_es_ = nullptr, *d_warp_sc_ = nullptr;
+  double* d_part_ = nullptr;  // split-K partials
+  int splits_ = 1;
+  long long part_stride_ = 0;
+  uint32_t* d_cand_ = nullptr;
+  int* d_map_state_ = nullptr;
+  double* d_map_mass_ = nullptr;
+  int* d_err_ = nullptr;
+  // M-step workspace
+  double *d_bm_ = nullptr, *d_x_ = nullptr;
+  void* d_msc_ = nullptr;
+
+  int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
+  bool timing_ = false;
+  EngineTimings t_{};
+  int launches_ = 0;
+  void* ev_[8] = {};
+};
+
+}  // namespace bscgpu

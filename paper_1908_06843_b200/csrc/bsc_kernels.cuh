@@ -1,0 +1,620 @@
+// Hand-written sm_100a kernels of the BSC truncated-EM E/M-step.
+//
+// Reference path: LinearDiscreteModel::estep_impl (linear_discrete.cpp:202-325)
+// and ::mstep (:336-408) of /root/reference/proj/src. Layout in HBM (all fp64,
+// leading dims padded to multiples of 8 doubles, pads zero):
+//   Y  N × Dp   data points (one per row), resident for the whole run
+//   W  D × Hp   dictionary
+//   G  H × H    Gram WᵀW, every entry summed left-to-right over d exactly as
+//               the reference's Eigen product (oracle order), so selection
+//               scores are reproducible bit for bit
+//   B  N × Hp   Y·W (DMMA GEMM)
+//   ES N × Hp   posterior means ⟨s_n⟩ (dense: singletons span all H units)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bscgpu {
+
+constexpr int kMaxHprime = 64;  // candidate positions fit a uint64 mask
+
+// Error flags raised by device code (bit set in *err).
+enum : int { kErrNonFiniteScore = 1, kErrNonFiniteLogJoint = 2 };
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_isum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// (value desc, index asc): true when (v1,i1) ranks before (v2,i2).
+__device__ __forceinline__ bool ranks_before(double v1, int i1, double v2, int i2) {
+  return v1 > v2 || (v1 == v2 && i1 < i2);
+}
+
+// ---------------------------------------------------------------------------
+// K0: Gram matrix G = WᵀW in the oracle's order (acc = 0; acc += w·w over d,
+// separately rounded), plus column norms for the selection error bound.
+// One thread per (i, j); W is L2-resident (≤ 4.6 MB at c3).
+__global__ void gram_exact_kernel(const double* __restrict__ W, int D, int H, int ldw,
+                                  double* __restrict__ G, double* __restrict__ wnorm,
+                                  double* __restrict__ gdiag) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= H) return;
+  double acc = 0.0;
+  for (int d = 0; d < D; ++d) {
+    const double a = W[(long long)d * ldw + i], b = W[(long long)d * ldw + j];
+    acc = __dadd_rn(acc, __dmul_rn(a, b));
+  }
+  G[(long long)i * H + j] = acc;
+  if (i == j) {
+    wnorm[i] = sqrt(acc);
+    gdiag[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2+K3: per data point (one warp each, grid-stride): selection scores from
+// the DMMA product row B[n,:], deterministic top-H' (value desc, lowest index
+// wins ties, bit-exact against the oracle through the exact re-rank of the
+// near-tie band), log-joints of all truncated states, warp log-sum-exp,
+// posterior q, ⟨s_n⟩ and the candidate-pair block of ⟨s sᵀ⟩.
+//
+// State table (host-built, shared by all points). Candidate subsets of size
+// 1..γ in level-lexicographic order: entries [0, H') are the level-1 nodes
+// {p}; the multi-active states (levels 2..γ, truncation.cpp:116-147) follow.
+// For S = A ∪ {z} (z = max S, parent A, x = max A, sibling A\{x} ∪ {z}):
+//   coup(S) = Σ_{p∈A} P[p][z] = coup(sibling) + P[x][z]
+//   rel(S)  = rel(A) + u[z] + coup(S)
+// so every log-joint costs O(1) whatever |S|. Posterior moments use subtree
+// sums of the prefix tree (children of A are contiguous in the next level):
+//   sub(A) = q(A) + Σ_children sub(child)
+//   ⟨s_p⟩  = Σ_{A: max A = p} sub(A),  ⟨s_p s_q⟩ = Σ_{A: max A = q, p ∈ A} sub(A).
+struct StateDesc {
+  int par, sib, xz, dfs;  // xz = x | z << 8; dfs = index in the reference order
+};
+
+struct EnumArgs {
+  int N, D, H, Dp, Hp, hprime, gamma;
+  const double* Y;
+  const double* W;
+  const double* B;
+  const double* G;
+  const double* wnorm;
+  const double* gdiag;    // diag(G), contiguous
+  double* ES;             // N × Hp
+  double* ssT;            // H × H, off-diagonal candidate pairs via RED (upper triangle)
+  double* s_multi;        // H, multi-state part of Σ⟨s⟩ via RED
+  double* warp_es;        // [nwarps][H] per-warp Σ of singleton posteriors
+  double* warp_scalars;   // [nwarps][2] Σ lse_n, Σ ‖y_n‖²
+  uint32_t* cand_out;     // N × hprime or null
+  double* map_mass;       // inference outputs or null
+  int* map_state;         // N: index of the MAP state in reference order
+  int* err;
+  const StateDesc* desc;  // [n_tab], entries < hprime unused
+  const int2* child;      // [n_coup + hprime]: (first child, count) for levels < γ
+  const int* level_off;   // [gamma + 1]: level k occupies [level_off[k-1], level_off[k])
+  int n_multi, n_tab, n_coup;  // n_tab = hprime + n_multi; n_coup = states of levels 2..γ-1
+  // gather work items: item k sums sub over gather_idx[item_off[k] .. item_off[k+1])
+  const int* gather_idx;
+  const int* item_off;
+  const int* out_item_off;  // output o owns items [out_item_off[o], out_item_off[o+1])
+  int n_items, n_out;       // n_out = hprime + hprime·(hprime−1)/2
+  double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
+  double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
+};
+
+constexpr int kPoolCap = 64;
+
+struct EnumSmem {
+  // offsets (in doubles) of the per-warp region
+  int u, P, tab, coup, part, outs, qs, pool_v, pool_i, cand, total;
+  __host__ __device__ static EnumSmem make(int hprime, int n_tab, int n_coup, int n_items, int n_out) {
+    EnumSmem s;
+    s.u = 0;
+    s.P = s.u + hprime;
+    s.tab = s.P + hprime * hprime;
+    s.coup = s.tab + n_tab;
+    s.part = s.coup + n_coup;
+    s.outs = s.part + n_items;
+    s.qs = s.outs + n_out;
+    s.pool_v = s.qs + hprime;
+    s.pool_i = s.pool_v + kPoolCap + 2;
+    s.cand = s.pool_i + kPoolCap / 2 + 1;      // ints packed 2 per double
+    s.total = s.cand + (hprime + 1) / 2 + 1;  // uint32 candidates packed 2 per double
+    s.total = (s.total + 1) & ~1;
+    return s;
+  }
+};
+
+// One round of the warp arg-max over register-resident keys (lane owns units
+// lane + 32·j): best by (key desc, index asc) among units not yet removed.
+template <int MAXJ>
+__device__ __forceinline__ void select_round(const double (&key)[MAXJ], uint32_t rem, int lane, double& wv,
+                                             int& wi) {
+  double bv = -INFINITY;
+  int bi = 0x7fffffff;
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) {
+    const int h = lane + 32 * j;
+    if (!((rem >> j) & 1u) && ranks_before(key[j], h, bv, bi)) {
+      bv = key[j];
+      bi = h;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ranks_before(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  wv = bv;
+  wi = bi;
+}
+
+// Top-k (k = H' picks written to cand[0..k) in rank order) over register keys,
+// plus the (k+1)-th key. Pool method: the (k+1)-th best of the 32 lane bests
+// bounds the top k+1 from below, the pool of units ranking at or above it is
+// ranked exactly. Falls back to k+1 arg-max rounds when k ≥ 31 or the pool
+// overflows. `valid` marks lanes' real units (h < H).
+template <int MAXJ>
+__device__ __forceinline__ void top_k(const double (&f)[MAXJ], uint32_t removed, int k, int H, int lane,
+                                      double* pool_v, int* pool_i, uint32_t* cand, double& t_k, double& t_next) {
+  bool done = false;
+  if (k < 31) {
+    double lv = -INFINITY;
+    int li = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      if (!((removed >> j) & 1u) && ranks_before(f[j], h, lv, li)) {
+        lv = f[j];
+        li = h;
+      }
+    }
+    int rk = 0;
+#pragma unroll 8
+    for (int s = 0; s < 32; ++s) {
+      const double ov = __shfl_sync(0xffffffffu, lv, s);
+      const int oi = __shfl_sync(0xffffffffu, li, s);
+      rk += ranks_before(ov, oi, lv, li);
+    }
+    // τ = lane best of rank k (the (k+1)-th of the lane bests)
+    const unsigned who = __ballot_sync(0xffffffffu, rk == k);
+    const int src = __ffs(who) - 1;
+    const double tv = __shfl_sync(0xffffffffu, lv, src);
+    const int ti = __shfl_sync(0xffffffffu, li, src);
+    int base = 0;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      const bool in = h < H && !ranks_before(tv, ti, f[j], h);  // (f,h) ⪯ τ
+      const unsigned b = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int pos = base + __popc(b & ((1u << lane) - 1u));
+        if (pos < kPoolCap) {
+          pool_v[pos] = f[j];
+          pool_i[pos] = h;
+        }
+      }
+      base += __popc(b);
+    }
+    __syncwarp();
+    if (base <= kPoolCap) {
+      for (int e = lane; e < base; e += 32) {
+        const double v = pool_v[e];
+        const int i = pool_i[e];
+        int r = 0;
+        for (int o = 0; o < base; ++o) r += ranks_before(pool_v[o], pool_i[o], v, i);
+        if (r < k) cand[r] = static_cast<uint32_t>(i);
+        if (r == k - 1) pool_v[kPoolCap] = v;
+        if (r == k) pool_v[kPoolCap + 1] = v;
+      }
+      __syncwarp();
+      t_k = pool_v[kPoolCap];
+      t_next = pool_v[kPoolCap + 1];
+      done = true;
+    }
+    __syncwarp();
+  }
+  if (!done) {
+    uint32_t rem = removed;
+    for (int r = 0; r <= k; ++r) {
+      double wv;
+      int wi;
+      select_round<MAXJ>(f, rem, lane, wv, wi);
+      if ((wi & 31) == lane) rem |= 1u << (wi >> 5);
+      if (r < k) {
+        if (lane == 0) cand[r] = static_cast<uint32_t>(wi);
+        t_k = wv;
+      } else {
+        t_next = wv;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int MAXJ>
+__global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
+  extern __shared__ __align__(16) double esm[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_items, a.n_out);
+  double* sm = esm + (long long)wib * L.total;
+  double* su = sm + L.u;
+  double* sP = sm + L.P;
+  double* tab = sm + L.tab;
+  double* coup = sm + L.coup;
+  double* spart = sm + L.part;
+  double* souts = sm + L.outs;
+  double* sqs = sm + L.qs;
+  double* pool_v = sm + L.pool_v;
+  int* pool_i = reinterpret_cast<int*>(sm + L.pool_i);
+  uint32_t* scand = reinterpret_cast<uint32_t*>(sm + L.cand);
+
+  const int H = a.H, HP = a.hprime, GM = a.gamma;
+  double es_acc[MAXJ];
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) es_acc[j] = 0.0;
+  double lse_acc = 0.0, y2_acc = 0.0;
+
+  for (int n = gwarp; n < a.N; n += nwarps) {
+    const double* y = a.Y + (long long)n * a.Dp;
+    const double* brow = a.B + (long long)n * a.Hp;
+
+    // ‖y‖² (any order: only the base term and the error bound use it)
+    double y2 = 0.0;
+    for (int d = lane; d < a.D; d += 32) y2 = fma(y[d], y[d], y2);
+    y2 = warp_sum(y2);
+
+    // ---- selection scores (linear_discrete.cpp:244-252), non-fused as the oracle
+    double f[MAXJ];
+    uint32_t removed = 0;
+    double bound = 0.0, mag = 0.0;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      if (h < H) {
+        const double b = brow[h], g = a.gdiag[h];
+        f[j] = __dadd_rn(a.log_pi, __dmul_rn(__dsub_rn(__dmul_rn(2.0, b), g), a.inv2s));
+        bad |= !isfinite(f[j]);
+        bound = fmax(bound, a.wnorm[h]);
+        mag = fmax(mag, fabs(f[j]) + a.inv2s * (2.0 * fabs(b) + g));
+      } else {
+        f[j] = -INFINITY;
+        removed |= 1u << j;
+      }
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) atomicOr(a.err, kErrNonFiniteScore);
+      continue;
+    }
+    // |f_fast − f_exact| ≤ eps: b error (any summation order, γ_D bound)
+    // propagated through ×2, −G, ×inv2s, +log π, plus the rounding of those ops.
+    mag = warp_max(mag) + fabs(a.log_pi);
+    bound = warp_max(bound);
+    const double eps = 2.5 * a.inv2s * a.eps_dot * bound * sqrt(y2) * 1.0001 + 0x1.0p-46 * mag;
+
+    // ---- top-H' by (score desc, index asc), truncation.cpp:38-57
+    if (HP < H) {
+      double t, nv;
+      top_k<MAXJ>(f, removed, HP, H, lane, pool_v, pool_i, scand, t, nv);
+      if (!(t - nv > 2.0 * eps)) {
+        // Near-tie band: rank the band by exact scores (the oracle's
+        // left-to-right b = Wᵀy), everything above it is in, below it out.
+        uint32_t rem2 = 0;
+#pragma unroll
+        for (int j = 0; j < MAXJ; ++j) {
+          const int h = lane + 32 * j;
+          if (h >= H) {
+            rem2 |= 1u << j;
+          } else if (f[j] > t + 2.0 * eps) {
+            f[j] = INFINITY;
+          } else if (f[j] < t - 2.0 * eps) {
+            f[j] = -INFINITY;
+          } else {
+            double acc = 0.0;
+            for (int d = 0; d < a.D; ++d)
+              acc = __dadd_rn(acc, __dmul_rn(a.W[(long long)d * a.Hp + h], y[d]));
+            f[j] = __dadd_rn(a.log_pi, __dmul_rn(__dsub_rn(__dmul_rn(2.0, acc), a.gdiag[h]), a.inv2s));
+          }
+        }
+        for (int r = 0; r < HP; ++r) {
+          double wv;
+          int wi;
+          select_round<MAXJ>(f, rem2, lane, wv, wi);
+          if ((wi & 31) == lane) rem2 |= 1u << (wi >> 5);
+          if (lane == 0) scand[r] = static_cast<uint32_t>(wi);
+        }
+      }
+    } else {
+      for (int p = lane; p < HP; p += 32) scand[p] = static_cast<uint32_t>(p);
+    }
+    __syncwarp();
+    // candidates ascending (truncation.cpp:55): rank by count of smaller picks
+    {
+      uint32_t mine[2] = {0xffffffffu, 0xffffffffu};
+      int pos[2] = {-1, -1};
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int p = lane + 32 * s;
+        if (p < HP) {
+          mine[s] = scand[p];
+          int rk = 0;
+          for (int q = 0; q < HP; ++q) rk += scand[q] < mine[s];
+          pos[s] = rk;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        if (pos[s] >= 0) scand[pos[s]] = mine[s];
+      __syncwarp();
+    }
+    if (a.cand_out)
+      for (int p = lane; p < HP; p += 32) a.cand_out[(long long)n * HP + p] = scand[p];
+
+    // ---- unary / pairwise log-joint terms relative to the zero state:
+    // lj(S) − base = Σ_a [dlp + inv2s(2b_a − G_aa)] + Σ_{a<c} (−2 inv2s G_ac)
+    for (int p = lane; p < HP; p += 32) {
+      const uint32_t c = scand[p];
+      const double v = a.dlp + a.inv2s * (2.0 * brow[c] - a.gdiag[c]);
+      su[p] = v;
+      tab[p] = v;  // level-1 node {p}
+    }
+    for (int e = lane; e < HP * HP; e += 32) {
+      const int p = e / HP, q = e - p * HP;
+      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * H + scand[q]];
+    }
+    __syncwarp();
+
+    // singletons over all H units and the zero state (rel = 0)
+    double(&rel1)[MAXJ] = f;  // scores are no longer needed: reuse the registers
+    double mx = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      rel1[j] = h < H ? a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) : -INFINITY;
+      mx = fmax(mx, rel1[j]);
+    }
+    // multi-active states, level by level
+    for (int k = 2; k <= GM; ++k) {
+      const int e = a.level_off[k];
+      const bool keep = k < GM;
+      for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
+        const StateDesc d = a.desc[i];
+        const int x = d.xz & 0xff, z = d.xz >> 8;
+        const double c = (d.sib < HP ? 0.0 : coup[d.sib - HP]) + sP[x * HP + z];
+        const double r = tab[d.par] + su[z] + c;
+        tab[i] = r;
+        if (keep) coup[i - HP] = c;
+        mx = fmax(mx, r);
+      }
+      __syncwarp();
+    }
+    mx = warp_max(mx);
+    if (!isfinite(mx)) {
+      if (lane == 0) atomicOr(a.err, kErrNonFiniteLogJoint);
+      continue;
+    }
+
+    // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
+    const bool t1 = a.inv_T == 1.0;
+    double z1 = 0.0, zt = 0.0;
+    if (lane == 0) {
+      z1 = exp(-mx);
+      zt = t1 ? z1 : exp(-mx * a.inv_T);
+    }
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const double e = exp(rel1[j] - mx);
+      z1 += e;
+      rel1[j] = t1 ? e : exp((rel1[j] - mx) * a.inv_T);
+      zt += rel1[j];
+    }
+    for (int i = lane; i < a.n_tab; i += 32) {
+      const double r = tab[i] - mx;
+      const double e = exp(r);
+      const double et = t1 ? e : exp(r * a.inv_T);
+      tab[i] = et;
+      if (i >= HP) {
+        z1 += e;
+        zt += et;
+      } else {
+        sqs[i] = et;
+      }
+    }
+    z1 = warp_sum(z1);
+    zt = t1 ? z1 : warp_sum(zt);
+    const double lse_rel = mx + log(z1);
+    const double base = a.base0 - y2 * a.inv2s;
+    const double inv_z = 1.0 / zt;
+    if (lane == 0) {
+      lse_acc += base + lse_rel;
+      y2_acc += y2;
+    }
+    __syncwarp();
+
+    if (a.map_state) {
+      // MAP state (linear_discrete.cpp:314-316: first maximum in reference
+      // order: zero, singletons 0..H−1, then multi-active in DFS order)
+      double bv = lane == 0 ? exp(-mx * a.inv_T) : -1.0;
+      int bi = lane == 0 ? 0 : 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) {
+        const int h = lane + 32 * j;
+        if (h < H && ranks_before(rel1[j], 1 + h, bv, bi)) {
+          bv = rel1[j];
+          bi = 1 + h;
+        }
+      }
+      for (int i = HP + lane; i < a.n_tab; i += 32) {
+        const int ri = 1 + H + a.desc[i].dfs;
+        if (ranks_before(tab[i], ri, bv, bi)) {
+          bv = tab[i];
+          bi = ri;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ranks_before(ov, oi, bv, bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        a.map_state[n] = bi;
+        a.map_mass[n] = bv * inv_z;
+      }
+    }
+
+    // subtree sums, bottom-up (level γ nodes are leaves)
+    for (int k = GM - 1; k >= 1; --k) {
+      const int e = a.level_off[k];
+      for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
+        const int2 ch = a.child[i];
+        double s = tab[i];
+        for (int c = ch.x; c < ch.x + ch.y; ++c) s += tab[c];
+        tab[i] = s;
+      }
+      __syncwarp();
+    }
+
+    // ---- gather ⟨s_p⟩ and ⟨s_p s_q⟩ over the prefix-tree nodes
+    for (int k = lane; k < a.n_items; k += 32) {
+      double s = 0.0;
+      const int e = a.item_off[k + 1];
+      for (int g = a.item_off[k]; g < e; ++g) s += tab[a.gather_idx[g]];
+      spart[k] = s;
+    }
+    __syncwarp();
+    for (int o = lane; o < a.n_out; o += 32) {
+      double s = 0.0;
+      for (int k = a.out_item_off[o]; k < a.out_item_off[o + 1]; ++k) s += spart[k];
+      souts[o] = s * inv_z;
+    }
+    __syncwarp();
+
+    // ---- ⟨s_n⟩ row: singleton mass for every unit; candidates then take their
+    // full marginal (linear_discrete.cpp:288-304)
+    double* esrow = a.ES + (long long)n * a.Hp;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      if (h < H) {
+        const double qh = rel1[j] * inv_z;
+        es_acc[j] += qh;
+        esrow[h] = qh;
+      }
+    }
+    __syncwarp();
+    for (int p = lane; p < HP; p += 32) {
+      const uint32_t c = scand[p];
+      const double tot = souts[p];
+      esrow[c] = tot;
+      atomicAdd(a.s_multi + c, tot - sqs[p] * inv_z);
+    }
+    // candidate pairs (upper triangle: scand ascending ⇒ c_p < c_q)
+    for (int o = HP + lane; o < a.n_out; o += 32) {
+      // o − HP enumerates (p, q), p < q, row-major
+      int idx = o - HP, p = 0;
+      while (idx >= HP - 1 - p) {
+        idx -= HP - 1 - p;
+        ++p;
+      }
+      const int q = p + 1 + idx;
+      atomicAdd(a.ssT + (long long)scand[p] * H + scand[q], souts[o]);
+    }
+    __syncwarp();
+  }
+
+  double* wes = a.warp_es + (long long)gwarp * H;
+#pragma unroll
+  for (int j = 0; j < MAXJ; ++j) {
+    const int h = lane + 32 * j;
+    if (h < H) wes[h] = es_acc[j];
+  }
+  if (lane == 0) {
+    a.warp_scalars[2 * gwarp] = lse_acc;
+    a.warp_scalars[2 * gwarp + 1] = y2_acc;
+  }
+}
+
+// Split-K partial reduction of Yᵀ⟨S⟩ (fixed order ⇒ deterministic) into the
+// packed statistics buffer.
+__global__ void reduce_ysT_kernel(const double* __restrict__ part, int splits, long long split_stride,
+                                  int D, int H, int ldp, double* __restrict__ out) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)D * H) return;
+  const int d = static_cast<int>(idx / H), h = static_cast<int>(idx % H);
+  double s = 0.0;
+  for (int z = 0; z < splits; ++z) s += part[z * split_stride + (long long)d * ldp + h];
+  out[idx] = s;
+}
+
+// Σ⟨s⟩, diag Σ⟨ssᵀ⟩, mirror of the upper triangle, value count, scalars.
+// Packed stats: [ysT D·H | s H | ssT H·H | counts | y2 | logZ | points].
+__global__ void finalize_stats_kernel(const double* __restrict__ warp_es, int nwarps,
+                                      const double* __restrict__ warp_scalars,
+                                      const double* __restrict__ s_multi, int H, long long npoints,
+                                      double* __restrict__ stats, long long off_s, long long off_ssT,
+                                      long long off_tail) {
+  double* s = stats + off_s;
+  double* ssT = stats + off_ssT;
+  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int w = 0; w < nwarps; ++w) acc += warp_es[(long long)w * H + h];
+    acc += s_multi[h];
+    s[h] = acc;
+    ssT[(long long)h * H + h] = acc;
+  }
+  // mirror: lower = upper
+  const long long HH = (long long)H * H;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < HH; e += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(e / H), j = static_cast<int>(e % H);
+    if (i > j) ssT[e] = ssT[(long long)j * H + i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    double l = 0.0, y2 = 0.0;
+    for (int w = threadIdx.x; w < nwarps; w += 32) {
+      l += warp_scalars[2 * w];
+      y2 += warp_scalars[2 * w + 1];
+    }
+    l = warp_sum(l);
+    y2 = warp_sum(y2);
+    if (threadIdx.x == 0) {
+      stats[off_tail + 1] = y2;
+      stats[off_tail + 2] = l;
+      stats[off_tail + 3] = static_cast<double>(npoints);
+    }
+  }
+}
+
+// value_counts = Σ_h Σ⟨s⟩_h (every active unit carries value 1)
+__global__ void counts_kernel(double* stats, long long off_s, int H, long long off_tail) {
+  double acc = 0.0;
+  for (int h = threadIdx.x; h < H; h += 32) acc += stats[off_s + h];
+  acc = warp_sum(acc);
+  if (threadIdx.x == 0) stats[off_tail] = acc;
+}
+
+}  // namespace bscgpu

@@ -1,0 +1,277 @@
+// C ABI (include/prsp_bsc_gpu.h) over BscEngine and the fixtures. Exceptions
+// map to prsp_status codes as the reference's `guarded` does
+// (/root/reference/proj/src/capi.cpp:63-82); outputs are written only on success.
+#include "prsp_bsc_gpu.h"
+
+#include <cuda_runtime_api.h>
+
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "bsc_engine.hpp"
+#include "fixtures.hpp"
+
+struct prsp_bsc_gpu {
+  bscgpu::BscEngine engine;
+  prsp_bsc_gpu(uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, int dev) : engine(d, h, hp, g, cap, dev) {}
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return 0;
+  } catch (const bscgpu::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of memory";
+    return bscgpu::kInternal;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return bscgpu::kInternal;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw bscgpu::Error(bscgpu::kConfig, std::string("null argument: ") + what);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* prsp_bsc_gpu_version(void) { return "0.1.0-b200"; }
+const char* prsp_bsc_gpu_last_error(void) { return g_err.c_str(); }
+
+int prsp_bsc_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int prsp_bsc_gpu_create(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
+                        int device, prsp_bsc_gpu** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = new prsp_bsc_gpu(dim, latents, hprime, gamma, state_cap, device);
+  });
+}
+
+void prsp_bsc_gpu_free(prsp_bsc_gpu* ctx) { delete ctx; }
+
+int prsp_bsc_gpu_set_stream(prsp_bsc_gpu* ctx, void* stream) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.set_stream(stream);
+  });
+}
+
+int prsp_bsc_gpu_sync(prsp_bsc_gpu* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.sync();
+  });
+}
+
+int prsp_bsc_gpu_states_per_point(const prsp_bsc_gpu* ctx, uint64_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *out = ctx->engine.states_per_point();
+  });
+}
+
+int prsp_bsc_gpu_load_data(prsp_bsc_gpu* ctx, const double* y, uint64_t n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(y, "y");
+    ctx->engine.load_data(y, n, false);
+    ctx->engine.sync();
+  });
+}
+
+int prsp_bsc_gpu_load_data_device(prsp_bsc_gpu* ctx, const double* y, uint64_t n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(y, "y");
+    ctx->engine.load_data(y, n, true);
+  });
+}
+
+int prsp_bsc_gpu_set_params(prsp_bsc_gpu* ctx, const double* w, double pi, double sigma2) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(w, "w");
+    ctx->engine.set_params(w, pi, sigma2);
+    ctx->engine.sync();
+  });
+}
+
+int prsp_bsc_gpu_get_params(prsp_bsc_gpu* ctx, double* w, double* pi, double* sigma2) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.get_params(w, pi, sigma2);
+  });
+}
+
+int prsp_bsc_gpu_estep(prsp_bsc_gpu* ctx, double temperature) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.estep(temperature);
+  });
+}
+
+int prsp_bsc_gpu_stats_buffer(prsp_bsc_gpu* ctx, double** ptr, uint64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *ptr = ctx->engine.stats_device();
+    *count = static_cast<uint64_t>(ctx->engine.layout().count());
+  });
+}
+
+int prsp_bsc_gpu_get_stats(prsp_bsc_gpu* ctx, double* sum_s, double* sum_ssT, double* sum_y_sT,
+                           double* value_counts, double* scalars) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.get_stats(sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
+  });
+}
+
+int prsp_bsc_gpu_set_stats(prsp_bsc_gpu* ctx, const double* sum_s, const double* sum_ssT, const double* sum_y_sT,
+                           const double* value_counts, const double* scalars) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(sum_s, "sum_s");
+    need(sum_ssT, "sum_ssT");
+    need(sum_y_sT, "sum_y_sT");
+    need(value_counts, "value_counts");
+    need(scalars, "scalars");
+    ctx->engine.set_stats(sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
+  });
+}
+
+int prsp_bsc_gpu_mstep(prsp_bsc_gpu* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.mstep();
+  });
+}
+
+int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    const double f = ctx->engine.step(temperature);
+    if (free_energy) *free_energy = f;
+  });
+}
+
+int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y, uint64_t n, const double* w, double pi,
+                           double sigma2, double temperature, double* w_out, double* pi_out, double* sigma2_out,
+                           double* free_energy) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(y, "y");
+    need(w, "w");
+    auto& e = ctx->engine;
+    e.load_data(y, n, false);
+    e.set_params(w, pi, sigma2);
+    const double f = e.step(temperature);
+    double p = 0, s2 = 0;
+    e.get_params(w_out, &p, &s2);
+    if (pi_out) *pi_out = p;
+    if (sigma2_out) *sigma2_out = s2;
+    if (free_energy) *free_energy = f;
+  });
+}
+
+int prsp_bsc_gpu_candidates(prsp_bsc_gpu* ctx, uint32_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->engine.estep(1.0, true);
+    ctx->engine.sync();
+    ctx->engine.get_candidates(out);
+  });
+}
+
+int prsp_bsc_gpu_inference(prsp_bsc_gpu* ctx, double* map_states, double* map_mass, double* expected) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(map_states, "map_states");
+    need(map_mass, "map_mass");
+    need(expected, "expected");
+    ctx->engine.inference(map_states, map_mass, expected);
+  });
+}
+
+int prsp_bsc_gpu_set_timing(prsp_bsc_gpu* ctx, int on) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.set_timing(on != 0);
+  });
+}
+
+int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    const auto& t = ctx->engine.timings();
+    const float v[6] = {t.gram_ms, t.gemm1_ms, t.enum_ms, t.gemm2_ms, t.finalize_ms, t.mstep_ms};
+    std::memcpy(out6, v, sizeof v);
+  });
+}
+
+int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *out = ctx->engine.kernel_launches_last_step();
+  });
+}
+
+int prsp_bsc_bars_generate(uint32_t size, uint64_t n, double prob, double amplitude, double noise, int max_mode,
+                           uint64_t seed, double* y_out, double* truth_out) {
+  return guarded([&] {
+    need(y_out, "y_out");
+    bscgpu::bars_generate(size, n, prob, amplitude, noise, max_mode != 0, seed, y_out, truth_out);
+  });
+}
+
+int prsp_bsc_generate(uint32_t dim, uint32_t latents, const double* w, double pi, double sigma2, uint64_t n,
+                      uint64_t seed, double* y_out) {
+  return guarded([&] {
+    need(w, "w");
+    need(y_out, "y_out");
+    bscgpu::generate(dim, latents, w, pi, sigma2, n, seed, y_out);
+  });
+}
+
+int prsp_bsc_random_dictionary(uint32_t dim, uint32_t latents, uint64_t seed, double scale, double* w_out) {
+  return guarded([&] {
+    need(w_out, "w_out");
+    bscgpu::random_dictionary(dim, latents, seed, scale, w_out);
+  });
+}
+
+int prsp_bsc_baseline_init(uint32_t dim, uint32_t latents, const double* y, uint64_t n, uint64_t seed,
+                           double* w_out, double* pi_out, double* sigma2_out) {
+  return guarded([&] {
+    need(y, "y");
+    bscgpu::baseline_init(dim, latents, y, n, seed, w_out, pi_out, sigma2_out);
+  });
+}
+
+int prsp_bsc_standard_init(uint32_t dim, uint32_t latents, uint32_t hprime, const double* y, uint64_t n,
+                           uint64_t seed, double* w_out, double* pi_out, double* sigma2_out) {
+  return guarded([&] {
+    need(y, "y");
+    bscgpu::standard_init(dim, latents, hprime, y, n, seed, w_out, pi_out, sigma2_out);
+  });
+}
+
+}  // extern "C"

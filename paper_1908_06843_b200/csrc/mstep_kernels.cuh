@@ -1,0 +1,192 @@
+// M-step kernels (linear_discrete.cpp:336-408): ridge, blocked Cholesky of
+// Σ⟨ssᵀ⟩ + ridge·I (panel factor + row-wise triangular solves here, trailing
+// updates on the DMMA GEMM), and the σ²/π updates.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bscgpu {
+
+constexpr int kCholNb = 64;
+
+// Device-side scalars of one EM iteration (kept resident; the host reads
+// back only what the StepResult API needs).
+struct MstepScalars {
+  double trace, ridge;
+  int chol_failed;  // LLT failure ⇒ keep the previous dictionary (:360-362)
+  int pad;
+  double t2, t3;
+  double sigma2, pi;
+};
+
+// Bm = Σ⟨ssᵀ⟩ + ridge·I with ridge = 1e-9·trace/H (:349-353); Xr = Σ y⟨s⟩ᵀ.
+__global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long off_ssT, int D, int H,
+                                     int ldb, double* __restrict__ Bm, double* __restrict__ X, int ldx,
+                                     MstepScalars* sc) {
+  __shared__ double tr;
+  if (threadIdx.x < 32) {
+    double acc = 0.0;
+    for (int h = threadIdx.x; h < H; h += 32) acc += stats[off_ssT + (long long)h * H + h];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) tr = acc;
+  }
+  __syncthreads();
+  const double trace = tr;
+  const double ridge = 1e-9 * trace / static_cast<double>(H);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->trace = trace;
+    sc->ridge = ridge;
+    sc->chol_failed = trace > 0.0 ? 0 : 1;
+  }
+  const long long HH = (long long)H * H;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < HH; e += (long long)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(e / H), j = static_cast<int>(e % H);
+    double v = stats[off_ssT + e];
+    if (i == j) v += ridge;
+    Bm[(long long)i * ldb + j] = v;
+  }
+  const long long DH = (long long)D * H;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < DH; e += (long long)gridDim.x * blockDim.x) {
+    const int d = static_cast<int>(e / H), h = static_cast<int>(e % H);
+    X[(long long)d * ldx + h] = stats[e];
+  }
+}
+
+// Unblocked Cholesky of the kb×kb diagonal block at (k0,k0), in shared memory.
+__global__ void potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int kb, MstepScalars* sc) {
+  __shared__ double L[kCholNb][kCholNb + 1];
+  __shared__ int fail;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kb * kb; e += blockDim.x) {
+    const int i = e / kb, j = e % kb;
+    L[i][j] = A[(long long)(k0 + i) * lda + k0 + j];
+  }
+  if (tid == 0) fail = sc->chol_failed;
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    if (tid == 0) {
+      double s = L[j][j];
+      for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
+      if (!(s > 0.0) || !isfinite(s)) {
+        fail = 1;
+        s = 1.0;
+      }
+      L[j][j] = sqrt(s);
+    }
+    __syncthreads();
+    for (int i = j + 1 + tid; i < kb; i += blockDim.x) {
+      double t = L[i][j];
+      for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
+      L[i][j] = t / L[j][j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < kb * kb; e += blockDim.x) {
+    const int i = e / kb, j = e % kb;
+    A[(long long)(k0 + i) * lda + k0 + j] = j <= i ? L[i][j] : 0.0;
+  }
+  if (tid == 0 && fail) sc->chol_failed = 1;
+}
+
+// Row-wise triangular solves against the kb×kb lower block Lkk stored at
+// (k0,k0) of L (leading dim ldl), applied to rows [r0, r0+nrows) of X at
+// columns [c0, c0+kb):
+//   FWD_T:  x · Lkkᵀ = x_in  (forward substitution)   — Cholesky panel / Z = R·L⁻ᵀ
+//   BWD  :  x · Lkk  = x_in  (backward substitution)  — X = Z·L⁻¹
+template <bool FWD_T>
+__global__ void trsm_rows_kernel(const double* __restrict__ Lm, int ldl, int k0, int kb,
+                                 double* __restrict__ X, int ldx, int r0, int nrows, int c0) {
+  __shared__ double L[kCholNb][kCholNb + 1];
+  extern __shared__ double xs[];  // [blockDim.x][kb + 1]
+  const int tid = threadIdx.x;
+  for (int e = tid; e < kb * kb; e += blockDim.x) {
+    const int i = e / kb, j = e % kb;
+    L[i][j] = Lm[(long long)(k0 + i) * ldl + k0 + j];
+  }
+  const int row0 = r0 + blockIdx.x * blockDim.x;
+  const int nr = min((int)blockDim.x, r0 + nrows - row0);
+  for (int e = tid; e < nr * kb; e += blockDim.x) {
+    const int r = e / kb, c = e % kb;
+    xs[r * (kb + 1) + c] = X[(long long)(row0 + r) * ldx + c0 + c];
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double* x = xs + tid * (kb + 1);
+    if (FWD_T) {
+      for (int c = 0; c < kb; ++c) {
+        double s = x[c];
+        for (int t = 0; t < c; ++t) s -= x[t] * L[c][t];
+        x[c] = s / L[c][c];
+      }
+    } else {
+      for (int c = kb - 1; c >= 0; --c) {
+        double s = x[c];
+        for (int t = c + 1; t < kb; ++t) s -= x[t] * L[t][c];
+        x[c] = s / L[c][c];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nr * kb; e += blockDim.x) {
+    const int r = e / kb, c = e % kb;
+    X[(long long)(row0 + r) * ldx + c0 + c] = xs[r * (kb + 1) + c];
+  }
+}
+
+// W ← X unless the factorisation failed (then the previous W is kept).
+__global__ void commit_w_kernel(const double* __restrict__ X, int ldx, double* __restrict__ W, int ldw, int D,
+                                int H, const MstepScalars* sc) {
+  if (sc->chol_failed) return;
+  const long long DH = (long long)D * H;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < DH; e += (long long)gridDim.x * blockDim.x) {
+    const int d = static_cast<int>(e / H), h = static_cast<int>(e % H);
+    W[(long long)d * ldw + h] = X[(long long)d * ldx + h];
+  }
+}
+
+// t2 = Σ W'∘Σy⟨s⟩ᵀ, t3 = Σ (W'ᵀW')∘Σ⟨ssᵀ⟩ (:366-368), single CTA, fixed order.
+__global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ G,
+                                    const double* __restrict__ stats, long long off_ssT, int D, int H,
+                                    MstepScalars* sc) {
+  __shared__ double red[2][32];
+  double t2 = 0.0, t3 = 0.0;
+  const long long DH = (long long)D * H, HH = (long long)H * H;
+  for (long long e = threadIdx.x; e < DH; e += blockDim.x)
+    t2 += W[(e / H) * ldw + e % H] * stats[e];
+  for (long long e = threadIdx.x; e < HH; e += blockDim.x) t3 += G[e] * stats[off_ssT + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+    t3 += __shfl_xor_sync(0xffffffffu, t3, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = t2;
+    red[1][threadIdx.x >> 5] = t3;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    sc->t2 = a;
+    sc->t3 = b;
+  }
+}
+
+// σ²' = max((t1 − 2t2 + t3)/(N·D), 1e-12), π' = clip(counts/(N·H), 1e-6, 1−1e-6)
+__global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long off_tail, int D, int H,
+                                     MstepScalars* sc) {
+  const double n = stats[off_tail + 3];
+  const double t1 = stats[off_tail + 1];
+  const double s2 = (t1 - 2.0 * sc->t2 + sc->t3) / (n * static_cast<double>(D));
+  sc->sigma2 = s2 < 1e-12 ? 1e-12 : s2;
+  double p = stats[off_tail] / (n * static_cast<double>(H));
+  p = p < 1e-6 ? 1e-6 : p;
+  p = (1.0 - 1e-6) < p ? (1.0 - 1e-6) : p;
+  sc->pi = p;
+}
+
+}  // namespace bscgpu
