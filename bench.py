@@ -1,0 +1,293 @@
+"""Benchmark: BSC truncated-EM data points/s per EM iteration on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+One "step" = one full EM iteration (E-step over the resident shard + sufficient
+statistics + all-reduce across ranks + M-step) of BASELINE.json's headline
+single-GPU workload c2 (D=256, H=300, H'=12, γ=4, N=200,000 points per GPU,
+fp64, synthetic seeded data — see paper_1908_06843_b200/configs.py). Prints one
+JSON line (rank 0). `--impl reference` times the reference's own CPU step
+(oracle/_ref: the prsp sources built against oracle/eigen_shim) on the host
+cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAKS = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+
+
+def flops_per_point(D, H, hprime, gamma):
+    """SURVEY.md §8(d) algorithmic flop convention (FMA = 2, exp not counted)."""
+    from math import comb
+
+    dense = 4 * D * H + 2 * D + 4 * H
+    state = 0
+    for k in range(0, gamma + 1):
+        cnt = 1 if k == 0 else (H if k == 1 else comb(hprime, k))
+        f_eval = 0 if k == 0 else 3 * k + k * (k - 1) + 4
+        f_acc = 2 * k + k * (k - 1) // 2
+        state += cnt * (f_eval + 2 + f_acc)
+    return dense, state
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak():
+    if os.path.exists(FP64_PEAKS):
+        with open(FP64_PEAKS) as f:
+            j = json.load(f)
+        return j["dmma_m8n8k4_tflops"], j["dfma_tflops"], "profiles/r01_fp64_peaks.json (measured, FP64 DMMA/DFMA)"
+    return 37.0, 37.0, "nominal B200 FP64 (no measurement found)"
+
+
+def cpu_reference_rate(w, n_sample, threads, use_ref=True):
+    """Reference (or C port) CPU EM step on a bounded sample: points/s."""
+    from oracle import oracle as O
+    from paper_1908_06843_b200 import configs
+
+    y = configs.data(w, n_sample)
+    p = configs.init(w, y)
+    kind = "reference" if (use_ref and O.Oracle.available("ref")) else "port"
+    if kind == "reference":
+        sess = O.RefSession(y, w.H, w.hprime, w.gamma)
+        t = time.perf_counter()
+        sess.step(p.W, p.pi, p.sigma2, threads, threads)
+        dt = time.perf_counter() - t
+    else:
+        orc = O.Oracle("port")
+        t = time.perf_counter()
+        orc.step(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma, shards=threads, workers=threads)
+        dt = time.perf_counter() - t
+    return n_sample / dt, kind, dt
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, kind, dt = cpu_reference_rate(w, sample, threads)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = float(np.mean([v for v, _ in vals]))
+    ms = float(np.mean([dt for _, dt in vals]) * 1e3)
+    line = {
+        "impl": "reference", "metric": "BSC truncated-EM data points/sec per iteration", "value": value,
+        "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {**w.describe(), "points_per_step": sample, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": kind,
+                         "sample": f"{sample} points of {w.name}, one full EM step per timed step, "
+                                   f"ShardPlan::with_shards({sample}, {threads}, {threads})"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--points", type=int, default=0, help="points per GPU (default: the config's N)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1908_06843_b200 import BscGpuModel, TruncationConfig, bsc
+    from paper_1908_06843_b200 import dist as bdist
+
+    n_local = args.points or w.N
+    # weak scaling: every rank holds its own N-point shard (seeded per rank)
+    y = configs.data(w, n_local, seed_offset=1000 * rank)
+    if world > 1:  # the same initial params on every rank (from rank 0's shard)
+        y0 = y if rank == 0 else configs.data(w, n_local, seed_offset=0)
+        p0 = configs.init(w, y0)
+    else:
+        p0 = configs.init(w, y)
+
+    model = BscGpuModel(w.D, w.H, TruncationConfig(w.H, w.hprime, w.gamma), device=local)
+    stream = torch.cuda.current_stream()
+    model.set_stream(stream.cuda_stream)
+    model.load(y)
+    model.set_params(p0)
+    stats_view = bdist.stats_tensor(model)
+
+    def one_step():
+        bdist.distributed_step(model, stats_view)
+
+    for _ in range(args.warmup):
+        one_step()
+    model.set_timing(True)
+    one_step()  # per-kernel breakdown of one step (engine CUDA events)
+    kern = model.timings()
+    launches_per_step = model.launches()
+    model.set_timing(False)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms = ms_total / args.steps
+    n_total = n_local * world
+    value = n_total / (ms / 1e3)
+
+    # ---- end to end through the reference-facing C ABI with host buffers
+    e2e = None
+    if world == 1:
+        ypin = torch.empty((n_local, w.D), dtype=torch.float64, pin_memory=True)
+        ypin.numpy()[:] = y
+        e2e_model = model
+        p = model.get_params()
+        e2e_model.step_host(p, ypin.numpy())  # warm
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            p = e2e_model.step_host(p, ypin.numpy()).params
+        dt = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": n_local / dt, "unit": "points/s", "h2d_bytes_per_step": int(ypin.numel() * 8 + w.D * w.H * 8),
+               "d2h_bytes_per_step": int(w.D * w.H * 8 + 3 * 8), "ms_per_step": dt * 1e3,
+               "path": "prsp_bsc_gpu_step_host (pinned Y + W in, W/pi/sigma2/F out)"}
+
+    # ---- roofline of the dominant kernel
+    dense, state = flops_per_point(w.D, w.H, w.hprime, w.gamma)
+    dmma_peak, dfma_peak, peak_src = fp64_peak()
+    gemm_flops = 2.0 * n_local * w.D * w.H
+    rows = {
+        "enumerate": (state * n_local, kern["enumerate"], dfma_peak, "fp64 pipe (DFMA/exp)"),
+        "gemm_yw": (gemm_flops, kern["gemm_yw"], dmma_peak, "tensor (DMMA)"),
+        "gemm_ytes": (gemm_flops, kern["gemm_ytes"], dmma_peak, "tensor (DMMA)"),
+    }
+    dom = max(rows, key=lambda k: rows[k][1])
+    fl, tms, pk, pipe = rows[dom]
+    achieved = fl / (tms / 1e3) / 1e12
+    kernels = {k: {"ms": round(v[1], 4), "tflops": round(v[0] / (v[1] / 1e3) / 1e12, 3) if v[1] else None,
+                   "frac": round(v[0] / (v[1] / 1e3) / 1e12 / v[2], 4) if v[1] else None} for k, v in rows.items()}
+    kernels.update({k: {"ms": round(kern[k], 4)} for k in ("gram", "finalize", "mstep")})
+    step_flops = (dense + state) * n_total
+    line = {
+        "metric": "BSC truncated-EM data points/sec per iteration", "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE.json recipe; random init of the stated architecture)",
+        "config": {**w.describe(), "points_per_gpu": n_local, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (Y 8·N·D = %.0f MB per GPU)" % (8 * n_local * w.D / 1e6)},
+        "roofline": {"kernel": dom, "bound": "tensor" if dom.startswith("gemm") else "fp64", "pipe": pipe,
+                     "achieved": round(achieved, 3), "peak": pk, "unit": "TFLOP/s", "frac": round(achieved / pk, 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic": "SURVEY.md §8(d): F_state=%d, F_dense=%d flops/point" % (state, dense)},
+        "step_roofline": {"flops_per_step": step_flops, "tflops": round(step_flops / (ms / 1e3) / 1e12 / world, 3),
+                          "frac_of_dmma_peak": round(step_flops / (ms / 1e3) / 1e12 / world / dmma_peak, 4)},
+        "kernels": kernels,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches_per_step * args.steps),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, kind, dt = cpu_reference_rate(w, args.ref_sample, threads)
+            line["cpu_baseline"] = {"value": v, "unit": "points/s", "cores": threads, "kind": kind,
+                                    "sample": f"{args.ref_sample} points of {w.name}, one EM step ({dt:.1f} s)"}
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    model.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,8 @@ int prsp_bsc_gpu_set_stats(prsp_bsc_gpu* ctx, const double* sum_s, const double*
 int prsp_bsc_gpu_mstep(prsp_bsc_gpu* ctx);
 /* estep + mstep on the resident shard; *free_energy = Σ_n log Z_n at the incoming params. */
 int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy);
+/* F = Σ_n log Z_n (all ranks, once the statistics were all-reduced) of the last M-step's input. */
+int prsp_bsc_gpu_free_energy(prsp_bsc_gpu* ctx, double* out);
 /* Reference-facing step: host Y and params in, host params and F out
  * (copies inside; Y may be pinned for full PCIe rate). */
 int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y_host, uint64_t n, const double* w, double pi,

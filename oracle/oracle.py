@@ -62,18 +62,18 @@ class Oracle:
         self.kind = kind
         self.lib = C.CDLL(path)
         self.pre = "bsc_" if kind == "port" else "ref_"
-        self.lib[self.pre + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.pre + "last_error").restype = C.c_char_p
 
     @staticmethod
     def available(kind: str) -> bool:
         return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
 
     def _call(self, name, *args):
-        fn = self.lib[self.pre + name]
+        fn = getattr(self.lib, self.pre + name)
         fn.restype = _int
         rc = fn(*args)
         if rc != 0:
-            msg = self.lib[self.pre + "last_error"]().decode()
+            msg = getattr(self.lib, self.pre + "last_error")().decode()
             raise OracleError(rc, msg)
 
     # ------------------------------------------------------------ fixtures

@@ -210,9 +210,13 @@ class BscGpuModel:
         N.call("prsp_bsc_gpu_mstep", self._h)
         return self.get_params()
 
-    def mstep_device(self) -> None:
-        """M-step from the (all-reduced) device statistics; params stay resident."""
+    def mstep_device(self) -> float:
+        """M-step from the (all-reduced) device statistics; params stay resident.
+        Returns F = Σ_n log Z_n of those statistics."""
         N.call("prsp_bsc_gpu_mstep", self._h)
+        f = _dbl()
+        N.call("prsp_bsc_gpu_free_energy", self._h, C.byref(f))
+        return f.value
 
     def candidates(self, params: BscParams, data=None) -> np.ndarray:
         """Per-point candidate sets (N×H', ascending) as estep_impl selects them (:240-253)."""

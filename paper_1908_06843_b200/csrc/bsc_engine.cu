@@ -108,6 +108,9 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
      "trsm smem");
   ck(cudaFuncSetAttribute(trsm_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 65 * 8),
      "trsm smem");
+  ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
+  ck(cudaMallocHost(&h_tail_, 4 * sizeof(double)), "pinned");
+  ck(cudaMallocHost(&h_err_, sizeof(int)), "pinned");
   for (auto& e : ev_) {
     cudaEvent_t ev;
     ck(cudaEventCreate(&ev), "event");
@@ -122,6 +125,8 @@ BscEngine::~BscEngine() {
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, d_msc_})
     dfree(p);
+  for (void* p : {h_msc_, h_tail_, h_err_})
+    if (p) cudaFreeHost(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (own_stream_ && stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
@@ -545,21 +550,25 @@ void BscEngine::mstep() {
   ck(cudaGetLastError(), "mstep scalars");
   launches_ += 3;
   if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[6]), s), "event");
-  MstepScalars h{};
-  ck(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s), "mstep scalars D2H");
+  // one synchronisation per iteration: new π, σ², the (all-reduced) F and the
+  // E-step error flag come back together
+  ck(cudaMemcpyAsync(h_msc_, sc, sizeof(MstepScalars), cudaMemcpyDeviceToHost, s), "mstep scalars D2H");
+  ck(cudaMemcpyAsync(h_tail_, d_stats_ + lay_.off_tail(), 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "F D2H");
+  ck(cudaMemcpyAsync(h_err_, d_err_, sizeof(int), cudaMemcpyDeviceToHost, s), "err D2H");
   sync();
-  pi_ = h.pi;
-  sigma2_ = h.sigma2;
+  const int err = *static_cast<int*>(h_err_);
+  if (err & kErrNonFiniteScore) throw Error(kConfig, "select_candidates: scores must be finite");
+  if (err & kErrNonFiniteLogJoint) throw Error(kNumeric, "log_sum_exp: empty support");
+  const auto* h = static_cast<const MstepScalars*>(h_msc_);
+  pi_ = h->pi;
+  sigma2_ = h->sigma2;
+  last_F_ = static_cast<const double*>(h_tail_)[2];
 }
 
 double BscEngine::step(double temperature) {
   estep(temperature);
-  double F = 0.0;
-  ck(cudaMemcpyAsync(&F, d_stats_ + lay_.off_tail() + 2, sizeof(double), cudaMemcpyDeviceToHost,
-                     static_cast<cudaStream_t>(stream_)),
-     "F");
-  check_err();
   mstep();
+  const double F = last_F_;
   if (timing_) {
     auto el = [&](int a, int b) {
       float ms = 0;

@@ -56,6 +56,7 @@ class BscEngine {
   double step(double temperature);
 
   double* stats_device() { return d_stats_; }
+  double last_free_energy() const { return last_F_; }
   const StatsLayout& layout() const { return lay_; }
   void get_stats(double* sum_s, double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars);
   void set_stats(const double* sum_s, const double* sum_ssT, const double* sum_y_sT, const double* value_counts,
@@ -117,6 +118,8 @@ class BscEngine {
   // M-step workspace
   double *d_bm_ = nullptr, *d_x_ = nullptr;
   void* d_msc_ = nullptr;
+  void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // pinned
+  double last_F_ = 0.0;
 
   int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
   bool timing_ = false;

@@ -172,6 +172,14 @@ int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy
   });
 }
 
+int prsp_bsc_gpu_free_energy(prsp_bsc_gpu* ctx, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    *out = ctx->engine.last_free_energy();
+  });
+}
+
 int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y, uint64_t n, const double* w, double pi,
                            double sigma2, double temperature, double* w_out, double* pi_out, double* sigma2_out,
                            double* free_energy) {

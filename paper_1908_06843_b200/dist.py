@@ -1,0 +1,84 @@
+"""Data-parallel EM over ranks: one process per GPU, contiguous row shards,
+one all-reduce of the packed sufficient statistics per EM iteration, then a
+replicated deterministic M-step.
+
+The reference's only parallelism is the thread map_reduce over ShardPlan
+shards (/root/reference/proj/src/parallel.cpp:27-43, :109-158); here each
+rank owns one shard and the ordered fold becomes a sum all-reduce
+(``torch.distributed``: NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """ShardPlan::with_shards(n, world, ·).shards[rank] (parallel.cpp:27-43):
+    contiguous near-equal shards, the first n % world one row longer."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("shard plan: bad world/rank")
+    base, extra = divmod(n, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def stats_count(d: int, h: int) -> int:
+    return d * h + h + h * h + 4
+
+
+def pack_stats(st: dict, d: int, h: int) -> np.ndarray:
+    """Host copy of the device layout [sum_y_sT D·H | sum_s H | sum_ssT H·H |
+    value_counts | sum_y2 | log_partition | points] (bsc_engine.hpp StatsLayout)."""
+    out = np.empty(stats_count(d, h))
+    o = 0
+    out[o:o + d * h] = np.asarray(st["sum_y_sT"]).ravel()
+    o += d * h
+    out[o:o + h] = np.asarray(st["sum_s"]).ravel()
+    o += h
+    out[o:o + h * h] = np.asarray(st["sum_ssT"]).ravel()
+    o += h * h
+    out[o:o + 4] = [float(np.atleast_1d(st["value_counts"])[0]), st["sum_y2"], st["log_partition"],
+                    float(st["points"])]
+    return out
+
+
+def unpack_stats(buf: np.ndarray, d: int, h: int) -> dict:
+    o = 0
+    ysT = buf[o:o + d * h].reshape(d, h).copy()
+    o += d * h
+    s = buf[o:o + h].copy()
+    o += h
+    ssT = buf[o:o + h * h].reshape(h, h).copy()
+    o += h * h
+    t = buf[o:o + 4]
+    return dict(sum_s=s, sum_ssT=ssT, sum_y_sT=ysT, value_counts=np.array([t[0]]), sum_y2=float(t[1]),
+                log_partition=float(t[2]), points=int(round(t[3])))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ over an engine-owned device buffer (zero copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def stats_tensor(model):
+    """A torch view of the model's device statistics buffer (for all_reduce)."""
+    import torch
+
+    ptr, count = model.stats_buffer()
+    return torch.as_tensor(_CudaArray(ptr, count), device=f"cuda:{torch.cuda.current_device()}")
+
+
+def distributed_step(model, stats_view, temperature: float = 1.0, group=None) -> None:
+    """One EM iteration across ranks: local E-step → all-reduce(Σ stats) → M-step.
+    The model must run on torch's current stream (``model.set_stream``)."""
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    N.call("prsp_bsc_gpu_estep", model.handle, float(temperature))
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(stats_view, op=dist.ReduceOp.SUM, group=group)
+    model.mstep_device()

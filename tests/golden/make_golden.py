@@ -1,0 +1,71 @@
+"""Generates the golden fixtures in this directory from the REFERENCE ITSELF:
+oracle/_ref/libprsp_ref.so is the prsp sources under /root/reference/proj/src
+compiled unmodified (against oracle/eigen_shim) by oracle/Makefile. Run here
+(where /root/reference exists):  python tests/golden/make_golden.py
+
+Each .npz holds the inputs of one small case and the reference's outputs:
+per-point candidate sets, estep_stats fields, one-step params and F, a short
+free-running trajectory, and the inference readout.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle.oracle import Oracle  # noqa: E402
+
+R = Oracle("ref")
+
+
+def case(name, y, w0, pi0, s20, hprime, gamma, iters=3, temperature=1.0):
+    d, h = w0.shape
+    out = dict(y=y, W0=w0, pi0=pi0, sigma2_0=s20, hprime=hprime, gamma=gamma, temperature=temperature)
+    out["candidates"] = R.candidates(w0, pi0, s20, y, hprime)
+    st = R.estep_stats(w0, pi0, s20, y, hprime, gamma, temperature)
+    for k, v in st.items():
+        out["stats_" + k] = np.asarray(v)
+    w1, p1, s1, f = R.step(w0, pi0, s20, y, hprime, gamma, temperature, shards=3, workers=2)
+    out.update(W1=w1, pi1=p1, sigma2_1=s1, F0=f)
+    ws, ps, ss, fs = [], [], [], []
+    w, p, s = w0, pi0, s20
+    for _ in range(iters):
+        w, p, s, f = R.step(w, p, s, y, hprime, gamma, 1.0)
+        ws.append(w), ps.append(p), ss.append(s), fs.append(f)
+    out.update(traj_W=np.array(ws), traj_pi=np.array(ps), traj_sigma2=np.array(ss), traj_F=np.array(fs))
+    ms, mm, ex = R.inference(w0, pi0, s20, y, hprime, gamma)
+    out.update(map_states=ms, map_mass=mm, expected=ex)
+    if h <= 10:
+        out["exact_ll0"] = R.exact_log_likelihood(w0, pi0, s20, y)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
+def baseline_init(y, h, seed):
+    # BASELINE.json's init recipe is not reference code (SURVEY.md §8(d) pins
+    # it); the C restatement computes it. The reference then runs from it.
+    return Oracle("port").baseline_init(y, h, seed)
+
+
+if __name__ == "__main__":
+    # bars 5×5 (BASELINE c0 family), truncated
+    y, _ = R.make_bars(5, 200, seed=0)
+    w, p, s = baseline_init(y, 10, 0)
+    case("bars5_h10_hp6_g3", y, w, p, s, 6, 3)
+    # same data, exact mode H'=H=γ (the reference's exact_log_likelihood applies)
+    case("bars5_exact_h10", y, w, p, s, 10, 10, iters=3)
+    # bars 10×10 (c1 family) at T=2 (annealed posterior)
+    y, _ = R.make_bars(10, 150, seed=1)
+    w, p, s = baseline_init(y, 20, 1)
+    case("bars10_h20_hp10_g4_T2", y, w, p, s, 10, 4, temperature=2.0)
+    # random unit-norm dictionary (c2 family), reference generate()
+    wt = Oracle("port").random_dictionary(32, 40, 5, 5.0)
+    y = R.generate(wt, 4 / 40, 0.25, 300, 5)
+    w, p, s = baseline_init(y, 40, 5)
+    case("rand_d32_h40_hp8_g3", y, w, p, s, 8, 3)
+    # SPEC acceptance 1 shape: D=9, H=6, N=200, H'=H=γ=6
+    wt = Oracle("port").random_dictionary(9, 6, 7, 3.0)
+    y = R.generate(wt, 0.3, 0.5, 200, 7)
+    w, p, s = R.standard_init(y, 6, 6, 6, 11)
+    case("spec_acc1_d9_h6_exact", y, w, p, s, 6, 6, iters=5)

@@ -1,0 +1,265 @@
+"""GPU parity of the sm_100a path (through the C ABI) against the oracle.
+
+Bar: candidate sets bit-exact (uint32, every point); sufficient statistics,
+free energy and one-step W, π, σ² within the tolerances below (north star:
+1e-6 relative per iteration, fp64; Frobenius-relative for
+matrices). Small cases compare with the oracle directly; the full BASELINE
+sizes are checked through size-independent properties.
+"""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-6  # north-star tolerance (W Frobenius-relative, π, σ², F relative)
+TOL_STATS = 1e-10  # per-field Frobenius-relative on E-step statistics
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1908_06843_b200 as P
+
+    assert P._native.lib().prsp_bsc_gpu_device_count() > 0, "no CUDA device: the sm_100a path cannot run"
+    return P
+
+
+def model_for(P, d, h, hp, g):
+    return P.BscGpuModel(d, h, P.TruncationConfig(h, hp, g))
+
+
+def check_stats(sg, so, tol=TOL_STATS):
+    for k in ["sum_s", "sum_ssT", "sum_y_sT", "value_counts"]:
+        assert rel(getattr(sg, k), so[k]) < tol, (k, rel(getattr(sg, k), so[k]))
+    assert abs(sg.sum_y2 - so["sum_y2"]) <= tol * abs(so["sum_y2"])
+    assert abs(sg.log_partition - so["log_partition"]) <= tol * abs(so["log_partition"])
+    assert sg.points == so["points"]
+
+
+def check_step(res, w, pi, s2, f, tol=TOL_STEP):
+    assert rel(res.params.W, w) < tol, rel(res.params.W, w)
+    assert abs(res.params.pi - pi) <= tol * pi
+    assert abs(res.params.sigma2 - s2) <= tol * s2
+    assert abs(res.free_energy - f) <= tol * abs(f)
+
+
+# ------------------------------------------------------------ golden fixtures
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_golden(pkg, name):
+    g = load_golden(name)
+    y, d, h = g["y"], g["W0"].shape[0], g["W0"].shape[1]
+    hp, gm, T = int(g["hprime"]), int(g["gamma"]), float(g["temperature"])
+    p0 = pkg.BscParams(g["W0"], float(g["pi0"]), float(g["sigma2_0"]))
+    m = model_for(pkg, d, h, hp, gm)
+    m.load(y)
+    assert np.array_equal(m.candidates(p0), g["candidates"])
+    sg = m.estep_stats(p0, temperature=T)
+    check_stats(sg, {k[6:]: g[k] for k in g if k.startswith("stats_")})
+    r = m.step(p0, temperature=T)
+    check_step(r, g["W1"], float(g["pi1"]), float(g["sigma2_1"]), float(g["F0"]))
+    # free-running trajectory (secondary gate)
+    p = p0
+    for i in range(len(g["traj_F"])):
+        r = m.step(p)
+        check_step(r, g["traj_W"][i], float(g["traj_pi"][i]), float(g["traj_sigma2"][i]), float(g["traj_F"][i]))
+        p = r.params
+    inf = m.inference(p0)
+    assert np.array_equal(inf.map_states, g["map_states"])
+    assert rel(inf.map_mass, g["map_mass"]) < 1e-10
+    assert rel(inf.expected_states, g["expected"]) < 1e-10
+    m.close()
+
+
+# ------------------------------------------------------ BASELINE workloads, sampled
+@pytest.mark.parametrize("cfg,n", [("c0", 1000), ("c1", 3000), ("c2", 4000), ("c3", 600)])
+def test_config_parity(pkg, port, cfg, n):
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS[cfg]
+    y = configs.data(w, n)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m.load(y)
+    assert np.array_equal(m.candidates(p), port.candidates(p.W, p.pi, p.sigma2, y, w.hprime))
+    check_stats(m.estep_stats(p), port.estep_stats(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma))
+    wo, pio, s2o, fo = port.step(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma)
+    check_step(m.step(p), wo, pio, s2o, fo)
+    m.close()
+
+
+def test_one_step_parity_along_trajectory(pkg, port):
+    """Primary gate: at every iteration, oracle params in → params out within 1e-6."""
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c1"]
+    y = configs.data(w, 2000)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m.load(y)
+    for _ in range(8):
+        wo, pio, s2o, fo = port.step(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma)
+        assert np.array_equal(m.candidates(p), port.candidates(p.W, p.pi, p.sigma2, y, w.hprime))
+        check_step(m.step(p), wo, pio, s2o, fo)
+        p = pkg.BscParams(wo, pio, s2o)
+    m.close()
+
+
+def test_mstep_from_oracle_stats(pkg, port):
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c2"]
+    y = configs.data(w, 1500)
+    p = configs.init(w, y)
+    st = port.estep_stats(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    pm = m.mstep(st, p)
+    wo, pio, s2o = port.mstep(st, p.W, p.pi, p.sigma2)
+    assert rel(pm.W, wo) < 1e-10 and abs(pm.pi - pio) <= 1e-14 * pio and abs(pm.sigma2 - s2o) <= 1e-10 * s2o
+    m.close()
+
+
+# ----------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("d,h,hp,g,n", [
+    (25, 10, 10, 10, 37),   # exact mode, odd N
+    (7, 5, 1, 1, 9),        # H' = γ = 1
+    (13, 11, 11, 1, 16),    # γ = 1 with H' = H (no multi-active states)
+    (33, 70, 9, 2, 1),      # single point, ragged D and H (padding)
+    (9, 40, 20, 3, 50),     # large H' relative to H
+    (16, 33, 32, 2, 40),    # H' ≥ 31: round-based selection path
+])
+def test_edge_shapes(pkg, port, d, h, hp, g, n):
+    wt = port.random_dictionary(d, h, 3, 2.0)
+    y = port.generate(wt, 0.15, 0.3, n, 4)
+    w0, pi0, s20 = port.baseline_init(np.r_[y, y + 0.1], h, 5)  # ≥ 2 rows for the init recipe
+    p = pkg.BscParams(w0, pi0, s20)
+    m = model_for(pkg, d, h, hp, g)
+    m.load(y)
+    assert np.array_equal(m.candidates(p), port.candidates(w0, pi0, s20, y, hp))
+    check_stats(m.estep_stats(p), port.estep_stats(w0, pi0, s20, y, hp, g))
+    wo, pio, s2o, fo = port.step(w0, pi0, s20, y, hp, g)
+    check_step(m.step(p), wo, pio, s2o, fo)
+    m.close()
+
+
+def test_exact_ties_lowest_index_wins(pkg, port):
+    """Duplicate dictionary columns and all-zero points make selection scores tie
+    exactly; the lowest index must win (truncation.cpp:48-53)."""
+    rng = np.random.default_rng(0)
+    d, h, hp, g = 20, 16, 5, 3
+    w = rng.normal(size=(d, h))
+    w[:, 9] = w[:, 3]
+    w[:, 12] = w[:, 3]
+    w[:, 14] = w[:, 7]
+    y = rng.normal(size=(64, d)) + w[:, 3]
+    y[5] = 0.0
+    y[17] = w[:, 7] * 2.0
+    m = model_for(pkg, d, h, hp, g)
+    m.load(y)
+    p = pkg.BscParams(w, 0.2, 0.7)
+    assert np.array_equal(m.candidates(p), port.candidates(w, 0.2, 0.7, y, hp))
+    wo, pio, s2o, fo = port.step(w, 0.2, 0.7, y, hp, g)
+    check_step(m.step(p), wo, pio, s2o, fo)
+    m.close()
+
+
+def test_near_tie_band_uses_exact_scores(pkg, port):
+    """Columns that differ in the last bits put two scores within the fast-path
+    error bound; the exact re-rank must reproduce the oracle's choice."""
+    rng = np.random.default_rng(1)
+    d, h, hp = 64, 24, 6
+    w = rng.normal(size=(d, h))
+    for j, k in [(2, 5), (8, 11), (13, 20)]:
+        w[:, k] = w[:, j] * (1 + 1e-15 * rng.normal(size=d))
+    y = rng.normal(size=(300, d)) + w[:, 2] + w[:, 8] + w[:, 13]
+    m = model_for(pkg, d, h, hp, 3)
+    m.load(y)
+    p = pkg.BscParams(w, 0.1, 1.3)
+    assert np.array_equal(m.candidates(p), port.candidates(w, 0.1, 1.3, y, hp))
+    m.close()
+
+
+def test_temperature(pkg, port):
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c1"]
+    y = configs.data(w, 500)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m.load(y)
+    for T in [1.0, 1.5, 4.0]:
+        check_stats(m.estep_stats(p, temperature=T), port.estep_stats(p.W, p.pi, p.sigma2, y, 10, 4, T))
+    m.close()
+
+
+def test_errors(pkg):
+    m = model_for(pkg, 4, 6, 3, 2)
+    m.load(np.ones((5, 4)))
+    bad = np.ones((4, 6))
+    bad[1, 2] = np.nan
+    with pytest.raises(pkg.NumericError):
+        m.set_params(pkg.BscParams(bad, 0.2, 1.0))
+    with pytest.raises(pkg.ConfigError):
+        m.set_params(pkg.BscParams(np.ones((4, 6)), 1.2, 1.0))
+    with pytest.raises(pkg.ConfigError):
+        m.set_params(pkg.BscParams(np.ones((4, 6)), 0.2, -1.0))
+    with pytest.raises(pkg.ConfigError):  # state explosion (truncation.cpp:111-114)
+        pkg.BscGpuModel(8, 40, pkg.TruncationConfig(40, 30, 20, state_cap=1000))
+    with pytest.raises(pkg.ConfigError):  # non-finite selection scores (truncation.cpp:43-45)
+        m.step(pkg.BscParams(np.full((4, 6), 1e308), 0.2, 1e-300))
+    m.close()
+
+
+# --------------------------------------------------- full-size properties
+def test_full_c2_properties(pkg, port):
+    """c2 at N = 200,000: candidates of a row sample bit-exact vs the oracle,
+    shard additivity of the statistics, ⟨ssᵀ⟩ symmetry, Σ⟨s⟩ = value count,
+    F = Σ log Z and EM monotone over a few iterations."""
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c2"]
+    y = configs.data(w)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m.load(y)
+    cand = m.candidates(p)
+    rows = np.random.default_rng(0).choice(len(y), 1500, replace=False)
+    assert np.array_equal(cand[rows], port.candidates(p.W, p.pi, p.sigma2, y[rows], w.hprime))
+    st = m.estep_stats(p)
+    assert np.allclose(st.sum_ssT, st.sum_ssT.T, rtol=0, atol=0)
+    assert abs(st.value_counts[0] - st.sum_s.sum()) <= 1e-12 * st.value_counts[0]
+    assert np.allclose(np.diag(st.sum_ssT), st.sum_s, rtol=1e-14)
+    assert st.points == len(y)
+    # additivity over two shards (linearity of the E-step statistics)
+    ma = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    ma.load(y[:77_777])
+    sa = ma.estep_stats(p)
+    ma.load(y[77_777:])
+    sb = ma.estep_stats(p)
+    for k in ["sum_s", "sum_ssT", "sum_y_sT"]:
+        assert rel(getattr(sa, k) + getattr(sb, k), getattr(st, k)) < 1e-12
+    assert abs(sa.log_partition + sb.log_partition - st.log_partition) <= 1e-12 * abs(st.log_partition)
+    fs = []
+    for _ in range(4):
+        r = m.step(p)
+        fs.append(r.free_energy)
+        p = r.params
+    assert all(b >= a - 1e-9 * abs(a) for a, b in zip(fs, fs[1:])), fs
+    m.close()
+    ma.close()
+
+
+def test_e2e_host_step_matches_resident(pkg):
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c1"]
+    y = configs.data(w, 1000)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    a = m.step_host(p, y)
+    m2 = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m2.load(y)
+    b = m2.step(p)
+    assert rel(a.params.W, b.params.W) < 1e-13 and abs(a.free_energy - b.free_energy) <= 1e-13 * abs(b.free_energy)
+    m.close()
+    m2.close()
