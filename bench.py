@@ -144,12 +144,14 @@ def run_reference(args, w, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--points", type=int, default=0, help="points per GPU (default: the config's N)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=4000)
+    ap.add_argument("--ref-sample", type=int, default=20000, help="points per reference-arm step")
+    ap.add_argument("--baseline-sample", type=int, default=0,
+                    help="points in the cpu_baseline sample (default: the whole per-GPU workload)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -195,19 +197,18 @@ def main():
     def one_step():
         bdist.distributed_step(model, stats_view)
 
-    for _ in range(args.warmup):
-        one_step()
-    model.set_timing(True)
-    one_step()  # per-kernel breakdown of one step (engine CUDA events)
-    kern = model.timings()
-    launches_per_step = model.launches()
-    model.set_timing(False)
-
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:  # sampled over warm-up + timed steps (≥ 0.2 s of load)
+        for _ in range(args.warmup):
+            one_step()
+        model.set_timing(True)
+        one_step()  # per-kernel breakdown of one step (engine CUDA events)
+        kern = model.timings()
+        launches_per_step = model.launches()
+        model.set_timing(False)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             one_step()
@@ -277,9 +278,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            v, kind, dt = cpu_reference_rate(w, args.ref_sample, threads)
+            v, kind, dt = cpu_reference_rate(w, args.baseline_sample or n_local, threads)
             line["cpu_baseline"] = {"value": v, "unit": "points/s", "cores": threads, "kind": kind,
-                                    "sample": f"{args.ref_sample} points of {w.name}, one EM step ({dt:.1f} s)"}
+                                    "sample": f"{args.baseline_sample or n_local} points of {w.name}, one full EM "
+                                              f"step on all host threads ({dt:.1f} s)"}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:

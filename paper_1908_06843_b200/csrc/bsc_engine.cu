@@ -563,12 +563,6 @@ void BscEngine::mstep() {
   pi_ = h->pi;
   sigma2_ = h->sigma2;
   last_F_ = static_cast<const double*>(h_tail_)[2];
-}
-
-double BscEngine::step(double temperature) {
-  estep(temperature);
-  mstep();
-  const double F = last_F_;
   if (timing_) {
     auto el = [&](int a, int b) {
       float ms = 0;
@@ -582,7 +576,12 @@ double BscEngine::step(double temperature) {
     t_.finalize_ms = el(4, 5);
     t_.mstep_ms = el(5, 6);
   }
-  return F;
+}
+
+double BscEngine::step(double temperature) {
+  estep(temperature);
+  mstep();
+  return last_F_;
 }
 
 void BscEngine::get_stats(double* sum_s, double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars) {
