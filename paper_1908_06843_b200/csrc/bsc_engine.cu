@@ -62,7 +62,7 @@ constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
 // GEMM1  B = Y·W:     M = points, N = Hp, K = Dp.
 #define GEMM1_CFG 128, 64, 16, 32, 32, true, true, 3
 // GEMM2  Yᵀ·⟨S⟩:      M = Dp, N = Hp, K = points (split-K).
-#define GEMM2_CFG 64, 64, 16, 32, 32, false, true, 3
+#define GEMM2_CFG 128, 64, 16, 32, 32, false, true, 3
 // M-step products (C −= A·Bᵀ and C −= A·B).
 #define SYRK_CFG 64, 64, 16, 32, 32, true, false, 3
 #define SOLVE_CFG 64, 64, 16, 32, 32, true, true, 3
@@ -103,11 +103,6 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   d_bm_ = dalloc<double>((size_t)H_ * Hp_, "Bm");
   d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
   d_msc_ = dalloc<MstepScalars>(1, "mstep scalars");
-  // row-wise triangular solves stage 128 rows × (64+1) doubles dynamically
-  ck(cudaFuncSetAttribute(trsm_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 65 * 8),
-     "trsm smem");
-  ck(cudaFuncSetAttribute(trsm_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 65 * 8),
-     "trsm smem");
   ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
   ck(cudaMallocHost(&h_tail_, 4 * sizeof(double)), "pinned");
   ck(cudaMallocHost(&h_err_, sizeof(int)), "pinned");
@@ -120,7 +115,7 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
 
 BscEngine::~BscEngine() {
   cudaSetDevice(device_);
-  for (void* p : {(void*)d_desc_, (void*)d_child_, (void*)d_level_off_, (void*)d_gather_, (void*)d_item_off_, (void*)d_out_off_, (void*)d_y_,
+  for (void* p : {(void*)d_desc_, (void*)d_dfs_, (void*)d_child_, (void*)d_level_off_, (void*)d_gather_, (void*)d_item_off_, (void*)d_out_off_, (void*)d_y_, (void*)d_y2_,
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, d_msc_})
@@ -215,7 +210,12 @@ void BscEngine::build_template() {
   for (int i = 0; i < n_tab; ++i) index_of[key(sets[i])] = i;
   for (int i = 0; i < n_multi_; ++i) dfs_of[masks[i]] = i;
   const int n_coup = gamma_ >= 3 ? level_off[gamma_ - 1] - hp : 0;
-  std::vector<StateDesc> desc(n_tab, StateDesc{0, 0, 0, -1});
+  // byte offsets into a warp's shared region (the tab/coup/P/u part of the
+  // layout does not depend on the gather sizes)
+  const EnumSmem L0 = EnumSmem::make(hp, n_tab, n_coup, 0, 0, 0);
+  auto tab_off = [&](int i) { return (L0.tab + i) * 8; };
+  std::vector<int4> desc(n_tab, int4{0, 0, 0, 0});
+  std::vector<int> dfs_idx(n_tab, -1);
   std::vector<int2> child(hp + n_coup, int2{0, 0});
   for (int i = hp; i < n_tab; ++i) {
     const auto& S = sets[i];
@@ -224,7 +224,10 @@ void BscEngine::build_template() {
     const int x = A.back();
     std::vector<int> sib(A.begin(), A.end() - 1);
     sib.push_back(z);
-    desc[i] = StateDesc{index_of.at(key(A)), index_of.at(key(sib)), x | (z << 8), dfs_of.at(key(S))};
+    const int si = index_of.at(key(sib));
+    desc[i] = int4{tab_off(index_of.at(key(A))), si < hp ? tab_off(n_tab) : (L0.coup + si - hp) * 8,
+                   (L0.P + x * hp + z) * 8, (L0.u + z) * 8};
+    dfs_idx[i] = dfs_of.at(key(S));
   }
   for (int i = 0; i < hp + n_coup; ++i) {
     const auto& A = sets[i];
@@ -258,24 +261,29 @@ void BscEngine::build_template() {
   }
   size_t tot = 0;
   for (auto& l : lists) tot += l.size();
-  const size_t chunk = std::max<size_t>(8, (tot + 95) / 96);
+  // items of ≈ tot/96 entries, each padded to a multiple of 4 with the zero
+  // slot n_tab so the kernel reads indices as int4; item_off counts int4s
+  const size_t chunk = std::max<size_t>(8, ((tot + 95) / 96 + 3) / 4 * 4);
   std::vector<int> gather, item_off{0}, out_off{0};
   for (auto& l : lists) {
     for (size_t s = 0; s < l.size(); s += chunk) {
       const size_t e = std::min(l.size(), s + chunk);
-      gather.insert(gather.end(), l.begin() + s, l.begin() + e);
-      item_off.push_back(static_cast<int>(gather.size()));
+      for (size_t g = s; g < e; ++g) gather.push_back(tab_off(l[g]));
+      while (gather.size() % 4) gather.push_back(tab_off(n_tab));
+      item_off.push_back(static_cast<int>(gather.size() / 4));
     }
     out_off.push_back(static_cast<int>(item_off.size() - 1));
   }
   n_items_ = static_cast<int>(item_off.size() - 1);
-  d_desc_ = dalloc<StateDesc>(desc.size(), "desc");
+  d_desc_ = dalloc<int4>(desc.size(), "desc");
+  d_dfs_ = dalloc<int>(dfs_idx.size(), "dfs");
+  ck(cudaMemcpy(d_dfs_, dfs_idx.data(), dfs_idx.size() * 4, cudaMemcpyHostToDevice), "dfs");
   d_child_ = dalloc<int2>(child.size(), "child");
   d_level_off_ = dalloc<int>(level_off.size(), "level_off");
   d_gather_ = dalloc<int>(gather.size(), "gather");
   d_item_off_ = dalloc<int>(item_off.size(), "item_off");
   d_out_off_ = dalloc<int>(out_off.size(), "out_off");
-  ck(cudaMemcpy(d_desc_, desc.data(), desc.size() * sizeof(StateDesc), cudaMemcpyHostToDevice), "desc");
+  ck(cudaMemcpy(d_desc_, desc.data(), desc.size() * sizeof(int4), cudaMemcpyHostToDevice), "desc");
   if (!child.empty()) ck(cudaMemcpy(d_child_, child.data(), child.size() * sizeof(int2), cudaMemcpyHostToDevice), "child");
   ck(cudaMemcpy(d_level_off_, level_off.data(), level_off.size() * 4, cudaMemcpyHostToDevice), "level_off");
   if (!gather.empty()) ck(cudaMemcpy(d_gather_, gather.data(), gather.size() * 4, cudaMemcpyHostToDevice), "gather");
@@ -285,11 +293,12 @@ void BscEngine::build_template() {
 
 void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
-  for (void* p : {(void*)d_y_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_, (void*)d_map_mass_,
-                  (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_})
+  for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
+                  (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
   d_y_ = dalloc<double>(rows * Dp_, "Y");
+  d_y2_ = dalloc<double>(rows, "y2");
   d_b_ = dalloc<double>(rows * Hp_, "B");
   d_es_ = dalloc<double>(rows * Hp_, "ES");
   d_cand_ = dalloc<uint32_t>(rows * hprime_, "cand");
@@ -300,14 +309,14 @@ void BscEngine::ensure_work(uint64_t n) {
   // split-K for Yᵀ⟨S⟩: ≈4 waves of 148 SMs over the output tiles
   cudaDeviceProp prop;
   ck(cudaGetDeviceProperties(&prop, device_), "props");
-  const int tiles = ((Dp_ + 63) / 64) * ((Hp_ + 63) / 64);
+  const int tiles = ((Dp_ + 127) / 128) * ((Hp_ + 63) / 64);
   splits_ = std::max(1, std::min<int>((4 * prop.multiProcessorCount + tiles - 1) / tiles,
                                       static_cast<int>(std::max<uint64_t>(1, rows / 512))));
   part_stride_ = (long long)Dp_ * Hp_;
   d_part_ = dalloc<double>((size_t)splits_ * part_stride_, "splitK partials");
 
   // enumerator launch shape: per-warp shared region, as many warps as fit
-  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_items_, n_out_);
+  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_items_, n_out_, static_cast<int>(H_));
   const int per_warp = L.total * 8;
   int warps = 8;
   while (warps > 1 && warps * per_warp > 200 * 1024) warps /= 2;
@@ -325,8 +334,8 @@ void BscEngine::ensure_work(uint64_t n) {
   const uint64_t need = (n + warps - 1) / warps;
   enum_ctas_ = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(enum_ctas_, need)));
   enum_warps_total_ = enum_ctas_ * warps;
-  d_warp_es_ = dalloc<double>((size_t)enum_warps_total_ * H_, "warp_es");
-  d_warp_sc_ = dalloc<double>((size_t)enum_warps_total_ * 2, "warp_scalars");
+  d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
+  d_warp_sc_ = dalloc<double>((size_t)enum_ctas_ * 2, "cta_scalars");
 }
 
 void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
@@ -342,6 +351,9 @@ void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
   ck(cudaMemcpy2DAsync(d_y_, (size_t)Dp_ * 8, y, (size_t)D_ * 8, (size_t)D_ * 8, n,
                        device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
      "upload Y");
+  row_sqnorm_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(d_y_, static_cast<long long>(n), D_, Dp_,
+                                                                       d_y2_);
+  ck(cudaGetLastError(), "y2");
   n_ = n;
 }
 
@@ -403,16 +415,16 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
   a.G = d_g_;
   a.wnorm = d_wnorm_;
   a.gdiag = d_gdiag_;
+  a.y2 = d_y2_;
   a.ES = d_es_;
   a.ssT = d_stats_ + lay_.off_ssT();
-  a.s_multi = d_smulti_;
-  a.warp_es = d_warp_es_;
   a.warp_scalars = d_warp_sc_;
   a.cand_out = cands ? d_cand_ : nullptr;
   a.map_mass = infer ? d_map_mass_ : nullptr;
   a.map_state = infer ? d_map_state_ : nullptr;
   a.err = d_err_;
-  a.desc = static_cast<const StateDesc*>(d_desc_);
+  a.sdesc = static_cast<const int4*>(d_desc_);
+  a.dfs = d_dfs_;
   a.child = static_cast<const int2*>(d_child_);
   a.level_off = d_level_off_;
   a.n_multi = n_multi_;
@@ -458,27 +470,25 @@ void BscEngine::estep(double temperature, bool want_candidates) {
   }
   ev(2);
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
-  ck(cudaMemsetAsync(d_smulti_, 0, (size_t)H_ * 8, s), "zero s_multi");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
   launch_enumerate(temperature, want_candidates, false);
   ev(3);
-  {  // K4: Σ y⟨s⟩ᵀ = Yᵀ·ES, split-K over points, reduced in fixed order
+  {  // K4: Σ y⟨s⟩ᵀ = Yᵀ·ES (+ fused Σ⟨s⟩), split-K over points, reduced in fixed order
     const int rows = static_cast<int>((n_ + 1) & ~1ull);
     int kchunk = (rows + splits_ - 1) / splits_;
     kchunk = (kchunk + 1) & ~1;
     const int splits = (rows + kchunk - 1) / kchunk;
-    GemmArgs g{Dp_, Hp_, rows, d_y_, Dp_, d_es_, Hp_, d_part_, Hp_, 1.0, 0.0, kchunk, part_stride_};
+    GemmArgs g{Dp_, Hp_, rows, d_y_, Dp_, d_es_, Hp_, d_part_, Hp_, 1.0, 0.0, kchunk, part_stride_, d_warp_es_};
     ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
     const long long DH = (long long)D_ * H_;
-    reduce_ysT_kernel<<<(DH + 255) / 256, 256, 0, s>>>(d_part_, splits, part_stride_, D_, H_, Hp_,
-                                                        d_stats_ + lay_.off_ysT());
+    reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits, part_stride_, D_, H_, Hp_,
+                                                             d_stats_, lay_.off_s(), lay_.off_ssT());
     ck(cudaGetLastError(), "reduce ysT");
     launches_ += 2;
   }
   ev(4);
   finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
-      d_warp_es_, enum_warps_total_, d_warp_sc_, d_smulti_, H_, static_cast<long long>(n_), d_stats_,
-      lay_.off_s(), lay_.off_ssT(), lay_.off_tail());
+      enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n_), d_stats_, lay_.off_ssT(), lay_.off_tail());
   counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
   ck(cudaGetLastError(), "finalize");
   launches_ += 2;
@@ -509,7 +519,7 @@ void BscEngine::mstep() {
     ++launches_;
     if (k1 < H) {
       const int rows = H - k1, tpb = 128;
-      trsm_rows_kernel<true><<<(rows + tpb - 1) / tpb, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, k0, kb, d_bm_, Hp_,
+      trsm_rows_kernel<true><<<(rows + tpb - 1) / tpb, tpb, 0, s>>>(d_bm_, Hp_, k0, kb, d_bm_, Hp_,
                                                                                    k1, rows, k0);
       GemmArgs g{rows, rows, kb, d_bm_ + (long long)k1 * Hp_ + k0, Hp_, d_bm_ + (long long)k1 * Hp_ + k0, Hp_,
                  d_bm_ + (long long)k1 * Hp_ + k1, Hp_, -1.0, 1.0, kb, 0};
@@ -527,7 +537,7 @@ void BscEngine::mstep() {
       ck(launch_dgemm<SYRK_CFG>(g, 1, s), "solve fwd gemm");
       ++launches_;
     }
-    trsm_rows_kernel<true><<<nblk, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
+    trsm_rows_kernel<true><<<nblk, tpb, 0, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
     ++launches_;
   }
   const int last0 = (H - 1) / kCholNb * kCholNb;
@@ -539,7 +549,7 @@ void BscEngine::mstep() {
       ck(launch_dgemm<SOLVE_CFG>(g, 1, s), "solve bwd gemm");
       ++launches_;
     }
-    trsm_rows_kernel<false><<<nblk, tpb, tpb * (kb + 1) * 8, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
+    trsm_rows_kernel<false><<<nblk, tpb, 0, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
     ++launches_;
   }
   ck(cudaGetLastError(), "solve");
@@ -634,7 +644,6 @@ void BscEngine::inference(double* map_states, double* map_mass, double* expected
   GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, d_w_, Hp_, d_b_, Hp_, 1.0, 0.0, Dp_, 0};
   ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
-  ck(cudaMemsetAsync(d_smulti_, 0, (size_t)H_ * 8, s), "zero s_multi");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
   launch_enumerate(1.0, true, true);
   std::vector<int> st(n_);

@@ -99,12 +99,14 @@ class BscEngine {
   int n_multi_ = 0, n_tab_ = 0, n_coup_ = 0, n_items_ = 0, n_out_ = 0;
   std::vector<uint64_t> dfs_masks_;  // multi-active supports in reference order
   void* d_desc_ = nullptr;
+  int* d_dfs_ = nullptr;
   void* d_child_ = nullptr;
   int* d_level_off_ = nullptr;
   int *d_gather_ = nullptr, *d_item_off_ = nullptr, *d_out_off_ = nullptr;
 
   uint64_t n_ = 0, cap_n_ = 0;
   double *d_y_ = nullptr, *d_w_ = nullptr, *d_g_ = nullptr, *d_wnorm_ = nullptr, *d_gdiag_ = nullptr;
+  double* d_y2_ = nullptr;  // ‖y_n‖² per resident point
   double *d_b_ = nullptr, *d_es_ = nullptr;
   double *d_stats_ = nullptr, *d_smulti_ = nullptr;
   double *d_warp_es_ = nullptr, *d_warp_sc_ = nullptr;

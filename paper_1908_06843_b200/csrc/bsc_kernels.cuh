@@ -63,6 +63,28 @@ __global__ void gram_exact_kernel(const double* __restrict__ W, int D, int H, in
   }
 }
 
+// e^x for x < −32 (only ever added to sums whose largest term is 1): fp32
+// ex2 — its 2⁻²² relative error is < 2⁻⁶⁸ of the sum. Underflow flushes to 0.
+__device__ __forceinline__ double small_exp(double x) {
+  float r;
+  const float t = static_cast<float>(fmax(x, -300.0) * 1.4426950408889634);
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+  return static_cast<double>(r);
+}
+
+// ‖y_n‖² per data point (linear_discrete.cpp:242), once per resident dataset:
+// one warp per row.
+__global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int D, int ldy,
+                                  double* __restrict__ y2) {
+  const long long n = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int d = lane; d < D; d += 32) s = fma(Y[n * ldy + d], Y[n * ldy + d], s);
+  s = warp_sum(s);
+  if (lane == 0) y2[n] = s;
+}
+
 // ---------------------------------------------------------------------------
 // K2+K3: per data point (one warp each, grid-stride): selection scores from
 // the DMMA product row B[n,:], deterministic top-H' (value desc, lowest index
@@ -92,20 +114,21 @@ struct EnumArgs {
   const double* G;
   const double* wnorm;
   const double* gdiag;    // diag(G), contiguous
+  const double* y2;       // N: ‖y_n‖², computed once per dataset
   double* ES;             // N × Hp
   double* ssT;            // H × H, off-diagonal candidate pairs via RED (upper triangle)
-  double* s_multi;        // H, multi-state part of Σ⟨s⟩ via RED
-  double* warp_es;        // [nwarps][H] per-warp Σ of singleton posteriors
-  double* warp_scalars;   // [nwarps][2] Σ lse_n, Σ ‖y_n‖²
+  double* warp_scalars;   // [nctas][2] Σ lse_n, Σ ‖y_n‖²
   uint32_t* cand_out;     // N × hprime or null
   double* map_mass;       // inference outputs or null
   int* map_state;         // N: index of the MAP state in reference order
   int* err;
-  const StateDesc* desc;  // [n_tab], entries < hprime unused
+  const int4* sdesc;      // [n_tab] byte offsets {rel(parent), coup(sibling), P[x][z], u[z]}; < hprime unused
+  const int* dfs;         // [n_tab] index of the state in the reference (DFS) order
   const int2* child;      // [n_coup + hprime]: (first child, count) for levels < γ
   const int* level_off;   // [gamma + 1]: level k occupies [level_off[k-1], level_off[k])
   int n_multi, n_tab, n_coup;  // n_tab = hprime + n_multi; n_coup = states of levels 2..γ-1
-  // gather work items: item k sums sub over gather_idx[item_off[k] .. item_off[k+1])
+  // gather work items: item k sums the node values at byte offsets
+  // gather_idx[4·item_off[k] .. 4·item_off[k+1])
   const int* gather_idx;
   const int* item_off;
   const int* out_item_off;  // output o owns items [out_item_off[o], out_item_off[o+1])
@@ -119,19 +142,22 @@ constexpr int kPoolCap = 64;
 struct EnumSmem {
   // offsets (in doubles) of the per-warp region
   int u, P, tab, coup, part, outs, qs, pool_v, pool_i, cand, total;
-  __host__ __device__ static EnumSmem make(int hprime, int n_tab, int n_coup, int n_items, int n_out) {
+  __host__ __device__ static EnumSmem make(int hprime, int n_tab, int n_coup, int n_items, int n_out, int h) {
     EnumSmem s;
     s.u = 0;
     s.P = s.u + hprime;
-    s.tab = s.P + hprime * hprime;
-    s.coup = s.tab + n_tab;
-    s.part = s.coup + n_coup;
-    s.outs = s.part + n_items;
-    s.qs = s.outs + n_out;
+    s.qs = s.P + hprime * hprime;
     s.pool_v = s.qs + hprime;
     s.pool_i = s.pool_v + kPoolCap + 2;
-    s.cand = s.pool_i + kPoolCap / 2 + 1;      // ints packed 2 per double
-    s.total = s.cand + (hprime + 1) / 2 + 1;  // uint32 candidates packed 2 per double
+    s.cand = s.pool_i + kPoolCap / 2 + 1;   // ints packed 2 per double
+    s.tab = s.cand + (hprime + 1) / 2 + 1;  // uint32 candidates packed 2 per double
+    s.coup = s.tab + n_tab + 1;             // tab[n_tab] = 0: the padding slot of the gather lists
+    s.part = s.coup + n_coup;
+    s.outs = s.part + n_items;
+    s.total = s.outs + n_out;
+    // the exp compaction queue (n_tab ints) overlays coup/part/outs
+    if (s.total < s.coup + n_tab / 2 + 1) s.total = s.coup + n_tab / 2 + 1;
+    if (s.total < h + 2) s.total = h + 2;  // end-of-kernel CTA reduction reuses the regions
     s.total = (s.total + 1) & ~1;
     return s;
   }
@@ -255,7 +281,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   const int wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_items, a.n_out);
+  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_items, a.n_out, a.H);
   double* sm = esm + (long long)wib * L.total;
   double* su = sm + L.u;
   double* sP = sm + L.P;
@@ -269,24 +295,31 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   uint32_t* scand = reinterpret_cast<uint32_t*>(sm + L.cand);
 
   const int H = a.H, HP = a.hprime, GM = a.gamma;
-  double es_acc[MAXJ];
-#pragma unroll
-  for (int j = 0; j < MAXJ; ++j) es_acc[j] = 0.0;
   double lse_acc = 0.0, y2_acc = 0.0;
+  double bound = 0.0;  // max_h ‖W_h‖ (per iteration)
+  for (int h = lane; h < H; h += 32) bound = fmax(bound, a.wnorm[h]);
+  bound = warp_max(bound);
+  const int row_lines = (a.Hp * 8 + 127) / 128;
+  if (lane == 0) tab[a.n_tab] = 0.0;
+  __syncwarp();
 
   for (int n = gwarp; n < a.N; n += nwarps) {
     const double* y = a.Y + (long long)n * a.Dp;
     const double* brow = a.B + (long long)n * a.Hp;
-
-    // ‖y‖² (any order: only the base term and the error bound use it)
-    double y2 = 0.0;
-    for (int d = lane; d < a.D; d += 32) y2 = fma(y[d], y[d], y2);
-    y2 = warp_sum(y2);
+    {  // pull the B row two points ahead into L2 while this point is processed
+      const long long nn = n + 2LL * nwarps;
+      if (nn < a.N)
+        for (int l = lane; l < row_lines; l += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + nn * a.Hp + l * 16));
+    }
+    // ‖y‖² (precomputed once per dataset; any order: only the base term and
+    // the error bound use it)
+    const double y2 = a.y2[n];
 
     // ---- selection scores (linear_discrete.cpp:244-252), non-fused as the oracle
     double f[MAXJ];
     uint32_t removed = 0;
-    double bound = 0.0, mag = 0.0;
+    double mag = 0.0;
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
@@ -295,7 +328,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         const double b = brow[h], g = a.gdiag[h];
         f[j] = __dadd_rn(a.log_pi, __dmul_rn(__dsub_rn(__dmul_rn(2.0, b), g), a.inv2s));
         bad |= !isfinite(f[j]);
-        bound = fmax(bound, a.wnorm[h]);
         mag = fmax(mag, fabs(f[j]) + a.inv2s * (2.0 * fabs(b) + g));
       } else {
         f[j] = -INFINITY;
@@ -309,7 +341,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // |f_fast − f_exact| ≤ eps: b error (any summation order, γ_D bound)
     // propagated through ×2, −G, ×inv2s, +log π, plus the rounding of those ops.
     mag = warp_max(mag) + fabs(a.log_pi);
-    bound = warp_max(bound);
     const double eps = 2.5 * a.inv2s * a.eps_dot * bound * sqrt(y2) * 1.0001 + 0x1.0p-46 * mag;
 
     // ---- top-H' by (score desc, index asc), truncation.cpp:38-57
@@ -394,15 +425,16 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       rel1[j] = h < H ? a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) : -INFINITY;
       mx = fmax(mx, rel1[j]);
     }
-    // multi-active states, level by level
+    // multi-active states, level by level; table entries hold byte offsets
+    // into this warp's shared region (host-computed, EnumSmem layout)
+    char* smb = reinterpret_cast<char*>(sm);
     for (int k = 2; k <= GM; ++k) {
       const int e = a.level_off[k];
       const bool keep = k < GM;
       for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
-        const StateDesc d = a.desc[i];
-        const int x = d.xz & 0xff, z = d.xz >> 8;
-        const double c = (d.sib < HP ? 0.0 : coup[d.sib - HP]) + sP[x * HP + z];
-        const double r = tab[d.par] + su[z] + c;
+        const int4 d = __ldg(a.sdesc + i);  // {parent rel, sibling coup, P[x][z], u[z]}
+        const double c = *reinterpret_cast<const double*>(smb + d.y) + *reinterpret_cast<const double*>(smb + d.z);
+        const double r = *reinterpret_cast<const double*>(smb + d.x) + *reinterpret_cast<const double*>(smb + d.w) + c;
         tab[i] = r;
         if (keep) coup[i - HP] = c;
         mx = fmax(mx, r);
@@ -418,31 +450,75 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
     const bool t1 = a.inv_T == 1.0;
     double z1 = 0.0, zt = 0.0;
-    if (lane == 0) {
-      z1 = exp(-mx);
-      zt = t1 ? z1 : exp(-mx * a.inv_T);
-    }
+    if (t1) {
+      // q = exp(rel − max). Terms below e^-32 of the largest state change no
+      // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
+      // (MUFU.EX2); the others — typically a few dozen — in fp64, compacted.
+      if (lane == 0) z1 = exp(-mx);
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const double e = exp(rel1[j] - mx);
-      z1 += e;
-      rel1[j] = t1 ? e : exp((rel1[j] - mx) * a.inv_T);
-      zt += rel1[j];
-    }
-    for (int i = lane; i < a.n_tab; i += 32) {
-      const double r = tab[i] - mx;
-      const double e = exp(r);
-      const double et = t1 ? e : exp(r * a.inv_T);
-      tab[i] = et;
-      if (i >= HP) {
-        z1 += e;
-        zt += et;
-      } else {
-        sqs[i] = et;
+      for (int j = 0; j < MAXJ; ++j) {
+        const double x = rel1[j] - mx;
+        const bool big = x >= -32.0;
+        double v = small_exp(x);
+        if (__any_sync(0xffffffffu, big))
+          if (big) v = exp(x);
+        rel1[j] = v;
+        z1 += v;
       }
+      int* queue = reinterpret_cast<int*>(coup);  // coup/part/outs are free here
+      int nq = 0;
+      for (int b0 = 0; b0 < a.n_tab; b0 += 32) {
+        const int i = b0 + lane;
+        bool big = false;
+        if (i < a.n_tab) {
+          const double x = tab[i] - mx;
+          big = x >= -32.0;
+          tab[i] = big ? x : small_exp(x);
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, big);
+        if (big) queue[nq + __popc(bm & ((1u << lane) - 1u))] = i;
+        nq += __popc(bm);
+      }
+      __syncwarp();
+      for (int e = lane; e < nq; e += 32) {
+        const int i = queue[e];
+        tab[i] = exp(tab[i]);
+      }
+      __syncwarp();
+      for (int i = lane; i < a.n_tab; i += 32) {
+        const double v = tab[i];
+        if (i >= HP)
+          z1 += v;
+        else
+          sqs[i] = v;
+      }
+      z1 = warp_sum(z1);
+      zt = z1;
+    } else {
+      if (lane == 0) {
+        z1 = exp(-mx);
+        zt = exp(-mx * a.inv_T);
+      }
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) {
+        z1 += exp(rel1[j] - mx);
+        rel1[j] = exp((rel1[j] - mx) * a.inv_T);
+        zt += rel1[j];
+      }
+      for (int i = lane; i < a.n_tab; i += 32) {
+        const double r = tab[i] - mx;
+        const double et = exp(r * a.inv_T);
+        tab[i] = et;
+        if (i >= HP) {
+          z1 += exp(r);
+          zt += et;
+        } else {
+          sqs[i] = et;
+        }
+      }
+      z1 = warp_sum(z1);
+      zt = warp_sum(zt);
     }
-    z1 = warp_sum(z1);
-    zt = t1 ? z1 : warp_sum(zt);
     const double lse_rel = mx + log(z1);
     const double base = a.base0 - y2 * a.inv2s;
     const double inv_z = 1.0 / zt;
@@ -466,7 +542,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         }
       }
       for (int i = HP + lane; i < a.n_tab; i += 32) {
-        const int ri = 1 + H + a.desc[i].dfs;
+        const int ri = 1 + H + a.dfs[i];
         if (ranks_before(tab[i], ri, bv, bi)) {
           bv = tab[i];
           bi = ri;
@@ -491,20 +567,34 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     for (int k = GM - 1; k >= 1; --k) {
       const int e = a.level_off[k];
       for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
-        const int2 ch = a.child[i];
-        double s = tab[i];
-        for (int c = ch.x; c < ch.x + ch.y; ++c) s += tab[c];
-        tab[i] = s;
+        const int2 ch = __ldg(a.child + i);
+        double s = tab[i], s1 = 0.0;
+        int c = ch.x;
+        const int ce = ch.x + ch.y;
+        for (; c + 1 < ce; c += 2) {
+          s += tab[c];
+          s1 += tab[c + 1];
+        }
+        if (c < ce) s += tab[c];
+        tab[i] = s + s1;
       }
       __syncwarp();
     }
 
-    // ---- gather ⟨s_p⟩ and ⟨s_p s_q⟩ over the prefix-tree nodes
+    // ---- gather ⟨s_p⟩ and ⟨s_p s_q⟩ over the prefix-tree nodes: lists of byte
+    // offsets, padded to multiples of 4 with the zero slot tab[n_tab]
     for (int k = lane; k < a.n_items; k += 32) {
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       const int e = a.item_off[k + 1];
-      for (int g = a.item_off[k]; g < e; ++g) s += tab[a.gather_idx[g]];
-      spart[k] = s;
+      const int4* gi = reinterpret_cast<const int4*>(a.gather_idx);
+      for (int g = a.item_off[k]; g < e; ++g) {
+        const int4 v = __ldg(gi + g);
+        s0 += *reinterpret_cast<const double*>(smb + v.x);
+        s1 += *reinterpret_cast<const double*>(smb + v.y);
+        s2 += *reinterpret_cast<const double*>(smb + v.z);
+        s3 += *reinterpret_cast<const double*>(smb + v.w);
+      }
+      spart[k] = (s0 + s1) + (s2 + s3);
     }
     __syncwarp();
     for (int o = lane; o < a.n_out; o += 32) {
@@ -515,24 +605,16 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     __syncwarp();
 
     // ---- ⟨s_n⟩ row: singleton mass for every unit; candidates then take their
-    // full marginal (linear_discrete.cpp:288-304)
+    // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
+    // Yᵀ⟨S⟩ GEMM from these rows.
     double* esrow = a.ES + (long long)n * a.Hp;
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const int h = lane + 32 * j;
-      if (h < H) {
-        const double qh = rel1[j] * inv_z;
-        es_acc[j] += qh;
-        esrow[h] = qh;
-      }
+      if (h < H) esrow[h] = rel1[j] * inv_z;
     }
     __syncwarp();
-    for (int p = lane; p < HP; p += 32) {
-      const uint32_t c = scand[p];
-      const double tot = souts[p];
-      esrow[c] = tot;
-      atomicAdd(a.s_multi + c, tot - sqs[p] * inv_z);
-    }
+    for (int p = lane; p < HP; p += 32) esrow[scand[p]] = souts[p];
     // candidate pairs (upper triangle: scand ascending ⇒ c_p < c_q)
     for (int o = HP + lane; o < a.n_out; o += 32) {
       // o − HP enumerates (p, q), p < q, row-major
@@ -547,47 +629,53 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     __syncwarp();
   }
 
-  double* wes = a.warp_es + (long long)gwarp * H;
-#pragma unroll
-  for (int j = 0; j < MAXJ; ++j) {
-    const int h = lane + 32 * j;
-    if (h < H) wes[h] = es_acc[j];
-  }
+  // per-CTA partial sums of Σ log Z_n and Σ ‖y_n‖² in fixed warp order
+  __syncthreads();
+  double* red = esm;
+  const int nw = blockDim.x >> 5;
   if (lane == 0) {
-    a.warp_scalars[2 * gwarp] = lse_acc;
-    a.warp_scalars[2 * gwarp + 1] = y2_acc;
+    red[2 * wib] = lse_acc;
+    red[2 * wib + 1] = y2_acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0, q = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      l += red[2 * w];
+      q += red[2 * w + 1];
+    }
+    a.warp_scalars[2 * blockIdx.x] = l;
+    a.warp_scalars[2 * blockIdx.x + 1] = q;
   }
 }
 
-// Split-K partial reduction of Yᵀ⟨S⟩ (fixed order ⇒ deterministic) into the
-// packed statistics buffer.
-__global__ void reduce_ysT_kernel(const double* __restrict__ part, int splits, long long split_stride,
-                                  int D, int H, int ldp, double* __restrict__ out) {
+// Split-K partial reduction (fixed order ⇒ deterministic) into the packed
+// statistics [ysT D·H | s H | ssT H·H | counts | y2 | logZ | points]:
+// Σ y⟨s⟩ᵀ from the GEMM partials, Σ⟨s⟩ (= diag Σ⟨ssᵀ⟩, v = 1) from its
+// fused column sums.
+__global__ void reduce_ysT_kernel(const double* __restrict__ part, const double* __restrict__ colsum, int splits,
+                                  long long split_stride, int D, int H, int ldp, double* __restrict__ stats,
+                                  long long off_s, long long off_ssT) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)D * H) return;
-  const int d = static_cast<int>(idx / H), h = static_cast<int>(idx % H);
-  double s = 0.0;
-  for (int z = 0; z < splits; ++z) s += part[z * split_stride + (long long)d * ldp + h];
-  out[idx] = s;
+  const long long DH = (long long)D * H;
+  if (idx < DH) {
+    const int d = static_cast<int>(idx / H), h = static_cast<int>(idx % H);
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[z * split_stride + (long long)d * ldp + h];
+    stats[idx] = s;
+  } else if (idx < DH + H) {
+    const int h = static_cast<int>(idx - DH);
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += colsum[(long long)z * ldp + h];
+    stats[off_s + h] = s;
+    stats[off_ssT + (long long)h * H + h] = s;
+  }
 }
 
-// Σ⟨s⟩, diag Σ⟨ssᵀ⟩, mirror of the upper triangle, value count, scalars.
-// Packed stats: [ysT D·H | s H | ssT H·H | counts | y2 | logZ | points].
-__global__ void finalize_stats_kernel(const double* __restrict__ warp_es, int nwarps,
-                                      const double* __restrict__ warp_scalars,
-                                      const double* __restrict__ s_multi, int H, long long npoints,
-                                      double* __restrict__ stats, long long off_s, long long off_ssT,
-                                      long long off_tail) {
-  double* s = stats + off_s;
+// Mirror of the upper triangle of Σ⟨ssᵀ⟩ and the scalars.
+__global__ void finalize_stats_kernel(int nctas, const double* __restrict__ cta_scalars, int H, long long npoints,
+                                      double* __restrict__ stats, long long off_ssT, long long off_tail) {
   double* ssT = stats + off_ssT;
-  for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < H; h += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < nwarps; ++w) acc += warp_es[(long long)w * H + h];
-    acc += s_multi[h];
-    s[h] = acc;
-    ssT[(long long)h * H + h] = acc;
-  }
-  // mirror: lower = upper
   const long long HH = (long long)H * H;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < HH; e += (long long)gridDim.x * blockDim.x) {
     const int i = static_cast<int>(e / H), j = static_cast<int>(e % H);
@@ -595,9 +683,9 @@ __global__ void finalize_stats_kernel(const double* __restrict__ warp_es, int nw
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     double l = 0.0, y2 = 0.0;
-    for (int w = threadIdx.x; w < nwarps; w += 32) {
-      l += warp_scalars[2 * w];
-      y2 += warp_scalars[2 * w + 1];
+    for (int w = threadIdx.x; w < nctas; w += 32) {
+      l += cta_scalars[2 * w];
+      y2 += cta_scalars[2 * w + 1];
     }
     l = warp_sum(l);
     y2 = warp_sum(y2);

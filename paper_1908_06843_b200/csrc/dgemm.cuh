@@ -31,6 +31,7 @@ struct GemmArgs {
   double alpha, beta;
   int kchunk;
   long long c_split_stride;
+  double* colsum = nullptr;  // optional [splits][N]: Σ_k B[k, n] per split (B_ROW only)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -142,6 +143,8 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, BK, WM, WN, A_ROW, B_ROW, STA
   }
 
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / k index
+  const bool colsum_cta = g.colsum != nullptr && blockIdx.y == 0;
+  double cs = 0.0;
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -152,6 +155,12 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, BK, WM, WN, A_ROW, B_ROW, STA
     }
     const double* As = smem + (kt % STAGES) * Cfg::kStageDoubles;
     const double* Bs = As + Cfg::kSizeA;
+    if constexpr (B_ROW) {
+      if (colsum_cta) {  // Σ_k B[k, n] of this split (e.g. Σ_n ⟨s_n⟩ beside Yᵀ⟨S⟩)
+#pragma unroll
+        for (int r = tid / BN; r < BK; r += Cfg::kThreads / BN) cs += Bs[r * Cfg::kLdB + tid % BN];
+      }
+    }
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[MI], b[NI];
@@ -192,6 +201,20 @@ __global__ void __launch_bounds__(DgemmCfg<BM, BN, BK, WM, WN, A_ROW, B_ROW, STA
         v.y += g.beta * o.y;
       }
       *dst = v;
+    }
+  }
+  if constexpr (B_ROW) {
+    if (colsum_cta) {  // fold the row groups in fixed order → colsum[z][n]
+      __syncthreads();
+      double* red = smem;
+      red[tid] = cs;
+      __syncthreads();
+      if (tid < BN) {
+        double s = 0.0;
+        for (int r = 0; r < Cfg::kThreads / BN; ++r) s += red[r * BN + tid];
+        const int n = n_base + tid;
+        if (n < g.N) g.colsum[(long long)blockIdx.z * g.N + n] = s;
+      }
     }
   }
 }

@@ -53,32 +53,36 @@ __global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long
   }
 }
 
-// Unblocked Cholesky of the kb×kb diagonal block at (k0,k0), in shared memory.
-__global__ void potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int kb, MstepScalars* sc) {
+// Right-looking Cholesky of the kb×kb diagonal block at (k0,k0) in shared
+// memory (a partial last block is padded with the identity). One column per
+// step: pivot, scale, rank-1 update of the trailing triangle.
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int kb,
+                                                         MstepScalars* sc) {
   __shared__ double L[kCholNb][kCholNb + 1];
   __shared__ int fail;
   const int tid = threadIdx.x;
-  for (int e = tid; e < kb * kb; e += blockDim.x) {
-    const int i = e / kb, j = e % kb;
-    L[i][j] = A[(long long)(k0 + i) * lda + k0 + j];
+  for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
+    const int i = e / kCholNb, j = e % kCholNb;
+    L[i][j] = (i < kb && j < kb) ? A[(long long)(k0 + i) * lda + k0 + j] : (i == j ? 1.0 : 0.0);
   }
   if (tid == 0) fail = sc->chol_failed;
   __syncthreads();
-  for (int j = 0; j < kb; ++j) {
+  for (int j = 0; j < kCholNb; ++j) {
     if (tid == 0) {
-      double s = L[j][j];
-      for (int k = 0; k < j; ++k) s -= L[j][k] * L[j][k];
-      if (!(s > 0.0) || !isfinite(s)) {
+      double d = L[j][j];
+      if (!(d > 0.0) || !isfinite(d)) {
         fail = 1;
-        s = 1.0;
+        d = 1.0;
       }
-      L[j][j] = sqrt(s);
+      L[j][j] = sqrt(d);
     }
     __syncthreads();
-    for (int i = j + 1 + tid; i < kb; i += blockDim.x) {
-      double t = L[i][j];
-      for (int k = 0; k < j; ++k) t -= L[i][k] * L[j][k];
-      L[i][j] = t / L[j][j];
+    const double inv = 1.0 / L[j][j];
+    if (tid > j && tid < kCholNb) L[tid][j] *= inv;
+    __syncthreads();
+    for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
+      const int i = e / kCholNb, k = e % kCholNb;
+      if (k > j && i >= k) L[i][k] -= L[i][j] * L[k][j];
     }
     __syncthreads();
   }
@@ -91,47 +95,47 @@ __global__ void potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int k
 
 // Row-wise triangular solves against the kb×kb lower block Lkk stored at
 // (k0,k0) of L (leading dim ldl), applied to rows [r0, r0+nrows) of X at
-// columns [c0, c0+kb):
+// columns [c0, c0+kb); one thread per row, the row held in registers (the
+// 64-wide block is fully unrolled, padded with the identity past kb):
 //   FWD_T:  x · Lkkᵀ = x_in  (forward substitution)   — Cholesky panel / Z = R·L⁻ᵀ
 //   BWD  :  x · Lkk  = x_in  (backward substitution)  — X = Z·L⁻¹
 template <bool FWD_T>
-__global__ void trsm_rows_kernel(const double* __restrict__ Lm, int ldl, int k0, int kb,
-                                 double* __restrict__ X, int ldx, int r0, int nrows, int c0) {
+__global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict__ Lm, int ldl, int k0, int kb,
+                                                        double* __restrict__ X, int ldx, int r0, int nrows, int c0) {
   __shared__ double L[kCholNb][kCholNb + 1];
-  extern __shared__ double xs[];  // [blockDim.x][kb + 1]
+  __shared__ double rinv[kCholNb];
   const int tid = threadIdx.x;
-  for (int e = tid; e < kb * kb; e += blockDim.x) {
-    const int i = e / kb, j = e % kb;
-    L[i][j] = Lm[(long long)(k0 + i) * ldl + k0 + j];
-  }
-  const int row0 = r0 + blockIdx.x * blockDim.x;
-  const int nr = min((int)blockDim.x, r0 + nrows - row0);
-  for (int e = tid; e < nr * kb; e += blockDim.x) {
-    const int r = e / kb, c = e % kb;
-    xs[r * (kb + 1) + c] = X[(long long)(row0 + r) * ldx + c0 + c];
+  for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
+    const int i = e / kCholNb, j = e % kCholNb;
+    L[i][j] = (i < kb && j < kb) ? Lm[(long long)(k0 + i) * ldl + k0 + j] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
-  if (tid < nr) {
-    double* x = xs + tid * (kb + 1);
-    if (FWD_T) {
-      for (int c = 0; c < kb; ++c) {
-        double s = x[c];
-        for (int t = 0; t < c; ++t) s -= x[t] * L[c][t];
-        x[c] = s / L[c][c];
-      }
-    } else {
-      for (int c = kb - 1; c >= 0; --c) {
-        double s = x[c];
-        for (int t = c + 1; t < kb; ++t) s -= x[t] * L[t][c];
-        x[c] = s / L[c][c];
-      }
+  if (tid < kCholNb) rinv[tid] = 1.0 / L[tid][tid];
+  __syncthreads();
+  const int row = r0 + blockIdx.x * blockDim.x + tid;
+  if (row >= r0 + nrows) return;
+  double* xr = X + (long long)row * ldx + c0;
+  double x[kCholNb];
+#pragma unroll
+  for (int c = 0; c < kCholNb; ++c) x[c] = c < kb ? xr[c] : 0.0;
+  if (FWD_T) {
+#pragma unroll
+    for (int c = 0; c < kCholNb; ++c) {
+      x[c] *= rinv[c];
+#pragma unroll
+      for (int t = c + 1; t < kCholNb; ++t) x[t] -= x[c] * L[t][c];
+    }
+  } else {
+#pragma unroll
+    for (int c = kCholNb - 1; c >= 0; --c) {
+      x[c] *= rinv[c];
+#pragma unroll
+      for (int t = 0; t < c; ++t) x[t] -= x[c] * L[c][t];
     }
   }
-  __syncthreads();
-  for (int e = tid; e < nr * kb; e += blockDim.x) {
-    const int r = e / kb, c = e % kb;
-    X[(long long)(row0 + r) * ldx + c0 + c] = xs[r * (kb + 1) + c];
-  }
+#pragma unroll
+  for (int c = 0; c < kCholNb; ++c)
+    if (c < kb) xr[c] = x[c];
 }
 
 // W ← X unless the factorisation failed (then the previous W is kept).
