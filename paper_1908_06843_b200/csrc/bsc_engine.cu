@@ -64,8 +64,11 @@ constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
 // GEMM2  Yᵀ·⟨S⟩:      M = Dp, N = Hp, K = points (split-K).
 #define GEMM2_CFG 128, 64, 16, 32, 32, false, true, 3
 // M-step products (C −= A·Bᵀ and C −= A·B).
-#define SYRK_CFG 64, 64, 16, 32, 32, true, false, 3
-#define SOLVE_CFG 64, 64, 16, 32, 32, true, true, 3
+// (32×32 tiles: these products are skinny — N = 64 — so small tiles give the CTAs)
+#define SYRK_CFG 32, 32, 16, 16, 16, true, false, 3
+#define SOLVE_CFG 32, 32, 16, 16, 16, true, true, 3
+// Gram WᵀW: M = N = H, K = Dp.
+#define GRAM_CFG 64, 64, 16, 32, 32, false, true, 3
 
 }  // namespace
 
@@ -94,7 +97,8 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   build_template();
 
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
-  d_g_ = dalloc<double>((size_t)H_ * H_, "G");
+  d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
+  d_trace_part_ = dalloc<double>(2 * kTraceCtas, "trace partials");
   d_wnorm_ = dalloc<double>(H_, "wnorm");
   d_gdiag_ = dalloc<double>(H_, "gdiag");
   d_stats_ = dalloc<double>(lay_.count(), "stats");
@@ -118,12 +122,13 @@ BscEngine::~BscEngine() {
   for (void* p : {(void*)d_desc_, (void*)d_dfs_, (void*)d_child_, (void*)d_level_off_, (void*)d_gather_, (void*)d_item_off_, (void*)d_out_off_, (void*)d_y_, (void*)d_y2_,
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
-                  (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, d_msc_})
+                  (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  if (mstep_exec_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(mstep_exec_));
   if (own_stream_ && stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -384,12 +389,20 @@ void BscEngine::get_params(double* w, double* pi, double* sigma2) {
 }
 
 void BscEngine::refresh_gram() {
-  auto s = static_cast<cudaStream_t>(stream_);
-  dim3 grid((H_ + 127) / 128, H_);
-  gram_exact_kernel<<<grid, 128, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, d_wnorm_, d_gdiag_);
-  ck(cudaGetLastError(), "gram");
-  ++launches_;
+  enqueue_gram(stream_);
   gram_fresh_ = true;
+}
+
+// G = WᵀW on the DMMA GEMM, then the diagonal (selection scores) recomputed in
+// the oracle's left-to-right order.
+void BscEngine::enqueue_gram(void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  const int H = static_cast<int>(H_);
+  GemmArgs g{H, H, Dp_, d_w_, Hp_, d_w_, Hp_, d_g_, Hp_, 1.0, 0.0, Dp_, 0};
+  ck(launch_dgemm<GRAM_CFG>(g, 1, s), "gram gemm");
+  gram_diag_exact_kernel<<<(H_ + 127) / 128, 128, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, Hp_, d_wnorm_, d_gdiag_);
+  ck(cudaGetLastError(), "gram");
+  launches_ += 2;
 }
 
 void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
@@ -504,9 +517,42 @@ void BscEngine::check_err() {
   if (err & kErrNonFiniteLogJoint) throw Error(kNumeric, "log_sum_exp: empty support");
 }
 
+// The M-step is a fixed sequence of ~40 small launches for a given (D, H):
+// it runs eagerly once, is then captured into a CUDA graph and replayed.
 void BscEngine::mstep() {
   ck(cudaSetDevice(device_), "set device");
   auto s = static_cast<cudaStream_t>(stream_);
+  auto* sc = static_cast<MstepScalars*>(d_msc_);
+  if (mstep_exec_) {
+    ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(mstep_exec_), s), "mstep graph");
+    launches_ += mstep_nodes_;
+  } else if (mstep_calls_++ == 0) {
+    const int before = launches_;
+    enqueue_mstep(s);
+    mstep_nodes_ = launches_ - before;
+  } else {
+    cudaStream_t cap;
+    ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+    ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+    const int before = launches_;
+    enqueue_mstep(cap);
+    cudaGraph_t graph;
+    ck(cudaStreamEndCapture(cap, &graph), "end capture");
+    cudaGraphExec_t exec;
+    ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    mstep_exec_ = exec;
+    mstep_nodes_ = launches_ - before;
+    launches_ = before;
+    ck(cudaGraphLaunch(exec, s), "mstep graph");
+    launches_ += mstep_nodes_;
+  }
+  finish_mstep();
+}
+
+void BscEngine::enqueue_mstep(void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
   auto* sc = static_cast<MstepScalars*>(d_msc_);
   const int H = static_cast<int>(H_), D = static_cast<int>(D_);
   mstep_prepare_kernel<<<64, 256, 0, s>>>(d_stats_, lay_.off_ssT(), D, H, Hp_, d_bm_, d_x_, Hp_, sc);
@@ -518,7 +564,7 @@ void BscEngine::mstep() {
     potrf_diag_kernel<<<1, 256, 0, s>>>(d_bm_, Hp_, k0, kb, sc);
     ++launches_;
     if (k1 < H) {
-      const int rows = H - k1, tpb = 128;
+      const int rows = H - k1, tpb = 32;
       trsm_rows_kernel<true><<<(rows + tpb - 1) / tpb, tpb, 0, s>>>(d_bm_, Hp_, k0, kb, d_bm_, Hp_,
                                                                                    k1, rows, k0);
       GemmArgs g{rows, rows, kb, d_bm_ + (long long)k1 * Hp_ + k0, Hp_, d_bm_ + (long long)k1 * Hp_ + k0, Hp_,
@@ -529,7 +575,7 @@ void BscEngine::mstep() {
   }
   ck(cudaGetLastError(), "cholesky");
   // X·L·Lᵀ = Σy⟨s⟩ᵀ: forward (Z·Lᵀ = R) then backward (X·L = Z), column blocks
-  const int tpb = 128, nblk = (D + tpb - 1) / tpb;
+  const int tpb = 32, nblk = (D + tpb - 1) / tpb;
   for (int j0 = 0; j0 < H; j0 += kCholNb) {
     const int kb = std::min(kCholNb, H - j0);
     if (j0 > 0) {
@@ -554,11 +600,19 @@ void BscEngine::mstep() {
   }
   ck(cudaGetLastError(), "solve");
   commit_w_kernel<<<64, 256, 0, s>>>(d_x_, Hp_, d_w_, Hp_, D, H, sc);
-  refresh_gram();  // Gram of W' (next E-step's G, exact order) also feeds t3
-  mstep_traces_kernel<<<1, 1024, 0, s>>>(d_w_, Hp_, d_g_, d_stats_, lay_.off_ssT(), D, H, sc);
-  mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, sc);
+  // Gram of W' (the next E-step's G; exact diagonal) also feeds t3
+  enqueue_gram(s);
+  mstep_traces_kernel<<<kTraceCtas, 256, 0, s>>>(d_w_, Hp_, d_g_, Hp_, d_stats_, lay_.off_ssT(), D, H,
+                                                  d_trace_part_);
+  mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, d_trace_part_, sc);
   ck(cudaGetLastError(), "mstep scalars");
   launches_ += 3;
+}
+
+void BscEngine::finish_mstep() {
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto* sc = static_cast<MstepScalars*>(d_msc_);
+  gram_fresh_ = true;
   if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[6]), s), "event");
   // one synchronisation per iteration: new π, σ², the (all-reduced) F and the
   // E-step error flag come back together

@@ -82,6 +82,9 @@ class BscEngine {
   void refresh_gram();
   void launch_enumerate(double temperature, bool cands, bool infer);
   void check_err();
+  void enqueue_mstep(void* stream);
+  void enqueue_gram(void* stream);
+  void finish_mstep();
 
   uint32_t D_, H_, hprime_, gamma_;
   uint64_t cap_;
@@ -118,10 +121,12 @@ class BscEngine {
   double* d_map_mass_ = nullptr;
   int* d_err_ = nullptr;
   // M-step workspace
-  double *d_bm_ = nullptr, *d_x_ = nullptr;
+  double *d_bm_ = nullptr, *d_x_ = nullptr, *d_trace_part_ = nullptr;
   void* d_msc_ = nullptr;
   void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // pinned
   double last_F_ = 0.0;
+  void* mstep_exec_ = nullptr;  // cudaGraphExec_t of the captured M-step
+  int mstep_calls_ = 0, mstep_nodes_ = 0;
 
   int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
   bool timing_ = false;

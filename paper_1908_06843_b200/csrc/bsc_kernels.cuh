@@ -42,25 +42,23 @@ __device__ __forceinline__ bool ranks_before(double v1, int i1, double v2, int i
 }
 
 // ---------------------------------------------------------------------------
-// K0: Gram matrix G = WᵀW in the oracle's order (acc = 0; acc += w·w over d,
-// separately rounded), plus column norms for the selection error bound.
-// One thread per (i, j); W is L2-resident (≤ 4.6 MB at c3).
-__global__ void gram_exact_kernel(const double* __restrict__ W, int D, int H, int ldw,
-                                  double* __restrict__ G, double* __restrict__ wnorm,
-                                  double* __restrict__ gdiag) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  if (j >= H) return;
+// K0: the Gram diagonal G_hh = Σ_d W_dh² in the oracle's order (acc = 0;
+// acc += w·w over d, separately rounded) — the selection scores use it, so it
+// must match bit for bit — plus column norms for the selection error bound.
+// The off-diagonal Gram (pairwise log-joint terms, t3) comes from the DMMA GEMM.
+__global__ void gram_diag_exact_kernel(const double* __restrict__ W, int D, int H, int ldw,
+                                       double* __restrict__ G, int ldg, double* __restrict__ wnorm,
+                                       double* __restrict__ gdiag) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= H) return;
   double acc = 0.0;
   for (int d = 0; d < D; ++d) {
-    const double a = W[(long long)d * ldw + i], b = W[(long long)d * ldw + j];
-    acc = __dadd_rn(acc, __dmul_rn(a, b));
+    const double a = W[(long long)d * ldw + h];
+    acc = __dadd_rn(acc, __dmul_rn(a, a));
   }
-  G[(long long)i * H + j] = acc;
-  if (i == j) {
-    wnorm[i] = sqrt(acc);
-    gdiag[i] = acc;
-  }
+  G[(long long)h * ldg + h] = acc;
+  wnorm[h] = sqrt(acc);
+  gdiag[h] = acc;
 }
 
 // e^x for x < −32 (only ever added to sums whose largest term is 1): fp32
@@ -111,7 +109,7 @@ struct EnumArgs {
   const double* Y;
   const double* W;
   const double* B;
-  const double* G;
+  const double* G;        // H × Hp
   const double* wnorm;
   const double* gdiag;    // diag(G), contiguous
   const double* y2;       // N: ‖y_n‖², computed once per dataset
@@ -412,7 +410,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     for (int e = lane; e < HP * HP; e += 32) {
       const int p = e / HP, q = e - p * HP;
-      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * H + scand[q]];
+      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
     }
     __syncwarp();
 

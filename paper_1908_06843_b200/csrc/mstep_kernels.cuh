@@ -55,12 +55,14 @@ __global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long
 
 // Right-looking Cholesky of the kb×kb diagonal block at (k0,k0) in shared
 // memory (a partial last block is padded with the identity). One column per
-// step: pivot, scale, rank-1 update of the trailing triangle.
+// step: pivot (one thread), scale, rank-1 update of the trailing triangle by a
+// 16×16 thread grid (each thread a fixed 4×4 set of entries).
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int kb,
                                                          MstepScalars* sc) {
   __shared__ double L[kCholNb][kCholNb + 1];
+  __shared__ double rinv;
   __shared__ int fail;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
     const int i = e / kCholNb, j = e % kCholNb;
     L[i][j] = (i < kb && j < kb) ? A[(long long)(k0 + i) * lda + k0 + j] : (i == j ? 1.0 : 0.0);
@@ -74,16 +76,26 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
         fail = 1;
         d = 1.0;
       }
-      L[j][j] = sqrt(d);
+      d = sqrt(d);
+      L[j][j] = d;
+      rinv = 1.0 / d;
     }
     __syncthreads();
-    const double inv = 1.0 / L[j][j];
-    if (tid > j && tid < kCholNb) L[tid][j] *= inv;
+    if (tid > j && tid < kCholNb) L[tid][j] *= rinv;
     __syncthreads();
-    for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
-      const int i = e / kCholNb, k = e % kCholNb;
-      if (k > j && i >= k) L[i][k] -= L[i][j] * L[k][j];
+    double li[4], lk[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      li[a] = L[ty + 16 * a][j];
+      lk[a] = L[tx + 16 * a][j];
     }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, k = tx + 16 * b;
+        if (k > j && i >= k) L[i][k] -= li[a] * lk[b];
+      }
     __syncthreads();
   }
   for (int e = tid; e < kb * kb; e += blockDim.x) {
@@ -110,7 +122,7 @@ __global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict
     L[i][j] = (i < kb && j < kb) ? Lm[(long long)(k0 + i) * ldl + k0 + j] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
-  if (tid < kCholNb) rinv[tid] = 1.0 / L[tid][tid];
+  for (int c = tid; c < kCholNb; c += blockDim.x) rinv[c] = 1.0 / L[c][c];
   __syncthreads();
   const int row = r0 + blockIdx.x * blockDim.x + tid;
   if (row >= r0 + nrows) return;
@@ -149,16 +161,20 @@ __global__ void commit_w_kernel(const double* __restrict__ X, int ldx, double* _
   }
 }
 
-// t2 = Σ W'∘Σy⟨s⟩ᵀ, t3 = Σ (W'ᵀW')∘Σ⟨ssᵀ⟩ (:366-368), single CTA, fixed order.
-__global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ G,
+// Partial sums of t2 = Σ W'∘Σy⟨s⟩ᵀ and t3 = Σ (W'ᵀW')∘Σ⟨ssᵀ⟩ (:366-368):
+// one pair per CTA, folded in fixed order by mstep_scalars_kernel.
+constexpr int kTraceCtas = 64;
+__global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ G, int ldg,
                                     const double* __restrict__ stats, long long off_ssT, int D, int H,
-                                    MstepScalars* sc) {
+                                    double* __restrict__ partial) {
   __shared__ double red[2][32];
   double t2 = 0.0, t3 = 0.0;
   const long long DH = (long long)D * H, HH = (long long)H * H;
-  for (long long e = threadIdx.x; e < DH; e += blockDim.x)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < DH; e += stride)
     t2 += W[(e / H) * ldw + e % H] * stats[e];
-  for (long long e = threadIdx.x; e < HH; e += blockDim.x) t3 += G[e] * stats[off_ssT + e];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < HH; e += stride)
+    t3 += G[(e / H) * ldg + e % H] * stats[off_ssT + e];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     t2 += __shfl_xor_sync(0xffffffffu, t2, o);
@@ -175,14 +191,21 @@ __global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const
       a += red[0][w];
       b += red[1][w];
     }
-    sc->t2 = a;
-    sc->t3 = b;
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
   }
 }
 
 // σ²' = max((t1 − 2t2 + t3)/(N·D), 1e-12), π' = clip(counts/(N·H), 1e-6, 1−1e-6)
 __global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long off_tail, int D, int H,
-                                     MstepScalars* sc) {
+                                     const double* __restrict__ partial, MstepScalars* sc) {
+  double t2 = 0.0, t3 = 0.0;
+  for (int c = 0; c < kTraceCtas; ++c) {
+    t2 += partial[2 * c];
+    t3 += partial[2 * c + 1];
+  }
+  sc->t2 = t2;
+  sc->t3 = t3;
   const double n = stats[off_tail + 3];
   const double t1 = stats[off_tail + 1];
   const double s2 = (t1 - 2.0 * sc->t2 + sc->t3) / (n * static_cast<double>(D));
