@@ -89,6 +89,10 @@ int prsp_bsc_gpu_inference(prsp_bsc_gpu* ctx, double* map_states, double* map_ma
 int prsp_bsc_gpu_set_timing(prsp_bsc_gpu* ctx, int on);
 int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6);
 int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out);
+/* Enumerator cycles per phase (summed over warps) of the last E-step when the
+ * process runs with BSC_ENUM_PROFILE=1, else zeros: scores, selection, log-joint
+ * terms, state log-joints, exp, MAP, subtree + moment sums, output + loop. */
+int prsp_bsc_gpu_enum_phase_cycles(prsp_bsc_gpu* ctx, uint64_t* out8);
 
 /* ---- fixtures (CPU; the reference's generators, same draw order) -------- */
 int prsp_bsc_bars_generate(uint32_t size, uint64_t n, double prob, double amplitude, double noise, int max_mode,

@@ -44,6 +44,7 @@ SIGNATURES = {
     "prsp_bsc_gpu_set_timing": [_ptr, _int],
     "prsp_bsc_gpu_timings": [_ptr, _ptr],
     "prsp_bsc_gpu_launches": [_ptr, C.POINTER(_int)],
+    "prsp_bsc_gpu_enum_phase_cycles": [_ptr, _ptr],
     "prsp_bsc_bars_generate": [_u32, _u64, _dbl, _dbl, _dbl, _int, _u64, _ptr, _ptr],
     "prsp_bsc_generate": [_u32, _u32, _ptr, _dbl, _dbl, _u64, _u64, _ptr],
     "prsp_bsc_random_dictionary": [_u32, _u32, _u64, _dbl, _ptr],

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 
@@ -95,6 +96,7 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   Hp_ = round_up(static_cast<int>(H_), 8);
   lay_ = StatsLayout{static_cast<long long>(D_), static_cast<long long>(H_)};
   build_template();
+  if (const char* e = std::getenv("BSC_ENUM_PROFILE")) prof_on_ = e[0] == '1';
 
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
@@ -119,7 +121,8 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
 
 BscEngine::~BscEngine() {
   cudaSetDevice(device_);
-  for (void* p : {(void*)d_desc_, (void*)d_dfs_, (void*)d_child_, (void*)d_level_off_, (void*)d_gather_, (void*)d_item_off_, (void*)d_out_off_, (void*)d_y_, (void*)d_y2_,
+  for (void* p : {(void*)d_desc_, (void*)d_dfs_, (void*)d_level_off_, d_sched_, (void*)d_sched_ent_,
+                  d_sched_split_, (void*)d_y_, (void*)d_y2_,
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_})
@@ -139,6 +142,15 @@ void BscEngine::set_stream(void* stream) {
 }
 
 void BscEngine::sync() { ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)), "sync"); }
+
+void BscEngine::enum_phase_cycles(unsigned long long* out8) {
+  std::memset(out8, 0, 8 * sizeof(unsigned long long));
+  if (!d_prof_) return;
+  ck(cudaMemcpyAsync(out8, d_prof_, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     static_cast<cudaStream_t>(stream_)),
+     "profile D2H");
+  sync();
+}
 
 // StateTemplate (truncation.cpp:95-151): multi-active supports of size
 // 2..γ over candidate positions, depth-first, prefixes first. The gather
@@ -219,7 +231,12 @@ void BscEngine::build_template() {
   // layout does not depend on the gather sizes)
   const EnumSmem L0 = EnumSmem::make(hp, n_tab, n_coup, 0, 0, 0);
   auto tab_off = [&](int i) { return (L0.tab + i) * 8; };
-  std::vector<int4> desc(n_tab, int4{0, 0, 0, 0});
+  // packed {parent rel | sibling coup << 16, P[x][z] | u[z] << 16}, offsets / 8
+  auto w16 = [](int byte_off) {
+    if (byte_off < 0 || byte_off / 8 > 0xffff) throw Error(kConfig, "gpu: state template exceeds the 16-bit table range");
+    return static_cast<unsigned>(byte_off / 8);
+  };
+  std::vector<uint2> desc(n_tab, uint2{0, 0});
   std::vector<int> dfs_idx(n_tab, -1);
   std::vector<int2> child(hp + n_coup, int2{0, 0});
   for (int i = hp; i < n_tab; ++i) {
@@ -230,8 +247,11 @@ void BscEngine::build_template() {
     std::vector<int> sib(A.begin(), A.end() - 1);
     sib.push_back(z);
     const int si = index_of.at(key(sib));
-    desc[i] = int4{tab_off(index_of.at(key(A))), si < hp ? tab_off(n_tab) : (L0.coup + si - hp) * 8,
-                   (L0.P + x * hp + z) * 8, (L0.u + z) * 8};
+    const int par_off = tab_off(index_of.at(key(A)));
+    const int sib_off = si < hp ? tab_off(n_tab) : (L0.coup + si - hp) * 8;
+    const int p_off = (L0.P + x * (2 * hp - x - 1) / 2 + (z - x - 1)) * 8;  // strict upper triangle
+    const int u_off = (L0.u + z) * 8;
+    desc[i] = uint2{w16(par_off) | (w16(sib_off) << 16), w16(p_off) | (w16(u_off) << 16)};
     dfs_idx[i] = dfs_of.at(key(S));
   }
   for (int i = 0; i < hp + n_coup; ++i) {
@@ -264,36 +284,109 @@ void BscEngine::build_template() {
     lists[q].push_back(i);
     for (size_t a = 0; a + 1 < S.size(); ++a) lists[pair_index(S[a], q)].push_back(i);
   }
-  size_t tot = 0;
-  for (auto& l : lists) tot += l.size();
-  // items of ≈ tot/96 entries, each padded to a multiple of 4 with the zero
-  // slot n_tab so the kernel reads indices as int4; item_off counts int4s
-  const size_t chunk = std::max<size_t>(8, ((tot + 95) / 96 + 3) / 4 * 4);
-  std::vector<int> gather, item_off{0}, out_off{0};
-  for (auto& l : lists) {
-    for (size_t s = 0; s < l.size(); s += chunk) {
-      const size_t e = std::min(l.size(), s + chunk);
-      for (size_t g = s; g < e; ++g) gather.push_back(tab_off(l[g]));
-      while (gather.size() % 4) gather.push_back(tab_off(n_tab));
-      item_off.push_back(static_cast<int>(gather.size() / 4));
+  // Balanced lane schedules (see SchedDesc): the lists of every output are
+  // concatenated in output order and cut into 32 equal runs. An output whose
+  // list lies inside one run is written directly by that lane; one that spans
+  // runs leaves a partial per run in consecutive slots, summed afterwards.
+  std::vector<SchedDesc> sched;
+  std::vector<uint32_t> ent;  // packed: src/8 | (int16 dst code) << 16
+  std::vector<int4> splits;
+  constexpr int R = kSchedRuns;
+  constexpr int kSlots = 2 * kSchedRuns;  // ≤ R−1 split outputs, ≤ 2R−2 partials
+  const EnumSmem L1 = EnumSmem::make(hp, n_tab, n_coup, kSlots, n_out_, 0);
+  if (L1.tab != L0.tab || L1.coup != L0.coup) throw Error(kInternal, "state template layout mismatch");
+  auto add_schedule = [&](const std::vector<std::vector<int>>& ls, const std::vector<int>& targets) {
+    std::vector<std::pair<int, int>> seq;  // (byte offset, output)
+    for (size_t o = 0; o < ls.size(); ++o) {
+      if (ls[o].empty()) seq.emplace_back(tab_off(n_tab), static_cast<int>(o));  // writes 0
+      for (int v : ls[o]) seq.emplace_back(v, static_cast<int>(o));
     }
-    out_off.push_back(static_cast<int>(item_off.size() - 1));
+    const int T = static_cast<int>(seq.size());
+    const int iters = (T + R - 1) / R;
+    std::vector<int> first_lane(ls.size(), 1 << 30), last_lane(ls.size(), -1);
+    for (int j = 0; j < T; ++j) {
+      const int o = seq[j].second, l = j / iters;
+      first_lane[o] = std::min(first_lane[o], l);
+      last_lane[o] = std::max(last_lane[o], l);
+    }
+    auto pack = [&](int src, int dst) {
+      if (dst >= 0) dst = static_cast<int>(w16(dst));  // target offset / 8 (< 2^15 checked below)
+      if (dst > 0x7fff || dst < -0x7fff) throw Error(kConfig, "gpu: schedule destination out of range");
+      return w16(src) | (static_cast<uint32_t>(static_cast<uint16_t>(static_cast<int16_t>(dst))) << 16);
+    };
+    std::vector<uint32_t> rows(static_cast<size_t>(iters) * R, pack(tab_off(n_tab), -1));
+    std::vector<int> slot_begin(ls.size(), -1);
+    int slot = 0;
+    for (int l = 0; l < R; ++l) {
+      const int b = l * iters, e = std::min(T, b + iters);
+      for (int j = b; j < e; ++j) {
+        const int o = seq[j].second;
+        const bool last = j + 1 == e || seq[j + 1].second != o;
+        int dst = -1;
+        if (last) {
+          if (first_lane[o] == last_lane[o]) {
+            dst = targets[o];
+          } else {
+            if (slot_begin[o] < 0) slot_begin[o] = slot;
+            dst = -(slot + 2);
+            ++slot;
+          }
+        }
+        rows[static_cast<size_t>(j - b) * R + l] = pack(seq[j].first, dst);
+      }
+    }
+    SchedDesc sd{iters, static_cast<int>(ent.size() / R), 0, static_cast<int>(splits.size())};
+    for (size_t o = 0; o < ls.size(); ++o)
+      if (first_lane[o] != last_lane[o]) {
+        const int nparts = last_lane[o] - first_lane[o] + 1;
+        splits.push_back(int4{targets[o], slot_begin[o], slot_begin[o] + nparts, 0});
+        ++sd.n_split;
+      }
+    if (sd.n_split >= R || slot > kSlots) throw Error(kInternal, "state template: schedule split overflow");
+    ent.insert(ent.end(), rows.begin(), rows.end());
+    sched.push_back(sd);
+  };
+  // subtree sums, level γ−1 down to 1: sub(A) = q(A) + Σ_{children} sub(c)
+  for (int k = static_cast<int>(gamma_) - 1; k >= 1; --k) {
+    std::vector<std::vector<int>> ls;
+    std::vector<int> tg;
+    for (int i = level_off[k - 1]; i < level_off[k]; ++i) {
+      std::vector<int> l{tab_off(i)};
+      for (int c = 0; c < child[i].y; ++c) l.push_back(tab_off(child[i].x + c));
+      ls.push_back(l);
+      tg.push_back(tab_off(i));
+    }
+    add_schedule(ls, tg);
   }
-  n_items_ = static_cast<int>(item_off.size() - 1);
-  d_desc_ = dalloc<int4>(desc.size(), "desc");
+  {  // moments into souts
+    std::vector<std::vector<int>> ls(lists.size());
+    std::vector<int> tg(lists.size());
+    for (size_t o = 0; o < lists.size(); ++o) {
+      for (int i : lists[o]) ls[o].push_back(tab_off(i));
+      tg[o] = (L1.outs + static_cast<int>(o)) * 8;
+    }
+    add_schedule(ls, tg);
+  }
+  n_slots_ = kSlots;
+
+  // 16-byte multiples: the kernel stages both tables into shared memory as int4
+  while ((desc.size() * sizeof(uint2)) % 16) desc.push_back(uint2{0, 0});
+  while ((ent.size() * sizeof(uint32_t)) % 16) ent.push_back(0);
+  desc_bytes_ = static_cast<int>(desc.size() * sizeof(uint2));
+  ent_bytes_ = static_cast<int>(ent.size() * sizeof(uint32_t));
+  d_desc_ = dalloc<uint2>(desc.size(), "desc");
   d_dfs_ = dalloc<int>(dfs_idx.size(), "dfs");
   ck(cudaMemcpy(d_dfs_, dfs_idx.data(), dfs_idx.size() * 4, cudaMemcpyHostToDevice), "dfs");
-  d_child_ = dalloc<int2>(child.size(), "child");
   d_level_off_ = dalloc<int>(level_off.size(), "level_off");
-  d_gather_ = dalloc<int>(gather.size(), "gather");
-  d_item_off_ = dalloc<int>(item_off.size(), "item_off");
-  d_out_off_ = dalloc<int>(out_off.size(), "out_off");
-  ck(cudaMemcpy(d_desc_, desc.data(), desc.size() * sizeof(int4), cudaMemcpyHostToDevice), "desc");
-  if (!child.empty()) ck(cudaMemcpy(d_child_, child.data(), child.size() * sizeof(int2), cudaMemcpyHostToDevice), "child");
+  d_sched_ = dalloc<SchedDesc>(sched.size(), "schedules");
+  d_sched_ent_ = dalloc<uint32_t>(ent.size(), "schedule entries");
+  d_sched_split_ = dalloc<int4>(splits.size(), "schedule splits");
+  ck(cudaMemcpy(d_desc_, desc.data(), desc_bytes_, cudaMemcpyHostToDevice), "desc");
   ck(cudaMemcpy(d_level_off_, level_off.data(), level_off.size() * 4, cudaMemcpyHostToDevice), "level_off");
-  if (!gather.empty()) ck(cudaMemcpy(d_gather_, gather.data(), gather.size() * 4, cudaMemcpyHostToDevice), "gather");
-  ck(cudaMemcpy(d_item_off_, item_off.data(), item_off.size() * 4, cudaMemcpyHostToDevice), "item_off");
-  ck(cudaMemcpy(d_out_off_, out_off.data(), out_off.size() * 4, cudaMemcpyHostToDevice), "out_off");
+  ck(cudaMemcpy(d_sched_, sched.data(), sched.size() * sizeof(SchedDesc), cudaMemcpyHostToDevice), "sched");
+  if (!ent.empty()) ck(cudaMemcpy(d_sched_ent_, ent.data(), ent_bytes_, cudaMemcpyHostToDevice), "ent");
+  if (!splits.empty())
+    ck(cudaMemcpy(d_sched_split_, splits.data(), splits.size() * sizeof(int4), cudaMemcpyHostToDevice), "splits");
 }
 
 void BscEngine::ensure_work(uint64_t n) {
@@ -321,14 +414,31 @@ void BscEngine::ensure_work(uint64_t n) {
   d_part_ = dalloc<double>((size_t)splits_ * part_stride_, "splitK partials");
 
   // enumerator launch shape: per-warp shared region, as many warps as fit
-  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_items_, n_out_, static_cast<int>(H_));
+  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_slots_, n_out_, static_cast<int>(H_));
   const int per_warp = L.total * 8;
-  int warps = 8;
-  while (warps > 1 && warps * per_warp > 200 * 1024) warps /= 2;
   if (per_warp > 200 * 1024)
     throw Error(kConfig, "gpu: state template too large for shared memory (" + std::to_string(n_multi_) + " states)");
+  // Pick (warps per CTA, staged tables) maximising resident warps per SM
+  // (registers cap it at 16 warps: 128 regs/thread), staged first on ties.
+  const int smem_cap = 227 * 1024 - 1024;
+  const int table_bytes = desc_bytes_ + ent_bytes_;
+  int best_w = 1, best_total = 0;
+  bool best_stage = false;
+  for (int stage = 1; stage >= 0; --stage)
+    for (int w : {8, 4, 2, 1}) {
+      const int cta_bytes = w * per_warp + (stage ? table_bytes : 0);
+      if (cta_bytes > smem_cap) continue;
+      const int ctas = std::min(smem_cap / cta_bytes, 16 / w);
+      if (ctas * w > best_total) {
+        best_total = ctas * w;
+        best_w = w;
+        best_stage = stage != 0;
+      }
+    }
+  const int warps = best_w;
+  stage_tables_ = best_stage;
   enum_block_ = warps * 32;
-  enum_smem_ = warps * per_warp;
+  enum_smem_ = warps * per_warp + (stage_tables_ ? table_bytes : 0);
   const int maxj = maxj_for(H_);
   const void* fn = enum_fn(maxj);
   ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "enum smem attr");
@@ -436,17 +546,23 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
   a.map_mass = infer ? d_map_mass_ : nullptr;
   a.map_state = infer ? d_map_state_ : nullptr;
   a.err = d_err_;
-  a.sdesc = static_cast<const int4*>(d_desc_);
+  if (prof_on_) {
+    if (!d_prof_) d_prof_ = dalloc<unsigned long long>(8, "enumerate phase profile");
+    ck(cudaMemsetAsync(d_prof_, 0, 8 * sizeof(unsigned long long), s), "zero profile");
+  }
+  a.prof = prof_on_ ? static_cast<unsigned long long*>(d_prof_) : nullptr;
+  a.sdesc = static_cast<const uint2*>(d_desc_);
+  a.stage_desc_bytes = stage_tables_ ? desc_bytes_ : 0;
+  a.stage_ent_bytes = stage_tables_ ? ent_bytes_ : 0;
   a.dfs = d_dfs_;
-  a.child = static_cast<const int2*>(d_child_);
   a.level_off = d_level_off_;
   a.n_multi = n_multi_;
   a.n_tab = n_tab_;
   a.n_coup = n_coup_;
-  a.gather_idx = d_gather_;
-  a.item_off = d_item_off_;
-  a.out_item_off = d_out_off_;
-  a.n_items = n_items_;
+  a.sched = static_cast<const SchedDesc*>(d_sched_);
+  a.sched_ent = static_cast<const uint32_t*>(d_sched_ent_);
+  a.sched_split = static_cast<const int4*>(d_sched_split_);
+  a.n_slots = n_slots_;
   a.n_out = n_out_;
   a.log_pi = log_p1;
   a.dlp = log_p1 - log_p0;

@@ -73,6 +73,9 @@ class BscEngine {
   int enum_warps() const { return enum_warps_total_; }
   const EngineTimings& timings() const { return t_; }
   void set_timing(bool on) { timing_ = on; }
+  // per-phase cycle accounting inside the enumerator (profiling builds of a
+  // run: BSC_ENUM_PROFILE=1); summed over warps, last E-step
+  void enum_phase_cycles(unsigned long long* out8);
   int kernel_launches_last_step() const { return launches_; }
   void sync();
 
@@ -99,13 +102,16 @@ class BscEngine {
   bool have_params_ = false, gram_fresh_ = false;
 
   // template tables
-  int n_multi_ = 0, n_tab_ = 0, n_coup_ = 0, n_items_ = 0, n_out_ = 0;
+  int n_multi_ = 0, n_tab_ = 0, n_coup_ = 0, n_slots_ = 0, n_out_ = 0;
+  int desc_bytes_ = 0, ent_bytes_ = 0;  // table sizes (16-byte multiples)
+  bool stage_tables_ = false;           // staged into shared memory per CTA
   std::vector<uint64_t> dfs_masks_;  // multi-active supports in reference order
   void* d_desc_ = nullptr;
   int* d_dfs_ = nullptr;
-  void* d_child_ = nullptr;
   int* d_level_off_ = nullptr;
-  int *d_gather_ = nullptr, *d_item_off_ = nullptr, *d_out_off_ = nullptr;
+  void* d_sched_ = nullptr;  // SchedDesc[γ]: subtree levels γ−1 … 1, then the moment gather
+  void* d_sched_ent_ = nullptr;  // int2 entries, [rows][32]
+  void* d_sched_split_ = nullptr;  // int4 {target, first slot, end slot, -} per split output
 
   uint64_t n_ = 0, cap_n_ = 0;
   double *d_y_ = nullptr, *d_w_ = nullptr, *d_g_ = nullptr, *d_wnorm_ = nullptr, *d_gdiag_ = nullptr;
@@ -130,6 +136,8 @@ class BscEngine {
 
   int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
   bool timing_ = false;
+  bool prof_on_ = false;
+  void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;
   void* ev_[8] = {};

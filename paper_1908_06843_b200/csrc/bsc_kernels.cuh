@@ -70,6 +70,37 @@ __device__ __forceinline__ double small_exp(double x) {
   return static_cast<double>(r);
 }
 
+// e^x for x ≤ 0 in fp64 (the posterior weights exp(lj − max)): Cody–Waite
+// reduction x = k·ln2 + r, |r| ≤ ln2/2, Taylor polynomial of degree 13
+// (truncation < 5e-18 relative), and 2^k applied as two exact power-of-two
+// factors so gradual underflow rounds once (x < −745.2 gives 0). About 1 ulp;
+// ~20 instructions against ~45 for the general-range exp().
+__device__ __forceinline__ double exp_nonpos(double x) {
+  x = fmax(x, -746.0);
+  const double k = rint(x * 1.4426950408889634);
+  double r = fma(k, -6.93147180559945286227e-01, x);
+  r = fma(k, -2.319046813846299558e-17, r);
+  double p = 1.6059043836821613e-10;           // 1/13!
+  p = fma(p, r, 2.08767569878680990e-09);      // 1/12!
+  p = fma(p, r, 2.50521083854417188e-08);      // 1/11!
+  p = fma(p, r, 2.75573192239858907e-07);      // 1/10!
+  p = fma(p, r, 2.75573192239858883e-06);      // 1/9!
+  p = fma(p, r, 2.48015873015873016e-05);      // 1/8!
+  p = fma(p, r, 1.98412698412698413e-04);      // 1/7!
+  p = fma(p, r, 1.38888888888888894e-03);      // 1/6!
+  p = fma(p, r, 8.33333333333333322e-03);      // 1/5!
+  p = fma(p, r, 4.16666666666666644e-02);      // 1/4!
+  p = fma(p, r, 1.66666666666666657e-01);      // 1/3!
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int ki = static_cast<int>(k);
+  const int k1 = ki >> 1, k2 = ki - k1;
+  const double s1 = __longlong_as_double(static_cast<long long>(k1 + 1023) << 52);
+  const double s2 = __longlong_as_double(static_cast<long long>(k2 + 1023) << 52);
+  return (p * s1) * s2;
+}
+
 // ‖y_n‖² per data point (linear_discrete.cpp:242), once per resident dataset:
 // one warp per row.
 __global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int D, int ldy,
@@ -100,9 +131,70 @@ __global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int
 // sums of the prefix tree (children of A are contiguous in the next level):
 //   sub(A) = q(A) + Σ_children sub(child)
 //   ⟨s_p⟩  = Σ_{A: max A = p} sub(A),  ⟨s_p s_q⟩ = Σ_{A: max A = q, p ∈ A} sub(A).
-struct StateDesc {
-  int par, sib, xz, dfs;  // xz = x | z << 8; dfs = index in the reference order
+//
+// Sums over node lists (children of a node, nodes feeding an output) run as a
+// balanced per-lane schedule: the host concatenates the lists in output order
+// and cuts the sequence into 32 equal runs; lane l walks run l, accumulating,
+// and at the end of each list segment stores the partial into a slot; a
+// second pass adds each output's (1–2) slots and writes the result.
+// Entry encoding (int2 {src, dst}): src = byte offset of the value to add;
+// dst = −1 continue, ≥ 0 segment complete in this lane: store acc·scale at
+// byte offset dst, ≤ −2 segment split across lanes: store acc in slot −dst−2.
+// Split outputs (at most one per lane boundary) are finished after a
+// __syncwarp from their slot ranges.
+struct SchedDesc {
+  int iters;      // entries per lane
+  int row_base;   // first row (of 32 int2) in sched_ent
+  int n_split;    // outputs split across lanes (≤ 31)
+  int split_base; // sched_split[split_base + l] = {target byte offset, first slot, end slot}
 };
+
+// Packed entry (uint32): low 16 bits = source offset / 8, high 16 bits =
+// signed destination code (see above; a target offset is stored / 8).
+__device__ __forceinline__ void seg_flush(uint32_t v, double& acc, char* smb, double* spart, double scale) {
+  const int dst = static_cast<int>(static_cast<short>(v >> 16));
+  if (dst >= 0) {
+    *reinterpret_cast<double*>(smb + dst * 8) = acc * scale;
+    acc = 0.0;
+  } else if (dst <= -2) {
+    spart[-dst - 2] = acc;
+    acc = 0.0;
+  }
+}
+__device__ __forceinline__ double ent_src(const char* smb, uint32_t v) {
+  return *reinterpret_cast<const double*>(smb + (v & 0xffffu) * 8);
+}
+
+// 128 runs: lane l walks runs l, l+32, l+64, l+96 interleaved — four
+// independent accumulation chains per lane.
+constexpr int kSchedRuns = 128;
+
+__device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t* ent,
+                                             const int4* __restrict__ split, char* smb, double* spart, double scale,
+                                             int lane) {
+  const uint32_t* e = ent + (long long)sd.row_base * kSchedRuns + lane;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int it = 0; it < sd.iters; ++it) {
+    const uint32_t* r = e + it * kSchedRuns;
+    const uint32_t v0 = r[0], v1 = r[32], v2 = r[64], v3 = r[96];
+    a0 += ent_src(smb, v0);
+    a1 += ent_src(smb, v1);
+    a2 += ent_src(smb, v2);
+    a3 += ent_src(smb, v3);
+    seg_flush(v0, a0, smb, spart, scale);
+    seg_flush(v1, a1, smb, spart, scale);
+    seg_flush(v2, a2, smb, spart, scale);
+    seg_flush(v3, a3, smb, spart, scale);
+  }
+  __syncwarp();
+  for (int k = lane; k < sd.n_split; k += 32) {
+    const int4 sp = __ldg(split + sd.split_base + k);
+    double s = 0.0;
+    for (int j = sp.y; j < sp.z; ++j) s += spart[j];
+    *reinterpret_cast<double*>(smb + sp.x) = s * scale;
+  }
+  __syncwarp();
+}
 
 struct EnumArgs {
   int N, D, H, Dp, Hp, hprime, gamma;
@@ -120,17 +212,20 @@ struct EnumArgs {
   double* map_mass;       // inference outputs or null
   int* map_state;         // N: index of the MAP state in reference order
   int* err;
-  const int4* sdesc;      // [n_tab] byte offsets {rel(parent), coup(sibling), P[x][z], u[z]}; < hprime unused
+  unsigned long long* prof;  // [8] cycles per phase (profiling mode) or null
+  // [n_tab] offsets/8 (u16) {rel(parent), coup(sibling) | P[x][z], u[z]}; < hprime unused
+  const uint2* sdesc;
+  // shared-memory staging of sdesc / sched_ent per CTA (bytes, 0 = read global)
+  int stage_desc_bytes, stage_ent_bytes;
   const int* dfs;         // [n_tab] index of the state in the reference (DFS) order
-  const int2* child;      // [n_coup + hprime]: (first child, count) for levels < γ
   const int* level_off;   // [gamma + 1]: level k occupies [level_off[k-1], level_off[k])
   int n_multi, n_tab, n_coup;  // n_tab = hprime + n_multi; n_coup = states of levels 2..γ-1
-  // gather work items: item k sums the node values at byte offsets
-  // gather_idx[4·item_off[k] .. 4·item_off[k+1])
-  const int* gather_idx;
-  const int* item_off;
-  const int* out_item_off;  // output o owns items [out_item_off[o], out_item_off[o+1])
-  int n_items, n_out;       // n_out = hprime + hprime·(hprime−1)/2
+  // schedules: sched[0 .. γ−2] the subtree levels γ−1 … 1, sched[γ−1] the
+  // moment gather into souts (n_out = hprime + hprime·(hprime−1)/2 outputs)
+  const SchedDesc* sched;
+  const uint32_t* sched_ent;  // packed entries [rows][kSchedRuns]
+  const int4* sched_split;
+  int n_slots, n_out;
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
 };
@@ -143,17 +238,22 @@ struct EnumSmem {
   __host__ __device__ static EnumSmem make(int hprime, int n_tab, int n_coup, int n_items, int n_out, int h) {
     EnumSmem s;
     s.u = 0;
-    s.P = s.u + hprime;
-    s.qs = s.P + hprime * hprime;
-    s.pool_v = s.qs + hprime;
-    s.pool_i = s.pool_v + kPoolCap + 2;
-    s.cand = s.pool_i + kPoolCap / 2 + 1;   // ints packed 2 per double
-    s.tab = s.cand + (hprime + 1) / 2 + 1;  // uint32 candidates packed 2 per double
-    s.coup = s.tab + n_tab + 1;             // tab[n_tab] = 0: the padding slot of the gather lists
-    s.part = s.coup + n_coup;
+    s.P = s.u + hprime;                           // strict upper triangle, row-major
+    s.qs = s.P + hprime * (hprime - 1) / 2 + 1;
+    s.cand = s.qs + hprime;                       // uint32 candidates packed 2 per double
+    s.tab = s.cand + (hprime + 1) / 2 + 1;
+    // the selection pool (values + indices) is dead before the table is filled
+    s.pool_v = s.tab;
+    s.pool_i = s.pool_v + kPoolCap + 2;          // ints packed 2 per double
+    int tab_end = s.tab + n_tab + 1;              // tab[n_tab] = 0: padding slot of the lists
+    if (tab_end < s.pool_i + kPoolCap / 2 + 1) tab_end = s.pool_i + kPoolCap / 2 + 1;
+    s.coup = tab_end;
+    // coup (rel pass), the exp compaction queue (n_tab ints) and the schedule
+    // slots + outputs (moment pass) are live one after the other: they overlay
+    s.part = s.coup;
     s.outs = s.part + n_items;
     s.total = s.outs + n_out;
-    // the exp compaction queue (n_tab ints) overlays coup/part/outs
+    if (s.total < s.coup + n_coup) s.total = s.coup + n_coup;
     if (s.total < s.coup + n_tab / 2 + 1) s.total = s.coup + n_tab / 2 + 1;
     if (s.total < h + 2) s.total = h + 2;  // end-of-kernel CTA reduction reuses the regions
     s.total = (s.total + 1) & ~1;
@@ -279,8 +379,25 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   const int wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_items, a.n_out, a.H);
-  double* sm = esm + (long long)wib * L.total;
+  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
+  // The state descriptors and schedule entries are the same for every point:
+  // staged once per CTA in shared memory when they fit (else read from L1/L2).
+  const uint2* sdesc = a.sdesc;
+  const uint32_t* sent = a.sched_ent;
+  const int stage_bytes = a.stage_desc_bytes + a.stage_ent_bytes;
+  if (stage_bytes > 0) {
+    char* cta = reinterpret_cast<char*>(esm);
+    const int4* src0 = reinterpret_cast<const int4*>(a.sdesc);
+    const int4* src1 = reinterpret_cast<const int4*>(a.sched_ent);
+    int4* dst0 = reinterpret_cast<int4*>(cta);
+    int4* dst1 = reinterpret_cast<int4*>(cta + a.stage_desc_bytes);
+    for (int i = threadIdx.x; i < a.stage_desc_bytes / 16; i += blockDim.x) dst0[i] = __ldg(src0 + i);
+    for (int i = threadIdx.x; i < a.stage_ent_bytes / 16; i += blockDim.x) dst1[i] = __ldg(src1 + i);
+    __syncthreads();
+    sdesc = reinterpret_cast<const uint2*>(cta);
+    sent = reinterpret_cast<const uint32_t*>(cta + a.stage_desc_bytes);
+  }
+  double* sm = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + stage_bytes) + (long long)wib * L.total;
   double* su = sm + L.u;
   double* sP = sm + L.P;
   double* tab = sm + L.tab;
@@ -298,10 +415,17 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   for (int h = lane; h < H; h += 32) bound = fmax(bound, a.wnorm[h]);
   bound = warp_max(bound);
   const int row_lines = (a.Hp * 8 + 127) / 128;
-  if (lane == 0) tab[a.n_tab] = 0.0;
-  __syncwarp();
+  // optional per-phase cycle accounting (engine profiling mode only)
+  long long t_last = a.prof ? clock64() : 0;
+#define ENUM_PHASE(k)                                                                   \
+  if (a.prof) {                                                                         \
+    const long long t_ = clock64();                                                     \
+    if (lane == 0) atomicAdd(a.prof + (k), static_cast<unsigned long long>(t_ - t_last)); \
+    t_last = t_;                                                                        \
+  }
 
   for (int n = gwarp; n < a.N; n += nwarps) {
+    ENUM_PHASE(7);
     const double* y = a.Y + (long long)n * a.Dp;
     const double* brow = a.B + (long long)n * a.Hp;
     {  // pull the B row two points ahead into L2 while this point is processed
@@ -341,6 +465,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     mag = warp_max(mag) + fabs(a.log_pi);
     const double eps = 2.5 * a.inv2s * a.eps_dot * bound * sqrt(y2) * 1.0001 + 0x1.0p-46 * mag;
 
+    ENUM_PHASE(0);
     // ---- top-H' by (score desc, index asc), truncation.cpp:38-57
     if (HP < H) {
       double t, nv;
@@ -400,6 +525,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     if (a.cand_out)
       for (int p = lane; p < HP; p += 32) a.cand_out[(long long)n * HP + p] = scand[p];
 
+    ENUM_PHASE(1);
     // ---- unary / pairwise log-joint terms relative to the zero state:
     // lj(S) − base = Σ_a [dlp + inv2s(2b_a − G_aa)] + Σ_{a<c} (−2 inv2s G_ac)
     for (int p = lane; p < HP; p += 32) {
@@ -410,10 +536,13 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     for (int e = lane; e < HP * HP; e += 32) {
       const int p = e / HP, q = e - p * HP;
-      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
+      if (p < q)  // strict upper triangle, row-major
+        sP[p * (2 * HP - p - 1) / 2 + (q - p - 1)] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
     }
+    if (lane == 0) tab[a.n_tab] = 0.0;  // zero slot (the selection pool overlays the table)
     __syncwarp();
 
+    ENUM_PHASE(2);
     // singletons over all H units and the zero state (rel = 0)
     double(&rel1)[MAXJ] = f;  // scores are no longer needed: reuse the registers
     double mx = 0.0;
@@ -426,16 +555,36 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // multi-active states, level by level; table entries hold byte offsets
     // into this warp's shared region (host-computed, EnumSmem layout)
     char* smb = reinterpret_cast<char*>(sm);
+    // Four states per lane per iteration, all loads before any store (a
+    // level only reads earlier levels): four independent chains.
+    const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
     for (int k = 2; k <= GM; ++k) {
       const int e = a.level_off[k];
       const bool keep = k < GM;
-      for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
-        const int4 d = __ldg(a.sdesc + i);  // {parent rel, sibling coup, P[x][z], u[z]}
-        const double c = *reinterpret_cast<const double*>(smb + d.y) + *reinterpret_cast<const double*>(smb + d.z);
-        const double r = *reinterpret_cast<const double*>(smb + d.x) + *reinterpret_cast<const double*>(smb + d.w) + c;
-        tab[i] = r;
-        if (keep) coup[i - HP] = c;
-        mx = fmax(mx, r);
+      for (int i0 = a.level_off[k - 1] + lane; i0 < e; i0 += 128) {
+        uint2 d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + 32 * u;
+          d[u] = i < e ? sdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
+        }
+        double c[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // {parent rel | sibling coup, P[x][z] | u[z]} as offsets / 8
+          c[u] = *reinterpret_cast<const double*>(smb + (d[u].x >> 16) * 8) +
+                 *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
+          r[u] = *reinterpret_cast<const double*>(smb + (d[u].x & 0xffffu) * 8) +
+                 *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) + c[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + 32 * u;
+          if (i < e) {
+            tab[i] = r[u];
+            if (keep) coup[i - HP] = c[u];
+            mx = fmax(mx, r[u]);
+          }
+        }
       }
       __syncwarp();
     }
@@ -445,42 +594,55 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       continue;
     }
 
+    ENUM_PHASE(3);
     // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
     const bool t1 = a.inv_T == 1.0;
     double z1 = 0.0, zt = 0.0;
     if (t1) {
-      // q = exp(rel − max). Terms below e^-32 of the largest state change no
+      // q = exp_nonpos(rel − max). Terms below e^-32 of the largest state change no
       // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
       // (MUFU.EX2); the others — typically a few dozen — in fp64, compacted.
-      if (lane == 0) z1 = exp(-mx);
+      if (lane == 0) z1 = exp_nonpos(-mx);
 #pragma unroll
-      for (int j = 0; j < MAXJ; ++j) {
-        const double x = rel1[j] - mx;
-        const bool big = x >= -32.0;
-        double v = small_exp(x);
-        if (__any_sync(0xffffffffu, big))
-          if (big) v = exp(x);
-        rel1[j] = v;
-        z1 += v;
+      for (int j = 0; j < MAXJ; ++j) {  // singletons: fp64, independent (unrolled)
+        rel1[j] = exp_nonpos(rel1[j] - mx);
+        z1 += rel1[j];
       }
       int* queue = reinterpret_cast<int*>(coup);  // coup/part/outs are free here
       int nq = 0;
-      for (int b0 = 0; b0 < a.n_tab; b0 += 32) {
-        const int i = b0 + lane;
-        bool big = false;
-        if (i < a.n_tab) {
-          const double x = tab[i] - mx;
-          big = x >= -32.0;
-          tab[i] = big ? x : small_exp(x);
+      for (int b0 = 0; b0 < a.n_tab; b0 += 128) {
+        double x[4];
+        bool big[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = b0 + 32 * u + lane;
+          x[u] = i < a.n_tab ? tab[i] - mx : -INFINITY;
+          big[u] = x[u] >= -32.0;
         }
-        const unsigned bm = __ballot_sync(0xffffffffu, big);
-        if (big) queue[nq + __popc(bm & ((1u << lane) - 1u))] = i;
-        nq += __popc(bm);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = b0 + 32 * u + lane;
+          if (i < a.n_tab) tab[i] = big[u] ? x[u] : small_exp(x[u]);
+          const unsigned bm = __ballot_sync(0xffffffffu, big[u]);
+          if (big[u]) queue[nq + __popc(bm & ((1u << lane) - 1u))] = i;
+          nq += __popc(bm);
+        }
       }
       __syncwarp();
-      for (int e = lane; e < nq; e += 32) {
-        const int i = queue[e];
-        tab[i] = exp(tab[i]);
+      for (int e0 = lane; e0 < nq; e0 += 128) {  // fp64 for the compacted terms, 4 chains
+        int idx[4];
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + 32 * u;
+          idx[u] = e < nq ? queue[e] : -1;
+          x[u] = idx[u] >= 0 ? tab[idx[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = exp_nonpos(x[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (idx[u] >= 0) tab[idx[u]] = x[u];
       }
       __syncwarp();
       for (int i = lane; i < a.n_tab; i += 32) {
@@ -494,21 +656,21 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       zt = z1;
     } else {
       if (lane == 0) {
-        z1 = exp(-mx);
-        zt = exp(-mx * a.inv_T);
+        z1 = exp_nonpos(-mx);
+        zt = exp_nonpos(-mx * a.inv_T);
       }
 #pragma unroll
       for (int j = 0; j < MAXJ; ++j) {
-        z1 += exp(rel1[j] - mx);
-        rel1[j] = exp((rel1[j] - mx) * a.inv_T);
+        z1 += exp_nonpos(rel1[j] - mx);
+        rel1[j] = exp_nonpos((rel1[j] - mx) * a.inv_T);
         zt += rel1[j];
       }
       for (int i = lane; i < a.n_tab; i += 32) {
         const double r = tab[i] - mx;
-        const double et = exp(r * a.inv_T);
+        const double et = exp_nonpos(r * a.inv_T);
         tab[i] = et;
         if (i >= HP) {
-          z1 += exp(r);
+          z1 += exp_nonpos(r);
           zt += et;
         } else {
           sqs[i] = et;
@@ -526,6 +688,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     __syncwarp();
 
+    ENUM_PHASE(4);
     if (a.map_state) {
       // MAP state (linear_discrete.cpp:314-316: first maximum in reference
       // order: zero, singletons 0..H−1, then multi-active in DFS order)
@@ -561,47 +724,14 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       }
     }
 
-    // subtree sums, bottom-up (level γ nodes are leaves)
-    for (int k = GM - 1; k >= 1; --k) {
-      const int e = a.level_off[k];
-      for (int i = a.level_off[k - 1] + lane; i < e; i += 32) {
-        const int2 ch = __ldg(a.child + i);
-        double s = tab[i], s1 = 0.0;
-        int c = ch.x;
-        const int ce = ch.x + ch.y;
-        for (; c + 1 < ce; c += 2) {
-          s += tab[c];
-          s1 += tab[c + 1];
-        }
-        if (c < ce) s += tab[c];
-        tab[i] = s + s1;
-      }
-      __syncwarp();
-    }
+    ENUM_PHASE(5);
+    // subtree sums, bottom-up (level γ nodes are leaves): sub(A) = q(A) + Σ
+    // children, one balanced schedule per level; then ⟨s_p⟩ and ⟨s_p s_q⟩ as
+    // sums of subtree values (the last schedule, scaled by 1/Z)
+    for (int k = 0; k < GM - 1; ++k) run_schedule(a.sched[k], sent, a.sched_split, smb, spart, 1.0, lane);
+    run_schedule(a.sched[GM - 1], sent, a.sched_split, smb, spart, inv_z, lane);
 
-    // ---- gather ⟨s_p⟩ and ⟨s_p s_q⟩ over the prefix-tree nodes: lists of byte
-    // offsets, padded to multiples of 4 with the zero slot tab[n_tab]
-    for (int k = lane; k < a.n_items; k += 32) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      const int e = a.item_off[k + 1];
-      const int4* gi = reinterpret_cast<const int4*>(a.gather_idx);
-      for (int g = a.item_off[k]; g < e; ++g) {
-        const int4 v = __ldg(gi + g);
-        s0 += *reinterpret_cast<const double*>(smb + v.x);
-        s1 += *reinterpret_cast<const double*>(smb + v.y);
-        s2 += *reinterpret_cast<const double*>(smb + v.z);
-        s3 += *reinterpret_cast<const double*>(smb + v.w);
-      }
-      spart[k] = (s0 + s1) + (s2 + s3);
-    }
-    __syncwarp();
-    for (int o = lane; o < a.n_out; o += 32) {
-      double s = 0.0;
-      for (int k = a.out_item_off[o]; k < a.out_item_off[o + 1]; ++k) s += spart[k];
-      souts[o] = s * inv_z;
-    }
-    __syncwarp();
-
+    ENUM_PHASE(6);
     // ---- ⟨s_n⟩ row: singleton mass for every unit; candidates then take their
     // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
     // Yᵀ⟨S⟩ GEMM from these rows.

@@ -242,6 +242,16 @@ int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out) {
   });
 }
 
+int prsp_bsc_gpu_enum_phase_cycles(prsp_bsc_gpu* ctx, uint64_t* out8) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out8, "out8");
+    unsigned long long v[8];
+    ctx->engine.enum_phase_cycles(v);
+    for (int i = 0; i < 8; ++i) out8[i] = v[i];
+  });
+}
+
 int prsp_bsc_bars_generate(uint32_t size, uint64_t n, double prob, double amplitude, double noise, int max_mode,
                            uint64_t seed, double* y_out, double* truth_out) {
   return guarded([&] {

@@ -16,3 +16,15 @@ m.load(y)
 for _ in range(steps):
     p = m.step(p).params
 print("done", name, n, steps, p.pi, p.sigma2)
+
+import numpy as np  # noqa: E402
+
+from paper_1908_06843_b200 import _native as N  # noqa: E402
+
+cyc = np.zeros(8, np.uint64)
+N.call("prsp_bsc_gpu_enum_phase_cycles", m.handle, cyc.ctypes.data_as(__import__("ctypes").c_void_p))
+if cyc.sum():
+    names = ["scores", "select", "uP", "rel", "exp", "map", "sub+gather", "out+loop"]
+    tot = cyc.sum()
+    print("enumerate phase cycles/point/warp:", {k: round(float(v) / n, 1) for k, v in zip(names, cyc)})
+    print("shares:", {k: f"{100 * float(v) / tot:.1f}%" for k, v in zip(names, cyc)})
