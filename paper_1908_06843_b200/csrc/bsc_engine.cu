@@ -112,6 +112,14 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
   ck(cudaMallocHost(&h_tail_, 4 * sizeof(double)), "pinned");
   ck(cudaMallocHost(&h_err_, sizeof(int)), "pinned");
+  cudaStream_t cs;
+  ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+  copy_stream_ = cs;
+  for (auto& e : chunk_ev_) {
+    cudaEvent_t ev;
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    e = ev;
+  }
   for (auto& e : ev_) {
     cudaEvent_t ev;
     ck(cudaEventCreate(&ev), "event");
@@ -132,6 +140,9 @@ BscEngine::~BscEngine() {
   for (auto& e : ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (mstep_exec_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(mstep_exec_));
+  for (auto& e : chunk_ev_)
+    if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  if (copy_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(copy_stream_));
   if (own_stream_ && stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
 }
 
@@ -451,6 +462,7 @@ void BscEngine::ensure_work(uint64_t n) {
   enum_warps_total_ = enum_ctas_ * warps;
   d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
   d_warp_sc_ = dalloc<double>((size_t)enum_ctas_ * 2, "cta_scalars");
+  colsum_chunks_ = 1;
 }
 
 void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
@@ -470,6 +482,26 @@ void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
                                                                        d_y2_);
   ck(cudaGetLastError(), "y2");
   n_ = n;
+}
+
+// Model::step with a host DataSet (the call em.cpp:39 makes): the data are
+// copied in chunks on the copy stream, each chunk's E-step starting as soon
+// as it lands, then the M-step. Returns F.
+double BscEngine::step_streamed(const double* y_host, uint64_t n, double temperature, uint64_t chunk) {
+  if (n == 0) throw Error(kData, "run: empty dataset");
+  if (!have_params_) throw Error(kConfig, "bsc: parameters not set");
+  if (!(temperature >= 1.0) || !std::isfinite(temperature))
+    throw Error(kConfig, "temperature must be finite and >= 1");
+  ck(cudaSetDevice(device_), "set device");
+  const uint64_t prev_cap = cap_n_;
+  ensure_work(n);
+  if (n < prev_cap && n_ > n)
+    ck(cudaMemsetAsync(d_y_ + n * Dp_, 0, (cap_n_ - n) * Dp_ * sizeof(double), static_cast<cudaStream_t>(stream_)),
+       "clear Y");
+  n_ = n;
+  estep_chunked(temperature, false, y_host, chunk);
+  mstep();
+  return last_F_;
 }
 
 void BscEngine::set_params(const double* w, double pi, double sigma2) {
@@ -515,7 +547,8 @@ void BscEngine::enqueue_gram(void* stream) {
   launches_ += 2;
 }
 
-void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
+void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
+                                 int chunk) {
   auto s = static_cast<cudaStream_t>(stream_);
   // value_table (:71-97, BSC :75-79) and the per-shard constants (:219-227),
   // computed on the host with the same libm as the reference.
@@ -525,26 +558,26 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer) {
   const double zero_prior = static_cast<double>(H_) * log_p0;
 
   EnumArgs a{};
-  a.N = static_cast<int>(n_);
+  a.N = static_cast<int>(rows);
   a.D = D_;
   a.H = H_;
   a.Dp = Dp_;
   a.Hp = Hp_;
   a.hprime = hprime_;
   a.gamma = gamma_;
-  a.Y = d_y_;
+  a.Y = d_y_ + off * Dp_;
   a.W = d_w_;
-  a.B = d_b_;
+  a.B = d_b_ + off * Hp_;
   a.G = d_g_;
   a.wnorm = d_wnorm_;
   a.gdiag = d_gdiag_;
-  a.y2 = d_y2_;
-  a.ES = d_es_;
+  a.y2 = d_y2_ + off;
+  a.ES = d_es_ + off * Hp_;
   a.ssT = d_stats_ + lay_.off_ssT();
-  a.warp_scalars = d_warp_sc_;
-  a.cand_out = cands ? d_cand_ : nullptr;
-  a.map_mass = infer ? d_map_mass_ : nullptr;
-  a.map_state = infer ? d_map_state_ : nullptr;
+  a.warp_scalars = d_warp_sc_ + (size_t)chunk * enum_ctas_ * 2;
+  a.cand_out = cands ? d_cand_ + off * hprime_ : nullptr;
+  a.map_mass = infer ? d_map_mass_ + off : nullptr;
+  a.map_state = infer ? d_map_state_ + off : nullptr;
   a.err = d_err_;
   if (prof_on_) {
     if (!d_prof_) d_prof_ = dalloc<unsigned long long>(8, "enumerate phase profile");
@@ -588,39 +621,88 @@ void BscEngine::estep(double temperature, bool want_candidates) {
   auto ev = [&](int i) {
     if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[i]), s), "event");
   };
+  estep_chunked(temperature, want_candidates, nullptr, n_);
+}
+
+// The E-step runs over row chunks: K1 (Y·W), the enumerator and K4 (Yᵀ⟨S⟩,
+// accumulated into the same split-K partials, chunk after chunk) per chunk.
+// With `host_y`, chunk c+1 is copied host→device on the copy stream while
+// chunk c computes (the reference-facing step that takes host data).
+void BscEngine::estep_chunked(double temperature, bool want_candidates, const double* host_y, uint64_t chunk) {
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto ev = [&](int i) {
+    if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[i]), s), "event");
+  };
+  const uint64_t n = n_;
+  chunk = std::max<uint64_t>(2, std::min<uint64_t>(n, chunk));
+  chunk = (chunk + 1) & ~1ull;  // even row offsets (K4 reads K in pairs)
+  const int nchunks = static_cast<int>((n + chunk - 1) / chunk);
+  if (nchunks > kMaxChunks) throw Error(kConfig, "gpu: too many E-step chunks");
+  if (nchunks > colsum_chunks_) {
+    dfree(d_warp_es_);
+    dfree(d_warp_sc_);
+    d_warp_es_ = dalloc<double>((size_t)nchunks * splits_ * Hp_, "split-K column sums");
+    d_warp_sc_ = dalloc<double>((size_t)nchunks * enum_ctas_ * 2, "cta scalars");
+    colsum_chunks_ = nchunks;
+  }
   launches_ = 0;
   ev(0);
   if (!gram_fresh_) refresh_gram();
   ev(1);
-  {  // K1: B = Y·W
-    GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, d_w_, Hp_, d_b_, Hp_, 1.0, 0.0, Dp_, 0};
-    ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
-    ++launches_;
-  }
-  ev(2);
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
-  launch_enumerate(temperature, want_candidates, false);
-  ev(3);
-  {  // K4: Σ y⟨s⟩ᵀ = Yᵀ·ES (+ fused Σ⟨s⟩), split-K over points, reduced in fixed order
-    const int rows = static_cast<int>((n_ + 1) & ~1ull);
-    int kchunk = (rows + splits_ - 1) / splits_;
-    kchunk = (kchunk + 1) & ~1;
-    const int splits = (rows + kchunk - 1) / kchunk;
-    GemmArgs g{Dp_, Hp_, rows, d_y_, Dp_, d_es_, Hp_, d_part_, Hp_, 1.0, 0.0, kchunk, part_stride_, d_warp_es_};
-    ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
-    const long long DH = (long long)D_ * H_;
-    reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits, part_stride_, D_, H_, Hp_,
-                                                             d_stats_, lay_.off_s(), lay_.off_ssT());
-    ck(cudaGetLastError(), "reduce ysT");
-    launches_ += 2;
+  ck(cudaMemsetAsync(d_part_, 0, (size_t)splits_ * part_stride_ * 8, s), "zero partials");
+  ck(cudaMemsetAsync(d_warp_es_, 0, (size_t)nchunks * splits_ * Hp_ * 8, s), "zero colsums");
+  auto cs = static_cast<cudaStream_t>(copy_stream_);
+  if (host_y) {
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(chunk_ev_[kMaxChunks]), s), "event");
+    ck(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(chunk_ev_[kMaxChunks]), 0), "wait");
+    for (int c = 0; c < nchunks; ++c) {  // all copies queued up front; compute waits per chunk
+      const uint64_t off = c * chunk, rows = std::min<uint64_t>(chunk, n - off);
+      ck(cudaMemcpy2DAsync(d_y_ + off * Dp_, (size_t)Dp_ * 8, host_y + off * D_, (size_t)D_ * 8, (size_t)D_ * 8, rows,
+                           cudaMemcpyHostToDevice, cs),
+         "upload Y chunk");
+      ck(cudaEventRecord(static_cast<cudaEvent_t>(chunk_ev_[c]), cs), "event");
+    }
   }
-  ev(4);
+  for (int c = 0; c < nchunks; ++c) {
+    const uint64_t off = c * chunk, rows = std::min<uint64_t>(chunk, n - off);
+    if (host_y) {
+      ck(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(chunk_ev_[c]), 0), "wait chunk");
+      row_sqnorm_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
+          d_y_ + off * Dp_, static_cast<long long>(rows), D_, Dp_, d_y2_ + off);
+      ++launches_;
+    }
+    {  // K1: B = Y·W
+      GemmArgs g{static_cast<int>(rows), Hp_, Dp_, d_y_ + off * Dp_, Dp_, d_w_, Hp_, d_b_ + off * Hp_, Hp_,
+                 1.0, 0.0, Dp_, 0};
+      ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
+      ++launches_;
+    }
+    if (c == 0) ev(2);
+    launch_enumerate(temperature, want_candidates, false, off, rows, c);
+    if (c == 0) ev(3);
+    {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES over this chunk (+ fused Σ⟨s⟩), split-K over its rows
+      const int krows = static_cast<int>((rows + 1) & ~1ull);
+      int kchunk = (krows + splits_ - 1) / splits_;
+      kchunk = (kchunk + 1) & ~1;
+      const int splits = (krows + kchunk - 1) / kchunk;
+      GemmArgs g{Dp_, Hp_, krows, d_y_ + off * Dp_, Dp_, d_es_ + off * Hp_, Hp_, d_part_, Hp_, 1.0, 1.0, kchunk,
+                 part_stride_, d_warp_es_ + (size_t)c * splits_ * Hp_};
+      ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
+      ++launches_;
+    }
+    if (c == 0) ev(4);
+  }
+  const long long DH = (long long)D_ * H_;
+  reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
+                                                           part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),
+                                                           lay_.off_ssT());
   finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
-      enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n_), d_stats_, lay_.off_ssT(), lay_.off_tail());
+      nchunks * enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
   counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
   ck(cudaGetLastError(), "finalize");
-  launches_ += 2;
+  launches_ += 3;
   ev(5);
 }
 
@@ -815,7 +897,7 @@ void BscEngine::inference(double* map_states, double* map_mass, double* expected
   ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
-  launch_enumerate(1.0, true, true);
+  launch_enumerate(1.0, true, true, 0, n_, 0);
   std::vector<int> st(n_);
   std::vector<uint32_t> cand(n_ * hprime_);
   ck(cudaMemcpyAsync(st.data(), d_map_state_, n_ * 4, cudaMemcpyDeviceToHost, s), "map D2H");

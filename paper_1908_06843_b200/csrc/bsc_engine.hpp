@@ -54,6 +54,9 @@ class BscEngine {
   void mstep();
   // estep + mstep; returns F = Σ_n log Z_n at the incoming params.
   double step(double temperature);
+  // The same step over host data (copied per call, chunk by chunk, the copies
+  // overlapping the E-step of earlier chunks).
+  double step_streamed(const double* y_host, uint64_t n, double temperature, uint64_t chunk);
 
   double* stats_device() { return d_stats_; }
   double last_free_energy() const { return last_F_; }
@@ -83,7 +86,8 @@ class BscEngine {
   void build_template();
   void ensure_work(uint64_t n);
   void refresh_gram();
-  void launch_enumerate(double temperature, bool cands, bool infer);
+  void launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows, int chunk);
+  void estep_chunked(double temperature, bool want_candidates, const double* host_y, uint64_t chunk);
   void check_err();
   void enqueue_mstep(void* stream);
   void enqueue_gram(void* stream);
@@ -135,6 +139,11 @@ class BscEngine {
   int mstep_calls_ = 0, mstep_nodes_ = 0;
 
   int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
+  // host-streamed E-step: copy stream + per-chunk events
+  static constexpr int kMaxChunks = 256;
+  void* copy_stream_ = nullptr;
+  void* chunk_ev_[kMaxChunks + 1] = {};
+  int colsum_chunks_ = 0;
   bool timing_ = false;
   bool prof_on_ = false;
   void* d_prof_ = nullptr;

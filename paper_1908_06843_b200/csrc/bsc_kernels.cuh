@@ -782,8 +782,8 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
 // Σ y⟨s⟩ᵀ from the GEMM partials, Σ⟨s⟩ (= diag Σ⟨ssᵀ⟩, v = 1) from its
 // fused column sums.
 __global__ void reduce_ysT_kernel(const double* __restrict__ part, const double* __restrict__ colsum, int splits,
-                                  long long split_stride, int D, int H, int ldp, double* __restrict__ stats,
-                                  long long off_s, long long off_ssT) {
+                                  int colsum_rows, long long split_stride, int D, int H, int ldp,
+                                  double* __restrict__ stats, long long off_s, long long off_ssT) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long DH = (long long)D * H;
   if (idx < DH) {
@@ -794,7 +794,7 @@ __global__ void reduce_ysT_kernel(const double* __restrict__ part, const double*
   } else if (idx < DH + H) {
     const int h = static_cast<int>(idx - DH);
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += colsum[(long long)z * ldp + h];
+    for (int z = 0; z < colsum_rows; ++z) s += colsum[(long long)z * ldp + h];
     stats[off_s + h] = s;
     stats[off_ssT + (long long)h * H + h] = s;
   }

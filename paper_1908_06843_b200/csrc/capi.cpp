@@ -5,6 +5,7 @@
 
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -188,9 +189,10 @@ int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y, uint64_t n, const
     need(y, "y");
     need(w, "w");
     auto& e = ctx->engine;
-    e.load_data(y, n, false);
     e.set_params(w, pi, sigma2);
-    const double f = e.step(temperature);
+    // ~8 chunks of ≥ 16k points: the H2D copy of chunk c+1 overlaps chunk c
+    const uint64_t chunk = std::max<uint64_t>(16384, (n + 7) / 8);
+    const double f = e.step_streamed(y, n, temperature, chunk);
     double p = 0, s2 = 0;
     e.get_params(w_out, &p, &s2);
     if (pi_out) *pi_out = p;
