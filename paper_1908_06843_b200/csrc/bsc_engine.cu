@@ -418,9 +418,12 @@ void BscEngine::ensure_work(uint64_t n) {
   // split-K for Yᵀ⟨S⟩: ≈4 waves of 148 SMs over the output tiles
   cudaDeviceProp prop;
   ck(cudaGetDeviceProperties(&prop, device_), "props");
+  // split-K for Yᵀ⟨S⟩: whole waves (2 resident CTAs per SM), never a ragged tail
   const int tiles = ((Dp_ + 127) / 128) * ((Hp_ + 63) / 64);
-  splits_ = std::max(1, std::min<int>((4 * prop.multiProcessorCount + tiles - 1) / tiles,
-                                      static_cast<int>(std::max<uint64_t>(1, rows / 512))));
+  const int slots = 2 * prop.multiProcessorCount;
+  int waves = 1;
+  while (waves < 8 && (waves * slots) / tiles < 8) ++waves;  // ≥ 8 splits when the output is small
+  splits_ = std::max(1, std::min<int>((waves * slots) / tiles, static_cast<int>(std::max<uint64_t>(1, rows / 512))));
   part_stride_ = (long long)Dp_ * Hp_;
   d_part_ = dalloc<double>((size_t)splits_ * part_stride_, "splitK partials");
 
