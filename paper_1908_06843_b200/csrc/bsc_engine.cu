@@ -325,27 +325,62 @@ void BscEngine::build_template() {
       if (dst > 0x7fff || dst < -0x7fff) throw Error(kConfig, "gpu: schedule destination out of range");
       return w16(src) | (static_cast<uint32_t>(static_cast<uint16_t>(static_cast<int16_t>(dst))) << 16);
     };
-    std::vector<uint32_t> rows(static_cast<size_t>(iters) * R, pack(tab_off(n_tab), -1));
+    // runs → list segments (the entries of one output inside one run)
+    struct Seg {
+      std::vector<int> src;
+      int dst;
+    };
+    std::vector<std::vector<Seg>> runs(R);
     std::vector<int> slot_begin(ls.size(), -1);
     int slot = 0;
     for (int l = 0; l < R; ++l) {
       const int b = l * iters, e = std::min(T, b + iters);
       for (int j = b; j < e; ++j) {
         const int o = seq[j].second;
-        const bool last = j + 1 == e || seq[j + 1].second != o;
-        int dst = -1;
-        if (last) {
+        if (j == b || seq[j - 1].second != o) runs[l].push_back(Seg{{}, -1});
+        runs[l].back().src.push_back(seq[j].first);
+        if (j + 1 == e || seq[j + 1].second != o) {
           if (first_lane[o] == last_lane[o]) {
-            dst = targets[o];
+            runs[l].back().dst = targets[o];
           } else {
             if (slot_begin[o] < 0) slot_begin[o] = slot;
-            dst = -(slot + 2);
+            runs[l].back().dst = -(slot + 2);
             ++slot;
           }
         }
-        rows[static_cast<size_t>(j - b) * R + l] = pack(seq[j].first, dst);
       }
     }
+    // Emit one entry per run per iteration. Within a segment the order is
+    // free (it is a sum), so each half-warp's 16 loads of one instruction are
+    // picked greedily to fall in distinct 8-byte shared-memory banks.
+    std::vector<uint32_t> rows(static_cast<size_t>(iters) * R, pack(tab_off(n_tab), -1));
+    std::vector<size_t> cur(R, 0);
+    std::vector<std::vector<int>> rem(R);
+    for (int l = 0; l < R; ++l)
+      if (!runs[l].empty()) rem[l] = runs[l][0].src;
+    for (int it = 0; it < iters; ++it)
+      for (int u = 0; u < R / 32; ++u)
+        for (int half = 0; half < 2; ++half) {
+          unsigned used = 0;
+          for (int k = 0; k < 16; ++k) {
+            const int l = 32 * u + 16 * half + k;
+            if (cur[l] >= runs[l].size()) continue;
+            auto& r = rem[l];
+            size_t pick = 0;
+            for (size_t q = 0; q < r.size(); ++q)
+              if (!((used >> ((r[q] / 8) & 15)) & 1u)) {
+                pick = q;
+                break;
+              }
+            const int src = r[pick];
+            used |= 1u << ((src / 8) & 15);
+            r[pick] = r.back();
+            r.pop_back();
+            const int dst = r.empty() ? runs[l][cur[l]].dst : -1;
+            rows[static_cast<size_t>(it) * R + l] = pack(src, dst);
+            if (r.empty() && ++cur[l] < runs[l].size()) r = runs[l][cur[l]].src;
+          }
+        }
     SchedDesc sd{iters, static_cast<int>(ent.size() / R), 0, static_cast<int>(splits.size())};
     for (size_t o = 0; o < ls.size(); ++o)
       if (first_lane[o] != last_lane[o]) {

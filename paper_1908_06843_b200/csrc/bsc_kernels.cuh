@@ -152,12 +152,10 @@ struct SchedDesc {
 // Packed entry (uint32): low 16 bits = source offset / 8, high 16 bits =
 // signed destination code (see above; a target offset is stored / 8).
 __device__ __forceinline__ void seg_flush(uint32_t v, double& acc, char* smb, double* spart, double scale) {
-  const int dst = static_cast<int>(static_cast<short>(v >> 16));
-  if (dst >= 0) {
-    *reinterpret_cast<double*>(smb + dst * 8) = acc * scale;
-    acc = 0.0;
-  } else if (dst <= -2) {
-    spart[-dst - 2] = acc;
+  if ((v >> 16) != 0xffffu) {  // segment end: one store, to its output or to its slot
+    const int dst = static_cast<int>(static_cast<short>(v >> 16));
+    double* p = dst >= 0 ? reinterpret_cast<double*>(smb + dst * 8) : spart + (-dst - 2);
+    *p = dst >= 0 ? acc * scale : acc;
     acc = 0.0;
   }
 }
@@ -165,26 +163,22 @@ __device__ __forceinline__ double ent_src(const char* smb, uint32_t v) {
   return *reinterpret_cast<const double*>(smb + (v & 0xffffu) * 8);
 }
 
-// 128 runs: lane l walks runs l, l+32, l+64, l+96 interleaved — four
-// independent accumulation chains per lane.
-constexpr int kSchedRuns = 128;
+// 64 runs: lane l walks runs l and l+32 interleaved — two independent
+// accumulation chains per lane, ≤ 63 outputs split across runs.
+constexpr int kSchedRuns = 64;
 
 __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t* ent,
                                              const int4* __restrict__ split, char* smb, double* spart, double scale,
                                              int lane) {
   const uint32_t* e = ent + (long long)sd.row_base * kSchedRuns + lane;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  double a0 = 0.0, a1 = 0.0;
   for (int it = 0; it < sd.iters; ++it) {
     const uint32_t* r = e + it * kSchedRuns;
-    const uint32_t v0 = r[0], v1 = r[32], v2 = r[64], v3 = r[96];
+    const uint32_t v0 = r[0], v1 = r[32];
     a0 += ent_src(smb, v0);
     a1 += ent_src(smb, v1);
-    a2 += ent_src(smb, v2);
-    a3 += ent_src(smb, v3);
     seg_flush(v0, a0, smb, spart, scale);
     seg_flush(v1, a1, smb, spart, scale);
-    seg_flush(v2, a2, smb, spart, scale);
-    seg_flush(v3, a3, smb, spart, scale);
   }
   __syncwarp();
   for (int k = lane; k < sd.n_split; k += 32) {
