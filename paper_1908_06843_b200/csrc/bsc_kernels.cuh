@@ -80,20 +80,19 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   const double k = rint(x * 1.4426950408889634);
   double r = fma(k, -6.93147180559945286227e-01, x);
   r = fma(k, -2.319046813846299558e-17, r);
-  double p = 1.6059043836821613e-10;           // 1/13!
-  p = fma(p, r, 2.08767569878680990e-09);      // 1/12!
-  p = fma(p, r, 2.50521083854417188e-08);      // 1/11!
-  p = fma(p, r, 2.75573192239858907e-07);      // 1/10!
-  p = fma(p, r, 2.75573192239858883e-06);      // 1/9!
-  p = fma(p, r, 2.48015873015873016e-05);      // 1/8!
-  p = fma(p, r, 1.98412698412698413e-04);      // 1/7!
-  p = fma(p, r, 1.38888888888888894e-03);      // 1/6!
-  p = fma(p, r, 8.33333333333333322e-03);      // 1/5!
-  p = fma(p, r, 4.16666666666666644e-02);      // 1/4!
-  p = fma(p, r, 1.66666666666666657e-01);      // 1/3!
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  // Estrin evaluation (dependency depth 6 instead of Horner's 14): the
+  // kernel's exp loops are latency-bound.
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double q0 = fma(r, 1.0, 1.0);
+  const double q1 = fma(r, 1.66666666666666657e-01, 0.5);                    // 1/2!, 1/3!
+  const double q2 = fma(r, 8.33333333333333322e-03, 4.16666666666666644e-02);  // 1/4!, 1/5!
+  const double q3 = fma(r, 1.98412698412698413e-04, 1.38888888888888894e-03);  // 1/6!, 1/7!
+  const double q4 = fma(r, 2.75573192239858883e-06, 2.48015873015873016e-05);  // 1/8!, 1/9!
+  const double q5 = fma(r, 2.50521083854417188e-08, 2.75573192239858907e-07);  // 1/10!, 1/11!
+  const double q6 = fma(r, 1.6059043836821613e-10, 2.08767569878680990e-09);   // 1/12!, 1/13!
+  const double v0 = fma(r2, q1, q0), v1 = fma(r2, q3, q2), v2 = fma(r2, q5, q4);
+  const double w0 = fma(r4, v1, v0), w1 = fma(r4, q6, v2);
+  const double p = fma(r8, w1, w0);
   const int ki = static_cast<int>(k);
   const int k1 = ki >> 1, k2 = ki - k1;
   const double s1 = __longlong_as_double(static_cast<long long>(k1 + 1023) << 52);
@@ -427,6 +426,11 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       if (nn < a.N)
         for (int l = lane; l < row_lines; l += 32)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + nn * a.Hp + l * 16));
+      // and the next point's row into L1
+      const long long n1 = n + nwarps;
+      if (n1 < a.N)
+        for (int l = lane; l < row_lines; l += 32)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.B + n1 * a.Hp + l * 16));
     }
     // ‖y‖² (precomputed once per dataset; any order: only the base term and
     // the error bound use it)
@@ -528,13 +532,32 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       su[p] = v;
       tab[p] = v;  // level-1 node {p}
     }
-    for (int e = lane; e < HP * HP; e += 32) {
-      const int p = e / HP, q = e - p * HP;
-      if (p < q)  // strict upper triangle, row-major
-        sP[p * (2 * HP - p - 1) / 2 + (q - p - 1)] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
+    // pairwise terms (strict upper triangle, row-major): the Gram gathers are
+    // issued first and land while the singleton terms are computed
+    const int npairs = HP * (HP - 1) / 2;
+    double gp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = lane + 32 * u;
+      gp[u] = 0.0;
+      if (e < npairs) {
+        int idx = e, p = 0;
+        while (idx >= HP - 1 - p) {
+          idx -= HP - 1 - p;
+          ++p;
+        }
+        gp[u] = a.G[(long long)scand[p] * a.Hp + scand[p + 1 + idx]];
+      }
+    }
+    for (int e = lane + 128; e < npairs; e += 32) {  // H' > 16
+      int idx = e, p = 0;
+      while (idx >= HP - 1 - p) {
+        idx -= HP - 1 - p;
+        ++p;
+      }
+      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[p + 1 + idx]];
     }
     if (lane == 0) tab[a.n_tab] = 0.0;  // zero slot (the selection pool overlays the table)
-    __syncwarp();
 
     ENUM_PHASE(2);
     // singletons over all H units and the zero state (rel = 0)
@@ -546,6 +569,10 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       rel1[j] = h < H ? a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) : -INFINITY;
       mx = fmax(mx, rel1[j]);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < npairs) sP[lane + 32 * u] = -2.0 * a.inv2s * gp[u];
+    __syncwarp();
     // multi-active states, level by level; table entries hold byte offsets
     // into this warp's shared region (host-computed, EnumSmem layout)
     char* smb = reinterpret_cast<char*>(sm);
