@@ -97,6 +97,9 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   lay_ = StatsLayout{static_cast<long long>(D_), static_cast<long long>(H_)};
   build_template();
   if (const char* e = std::getenv("BSC_ENUM_PROFILE")) prof_on_ = e[0] == '1';
+  // posterior-weight path (tests and A/B runs): 0 auto, 1 multiplicative after the
+  // exact maximum, 2 exp per state
+  if (const char* e = std::getenv("BSC_WEIGHT_MODE")) weight_mode_ = std::atoi(e);
 
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
@@ -640,6 +643,7 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   a.inv2s = inv2s;
   a.base0 = zero_prior + norm_const;
   a.inv_T = 1.0 / temperature;
+  a.weight_mode = weight_mode_;
   a.eps_dot = 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
 
   const int maxj = maxj_for(H_);

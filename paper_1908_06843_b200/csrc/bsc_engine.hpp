@@ -146,6 +146,7 @@ class BscEngine {
   int colsum_chunks_ = 0;
   bool timing_ = false;
   bool prof_on_ = false;
+  int weight_mode_ = 0;
   void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;

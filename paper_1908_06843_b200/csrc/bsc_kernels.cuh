@@ -219,6 +219,7 @@ struct EnumArgs {
   const uint32_t* sched_ent;  // packed entries [rows][kSchedRuns]
   const int4* sched_split;
   int n_slots, n_out;
+  int weight_mode;  // 0 auto, 1 multiplicative after the exact maximum, 2 exp per state
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
 };
@@ -573,12 +574,62 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     for (int u = 0; u < 4; ++u)
       if (lane + 32 * u < npairs) sP[lane + 32 * u] = -2.0 * a.inv2s * gp[u];
     __syncwarp();
+    // finiteness of every log-joint term (a non-finite log-joint is an error,
+    // core.cpp:36-45) and the range guard of the multiplicative weight pass
+    double umax = -INFINITY, uabs = 0.0, pmax = -INFINITY, pabs = 0.0;
+    bool fin = true;
+    for (int p = lane; p < HP; p += 32) {
+      const double v = su[p];
+      fin = fin && isfinite(v);
+      umax = fmax(umax, v);
+      uabs = fmax(uabs, fabs(v));
+    }
+    for (int e = lane; e < npairs; e += 32) {
+      const double v = sP[e];
+      fin = fin && isfinite(v);
+      pmax = fmax(pmax, v);
+      pabs = fmax(pabs, fabs(v));
+    }
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) fin = fin && (lane + 32 * j >= H || isfinite(rel1[j]));
+    if (!__all_sync(0xffffffffu, fin)) {
+      if (lane == 0) atomicOr(a.err, kErrNonFiniteLogJoint);
+      continue;
+    }
+    mx = warp_max(mx);
+    umax = warp_max(umax);
+    uabs = warp_max(uabs);
+    pmax = warp_max(pmax);
+    pabs = warp_max(pabs);
+    const bool t1 = a.inv_T == 1.0;
+    // singleton weights, summed relative to the singleton maximum; rel1 dies
+    // here (the MAP and moment passes recompute single_q from B) so the state
+    // passes below run with MAXJ more registers of ILP
+    const double mxs = mx;
+    double zs1 = lane == 0 ? exp_nonpos(-mxs) : 0.0;
+    double zsT = lane == 0 && !t1 ? exp_nonpos(-mxs * a.inv_T) : 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const double x = rel1[j] - mxs;  // −inf beyond H: exp_nonpos gives 0
+      zs1 += exp_nonpos(x);
+      if (!t1) zsT += exp_nonpos(x * a.inv_T);
+    }
+    if (t1) zsT = zs1;
+    // q(S) = q(A)·e^{u_z}·e^{coup(S)} keeps every factor and partial product in
+    // fp64 range when |u| ≤ 300 and (γ−1)|P| ≤ 300 (phase 3)
+    const bool mult_ok = t1 && a.weight_mode != 2 && uabs <= 300.0 && (GM - 1) * pabs <= 300.0;
+    // the multiplicative pass needs no maximum: any shift ≥ max rel works, and
+    // an upper bound within e^300 of the true maximum loses nothing to underflow
+    const double ub = GM * fmax(umax, 0.0) + 0.5 * GM * (GM - 1) * fmax(pmax, 0.0);
+    char* smb = reinterpret_cast<char*>(sm);
+    const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
+    if (mult_ok && a.weight_mode == 0 && ub - mx <= 300.0) {
+      mx = fmax(mx, ub);
+    } else {
     // multi-active states, level by level; table entries hold byte offsets
     // into this warp's shared region (host-computed, EnumSmem layout)
-    char* smb = reinterpret_cast<char*>(sm);
     // Four states per lane per iteration, all loads before any store (a
     // level only reads earlier levels): four independent chains.
-    const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
     for (int k = 2; k <= GM; ++k) {
       const int e = a.level_off[k];
       const bool keep = k < GM;
@@ -614,21 +665,63 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       if (lane == 0) atomicOr(a.err, kErrNonFiniteLogJoint);
       continue;
     }
+    }
 
     ENUM_PHASE(3);
     // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
-    const bool t1 = a.inv_T == 1.0;
-    double z1 = 0.0, zt = 0.0;
+    double z1 = zs1 * exp_nonpos(mxs - mx), zt = 0.0;
+    // q of singleton unit h at temperature T, bit-identical wherever recomputed
+    auto single_q = [&](int h) {
+      return exp_nonpos((a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) - mx) * a.inv_T);
+    };
     if (t1) {
       // q = exp_nonpos(rel − max). Terms below e^-32 of the largest state change no
       // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
       // (MUFU.EX2); the others — typically a few dozen — in fp64, compacted.
-      if (lane == 0) z1 = exp_nonpos(-mx);
+      if (mult_ok) {
+        // Multiplicative posterior weights: with |u| ≤ 300 and (γ−1)·|P| ≤ 300
+        // every factor and partial product stays inside fp64 range, and
+        //   q(S) = q(A) · e^{u_z} · e^{coup(S)},  e^{coup(S)} = e^{coup(sib)} · e^{P_xz},
+        // so a multi-active state costs three multiplications instead of an
+        // exp (a state whose parent underflowed is below e^-145 of the sum).
+        for (int p = lane; p < HP; p += 32) {
+          tab[p] = exp_nonpos(tab[p] - mx);  // level-1 nodes {p}
+          sqs[p] = tab[p];
+          su[p] = exp(su[p]);
+        }
+        for (int e = lane; e < npairs; e += 32) sP[e] = exp(sP[e]);
+        __syncwarp();
+        for (int k = 2; k <= GM; ++k) {
+          const int e = a.level_off[k];
+          const bool keep = k < GM, first = k == 2;
+          for (int i0 = a.level_off[k - 1] + lane; i0 < e; i0 += 128) {
+            uint2 d[4];
 #pragma unroll
-      for (int j = 0; j < MAXJ; ++j) {  // singletons: fp64, independent (unrolled)
-        rel1[j] = exp_nonpos(rel1[j] - mx);
-        z1 += rel1[j];
-      }
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + 32 * u;
+              d[u] = i < e ? sdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
+            }
+            double c[4], q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double es = first ? 1.0 : *reinterpret_cast<const double*>(smb + (d[u].x >> 16) * 8);
+              c[u] = es * *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
+              q[u] = *reinterpret_cast<const double*>(smb + (d[u].x & 0xffffu) * 8) *
+                     *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) * c[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + 32 * u;
+              if (i < e) {
+                tab[i] = q[u];
+                if (keep) coup[i - HP] = c[u];
+                z1 += q[u];
+              }
+            }
+          }
+          __syncwarp();
+        }
+      } else {
       int* queue = reinterpret_cast<int*>(coup);  // coup/part/outs are free here
       int nq = 0;
       for (int b0 = 0; b0 < a.n_tab; b0 += 128) {
@@ -673,19 +766,11 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         else
           sqs[i] = v;
       }
+      }
       z1 = warp_sum(z1);
       zt = z1;
     } else {
-      if (lane == 0) {
-        z1 = exp_nonpos(-mx);
-        zt = exp_nonpos(-mx * a.inv_T);
-      }
-#pragma unroll
-      for (int j = 0; j < MAXJ; ++j) {
-        z1 += exp_nonpos(rel1[j] - mx);
-        rel1[j] = exp_nonpos((rel1[j] - mx) * a.inv_T);
-        zt += rel1[j];
-      }
+      zt = zsT * exp_nonpos((mxs - mx) * a.inv_T);
       for (int i = lane; i < a.n_tab; i += 32) {
         const double r = tab[i] - mx;
         const double et = exp_nonpos(r * a.inv_T);
@@ -715,11 +800,10 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       // order: zero, singletons 0..H−1, then multi-active in DFS order)
       double bv = lane == 0 ? exp(-mx * a.inv_T) : -1.0;
       int bi = lane == 0 ? 0 : 0x7fffffff;
-#pragma unroll
-      for (int j = 0; j < MAXJ; ++j) {
-        const int h = lane + 32 * j;
-        if (h < H && ranks_before(rel1[j], 1 + h, bv, bi)) {
-          bv = rel1[j];
+      for (int h = lane; h < H; h += 32) {
+        const double q = single_q(h);
+        if (ranks_before(q, 1 + h, bv, bi)) {
+          bv = q;
           bi = 1 + h;
         }
       }
@@ -757,10 +841,11 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
     // Yᵀ⟨S⟩ GEMM from these rows.
     double* esrow = a.ES + (long long)n * a.Hp;
-#pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const int h = lane + 32 * j;
-      if (h < H) esrow[h] = rel1[j] * inv_z;
+    for (int h0 = lane; h0 < H; h0 += 64) {  // two independent exps per iteration
+      const int h1 = h0 + 32;
+      const double q0 = single_q(h0), q1 = h1 < H ? single_q(h1) : 0.0;
+      esrow[h0] = q0 * inv_z;
+      if (h1 < H) esrow[h1] = q1 * inv_z;
     }
     __syncwarp();
     for (int p = lane; p < HP; p += 32) esrow[scand[p]] = souts[p];

@@ -179,6 +179,26 @@ def test_near_tie_band_uses_exact_scores(pkg, port):
     m.close()
 
 
+@pytest.mark.parametrize("s2", [1e-3, 0.02, 0.3, 1.0, 40.0])
+def test_posterior_weight_paths(pkg, port, s2):
+    """σ² sweeps |log-joint| terms from e^±1000 (range guard fails: exp path)
+    through mixed per-point paths to flat posteriors (multiplicative path)."""
+    d, h, hp, g = 24, 30, 9, 4
+    wt = port.random_dictionary(d, h, 11, 2.0)
+    y = port.generate(wt, 0.1, 0.05, 400, 12)
+    p = pkg.BscParams(wt * 1.1, 0.1, s2)
+    m = model_for(pkg, d, h, hp, g)
+    m.load(y)
+    assert np.array_equal(m.candidates(p), port.candidates(p.W, p.pi, s2, y, hp))
+    check_stats(m.estep_stats(p), port.estep_stats(p.W, p.pi, s2, y, hp, g))
+    inf = m.inference(p)
+    ms, mm, ex = port.inference(p.W, p.pi, s2, y, hp, g)
+    assert np.array_equal(inf.map_states, ms)
+    assert rel(inf.map_mass, mm) < 1e-10
+    assert rel(inf.expected_states, ex) < 1e-10
+    m.close()
+
+
 def test_temperature(pkg, port):
     from paper_1908_06843_b200 import configs
 
