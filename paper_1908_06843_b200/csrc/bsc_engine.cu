@@ -42,20 +42,22 @@ int maxj_for(uint32_t h) {
     if (need <= m) return m;
   return 32;
 }
-const void* enum_fn(int maxj) {
+template <bool STAGED>
+const void* enum_fn_t(int maxj) {
   switch (maxj) {
-    case 1: return (const void*)enumerate_kernel<1>;
-    case 2: return (const void*)enumerate_kernel<2>;
-    case 4: return (const void*)enumerate_kernel<4>;
-    case 6: return (const void*)enumerate_kernel<6>;
-    case 8: return (const void*)enumerate_kernel<8>;
-    case 10: return (const void*)enumerate_kernel<10>;
-    case 12: return (const void*)enumerate_kernel<12>;
-    case 16: return (const void*)enumerate_kernel<16>;
-    case 24: return (const void*)enumerate_kernel<24>;
-    default: return (const void*)enumerate_kernel<32>;
+    case 1: return (const void*)enumerate_kernel<1, STAGED>;
+    case 2: return (const void*)enumerate_kernel<2, STAGED>;
+    case 4: return (const void*)enumerate_kernel<4, STAGED>;
+    case 6: return (const void*)enumerate_kernel<6, STAGED>;
+    case 8: return (const void*)enumerate_kernel<8, STAGED>;
+    case 10: return (const void*)enumerate_kernel<10, STAGED>;
+    case 12: return (const void*)enumerate_kernel<12, STAGED>;
+    case 16: return (const void*)enumerate_kernel<16, STAGED>;
+    case 24: return (const void*)enumerate_kernel<24, STAGED>;
+    default: return (const void*)enumerate_kernel<32, STAGED>;
   }
 }
+const void* enum_fn(int maxj, bool staged) { return staged ? enum_fn_t<true>(maxj) : enum_fn_t<false>(maxj); }
 
 constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
 
@@ -323,10 +325,14 @@ void BscEngine::build_template() {
       first_lane[o] = std::min(first_lane[o], l);
       last_lane[o] = std::max(last_lane[o], l);
     }
+    // dst: ≥ 0 output byte offset, −1 continue, ≤ −2 split slot −dst−2 (see seg_flush)
     auto pack = [&](int src, int dst) {
-      if (dst >= 0) dst = static_cast<int>(w16(dst));  // target offset / 8 (< 2^15 checked below)
-      if (dst > 0x7fff || dst < -0x7fff) throw Error(kConfig, "gpu: schedule destination out of range");
-      return w16(src) | (static_cast<uint32_t>(static_cast<uint16_t>(static_cast<int16_t>(dst))) << 16);
+      uint32_t code = 0xffffu;
+      if (dst >= 0) code = w16(dst);
+      else if (dst <= -2) code = 0x8000u | static_cast<uint32_t>(L1.part + (-dst - 2));
+      if (dst != -1 && (code & 0x7fffu) >= 0x7fffu) throw Error(kConfig, "gpu: schedule destination out of range");
+      if (dst >= 0 && code > 0x7fffu) throw Error(kConfig, "gpu: schedule destination out of range");
+      return w16(src) | (code << 16);
     };
     // runs → list segments (the entries of one output inside one run)
     struct Seg {
@@ -492,7 +498,7 @@ void BscEngine::ensure_work(uint64_t n) {
   enum_block_ = warps * 32;
   enum_smem_ = warps * per_warp + (stage_tables_ ? table_bytes : 0);
   const int maxj = maxj_for(H_);
-  const void* fn = enum_fn(maxj);
+  const void* fn = enum_fn(maxj, stage_tables_);
   ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "enum smem attr");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, enum_block_, enum_smem_), "occupancy");
@@ -648,7 +654,7 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
 
   const int maxj = maxj_for(H_);
   void* args[] = {&a};
-  ck(cudaLaunchKernel(enum_fn(maxj), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s), "enumerate launch");
+  ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s), "enumerate launch");
   ck(cudaGetLastError(), "enumerate");
   ++launches_;
 }

@@ -148,15 +148,15 @@ struct SchedDesc {
   int split_base; // sched_split[split_base + l] = {target byte offset, first slot, end slot}
 };
 
-// Packed entry (uint32): low 16 bits = source offset / 8, high 16 bits =
-// signed destination code (see above; a target offset is stored / 8).
-__device__ __forceinline__ void seg_flush(uint32_t v, double& acc, char* smb, double* spart, double scale) {
-  if ((v >> 16) != 0xffffu) {  // segment end: one store, to its output or to its slot
-    const int dst = static_cast<int>(static_cast<short>(v >> 16));
-    double* p = dst >= 0 ? reinterpret_cast<double*>(smb + dst * 8) : spart + (-dst - 2);
-    *p = dst >= 0 ? acc * scale : acc;
-    acc = 0.0;
-  }
+// Packed entry (uint32): low 16 bits = source offset / 8; high 16 bits =
+// 0xffff continue, else segment end: bit 15 clear → store acc·scale at
+// offset (bits 0-14)·8 (an output), set → store acc unscaled (a split slot).
+__device__ __forceinline__ void seg_flush(uint32_t v, double& acc, char* smb, double scale) {
+  const uint32_t hi = v >> 16;
+  const bool fl = hi != 0xffffu;
+  const double val = (hi & 0x8000u) ? acc : acc * scale;
+  if (fl) *reinterpret_cast<double*>(smb + (hi & 0x7fffu) * 8) = val;
+  acc = fl ? 0.0 : acc;
 }
 __device__ __forceinline__ double ent_src(const char* smb, uint32_t v) {
   return *reinterpret_cast<const double*>(smb + (v & 0xffffu) * 8);
@@ -166,18 +166,32 @@ __device__ __forceinline__ double ent_src(const char* smb, uint32_t v) {
 // accumulation chains per lane, ≤ 63 outputs split across runs.
 constexpr int kSchedRuns = 64;
 
+// Software-pipelined: the next entry pair and its values are loaded before
+// this iteration's stores. Safe because a store only ever targets the node
+// (or slot) of a segment that has just ended in this lane, and no later entry
+// of the same schedule reads it.
 __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t* ent,
                                              const int4* __restrict__ split, char* smb, double* spart, double scale,
                                              int lane) {
+  const int n = sd.iters;
   const uint32_t* e = ent + (long long)sd.row_base * kSchedRuns + lane;
-  double a0 = 0.0, a1 = 0.0;
-  for (int it = 0; it < sd.iters; ++it) {
-    const uint32_t* r = e + it * kSchedRuns;
-    const uint32_t v0 = r[0], v1 = r[32];
-    a0 += ent_src(smb, v0);
-    a1 += ent_src(smb, v1);
-    seg_flush(v0, a0, smb, spart, scale);
-    seg_flush(v1, a1, smb, spart, scale);
+  if (n > 0) {
+    double a0 = 0.0, a1 = 0.0;
+    uint32_t v0 = e[0], v1 = e[32];
+    double x0 = ent_src(smb, v0), x1 = ent_src(smb, v1);
+    for (int it = 0; it < n; ++it) {
+      const uint32_t* r = e + (it + 1 < n ? it + 1 : it) * kSchedRuns;
+      const uint32_t w0 = r[0], w1 = r[32];
+      const double y0 = ent_src(smb, w0), y1 = ent_src(smb, w1);
+      a0 += x0;
+      a1 += x1;
+      seg_flush(v0, a0, smb, scale);
+      seg_flush(v1, a1, smb, scale);
+      v0 = w0;
+      v1 = w1;
+      x0 = y0;
+      x1 = y1;
+    }
   }
   __syncwarp();
   for (int k = lane; k < sd.n_split; k += 32) {
@@ -366,7 +380,9 @@ __device__ __forceinline__ void top_k(const double (&f)[MAXJ], uint32_t removed,
   }
 }
 
-template <int MAXJ>
+// STAGED: the state descriptors and schedule entries are staged in shared
+// memory (compile-time, so every table access is an LDS, not a generic load)
+template <int MAXJ, bool STAGED>
 __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   extern __shared__ __align__(16) double esm[];
   const int lane = threadIdx.x & 31;
@@ -378,8 +394,8 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   // staged once per CTA in shared memory when they fit (else read from L1/L2).
   const uint2* sdesc = a.sdesc;
   const uint32_t* sent = a.sched_ent;
-  const int stage_bytes = a.stage_desc_bytes + a.stage_ent_bytes;
-  if (stage_bytes > 0) {
+  const int stage_bytes = STAGED ? a.stage_desc_bytes + a.stage_ent_bytes : 0;
+  if (STAGED) {
     char* cta = reinterpret_cast<char*>(esm);
     const int4* src0 = reinterpret_cast<const int4*>(a.sdesc);
     const int4* src1 = reinterpret_cast<const int4*>(a.sched_ent);
