@@ -26,6 +26,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAKS = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "r01_traffic.json")
+
+
+def measured_traffic(workload, kernel, points):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture, scaled
+    to this run's points per launch (null when no capture matches)."""
+    if not os.path.exists(TRAFFIC):
+        return None
+    with open(TRAFFIC) as f:
+        t = json.load(f)
+    if t.get("workload") != workload or kernel not in t.get("per_launch_bytes", {}):
+        return None
+    return int(t["per_launch_bytes"][kernel] * points / t["points_per_launch"])
 
 
 def flops_per_point(D, H, hprime, gamma):
@@ -266,7 +279,7 @@ def main():
                    "l2": "inputs larger than L2 (Y 8·N·D = %.0f MB per GPU)" % (8 * n_local * w.D / 1e6)},
         "roofline": {"kernel": dom, "bound": "tensor" if dom.startswith("gemm") else "fp64", "pipe": pipe,
                      "achieved": round(achieved, 3), "peak": pk, "unit": "TFLOP/s", "frac": round(achieved / pk, 4),
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": measured_traffic(w.name, dom, n_local), "peak_source": peak_src,
                      "algorithmic": "SURVEY.md §8(d): F_state=%d, F_dense=%d flops/point" % (state, dense)},
         "step_roofline": {"flops_per_step": step_flops, "tflops": round(step_flops / (ms / 1e3) / 1e12 / world, 3),
                           "frac_of_dmma_peak": round(step_flops / (ms / 1e3) / 1e12 / world / dmma_peak, 4)},

@@ -151,12 +151,15 @@ struct SchedDesc {
 // Packed entry (uint32): low 16 bits = source offset / 8; high 16 bits =
 // 0xffff continue, else segment end: bit 15 clear → store acc·scale at
 // offset (bits 0-14)·8 (an output), set → store acc unscaled (a split slot).
-__device__ __forceinline__ void seg_flush(uint32_t v, double& acc, char* smb, double scale) {
+__device__ __forceinline__ void seg_flush(uint32_t v, double& acc, uint32_t sbase, double scale) {
   const uint32_t hi = v >> 16;
-  const bool fl = hi != 0xffffu;
   const double val = (hi & 0x8000u) ? acc : acc * scale;
-  if (fl) *reinterpret_cast<double*>(smb + (hi & 0x7fffu) * 8) = val;
-  acc = fl ? 0.0 : acc;
+  // predicated store (no branch): taken only at a segment end
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t@p st.shared.f64 [%1], %2;\n\t}" ::"r"(hi),
+      "r"(sbase + (hi & 0x7fffu) * 8), "d"(val)
+      : "memory");
+  acc = hi != 0xffffu ? 0.0 : acc;
 }
 __device__ __forceinline__ double ent_src(const char* smb, uint32_t v) {
   return *reinterpret_cast<const double*>(smb + (v & 0xffffu) * 8);
@@ -175,6 +178,10 @@ __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t
                                              int lane) {
   const int n = sd.iters;
   const uint32_t* e = ent + (long long)sd.row_base * kSchedRuns + lane;
+  // split descriptors (≤ 63) fetched up front: they land during the main loop
+  const int4 sp0 = lane < sd.n_split ? __ldg(split + sd.split_base + lane) : int4{0, 0, 0, 0};
+  const int4 sp1 = lane + 32 < sd.n_split ? __ldg(split + sd.split_base + lane + 32) : int4{0, 0, 0, 0};
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smb));
   if (n > 0) {
     double a0 = 0.0, a1 = 0.0;
     uint32_t v0 = e[0], v1 = e[32];
@@ -185,8 +192,8 @@ __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t
       const double y0 = ent_src(smb, w0), y1 = ent_src(smb, w1);
       a0 += x0;
       a1 += x1;
-      seg_flush(v0, a0, smb, scale);
-      seg_flush(v1, a1, smb, scale);
+      seg_flush(v0, a0, sbase, scale);
+      seg_flush(v1, a1, sbase, scale);
       v0 = w0;
       v1 = w1;
       x0 = y0;
@@ -194,11 +201,14 @@ __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t
     }
   }
   __syncwarp();
-  for (int k = lane; k < sd.n_split; k += 32) {
-    const int4 sp = __ldg(split + sd.split_base + k);
-    double s = 0.0;
-    for (int j = sp.y; j < sp.z; ++j) s += spart[j];
-    *reinterpret_cast<double*>(smb + sp.x) = s * scale;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int4 sp = u ? sp1 : sp0;
+    if (lane + 32 * u < sd.n_split) {
+      double s = 0.0;
+      for (int j = sp.y; j < sp.z; ++j) s += spart[j];
+      *reinterpret_cast<double*>(smb + sp.x) = s * scale;
+    }
   }
   __syncwarp();
 }
@@ -686,10 +696,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     ENUM_PHASE(3);
     // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
     double z1 = zs1 * exp_nonpos(mxs - mx), zt = 0.0;
-    // q of singleton unit h at temperature T, bit-identical wherever recomputed
-    auto single_q = [&](int h) {
-      return exp_nonpos((a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) - mx) * a.inv_T);
-    };
     if (t1) {
       // q = exp_nonpos(rel − max). Terms below e^-32 of the largest state change no
       // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
@@ -810,15 +816,28 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     __syncwarp();
 
+    // B row and Gram diagonal for the singleton weights of phases 4/6, loaded
+    // now so the loads land during the subtree pass
+    double bb[MAXJ], gg[MAXJ];
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      bb[j] = h < H ? brow[h] : 0.0;
+      gg[j] = h < H ? a.gdiag[h] : 0.0;
+    }
+    auto single_qj = [&](int j) { return exp_nonpos((a.dlp + a.inv2s * (2.0 * bb[j] - gg[j]) - mx) * a.inv_T); };
+
     ENUM_PHASE(4);
     if (a.map_state) {
       // MAP state (linear_discrete.cpp:314-316: first maximum in reference
       // order: zero, singletons 0..H−1, then multi-active in DFS order)
       double bv = lane == 0 ? exp(-mx * a.inv_T) : -1.0;
       int bi = lane == 0 ? 0 : 0x7fffffff;
-      for (int h = lane; h < H; h += 32) {
-        const double q = single_q(h);
-        if (ranks_before(q, 1 + h, bv, bi)) {
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) {
+        const int h = lane + 32 * j;
+        const double q = single_qj(j);
+        if (h < H && ranks_before(q, 1 + h, bv, bi)) {
           bv = q;
           bi = 1 + h;
         }
@@ -857,11 +876,10 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
     // Yᵀ⟨S⟩ GEMM from these rows.
     double* esrow = a.ES + (long long)n * a.Hp;
-    for (int h0 = lane; h0 < H; h0 += 64) {  // two independent exps per iteration
-      const int h1 = h0 + 32;
-      const double q0 = single_q(h0), q1 = h1 < H ? single_q(h1) : 0.0;
-      esrow[h0] = q0 * inv_z;
-      if (h1 < H) esrow[h1] = q1 * inv_z;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      if (h < H) esrow[h] = single_qj(j) * inv_z;
     }
     __syncwarp();
     for (int p = lane; p < HP; p += 32) esrow[scand[p]] = souts[p];
