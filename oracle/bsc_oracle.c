@@ -367,7 +367,88 @@ static int validate_trunc(uint32_t h, uint32_t hprime, uint32_t gamma) {
   return OK;
 }
 
-/* truncation.cpp:61-93 (V = 1), saturating. */
+/* ------------------------------------------------------- value tables */
+/* LinearDiscreteModel::value_table, linear_discrete.cpp:71-97: the non-zero
+ * alphabet with its log-probabilities and log P(s = 0). family 0 = bsc,
+ * 1 = tsc, 2 = dsc (alphabet ascending with 0, probabilities aligned). */
+#define LD_MAX_V 8
+typedef struct {
+  uint32_t family, nalpha;
+  const double* alpha;
+  const double* probs;
+  double pi;
+} prior_t;
+
+typedef struct {
+  uint32_t nv;
+  double values[LD_MAX_V];
+  double log_probs[LD_MAX_V];
+  double log_p0;
+} vtab_t;
+
+static const char* family_name(uint32_t f) { return f == 0 ? "bsc" : f == 1 ? "tsc" : "dsc"; }
+
+static int value_table(const prior_t* pr, vtab_t* t) {
+  t->nv = 0;
+  switch (pr->family) {
+    case 0:
+      t->nv = 1;
+      t->values[0] = 1.0;
+      t->log_probs[0] = log(pr->pi);
+      t->log_p0 = log(1.0 - pr->pi);
+      break;
+    case 1:
+      t->nv = 2;
+      t->values[0] = -1.0;
+      t->values[1] = 1.0;
+      t->log_probs[0] = log(pr->pi / 2.0);
+      t->log_probs[1] = log(pr->pi / 2.0);
+      t->log_p0 = log(1.0 - pr->pi);
+      break;
+    case 2:
+      for (uint32_t k = 0; k < pr->nalpha; ++k) {
+        if (pr->alpha[k] == 0.0) {
+          t->log_p0 = log(pr->probs[k]);
+        } else {
+          if (t->nv == LD_MAX_V) return fail(E_CONFIG, "oracle: more than %d non-zero values", LD_MAX_V);
+          t->values[t->nv] = pr->alpha[k];
+          t->log_probs[t->nv] = log(pr->probs[k]);
+          t->nv++;
+        }
+      }
+      break;
+    default:
+      return fail(E_CONFIG, "oracle: unknown family %u", pr->family);
+  }
+  return OK;
+}
+
+/* LinearDiscreteModel::validate, linear_discrete.cpp:99-127. */
+static int validate_ld(uint32_t d, uint32_t h, const double* w, double sigma2, const prior_t* pr) {
+  const char* nm = family_name(pr->family);
+  for (size_t i = 0; i < (size_t)d * h; ++i)
+    if (!isfinite(w[i])) return fail(E_NUMERIC, "%s: non-finite dictionary", nm);
+  if (!(sigma2 > 0.0) || !isfinite(sigma2)) return fail(E_CONFIG, "%s: sigma2 must be positive", nm);
+  if (pr->family == 2) {
+    if (pr->nalpha < 2) return fail(E_CONFIG, "dsc: values/probs size mismatch");
+    for (uint32_t k = 1; k < pr->nalpha; ++k)
+      if (pr->alpha[k] < pr->alpha[k - 1]) return fail(E_CONFIG, "dsc: values must be ascending");
+    int zero = 0;
+    for (uint32_t k = 0; k < pr->nalpha; ++k) zero |= pr->alpha[k] == 0.0;
+    if (!zero) return fail(E_CONFIG, "dsc: alphabet must contain 0");
+    double total = 0.0;
+    for (uint32_t k = 0; k < pr->nalpha; ++k) {
+      if (!(pr->probs[k] > 0.0)) return fail(E_CONFIG, "dsc: probabilities must be positive");
+      total += pr->probs[k];
+    }
+    if (fabs(total - 1.0) > 1e-6) return fail(E_CONFIG, "dsc: probabilities must sum to 1");
+  } else if (!(pr->pi > 0.0 && pr->pi < 1.0)) {
+    return fail(E_CONFIG, "%s: pi must lie in (0,1)", nm);
+  }
+  return OK;
+}
+
+/* truncation.cpp:61-93, saturating. */
 static uint64_t sat_mul(uint64_t a, uint64_t b) {
   if (a != 0 && b > UINT64_MAX / a) return UINT64_MAX;
   return a * b;
@@ -385,35 +466,63 @@ static uint64_t binom(uint64_t n, uint64_t k) {
   }
   return r;
 }
-static uint64_t state_count(uint32_t h, uint32_t hprime, uint32_t gamma) {
-  uint64_t total = sat_add(1, h);
-  for (uint32_t k = 2; k <= gamma; ++k) total = sat_add(total, binom(hprime, k));
+static uint64_t state_count_v(uint32_t h, uint32_t hprime, uint32_t gamma, uint32_t nv) {
+  uint64_t total = sat_add(1, sat_mul(h, nv));
+  uint64_t vpow = nv;
+  for (uint32_t k = 2; k <= gamma; ++k) {
+    vpow = sat_mul(vpow, nv);
+    total = sat_add(total, sat_mul(binom(hprime, k), vpow));
+  }
   return total;
 }
 
 int bsc_state_count(uint32_t h, uint32_t hprime, uint32_t gamma, uint64_t* out) {
   int rc = validate_trunc(h, hprime, gamma);
   if (rc) return rc;
-  *out = state_count(h, hprime, gamma);
+  *out = state_count_v(h, hprime, gamma, 1);
   return OK;
 }
 
-/* StateTemplate multi-active patterns, truncation.cpp:116-147: depth-first
- * over candidate positions, supports of size 2..gamma in lexicographic order
- * with prefixes first. Patterns are stored as position lists. */
+int ld_state_count(uint32_t h, uint32_t hprime, uint32_t gamma, uint32_t nv, uint64_t* out) {
+  int rc = validate_trunc(h, hprime, gamma);
+  if (rc) return rc;
+  *out = state_count_v(h, hprime, gamma, nv);
+  return OK;
+}
+
+/* StateTemplate multi-active patterns, truncation.cpp:95-151: depth-first
+ * over candidate positions (supports of size 2..gamma, lexicographic,
+ * prefixes first); within a support the value odometer runs, last slot
+ * fastest. Patterns are stored as (position, value index) lists. */
 typedef struct {
-  uint32_t hprime, gamma;
+  uint32_t hprime, gamma, nv;
   size_t count;
   uint8_t* len;  /* [count] */
   uint8_t* pos;  /* [count * gamma] */
+  uint8_t* vix;  /* [count * gamma] */
 } tmpl_t;
 
-static void dfs(tmpl_t* t, uint8_t* support, uint32_t depth, uint32_t next) {
-  if (depth >= 2) {
-    t->len[t->count] = (uint8_t)depth;
-    memcpy(t->pos + t->count * t->gamma, support, depth);
+static void emit_values(tmpl_t* t, const uint8_t* support, uint32_t k) {
+  uint8_t vi[256];
+  memset(vi, 0, k);
+  for (;;) {
+    t->len[t->count] = (uint8_t)k;
+    memcpy(t->pos + t->count * t->gamma, support, k);
+    memcpy(t->vix + t->count * t->gamma, vi, k);
     t->count++;
+    uint32_t i = k; /* advance the odometer, last slot fastest */
+    for (;;) {
+      if (i == 0) return;
+      --i;
+      if (++vi[i] < t->nv) break;
+      vi[i] = 0;
+      if (i == 0) return;
+    }
   }
+}
+
+static void dfs(tmpl_t* t, uint8_t* support, uint32_t depth, uint32_t next) {
+  if (depth >= 2) emit_values(t, support, depth);
   if (depth == t->gamma) return;
   for (uint32_t p = next; p < t->hprime; ++p) {
     support[depth] = (uint8_t)p;
@@ -421,21 +530,23 @@ static void dfs(tmpl_t* t, uint8_t* support, uint32_t depth, uint32_t next) {
   }
 }
 
-static int tmpl_build(tmpl_t* t, uint32_t h, uint32_t hprime, uint32_t gamma,
+static int tmpl_build(tmpl_t* t, uint32_t h, uint32_t hprime, uint32_t gamma, uint32_t nv,
                       uint64_t cap) {
   int rc = validate_trunc(h, hprime, gamma);
   if (rc) return rc;
-  const uint64_t total = state_count(h, hprime, gamma);
+  const uint64_t total = state_count_v(h, hprime, gamma, nv);
   if (total > cap)
     return fail(E_CONFIG, "state explosion: %llu states per data point exceeds cap of %llu",
                 (unsigned long long)total, (unsigned long long)cap);
   if (hprime > 255) return fail(E_CONFIG, "oracle: hprime > 255 unsupported");
   t->hprime = hprime;
   t->gamma = gamma;
+  t->nv = nv;
   t->count = 0;
-  const size_t np = (size_t)(total - 1 - h);
+  const size_t np = (size_t)(total - 1 - (uint64_t)h * nv);
   t->len = malloc(np ? np : 1);
   t->pos = malloc((np ? np : 1) * gamma);
+  t->vix = malloc((np ? np : 1) * gamma);
   uint8_t support[256];
   if (gamma >= 2) dfs(t, support, 0, 0);
   return OK;
@@ -444,30 +555,49 @@ static int tmpl_build(tmpl_t* t, uint32_t h, uint32_t hprime, uint32_t gamma,
 static void tmpl_free(tmpl_t* t) {
   free(t->len);
   free(t->pos);
+  free(t->vix);
 }
 
-/* StateTemplate::instantiate, truncation.cpp:153-169, as (count, units) lists:
- * zero state, H singletons, then patterns mapped through the candidates. */
+/* StateTemplate::instantiate, truncation.cpp:153-169, as (count, units,
+ * values) lists: zero state, the (h, v) singletons over all H, then the
+ * patterns mapped through the candidates. */
 typedef struct {
   size_t n;
   uint8_t* len;   /* [n] */
-  uint32_t* act;  /* [n * gamma_max] ascending unit indices */
+  uint32_t* act;  /* [n * stride] ascending unit indices */
+  uint8_t* vix;   /* [n * stride] value indices */
   uint32_t stride;
 } states_t;
 
-static void instantiate(const tmpl_t* t, uint32_t h, const uint32_t* cand,
-                        states_t* s) {
+static void states_alloc(states_t* s, size_t total, uint32_t gamma) {
+  s->stride = gamma;
+  s->len = malloc(total);
+  s->act = malloc(total * gamma * sizeof(uint32_t));
+  s->vix = malloc(total * gamma);
+}
+
+static void states_free(states_t* s) {
+  free(s->len);
+  free(s->act);
+  free(s->vix);
+}
+
+static void instantiate(const tmpl_t* t, uint32_t h, const uint32_t* cand, states_t* s) {
   size_t k = 0;
   s->len[k++] = 0;
-  for (uint32_t u = 0; u < h; ++u) {
-    s->len[k] = 1;
-    s->act[k * s->stride] = u;
-    ++k;
-  }
+  for (uint32_t u = 0; u < h; ++u)
+    for (uint32_t v = 0; v < t->nv; ++v) {
+      s->len[k] = 1;
+      s->act[k * s->stride] = u;
+      s->vix[k * s->stride] = (uint8_t)v;
+      ++k;
+    }
   for (size_t p = 0; p < t->count; ++p) {
     s->len[k] = t->len[p];
-    for (uint32_t a = 0; a < t->len[p]; ++a)
+    for (uint32_t a = 0; a < t->len[p]; ++a) {
       s->act[k * s->stride + a] = cand[t->pos[p * t->gamma + a]];
+      s->vix[k * s->stride + a] = t->vix[p * t->gamma + a];
+    }
     ++k;
   }
   s->n = k;
@@ -482,13 +612,10 @@ int bsc_enumerate_binary(const uint32_t* cand, uint32_t hprime, uint32_t h,
     if (cand[i] >= h)
       return fail(E_CONFIG, "enumerate states: candidate index out of range");
   tmpl_t t;
-  int rc = tmpl_build(&t, h, hprime, gamma, 1000000);
+  int rc = tmpl_build(&t, h, hprime, gamma, 1, 1000000);
   if (rc) return rc;
   states_t s;
-  const size_t total = 1 + h + t.count;
-  s.stride = gamma;
-  s.len = malloc(total);
-  s.act = malloc(total * gamma * sizeof(uint32_t));
+  states_alloc(&s, 1 + h + t.count, gamma);
   instantiate(&t, h, cand, &s);
   *count = s.n;
   if (out) {
@@ -496,8 +623,7 @@ int bsc_enumerate_binary(const uint32_t* cand, uint32_t hprime, uint32_t h,
     for (size_t i = 0; i < s.n; ++i)
       for (uint32_t a = 0; a < s.len[i]; ++a) out[i * h + s.act[i * s.stride + a]] = 1.0;
   }
-  free(s.len);
-  free(s.act);
+  states_free(&s);
   tmpl_free(&t);
   return OK;
 }
@@ -507,18 +633,19 @@ static double gauss_log_norm(size_t dim, double sigma2) { /* :26-28 */
   return -0.5 * (double)dim * (K_LOG_2PI + log(sigma2));
 }
 
-/* log_prior :150-166 + log_joint :168-178 (BSC). */
-int bsc_log_joint(uint32_t d, uint32_t h, const double* w, double pi,
-                  double sigma2, const double* y, const double* s, double* out) {
-  const double lp1 = log(pi), lp0 = log(1.0 - pi);
+/* log_prior :150-166 + log_joint :168-178. */
+static int log_joint_v(uint32_t d, uint32_t h, const double* w, double sigma2, const vtab_t* vt,
+                       const char* nm, const double* y, const double* s, double* out) {
   double prior = 0.0;
   for (uint32_t j = 0; j < h; ++j) {
     if (s[j] == 0.0) {
-      prior += lp0;
+      prior += vt->log_p0;
       continue;
     }
-    if (s[j] != 1.0) return fail(E_CONFIG, "bsc: latent value outside the alphabet");
-    prior += lp1;
+    uint32_t k = 0;
+    while (k < vt->nv && vt->values[k] != s[j]) ++k;
+    if (k == vt->nv) return fail(E_CONFIG, "%s: latent value outside the alphabet", nm);
+    prior += vt->log_probs[k];
   }
   double resid = 0.0;
   for (uint32_t i = 0; i < d; ++i) {
@@ -531,17 +658,27 @@ int bsc_log_joint(uint32_t d, uint32_t h, const double* w, double pi,
   return OK;
 }
 
+int bsc_log_joint(uint32_t d, uint32_t h, const double* w, double pi,
+                  double sigma2, const double* y, const double* s, double* out) {
+  const prior_t pr = {0, 0, NULL, NULL, pi};
+  vtab_t vt;
+  value_table(&pr, &vt);
+  return log_joint_v(d, h, w, sigma2, &vt, "bsc", y, s, out);
+}
+
 /* Per-shard accumulators in the field order of linear_discrete.cpp:211-217. */
 typedef struct {
   double *sum_s, *sum_ssT, *sum_y_sT;
-  double counts, sum_y2, log_partition;
+  double counts[LD_MAX_V];
+  double sum_y2, log_partition;
   uint64_t points;
 } stats_t;
 
 typedef struct {
   uint32_t d, h, hprime, gamma;
   const double* w;
-  double pi, sigma2, temperature;
+  double sigma2, temperature;
+  vtab_t vt;
   const double* y;
   const double* gram; /* W^T W, left-to-right over d (linear_discrete.cpp:220) */
   const double* wt;   /* W^T, H x D */
@@ -552,7 +689,8 @@ static void stats_alloc(stats_t* s, uint32_t d, uint32_t h) {
   s->sum_s = calloc(h, sizeof(double));
   s->sum_ssT = calloc((size_t)h * h, sizeof(double));
   s->sum_y_sT = calloc((size_t)d * h, sizeof(double));
-  s->counts = s->sum_y2 = s->log_partition = 0.0;
+  for (int k = 0; k < LD_MAX_V; ++k) s->counts[k] = 0.0;
+  s->sum_y2 = s->log_partition = 0.0;
   s->points = 0;
 }
 
@@ -573,24 +711,36 @@ static void gram_of(const double* w, uint32_t d, uint32_t h, double* wt, double*
     }
 }
 
-/* LinearDiscreteModel::estep_impl, linear_discrete.cpp:202-325, BSC value
- * table {1} (:75-79). If `map_states` is non-NULL the inference readout of
- * :313-322 is written too. */
+/* Selection scores, linear_discrete.cpp:244-252: max over the non-zero
+ * alphabet of log p_v + (2 v b − v² G_uu)·inv2s. */
+static void scores_of(const vtab_t* vt, const double* b, const double* gram, uint32_t h, double inv2s,
+                      double* scores) {
+  for (uint32_t u = 0; u < h; ++u) {
+    double best = -INFINITY;
+    for (uint32_t k = 0; k < vt->nv; ++k) {
+      const double v = vt->values[k];
+      best = dmax(best, vt->log_probs[k] + (2.0 * v * b[u] - v * v * gram[(size_t)u * h + u]) * inv2s);
+    }
+    scores[u] = best;
+  }
+}
+
+/* LinearDiscreteModel::estep_impl, linear_discrete.cpp:202-325. If
+ * `map_states` is non-NULL the inference readout of :313-322 is written too. */
 static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
                       stats_t* st, double* map_states, double* map_mass,
                       double* expected) {
   const uint32_t d = c->d, h = c->h;
+  const vtab_t* vt = &c->vt;
   const double inv2s = 1.0 / (2.0 * c->sigma2);
   const double norm_const = gauss_log_norm(d, c->sigma2);
-  const double log_p1 = log(c->pi), log_p0 = log(1.0 - c->pi);
-  const double dlp = log_p1 - log_p0;
-  const double zero_prior = (double)h * log_p0;
+  double dlp[LD_MAX_V];
+  for (uint32_t k = 0; k < vt->nv; ++k) dlp[k] = vt->log_probs[k] - vt->log_p0;
+  const double zero_prior = (double)h * vt->log_p0;
 
-  const size_t total = 1 + h + c->tmpl->count;
+  const size_t total = 1 + (size_t)h * vt->nv + c->tmpl->count;
   states_t s;
-  s.stride = c->gamma;
-  s.len = malloc(total);
-  s.act = malloc(total * c->gamma * sizeof(uint32_t));
+  states_alloc(&s, total, c->gamma);
   double* b = malloc(h * sizeof(double));
   double* scores = malloc(h * sizeof(double));
   double* es = malloc(h * sizeof(double));
@@ -609,12 +759,7 @@ static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
     }
     double y2 = 0.0; /* :242 */
     for (uint32_t t = 0; t < d; ++t) y2 += y[t] * y[t];
-    for (uint32_t u = 0; u < h; ++u) { /* :244-252 */
-      const double v = 1.0;
-      double best = -INFINITY;
-      best = dmax(best, log_p1 + (2.0 * v * b[u] - v * v * c->gram[(size_t)u * h + u]) * inv2s);
-      scores[u] = best;
-    }
+    scores_of(vt, b, c->gram, h, inv2s, scores); /* :244-252 */
     rc = select_cands(scores, h, c->hprime, cand, scratch); /* :253 */
     if (rc) break;
     instantiate(c->tmpl, h, cand, &s); /* :254 */
@@ -622,15 +767,16 @@ static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
     const double base = zero_prior + norm_const - y2 * inv2s; /* :256 */
     for (size_t i = 0; i < s.n; ++i) {                      /* :257-270 */
       const uint32_t* act = s.act + i * s.stride;
+      const uint8_t* vix = s.vix + i * s.stride;
       double prior = 0.0, lin = 0.0, quad = 0.0;
       for (uint32_t a = 0; a < s.len[i]; ++a) {
         const uint32_t ha = act[a];
-        const double va = 1.0;
-        prior += dlp;
+        const double va = vt->values[vix[a]];
+        prior += dlp[vix[a]];
         lin += va * b[ha];
         quad += va * va * c->gram[(size_t)ha * h + ha];
         for (uint32_t cc = a + 1; cc < s.len[i]; ++cc)
-          quad += 2.0 * va * 1.0 * c->gram[(size_t)ha * h + act[cc]];
+          quad += 2.0 * va * vt->values[vix[cc]] * c->gram[(size_t)ha * h + act[cc]];
       }
       lj[i] = base + prior + (2.0 * lin - quad) * inv2s;
     }
@@ -655,14 +801,15 @@ static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
     for (size_t i = 0; i < s.n; ++i) {
       const double qi = q[i];
       const uint32_t* act = s.act + i * s.stride;
+      const uint8_t* vix = s.vix + i * s.stride;
       for (uint32_t a = 0; a < s.len[i]; ++a) {
         const uint32_t ha = act[a];
-        const double va = 1.0;
+        const double va = vt->values[vix[a]];
         es[ha] += qi * va;
-        st->counts += qi;
+        st->counts[vix[a]] += qi;
         st->sum_ssT[(size_t)ha * h + ha] += qi * va * va;
         for (uint32_t cc = a + 1; cc < s.len[i]; ++cc) {
-          const double cross = qi * va * 1.0;
+          const double cross = qi * va * vt->values[vix[cc]];
           st->sum_ssT[(size_t)ha * h + act[cc]] += cross;
           st->sum_ssT[(size_t)act[cc] * h + ha] += cross;
         }
@@ -684,12 +831,11 @@ static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
         if (q[i] > q[best]) best = i;
       map_mass[n] = q[best];
       for (uint32_t a = 0; a < s.len[best]; ++a)
-        map_states[n * h + s.act[best * s.stride + a]] = 1.0;
+        map_states[n * h + s.act[best * s.stride + a]] = vt->values[s.vix[best * s.stride + a]];
       for (uint32_t j = 0; j < h; ++j) expected[n * h + j] = es[j];
     }
   }
-  free(s.len);
-  free(s.act);
+  states_free(&s);
   free(b);
   free(scores);
   free(es);
@@ -701,16 +847,19 @@ static int estep_rows(const ctx_t* c, uint64_t row_begin, uint64_t row_end,
 }
 
 static int ctx_init(ctx_t* c, tmpl_t* t, uint32_t d, uint32_t h, uint32_t hprime,
-                    uint32_t gamma, const double* w, double pi, double sigma2,
+                    uint32_t gamma, const double* w, const prior_t* pr, double sigma2,
                     double temperature, const double* y) {
-  int rc = validate_params(d, h, w, pi, sigma2);
+  int rc = validate_ld(d, h, w, sigma2, pr);
   if (rc) return rc;
-  rc = tmpl_build(t, h, hprime, gamma, 1000000);
+  vtab_t vt;
+  rc = value_table(pr, &vt);
+  if (rc) return rc;
+  rc = tmpl_build(t, h, hprime, gamma, vt.nv, 1000000);
   if (rc) return rc;
   double* wt = malloc((size_t)d * h * sizeof(double));
   double* gram = malloc((size_t)h * h * sizeof(double));
   gram_of(w, d, h, wt, gram);
-  *c = (ctx_t){d, h, hprime, gamma, w, pi, sigma2, temperature, y, gram, wt, t};
+  *c = (ctx_t){d, h, hprime, gamma, w, sigma2, temperature, vt, y, gram, wt, t};
   return OK;
 }
 
@@ -720,13 +869,13 @@ static void ctx_free(ctx_t* c, tmpl_t* t) {
   tmpl_free(t);
 }
 
-static void stats_out(const stats_t* st, uint32_t d, uint32_t h, double* sum_s,
+static void stats_out(const stats_t* st, uint32_t d, uint32_t h, uint32_t nv, double* sum_s,
                       double* sum_ssT, double* sum_y_sT, double* value_counts,
                       double* scalars) {
   if (sum_s) memcpy(sum_s, st->sum_s, h * sizeof(double));
   if (sum_ssT) memcpy(sum_ssT, st->sum_ssT, (size_t)h * h * sizeof(double));
   if (sum_y_sT) memcpy(sum_y_sT, st->sum_y_sT, (size_t)d * h * sizeof(double));
-  if (value_counts) value_counts[0] = st->counts;
+  if (value_counts) memcpy(value_counts, st->counts, nv * sizeof(double));
   if (scalars) {
     scalars[0] = st->sum_y2;
     scalars[1] = st->log_partition;
@@ -735,24 +884,34 @@ static void stats_out(const stats_t* st, uint32_t d, uint32_t h, double* sum_s,
 }
 
 /* estep_stats, linear_discrete.cpp:327-334 */
+int ld_estep_stats(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                   double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                   const double* w, double sigma2, double temperature, const double* y,
+                   uint64_t n, uint64_t row_begin, uint64_t row_end, double* sum_s,
+                   double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars) {
+  if (row_end < row_begin || row_end > n) return fail(E_CONFIG, "bad row range");
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
+  ctx_t c;
+  tmpl_t t;
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, &pr, sigma2, temperature, y);
+  if (rc) return rc;
+  stats_t st;
+  stats_alloc(&st, d, h);
+  rc = estep_rows(&c, row_begin, row_end, &st, NULL, NULL, NULL);
+  if (!rc) stats_out(&st, d, h, c.vt.nv, sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
+  stats_free(&st);
+  ctx_free(&c, &t);
+  return rc;
+}
+
 int bsc_estep_stats(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
                     const double* w, double pi, double sigma2,
                     double temperature, const double* y, uint64_t n,
                     uint64_t row_begin, uint64_t row_end, double* sum_s,
                     double* sum_ssT, double* sum_y_sT, double* value_counts,
                     double* scalars) {
-  if (row_end < row_begin || row_end > n) return fail(E_CONFIG, "bad row range");
-  ctx_t c;
-  tmpl_t t;
-  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
-  if (rc) return rc;
-  stats_t st;
-  stats_alloc(&st, d, h);
-  rc = estep_rows(&c, row_begin, row_end, &st, NULL, NULL, NULL);
-  if (!rc) stats_out(&st, d, h, sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
-  stats_free(&st);
-  ctx_free(&c, &t);
-  return rc;
+  return ld_estep_stats(0, NULL, NULL, 0, pi, d, h, hprime, gamma, w, sigma2, temperature, y, n,
+                        row_begin, row_end, sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
 }
 
 /* Left-looking Cholesky + per-column substitution, the order fixed by
@@ -787,18 +946,18 @@ static void chol_solve(const double* l, size_t n, double* v) {
   }
 }
 
-/* LinearDiscreteModel::mstep, linear_discrete.cpp:336-408 (BSC branch :373-376). */
-int bsc_mstep(uint32_t d, uint32_t h, const double* w_prev, double pi_prev,
-              double sigma2_prev, const double* sum_s, const double* sum_ssT,
-              const double* sum_y_sT, const double* value_counts,
-              const double* scalars, double* w_out, double* pi_out,
-              double* sigma2_out) {
+#define K_MIN_CATEGORICAL 1e-9 /* model.hpp:34 */
+
+/* LinearDiscreteModel::mstep, linear_discrete.cpp:336-408 (family branches
+ * :371-405). `probs_out` (dsc) is aligned with the alphabet. */
+int ld_mstep(uint32_t family, const double* alpha, uint32_t nalpha, uint32_t d, uint32_t h,
+             const double* w_prev, const double* sum_s, const double* sum_ssT,
+             const double* sum_y_sT, const double* value_counts, const double* scalars,
+             double* w_out, double* pi_out, double* probs_out, double* sigma2_out) {
   (void)sum_s;
-  (void)pi_prev;
-  (void)sigma2_prev;
   const uint64_t points = (uint64_t)scalars[2];
   const double n = (double)points, dd = (double)d, nh = n * (double)h;
-  if (points == 0) return fail(E_CONFIG, "bsc: mstep without data");
+  if (points == 0) return fail(E_CONFIG, "%s: mstep without data", family_name(family));
   if (w_out != w_prev) memcpy(w_out, w_prev, (size_t)d * h * sizeof(double));
 
   double trace = 0.0; /* :349 */
@@ -833,8 +992,51 @@ int bsc_mstep(uint32_t d, uint32_t h, const double* w_prev, double pi_prev,
       t3 += acc * sum_ssT[(size_t)i * h + j];
     }
   *sigma2_out = dmax((t1 - 2.0 * t2 + t3) / (n * dd), K_MIN_SIGMA2);
-  *pi_out = dmin(dmax(value_counts[0] / nh, K_MIN_PI), 1.0 - K_MIN_PI);
+
+  switch (family) {
+    case 0: /* :373-376 */
+      if (pi_out) *pi_out = dmin(dmax(value_counts[0] / nh, K_MIN_PI), 1.0 - K_MIN_PI);
+      break;
+    case 1: /* :377-381 */
+      if (pi_out) *pi_out = dmin(dmax((value_counts[0] + value_counts[1]) / nh, K_MIN_PI), 1.0 - K_MIN_PI);
+      break;
+    default: { /* :382-404 */
+      double nonzero_mass = 0.0;
+      uint32_t k = 0;
+      for (uint32_t i = 0; i < nalpha; ++i) {
+        if (alpha[i] == 0.0) continue;
+        probs_out[i] = value_counts[k] / nh;
+        nonzero_mass += probs_out[i];
+        ++k;
+      }
+      for (uint32_t i = 0; i < nalpha; ++i)
+        if (alpha[i] == 0.0) probs_out[i] = 1.0 - nonzero_mass;
+      int floored = 0;
+      for (uint32_t i = 0; i < nalpha; ++i)
+        if (probs_out[i] < K_MIN_CATEGORICAL) {
+          probs_out[i] = K_MIN_CATEGORICAL;
+          floored = 1;
+        }
+      if (floored) {
+        double tot = 0.0;
+        for (uint32_t i = 0; i < nalpha; ++i) tot += probs_out[i];
+        for (uint32_t i = 0; i < nalpha; ++i) probs_out[i] /= tot;
+      }
+      break;
+    }
+  }
   return OK;
+}
+
+int bsc_mstep(uint32_t d, uint32_t h, const double* w_prev, double pi_prev,
+              double sigma2_prev, const double* sum_s, const double* sum_ssT,
+              const double* sum_y_sT, const double* value_counts,
+              const double* scalars, double* w_out, double* pi_out,
+              double* sigma2_out) {
+  (void)pi_prev;
+  (void)sigma2_prev;
+  return ld_mstep(0, NULL, 0, d, h, w_prev, sum_s, sum_ssT, sum_y_sT, value_counts, scalars, w_out,
+                  pi_out, NULL, sigma2_out);
 }
 
 /* ------------------------------------------------- map_reduce over shards */
@@ -871,15 +1073,16 @@ static void* pool_worker(void* arg) {
 
 /* LinearDiscreteModel::step (:410-427) via map_reduce (parallel.cpp:109-158):
  * per-shard stats, ordered fold (SuffStats::combine, :89-107), then mstep. */
-int bsc_step(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
-             const double* w, double pi, double sigma2, double temperature,
-             const double* y, uint64_t n, uint32_t shards, uint32_t workers,
-             double* w_out, double* pi_out, double* sigma2_out,
-             double* free_energy) {
+int ld_step(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+            double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+            const double* w, double sigma2, double temperature, const double* y, uint64_t n,
+            uint32_t shards, uint32_t workers, double* w_out, double* pi_out,
+            double* probs_out, double* sigma2_out, double* free_energy) {
   if (shards == 0 || workers == 0) return fail(E_CONFIG, "shard plan: shards and workers must be >= 1");
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
   ctx_t c;
   tmpl_t t;
-  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, &pr, sigma2, temperature, y);
   if (rc) return rc;
   pool_t p;
   p.c = &c;
@@ -909,15 +1112,14 @@ int bsc_step(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
       for (uint32_t j = 0; j < h; ++j) tot->sum_s[j] += o->sum_s[j];
       for (size_t j = 0; j < (size_t)h * h; ++j) tot->sum_ssT[j] += o->sum_ssT[j];
       for (size_t j = 0; j < (size_t)d * h; ++j) tot->sum_y_sT[j] += o->sum_y_sT[j];
-      tot->counts += o->counts;
+      for (uint32_t k = 0; k < c.vt.nv; ++k) tot->counts[k] += o->counts[k];
       tot->sum_y2 += o->sum_y2;
       tot->log_partition += o->log_partition;
       tot->points += o->points;
     }
     double scal[3] = {tot->sum_y2, tot->log_partition, (double)tot->points};
-    double vc = tot->counts;
-    rc = bsc_mstep(d, h, w, pi, sigma2, tot->sum_s, tot->sum_ssT, tot->sum_y_sT,
-                   &vc, scal, w_out, pi_out, sigma2_out);
+    rc = ld_mstep(family, alpha, nalpha, d, h, w, tot->sum_s, tot->sum_ssT, tot->sum_y_sT,
+                  tot->counts, scal, w_out, pi_out, probs_out, sigma2_out);
     *free_energy = tot->log_partition;
   }
   for (uint32_t i = 0; i < shards; ++i) stats_free(&p.partial[i]);
@@ -929,42 +1131,65 @@ int bsc_step(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
   return rc;
 }
 
+int bsc_step(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+             const double* w, double pi, double sigma2, double temperature,
+             const double* y, uint64_t n, uint32_t shards, uint32_t workers,
+             double* w_out, double* pi_out, double* sigma2_out,
+             double* free_energy) {
+  return ld_step(0, NULL, NULL, 0, pi, d, h, hprime, gamma, w, sigma2, temperature, y, n, shards,
+                 workers, w_out, pi_out, NULL, sigma2_out, free_energy);
+}
+
 /* Per-point candidate sets exactly as estep_impl selects them (:240-253). */
-int bsc_candidates(uint32_t d, uint32_t h, uint32_t hprime, const double* w,
-                   double pi, double sigma2, const double* y, uint64_t n,
-                   uint32_t* out) {
-  int rc = validate_params(d, h, w, pi, sigma2);
+int ld_candidates(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                  double pi, uint32_t d, uint32_t h, uint32_t hprime, const double* w,
+                  double sigma2, const double* y, uint64_t n, uint32_t* out) {
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
+  int rc = validate_ld(d, h, w, sigma2, &pr);
+  if (rc) return rc;
+  vtab_t vt;
+  rc = value_table(&pr, &vt);
   if (rc) return rc;
   double* wt = malloc((size_t)d * h * sizeof(double));
   double* gram = malloc((size_t)h * h * sizeof(double));
+  double* b = malloc(h * sizeof(double));
   double* scores = malloc(h * sizeof(double));
   keyed_t* scratch = malloc(h * sizeof(keyed_t));
   gram_of(w, d, h, wt, gram);
-  const double inv2s = 1.0 / (2.0 * sigma2), lp = log(pi);
+  const double inv2s = 1.0 / (2.0 * sigma2);
   for (uint64_t i = 0; i < n && !rc; ++i) {
     const double* yy = y + i * d;
     for (uint32_t u = 0; u < h; ++u) {
       double acc = 0.0;
       for (uint32_t t = 0; t < d; ++t) acc += wt[(size_t)u * d + t] * yy[t];
-      scores[u] = dmax(-INFINITY, lp + (2.0 * 1.0 * acc - 1.0 * 1.0 * gram[(size_t)u * h + u]) * inv2s);
+      b[u] = acc;
     }
+    scores_of(&vt, b, gram, h, inv2s, scores);
     rc = select_cands(scores, h, hprime, out + i * hprime, scratch);
   }
   free(wt);
   free(gram);
+  free(b);
   free(scores);
   free(scratch);
   return rc;
 }
 
+int bsc_candidates(uint32_t d, uint32_t h, uint32_t hprime, const double* w,
+                   double pi, double sigma2, const double* y, uint64_t n,
+                   uint32_t* out) {
+  return ld_candidates(0, NULL, NULL, 0, pi, d, h, hprime, w, sigma2, y, n, out);
+}
+
 /* LinearDiscreteModel::inference, linear_discrete.cpp:429-450 (T = 1). */
-int bsc_inference(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
-                  const double* w, double pi, double sigma2, const double* y,
-                  uint64_t n, double* map_states, double* map_mass,
-                  double* expected) {
+int ld_inference(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                 double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                 const double* w, double sigma2, const double* y, uint64_t n,
+                 double* map_states, double* map_mass, double* expected) {
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
   ctx_t c;
   tmpl_t t;
-  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, pi, sigma2, 1.0, y);
+  int rc = ctx_init(&c, &t, d, h, hprime, gamma, w, &pr, sigma2, 1.0, y);
   if (rc) return rc;
   memset(map_states, 0, n * h * sizeof(double));
   stats_t st;
@@ -975,32 +1200,109 @@ int bsc_inference(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
   return rc;
 }
 
-/* exact_log_likelihood, linear_discrete.cpp:481-508. */
-int bsc_exact_log_likelihood(uint32_t d, uint32_t h, const double* w, double pi,
-                             double sigma2, const double* y, uint64_t n,
-                             double* out) {
-  int rc = validate_params(d, h, w, pi, sigma2);
+int bsc_inference(uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                  const double* w, double pi, double sigma2, const double* y,
+                  uint64_t n, double* map_states, double* map_mass,
+                  double* expected) {
+  return ld_inference(0, NULL, NULL, 0, pi, d, h, hprime, gamma, w, sigma2, y, n, map_states,
+                      map_mass, expected);
+}
+
+/* exact_log_likelihood, linear_discrete.cpp:481-508: the full state space is
+ * the truncated enumeration with hprime = gamma = H. */
+int ld_exact_log_likelihood(uint32_t family, const double* alpha, const double* probs,
+                            uint32_t nalpha, double pi, uint32_t d, uint32_t h,
+                            const double* w, double sigma2, const double* y, uint64_t n,
+                            double* out) {
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
+  int rc = validate_ld(d, h, w, sigma2, &pr);
   if (rc) return rc;
-  const uint64_t count = state_count(h, h, h);
+  vtab_t vt;
+  rc = value_table(&pr, &vt);
+  if (rc) return rc;
+  const uint64_t count = state_count_v(h, h, h, vt.nv);
   if (count > (1u << 22))
-    return fail(E_CONFIG, "bsc: state space too large for exact evaluation");
+    return fail(E_CONFIG, "%s: state space too large for exact evaluation", family_name(family));
   uint32_t* all = malloc(h * sizeof(uint32_t));
   for (uint32_t i = 0; i < h; ++i) all[i] = i;
-  double* dense = malloc(count * h * sizeof(double));
-  uint64_t got;
-  rc = bsc_enumerate_binary(all, h, h, h, dense, &got);
+  tmpl_t t;
+  rc = tmpl_build(&t, h, h, h, vt.nv, 1u << 22);
+  if (rc) {
+    free(all);
+    return rc;
+  }
+  states_t s;
+  states_alloc(&s, count, h);
+  instantiate(&t, h, all, &s);
+  double* dense = malloc(h * sizeof(double));
   double* lj = malloc(count * sizeof(double));
   double total = 0.0;
   for (uint64_t i = 0; i < n && !rc; ++i) {
-    for (uint64_t s = 0; s < got && !rc; ++s)
-      rc = bsc_log_joint(d, h, w, pi, sigma2, y + i * d, dense + s * h, &lj[s]);
+    for (size_t k = 0; k < s.n && !rc; ++k) {
+      memset(dense, 0, h * sizeof(double));
+      for (uint32_t a = 0; a < s.len[k]; ++a)
+        dense[s.act[k * s.stride + a]] = vt.values[s.vix[k * s.stride + a]];
+      rc = log_joint_v(d, h, w, sigma2, &vt, family_name(family), y + i * d, dense, &lj[k]);
+    }
     double l;
-    if (!rc) rc = lse(lj, got, &l);
+    if (!rc) rc = lse(lj, s.n, &l);
     if (!rc) total += l;
   }
   *out = total;
   free(all);
   free(dense);
   free(lj);
+  states_free(&s);
+  tmpl_free(&t);
   return rc;
+}
+
+int bsc_exact_log_likelihood(uint32_t d, uint32_t h, const double* w, double pi,
+                             double sigma2, const double* y, uint64_t n,
+                             double* out) {
+  return ld_exact_log_likelihood(0, NULL, NULL, 0, pi, d, h, w, sigma2, y, n, out);
+}
+
+/* LinearDiscreteModel::generate, linear_discrete.cpp:452-479 (TSC / DSC
+ * draws; BSC is bsc_generate). mean = W s summed left to right over h. */
+static uint32_t rng_categorical(rng_t* r, const double* probs, uint32_t k) {
+  /* RngStream::categorical, core.cpp:80-91 */
+  double total = 0.0;
+  for (uint32_t i = 0; i < k; ++i) total += probs[i];
+  const double u = rng_uniform01(r) * total;
+  double acc = 0.0;
+  for (uint32_t i = 0; i + 1 < k; ++i) {
+    acc += probs[i];
+    if (u < acc) return i;
+  }
+  return k - 1;
+}
+
+int ld_generate(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                double pi, uint32_t d, uint32_t h, const double* w, double sigma2, uint64_t n,
+                uint64_t seed, double* y_out) {
+  if (family == 0) return bsc_generate(d, h, w, pi, sigma2, n, seed, y_out);
+  const prior_t pr = {family, nalpha, alpha, probs, pi};
+  int rc = validate_ld(d, h, w, sigma2, &pr);
+  if (rc) return rc;
+  const double noise_std = sqrt(sigma2);
+  double* s = malloc(h * sizeof(double));
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint64_t i = 0; i < n; ++i) {
+    for (uint32_t j = 0; j < h; ++j) {
+      if (family == 1)
+        s[j] = rng_bernoulli(&r, pi) ? (rng_bernoulli(&r, 0.5) ? 1.0 : -1.0) : 0.0;
+      else
+        s[j] = alpha[rng_categorical(&r, probs, nalpha)];
+    }
+    for (uint32_t di = 0; di < d; ++di) {
+      double acc = 0.0;
+      const double* row = w + (size_t)di * h;
+      for (uint32_t j = 0; j < h; ++j) acc += row[j] * s[j];
+      y_out[i * d + di] = acc + noise_std * rng_normal(&r);
+    }
+  }
+  free(s);
+  return OK;
 }

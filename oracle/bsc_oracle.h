@@ -80,6 +80,40 @@ int bsc_exact_log_likelihood(uint32_t d, uint32_t h, const double* w, double pi,
                              double sigma2, const double* y, uint64_t n,
                              double* out);
 
+/* Linear discrete families (linear_discrete.cpp): family 0 = bsc, 1 = tsc,
+ * 2 = dsc. `alpha`/`probs`/`nalpha`: the dsc alphabet (ascending, contains 0)
+ * and its probabilities (NULL/0 otherwise); `pi` for bsc/tsc. value_counts
+ * has one entry per non-zero value; probs_out (dsc) is aligned with alpha. */
+int ld_state_count(uint32_t h, uint32_t hprime, uint32_t gamma, uint32_t nv, uint64_t* out);
+int ld_estep_stats(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                   double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                   const double* w, double sigma2, double temperature, const double* y,
+                   uint64_t n, uint64_t row_begin, uint64_t row_end, double* sum_s,
+                   double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars);
+int ld_mstep(uint32_t family, const double* alpha, uint32_t nalpha, uint32_t d, uint32_t h,
+             const double* w_prev, const double* sum_s, const double* sum_ssT,
+             const double* sum_y_sT, const double* value_counts, const double* scalars,
+             double* w_out, double* pi_out, double* probs_out, double* sigma2_out);
+int ld_step(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+            double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+            const double* w, double sigma2, double temperature, const double* y, uint64_t n,
+            uint32_t shards, uint32_t workers, double* w_out, double* pi_out,
+            double* probs_out, double* sigma2_out, double* free_energy);
+int ld_candidates(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                  double pi, uint32_t d, uint32_t h, uint32_t hprime, const double* w,
+                  double sigma2, const double* y, uint64_t n, uint32_t* out);
+int ld_inference(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                 double pi, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                 const double* w, double sigma2, const double* y, uint64_t n,
+                 double* map_states, double* map_mass, double* expected);
+int ld_exact_log_likelihood(uint32_t family, const double* alpha, const double* probs,
+                            uint32_t nalpha, double pi, uint32_t d, uint32_t h,
+                            const double* w, double sigma2, const double* y, uint64_t n,
+                            double* out);
+int ld_generate(uint32_t family, const double* alpha, const double* probs, uint32_t nalpha,
+                double pi, uint32_t d, uint32_t h, const double* w, double sigma2, uint64_t n,
+                uint64_t seed, double* y_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,6 +52,39 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+FAMILIES = {"bsc": 0, "tsc": 1, "dsc": 2}
+
+
+class Prior:
+    """Value prior of a linear discrete family (linear_discrete.cpp:71-97):
+    ``pi`` for bsc/tsc; the dsc alphabet (ascending, containing 0) and its
+    probabilities for dsc."""
+
+    def __init__(self, family: str, pi: float = 0.1, alpha=None, probs=None):
+        self.family = family
+        self.code = FAMILIES[family]
+        self.pi = float(pi) if pi is not None else 0.0
+        self.alpha = None if alpha is None else _f64(alpha)
+        self.probs = None if probs is None else _f64(probs)
+
+    @property
+    def values(self):
+        """The non-zero alphabet in kernel order."""
+        if self.family == "bsc":
+            return np.array([1.0])
+        if self.family == "tsc":
+            return np.array([-1.0, 1.0])
+        return self.alpha[self.alpha != 0.0]
+
+    @property
+    def nv(self) -> int:
+        return len(self.values)
+
+    def args(self):
+        n = 0 if self.alpha is None else len(self.alpha)
+        return [_u32(self.code), _p(self.alpha), _p(self.probs), _u32(n), _dbl(self.pi)]
+
+
 class Oracle:
     """One CPU oracle library (``kind`` = "port" or "ref")."""
 
@@ -68,8 +101,11 @@ class Oracle:
     def available(kind: str) -> bool:
         return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
 
-    def _call(self, name, *args):
-        fn = getattr(self.lib, self.pre + name)
+    def _lcall(self, name, *args):
+        self._call(("ld_" if self.kind == "ref" else "") + name, *args, pre="ld_" if self.kind == "port" else None)
+
+    def _call(self, name, *args, pre=None):
+        fn = getattr(self.lib, (self.pre if pre is None else pre) + name)
         fn.restype = _int
         rc = fn(*args)
         if rc != 0:
@@ -229,6 +265,92 @@ class Oracle:
         self._call("exact_log_likelihood", _u32(w.shape[0]), _u32(w.shape[1]), _p(w), _dbl(pi), _dbl(sigma2),
                    _p(y), _u64(y.shape[0]), C.byref(out))
         return out.value
+
+
+    # ------------------------------------------- linear discrete families
+    def ld_state_count(self, h, hprime, gamma, nv):
+        out = _u64()
+        self._lcall("state_count", _u32(h), _u32(hprime), _u32(gamma), _u32(nv), C.byref(out))
+        return out.value
+
+    def ld_estep_stats(self, prior: Prior, w, sigma2, y, hprime, gamma, temperature=1.0, rows=None):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        b, e = (0, n) if rows is None else rows
+        st = dict(sum_s=np.empty(h), sum_ssT=np.empty((h, h)), sum_y_sT=np.empty((d, h)),
+                  value_counts=np.empty(prior.nv), scalars=np.empty(3))
+        self._lcall("estep_stats", *prior.args(), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w),
+                    _dbl(sigma2), _dbl(temperature), _p(y), _u64(n), _u64(b), _u64(e), _p(st["sum_s"]),
+                    _p(st["sum_ssT"]), _p(st["sum_y_sT"]), _p(st["value_counts"]), _p(st["scalars"]))
+        sc = st.pop("scalars")
+        st.update(sum_y2=sc[0], log_partition=sc[1], points=int(sc[2]))
+        return st
+
+    def ld_mstep(self, prior: Prior, stats, w_prev, sigma2_prev):
+        """→ (W, pi, probs, sigma2); probs (dsc) aligned with the alphabet."""
+        w_prev = _f64(w_prev)
+        d, h = w_prev.shape
+        w = np.empty((d, h))
+        pi, s2 = _dbl(), _dbl()
+        na = 0 if prior.alpha is None else len(prior.alpha)
+        probs = np.empty(max(na, 1))
+        sc = np.array([stats["sum_y2"], stats["log_partition"], float(stats["points"])])
+        vc = _f64(np.atleast_1d(stats["value_counts"]))
+        tail = [_p(_f64(stats["sum_s"])), _p(_f64(stats["sum_ssT"])), _p(_f64(stats["sum_y_sT"])), _p(vc), _p(sc),
+                _p(w), C.byref(pi), _p(probs), C.byref(s2)]
+        if self.kind == "port":
+            self._lcall("mstep", _u32(prior.code), _p(prior.alpha), _u32(na), _u32(d), _u32(h), _p(w_prev), *tail)
+        else:
+            self._lcall("mstep", _u32(prior.code), _p(prior.alpha), _p(prior.probs), _u32(na), _dbl(prior.pi),
+                        _u32(d), _u32(h), _u32(prior.nv), _p(w_prev), _dbl(sigma2_prev), *tail)
+        return w, (None if prior.family == "dsc" else pi.value), (probs[:na] if na else None), s2.value
+
+    def ld_step(self, prior: Prior, w, sigma2, y, hprime, gamma, temperature=1.0, shards=1, workers=1):
+        """→ (W, pi, probs, sigma2, F)."""
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        wo = np.empty((d, h))
+        na = 0 if prior.alpha is None else len(prior.alpha)
+        probs = np.empty(max(na, 1))
+        pio, s2o, f = _dbl(), _dbl(), _dbl()
+        self._lcall("step", *prior.args(), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(sigma2),
+                    _dbl(temperature), _p(y), _u64(y.shape[0]), _u32(shards), _u32(workers), _p(wo),
+                    C.byref(pio), _p(probs), C.byref(s2o), C.byref(f))
+        return wo, (None if prior.family == "dsc" else pio.value), (probs[:na] if na else None), s2o.value, f.value
+
+    def ld_candidates(self, prior: Prior, w, sigma2, y, hprime):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        out = np.empty((y.shape[0], hprime), np.uint32)
+        self._lcall("candidates", *prior.args(), _u32(d), _u32(h), _u32(hprime), _p(w), _dbl(sigma2), _p(y),
+                    _u64(y.shape[0]), _p(out))
+        return out
+
+    def ld_inference(self, prior: Prior, w, sigma2, y, hprime, gamma):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        ms, mm, ex = np.empty((n, h)), np.empty(n), np.empty((n, h))
+        extra = [] if self.kind == "port" else [_u32(1)]
+        self._lcall("inference", *prior.args(), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(sigma2),
+                    _p(y), _u64(n), *extra, _p(ms), _p(mm), _p(ex))
+        return ms, mm, ex
+
+    def ld_generate(self, prior: Prior, w, sigma2, n, seed):
+        w = _f64(w)
+        d, h = w.shape
+        y = np.empty((n, d))
+        self._lcall("generate", *prior.args(), _u32(d), _u32(h), _p(w), _dbl(sigma2), _u64(n), _u64(seed), _p(y))
+        return y
+
+    def ld_exact_log_likelihood(self, prior: Prior, w, sigma2, y):
+        w, y = _f64(w), _f64(y)
+        out = _dbl()
+        self._lcall("exact_log_likelihood", *prior.args(), _u32(w.shape[0]), _u32(w.shape[1]), _p(w),
+                    _dbl(sigma2), _p(y), _u64(y.shape[0]), C.byref(out))
+        return out.value
+
 
 
 class RefSession:

@@ -66,6 +66,30 @@ LinearDiscreteModel bsc_model(std::uint32_t d, std::uint32_t h,
                              TruncationConfig{h, hprime, gamma, 1000000});
 }
 
+DiscreteFamily fam_of(std::uint32_t f) {
+  return f == 0 ? DiscreteFamily::kBsc : f == 1 ? DiscreteFamily::kTsc : DiscreteFamily::kDsc;
+}
+
+LinearDiscreteModel ld_model(std::uint32_t family, std::uint32_t d, std::uint32_t h,
+                             std::uint32_t hprime, std::uint32_t gamma, const double* alpha,
+                             std::uint32_t nalpha) {
+  std::vector<double> vals;
+  if (family == 2) vals.assign(alpha, alpha + nalpha);
+  return LinearDiscreteModel(fam_of(family), d, h, TruncationConfig{h, hprime, gamma, 1000000},
+                             vals);
+}
+
+LinearDiscreteParams ld_params(std::uint32_t family, std::uint32_t d, std::uint32_t h,
+                               const double* w, double sigma2, double pi, const double* alpha,
+                               const double* probs, std::uint32_t nalpha) {
+  LinearDiscreteParams p = bsc_params(d, h, w, pi, sigma2);
+  if (family == 2) {
+    p.values.assign(alpha, alpha + nalpha);
+    p.probs.assign(probs, probs + nalpha);
+  }
+  return p;
+}
+
 void copy_stats(const SuffStats& s, double* sum_s, double* sum_ssT,
                 double* sum_y_sT, double* value_counts, double* scalars) {
   const auto put = [](const DenseMatrix& m, double* out) {
@@ -74,7 +98,7 @@ void copy_stats(const SuffStats& s, double* sum_s, double* sum_ssT,
   put(s.at("sum_s"), sum_s);
   put(s.at("sum_ssT"), sum_ssT);
   put(s.at("sum_y_sT"), sum_y_sT);
-  put(s.at("value_counts"), value_counts);
+  put(s.at("value_counts"), value_counts);  // one entry per non-zero value
   if (scalars) {
     scalars[0] = s.scalar("sum_y2");
     scalars[1] = s.scalar("log_partition");
@@ -346,6 +370,167 @@ int ref_standard_init(std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
 int ref_data_mean_variance(const double* y, std::uint64_t n, std::uint32_t d,
                            double* out) {
   return guarded([&] { *out = detail::data_mean_variance(wrap_data(y, n, d)); });
+}
+
+// ---- linear discrete families (bsc 0 / tsc 1 / dsc 2); the dsc alphabet
+// (ascending, with 0) and probabilities are passed as alpha/probs/nalpha.
+int ref_ld_estep_stats(std::uint32_t family, const double* alpha, const double* probs,
+                       std::uint32_t nalpha, double pi, std::uint32_t d, std::uint32_t h,
+                       std::uint32_t hprime, std::uint32_t gamma, const double* w, double sigma2,
+                       double temperature, const double* y, std::uint64_t n,
+                       std::uint64_t row_begin, std::uint64_t row_end, double* sum_s,
+                       double* sum_ssT, double* sum_y_sT, double* value_counts, double* scalars) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, hprime, gamma, alpha, nalpha);
+    DataSet ds = wrap_data(y, n, d);
+    SuffStats s = m.estep_stats(ld_params(family, d, h, w, sigma2, pi, alpha, probs, nalpha), ds,
+                                RowRange{row_begin, row_end}, temperature);
+    copy_stats(s, sum_s, sum_ssT, sum_y_sT, value_counts, scalars);
+  });
+}
+
+int ref_ld_mstep(std::uint32_t family, const double* alpha, const double* probs_prev,
+                 std::uint32_t nalpha, double pi_prev, std::uint32_t d, std::uint32_t h,
+                 std::uint32_t nv, const double* w_prev, double sigma2_prev, const double* sum_s,
+                 const double* sum_ssT, const double* sum_y_sT, const double* value_counts,
+                 const double* scalars, double* w_out, double* pi_out, double* probs_out,
+                 double* sigma2_out) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, h, 1, alpha, nalpha);
+    SuffStats s;
+    const auto fill = [&](const char* name, std::size_t r, std::size_t c, const double* src) {
+      DenseMatrix& f = s.field(name, r, c);
+      std::memcpy(f.data(), src, r * c * sizeof(double));
+    };
+    fill("sum_s", 1, h, sum_s);
+    fill("sum_ssT", h, h, sum_ssT);
+    fill("sum_y_sT", d, h, sum_y_sT);
+    fill("value_counts", 1, nv, value_counts);
+    s.scalar("sum_y2") = scalars[0];
+    s.scalar("log_partition") = scalars[1];
+    s.points = static_cast<std::uint64_t>(scalars[2]);
+    ModelParams out = m.mstep(
+        s, ld_params(family, d, h, w_prev, sigma2_prev, pi_prev, alpha, probs_prev, nalpha));
+    const auto& p = std::get<LinearDiscreteParams>(out);
+    std::memcpy(w_out, p.w.data(), p.w.size() * sizeof(double));
+    if (pi_out) *pi_out = p.pi;
+    if (probs_out && family == 2) std::memcpy(probs_out, p.probs.data(), nalpha * sizeof(double));
+    *sigma2_out = p.sigma2;
+  });
+}
+
+int ref_ld_step(std::uint32_t family, const double* alpha, const double* probs,
+                std::uint32_t nalpha, double pi, std::uint32_t d, std::uint32_t h,
+                std::uint32_t hprime, std::uint32_t gamma, const double* w, double sigma2,
+                double temperature, const double* y, std::uint64_t n, std::uint32_t shards,
+                std::uint32_t workers, double* w_out, double* pi_out, double* probs_out,
+                double* sigma2_out, double* free_energy) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, hprime, gamma, alpha, nalpha);
+    DataSet ds = wrap_data(y, n, d);
+    ShardPlan plan = ShardPlan::with_shards(n, shards, workers);
+    AnnealState st;
+    st.temperature = temperature;
+    StepResult r =
+        m.step(ld_params(family, d, h, w, sigma2, pi, alpha, probs, nalpha), st, ds, plan);
+    const auto& p = std::get<LinearDiscreteParams>(r.params);
+    std::memcpy(w_out, p.w.data(), p.w.size() * sizeof(double));
+    if (pi_out) *pi_out = p.pi;
+    if (probs_out && family == 2) std::memcpy(probs_out, p.probs.data(), nalpha * sizeof(double));
+    *sigma2_out = p.sigma2;
+    *free_energy = r.free_energy;
+  });
+}
+
+int ref_ld_inference(std::uint32_t family, const double* alpha, const double* probs,
+                     std::uint32_t nalpha, double pi, std::uint32_t d, std::uint32_t h,
+                     std::uint32_t hprime, std::uint32_t gamma, const double* w, double sigma2,
+                     const double* y, std::uint64_t n, std::uint32_t shards, double* map_states,
+                     double* map_mass, double* expected) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, hprime, gamma, alpha, nalpha);
+    DataSet ds = wrap_data(y, n, d);
+    InferenceResult r = m.inference(ld_params(family, d, h, w, sigma2, pi, alpha, probs, nalpha),
+                                    ds, ShardPlan::with_shards(n, shards, shards));
+    std::memcpy(map_states, r.map_states.data(), r.map_states.size() * sizeof(double));
+    std::memcpy(map_mass, r.map_mass.data(), r.map_mass.size() * sizeof(double));
+    std::memcpy(expected, r.expected_states.data(), r.expected_states.size() * sizeof(double));
+  });
+}
+
+// Candidates as estep_impl selects them (:240-253) with the family's value
+// table (:71-97, restated: value_table is private).
+int ref_ld_candidates(std::uint32_t family, const double* alpha, const double* probs,
+                      std::uint32_t nalpha, double pi, std::uint32_t d, std::uint32_t h,
+                      std::uint32_t hprime, const double* w, double sigma2, const double* y,
+                      std::uint64_t n, std::uint32_t* out) {
+  return guarded([&] {
+    std::vector<double> values, log_probs;
+    if (family == 0) {
+      values = {1.0};
+      log_probs = {std::log(pi)};
+    } else if (family == 1) {
+      values = {-1.0, 1.0};
+      log_probs = {std::log(pi / 2.0), std::log(pi / 2.0)};
+    } else {
+      for (std::uint32_t k = 0; k < nalpha; ++k)
+        if (alpha[k] != 0.0) {
+          values.push_back(alpha[k]);
+          log_probs.push_back(std::log(probs[k]));
+        }
+    }
+    const ConstMatView wv(w, d, h);
+    const Eigen::MatrixXd gram = wv.transpose() * wv;
+    const double inv2s = 1.0 / (2.0 * sigma2);
+    std::vector<double> scores(h);
+    Eigen::VectorXd b(h);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      ConstVecView yv(y + i * d, d);
+      b.noalias() = wv.transpose() * yv;
+      for (std::uint32_t u = 0; u < h; ++u) {
+        double best = -std::numeric_limits<double>::infinity();
+        for (std::size_t k = 0; k < values.size(); ++k) {
+          const double v = values[k];
+          best = std::max(best, log_probs[k] + (2.0 * v * b[u] - v * v * gram(u, u)) * inv2s);
+        }
+        scores[u] = best;
+      }
+      auto c = select_candidates(scores, hprime);
+      std::memcpy(out + i * hprime, c.data(), hprime * sizeof(std::uint32_t));
+    }
+  });
+}
+
+int ref_ld_generate(std::uint32_t family, const double* alpha, const double* probs,
+                    std::uint32_t nalpha, double pi, std::uint32_t d, std::uint32_t h,
+                    const double* w, double sigma2, std::uint64_t n, std::uint64_t seed,
+                    double* y_out) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, h, 1, alpha, nalpha);
+    RngStream rng(seed);
+    DataSet ds = m.generate(ld_params(family, d, h, w, sigma2, pi, alpha, probs, nalpha), n, rng);
+    std::memcpy(y_out, ds.y.data(), ds.y.size() * sizeof(double));
+  });
+}
+
+int ref_ld_exact_log_likelihood(std::uint32_t family, const double* alpha, const double* probs,
+                                std::uint32_t nalpha, double pi, std::uint32_t d,
+                                std::uint32_t h, const double* w, double sigma2, const double* y,
+                                std::uint64_t n, double* out) {
+  return guarded([&] {
+    auto m = ld_model(family, d, h, h, h, alpha, nalpha);
+    *out = m.exact_log_likelihood(ld_params(family, d, h, w, sigma2, pi, alpha, probs, nalpha),
+                                  wrap_data(y, n, d));
+  });
+}
+
+int ref_ld_state_count(std::uint32_t h, std::uint32_t hprime, std::uint32_t gamma,
+                       std::uint32_t nv, std::uint64_t* out) {
+  return guarded([&] {
+    TruncationConfig cfg{h, hprime, gamma, 1000000};
+    cfg.validate();
+    *out = truncated_state_count(cfg, nv);
+  });
 }
 
 }  // extern "C"

@@ -9,7 +9,19 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("ld_"))
+# linear discrete families other than BSC (tsc / dsc), SURVEY.md §8(f) row 2
+LD_GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f.startswith("ld_"))
+FAMILY_NAMES = {0: "bsc", 1: "tsc", 2: "dsc"}
+
+
+def golden_prior(g, pi_key="pi0", probs_key="probs0"):
+    from oracle.oracle import Prior
+
+    fam = FAMILY_NAMES[int(g["family"])]
+    if fam == "dsc":
+        return Prior(fam, 0.0, g["alpha"], g[probs_key])
+    return Prior(fam, float(g[pi_key]))
 
 
 def pytest_configure(config):

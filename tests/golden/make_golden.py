@@ -14,7 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle.oracle import Oracle  # noqa: E402
+from oracle.oracle import Oracle, Prior  # noqa: E402
 
 R = Oracle("ref")
 
@@ -38,6 +38,37 @@ def case(name, y, w0, pi0, s20, hprime, gamma, iters=3, temperature=1.0):
     out.update(map_states=ms, map_mass=mm, expected=ex)
     if h <= 10:
         out["exact_ll0"] = R.exact_log_likelihood(w0, pi0, s20, y)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
+def ld_case(name, prior, y, w0, s20, hprime, gamma, iters=3, temperature=1.0):
+    """A linear discrete family case (tsc/dsc): the prior's family code, pi,
+    alphabet and probabilities are stored beside the reference outputs."""
+    d, h = w0.shape
+    alpha = prior.alpha if prior.alpha is not None else np.zeros(0)
+    probs = prior.probs if prior.probs is not None else np.zeros(0)
+    out = dict(y=y, W0=w0, family=prior.code, pi0=prior.pi, alpha=alpha, probs0=probs, sigma2_0=s20,
+               hprime=hprime, gamma=gamma, temperature=temperature)
+    out["candidates"] = R.ld_candidates(prior, w0, s20, y, hprime)
+    st = R.ld_estep_stats(prior, w0, s20, y, hprime, gamma, temperature)
+    for k, v in st.items():
+        out["stats_" + k] = np.asarray(v)
+    w1, p1, q1, s1, f = R.ld_step(prior, w0, s20, y, hprime, gamma, temperature, shards=3, workers=2)
+    out.update(W1=w1, pi1=p1 if p1 is not None else 0.0, probs1=q1 if q1 is not None else np.zeros(0),
+               sigma2_1=s1, F0=f)
+    ws, ps, qs, ss, fs = [], [], [], [], []
+    w, pr, s = w0, prior, s20
+    for _ in range(iters):
+        w, p, q, s, f = R.ld_step(pr, w, s, y, hprime, gamma, 1.0)
+        pr = Prior(pr.family, p if p is not None else 0.0, pr.alpha, q)
+        ws.append(w), ps.append(pr.pi), qs.append(q if q is not None else np.zeros(0)), ss.append(s), fs.append(f)
+    out.update(traj_W=np.array(ws), traj_pi=np.array(ps), traj_probs=np.array(qs), traj_sigma2=np.array(ss),
+               traj_F=np.array(fs))
+    ms, mm, ex = R.ld_inference(prior, w0, s20, y, hprime, gamma)
+    out.update(map_states=ms, map_mass=mm, expected=ex)
+    if h <= 6:
+        out["exact_ll0"] = R.ld_exact_log_likelihood(prior, w0, s20, y)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(name, {k: np.shape(v) for k, v in out.items()})
 
@@ -69,3 +100,20 @@ if __name__ == "__main__":
     y = R.generate(wt, 0.3, 0.5, 200, 7)
     w, p, s = R.standard_init(y, 6, 6, 6, 11)
     case("spec_acc1_d9_h6_exact", y, w, p, s, 6, 6, iters=5)
+    # linear discrete families through the same path:
+    # ternary sparse coding, and a discrete alphabet with 0
+    wt = Oracle("port").random_dictionary(16, 12, 9, 3.0)
+    tsc = Prior("tsc", 0.2)
+    y = R.ld_generate(tsc, wt, 0.3, 160, 9)
+    w, _, s = baseline_init(y, 12, 9)
+    ld_case("ld_tsc_d16_h12_hp6_g3", Prior("tsc", 1.0 / 12), y, w, s, 6, 3)
+    ld_case("ld_tsc_d16_h12_hp6_g3_T2", Prior("tsc", 1.0 / 12), y, w, s, 6, 3, iters=2, temperature=2.0)
+    wt6 = Oracle("port").random_dictionary(10, 6, 13, 3.0)
+    y = R.ld_generate(tsc, wt6, 0.4, 80, 13)
+    w, _, s = baseline_init(y, 6, 13)
+    ld_case("ld_tsc_exact_d10_h6", Prior("tsc", 0.25), y, w, s, 6, 6, iters=2)
+    dsc = Prior("dsc", alpha=[-1.0, 0.0, 1.0, 2.0], probs=[0.05, 0.8, 0.1, 0.05])
+    wt = Oracle("port").random_dictionary(16, 10, 17, 3.0)
+    y = R.ld_generate(dsc, wt, 0.3, 160, 17)
+    w, _, s = baseline_init(y, 10, 17)
+    ld_case("ld_dsc_d16_h10_hp5_g3", Prior("dsc", alpha=dsc.alpha, probs=[0.1, 0.7, 0.1, 0.1]), y, w, s, 5, 3)
