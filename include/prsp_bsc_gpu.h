@@ -25,6 +25,15 @@
  *   prsp_bsc_generate          LinearDiscreteModel::generate (:452-479)
  *   prsp_bsc_bars_generate     make_bars (bars.cpp:33-65) / prsp_bars_generate (prsp.h:76-80)
  *   prsp_bsc_standard_init     LinearDiscreteModel::standard_init (:129-148)
+ *   prsp_bsc_gpu_create_model  LinearDiscreteModel(DiscreteFamily, …, dsc_values) (:32-61) for
+ *                              "bsc" / "tsc" / "dsc"; prsp_session_set_model / _set_values
+ *                              (prsp.h:95-101) name the family and the dsc alphabet the same way
+ *   prsp_bsc_gpu_set_params_ex LinearDiscreteParams{w, sigma2, pi, values, probs} (model.hpp:41-47)
+ *                              + LinearDiscreteModel::validate (:99-127)
+ *
+ * Families other than bsc: value_counts (get/set_stats and the statistics
+ * buffer) has one entry per non-zero latent value (SuffStats "value_counts"
+ * 1×V, linear_discrete.cpp:214), tail = [value_counts V | sum_y2 | log_partition | points].
  */
 #ifndef PRSP_BSC_GPU_H
 #define PRSP_BSC_GPU_H
@@ -45,6 +54,16 @@ int prsp_bsc_gpu_device_count(void);
 /* ---- context ----------------------------------------------------------- */
 int prsp_bsc_gpu_create(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
                         int device, prsp_bsc_gpu** out);
+/* model: "bsc", "tsc" or "dsc"; dsc takes its latent alphabet (`values`, n_values ≥ 2
+ * distinct values containing 0, any order: sorted like the reference ctor);
+ * values/n_values are ignored for bsc and tsc. */
+int prsp_bsc_gpu_create_model(const char* model, uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma,
+                              uint64_t state_cap, const double* values, uint32_t n_values, int device,
+                              prsp_bsc_gpu** out);
+/* family: 0 bsc, 1 tsc, 2 dsc; n_values: non-zero values (the value_counts length);
+ * alphabet_out (nullable) receives the sorted alphabet including 0 (alphabet_size entries). */
+int prsp_bsc_gpu_model_info(const prsp_bsc_gpu* ctx, int* family, uint32_t* n_values, uint32_t* alphabet_size,
+                            double* alphabet_out);
 void prsp_bsc_gpu_free(prsp_bsc_gpu* ctx);
 /* Run on an existing cudaStream_t (e.g. torch's current stream); NULL = own stream. */
 int prsp_bsc_gpu_set_stream(prsp_bsc_gpu* ctx, void* cuda_stream);
@@ -56,6 +75,11 @@ int prsp_bsc_gpu_load_data(prsp_bsc_gpu* ctx, const double* y_host, uint64_t n);
 int prsp_bsc_gpu_load_data_device(prsp_bsc_gpu* ctx, const double* y_device, uint64_t n);
 int prsp_bsc_gpu_set_params(prsp_bsc_gpu* ctx, const double* w, double pi, double sigma2);
 int prsp_bsc_gpu_get_params(prsp_bsc_gpu* ctx, double* w, double* pi, double* sigma2);
+/* Any family: pi for bsc/tsc; probs (alphabet_size entries, aligned with the
+ * sorted alphabet, summing to 1) for dsc. get_params_ex writes probs for dsc only. */
+int prsp_bsc_gpu_set_params_ex(prsp_bsc_gpu* ctx, const double* w, double pi, double sigma2, const double* probs,
+                               uint32_t n_probs);
+int prsp_bsc_gpu_get_params_ex(prsp_bsc_gpu* ctx, double* w, double* pi, double* sigma2, double* probs);
 
 /* ---- the hot path ------------------------------------------------------- */
 /* E-step over the resident shard into the device statistics buffer. */

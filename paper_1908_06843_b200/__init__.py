@@ -3,14 +3,17 @@
 Only the hot path named in BASELINE.json is built: the Expectation-Truncation
 E-step of Binary Sparse Coding with its M-step sufficient statistics and the
 parameter update, as hand-written sm_100a CUDA behind a C ABI
-(``include/prsp_bsc_gpu.h``). See DESIGN.md.
+(``include/prsp_bsc_gpu.h``), and the other linear discrete families (ternary
+and discrete sparse coding) through the same enumerator. See DESIGN.md.
 """
 from ._native import ConfigError, DataError, NumericError, PrspError, build
-from .bsc import (BscGpuModel, BscParams, InferenceResult, StepResult, SuffStats, TruncationConfig,
-                  bars_generate, baseline_init, generate, random_dictionary, standard_init)
+from .bsc import (BscGpuModel, BscParams, InferenceResult, LinearDiscreteGpuModel, LinearDiscreteParams, StepResult,
+                  SuffStats, TruncationConfig, bars_generate, baseline_init, generate, random_dictionary,
+                  standard_init)
 
 __all__ = [
-    "BscGpuModel", "BscParams", "InferenceResult", "StepResult", "SuffStats", "TruncationConfig",
+    "BscGpuModel", "BscParams", "InferenceResult", "LinearDiscreteGpuModel", "LinearDiscreteParams", "StepResult",
+    "SuffStats", "TruncationConfig",
     "bars_generate", "baseline_init", "generate", "random_dictionary", "standard_init", "build",
     "PrspError", "ConfigError", "DataError", "NumericError",
 ]

@@ -23,6 +23,8 @@ SIGNATURES = {
     "prsp_bsc_gpu_last_error": [],
     "prsp_bsc_gpu_device_count": [],
     "prsp_bsc_gpu_create": [_u32, _u32, _u32, _u32, _u64, _int, C.POINTER(_ptr)],
+    "prsp_bsc_gpu_create_model": [C.c_char_p, _u32, _u32, _u32, _u32, _u64, _ptr, _u32, _int, C.POINTER(_ptr)],
+    "prsp_bsc_gpu_model_info": [_ptr, C.POINTER(_int), C.POINTER(_u32), C.POINTER(_u32), _ptr],
     "prsp_bsc_gpu_free": [_ptr],
     "prsp_bsc_gpu_set_stream": [_ptr, _ptr],
     "prsp_bsc_gpu_sync": [_ptr],
@@ -31,6 +33,8 @@ SIGNATURES = {
     "prsp_bsc_gpu_load_data_device": [_ptr, _ptr, _u64],
     "prsp_bsc_gpu_set_params": [_ptr, _ptr, _dbl, _dbl],
     "prsp_bsc_gpu_get_params": [_ptr, _ptr, _dp, _dp],
+    "prsp_bsc_gpu_set_params_ex": [_ptr, _ptr, _dbl, _dbl, _ptr, _u32],
+    "prsp_bsc_gpu_get_params_ex": [_ptr, _ptr, _dp, _dp, _ptr],
     "prsp_bsc_gpu_estep": [_ptr, _dbl],
     "prsp_bsc_gpu_stats_buffer": [_ptr, C.POINTER(_ptr), C.POINTER(_u64)],
     "prsp_bsc_gpu_get_stats": [_ptr, _ptr, _ptr, _ptr, _ptr, _ptr],

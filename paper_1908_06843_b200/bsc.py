@@ -52,6 +52,22 @@ class BscParams:
 
 
 @dataclass
+class LinearDiscreteParams:
+    """LinearDiscreteParams (model.hpp:41-47) for any linear discrete family:
+    ``pi`` for bsc/tsc, ``probs`` (aligned with the model's sorted alphabet,
+    including 0) for dsc."""
+
+    W: np.ndarray
+    sigma2: float
+    pi: float = 0.0
+    probs: np.ndarray | None = None
+
+    def copy(self) -> "LinearDiscreteParams":
+        return LinearDiscreteParams(self.W.copy(), float(self.sigma2), float(self.pi),
+                                    None if self.probs is None else np.array(self.probs, float))
+
+
+@dataclass
 class StepResult:
     """model.hpp:78-81: params after the step, F at the incoming params (T = 1)."""
 
@@ -86,8 +102,11 @@ class InferenceResult:
     expected_states: np.ndarray
 
 
-class BscGpuModel:
-    """BSC truncated-EM on one B200: a drop-in for LinearDiscreteModel(kBsc).
+class LinearDiscreteGpuModel:
+    """Truncated EM of a linear discrete family on one B200: a drop-in for
+    ``LinearDiscreteModel(DiscreteFamily, dim, latents, TruncationConfig,
+    dsc_values)`` (linear_discrete.cpp:32-61) with ``model`` "bsc", "tsc" or
+    "dsc" (``values``: the dsc alphabet, must contain 0).
 
     The data shard is uploaded once by :meth:`load` (or implicitly by the
     reference-shaped :meth:`step` when it is handed a different array) and
@@ -95,15 +114,24 @@ class BscGpuModel:
     the reference API returns them.
     """
 
-    def __init__(self, dim: int, latents: int, trunc: TruncationConfig, device: int = 0):
+    def __init__(self, model: str, dim: int, latents: int, trunc: TruncationConfig, values=None, device: int = 0):
         self.dim, self.latents = int(dim), int(latents)
         self.trunc = TruncationConfig(latents, trunc.hprime, trunc.gamma, trunc.state_cap)
         h = C.c_void_p()
-        N.call("prsp_bsc_gpu_create", dim, latents, trunc.hprime, trunc.gamma, trunc.state_cap, device,
+        vals = None if values is None else _f64(values)
+        N.call("prsp_bsc_gpu_create_model", model.encode(), dim, latents, trunc.hprime, trunc.gamma,
+               trunc.state_cap, None if vals is None else _p(vals), 0 if vals is None else len(vals), device,
                C.byref(h))
         self._h = h
         self._data_key = None
         self.n = 0
+        fam, nv, na = C.c_int(), C.c_uint32(), C.c_uint32()
+        N.call("prsp_bsc_gpu_model_info", self._h, C.byref(fam), C.byref(nv), C.byref(na), None)
+        self.alphabet = np.empty(na.value)
+        N.call("prsp_bsc_gpu_model_info", self._h, None, None, None, _p(self.alphabet))
+        self.model = model
+        self.family = fam.value
+        self.n_values = nv.value
 
     # -------------------------------------------------------------- plumbing
     def close(self) -> None:
@@ -144,17 +172,25 @@ class BscGpuModel:
         self.n = n
         self._data_key = ("device", ptr, n)
 
-    def set_params(self, params: BscParams) -> None:
+    def set_params(self, params) -> None:
         w = _f64(params.W)
         if w.shape != (self.dim, self.latents):
-            raise N.ConfigError(2, "bsc: dictionary shape mismatch")
-        N.call("prsp_bsc_gpu_set_params", self._h, _p(w), float(params.pi), float(params.sigma2))
+            raise N.ConfigError(2, f"{self.model}: dictionary shape mismatch")
+        probs = getattr(params, "probs", None)
+        pr = None if probs is None else _f64(probs)
+        N.call("prsp_bsc_gpu_set_params_ex", self._h, _p(w), float(getattr(params, "pi", 0.0) or 0.0),
+               float(params.sigma2), None if pr is None else _p(pr), 0 if pr is None else len(pr))
 
-    def get_params(self) -> BscParams:
+    def get_params(self):
         w = np.empty((self.dim, self.latents))
         pi, s2 = _dbl(), _dbl()
-        N.call("prsp_bsc_gpu_get_params", self._h, _p(w), C.byref(pi), C.byref(s2))
-        return BscParams(w, pi.value, s2.value)
+        probs = np.empty(len(self.alphabet))
+        N.call("prsp_bsc_gpu_get_params_ex", self._h, _p(w), C.byref(pi), C.byref(s2), _p(probs))
+        if self.model == "bsc":
+            return BscParams(w, pi.value, s2.value)
+        if self.model == "tsc":
+            return LinearDiscreteParams(w, s2.value, pi.value)
+        return LinearDiscreteParams(w, s2.value, 0.0, probs)
 
     # ------------------------------------------------------- reference API
     def step(self, params: BscParams, data=None, temperature: float = 1.0) -> StepResult:
@@ -169,6 +205,8 @@ class BscGpuModel:
 
     def step_host(self, params: BscParams, y, temperature: float = 1.0) -> StepResult:
         """The reference call shape end to end: host Y and params in, host params and F out."""
+        if self.model == "dsc":
+            raise N.ConfigError(2, "dsc: step_host takes pi; use step() with LinearDiscreteParams")
         y = _f64(y)
         w = _f64(params.W)
         wo = np.empty_like(w)
@@ -177,7 +215,8 @@ class BscGpuModel:
                float(temperature), _p(wo), C.byref(pi), C.byref(s2), C.byref(f))
         self.n = y.shape[0]
         self._data_key = (y.__array_interface__["data"][0], y.shape)
-        return StepResult(BscParams(wo, pi.value, s2.value), f.value)
+        p = BscParams(wo, pi.value, s2.value) if self.model == "bsc" else LinearDiscreteParams(wo, s2.value, pi.value)
+        return StepResult(p, f.value)
 
     def estep_stats(self, params: BscParams, data=None, temperature: float = 1.0) -> SuffStats:
         """LinearDiscreteModel::estep_stats (:327-334) over the resident shard."""
@@ -189,7 +228,7 @@ class BscGpuModel:
 
     def get_stats(self) -> SuffStats:
         d, h = self.dim, self.latents
-        s, ssT, ysT, vc, sc = np.empty(h), np.empty((h, h)), np.empty((d, h)), np.empty(1), np.empty(3)
+        s, ssT, ysT, vc, sc = np.empty(h), np.empty((h, h)), np.empty((d, h)), np.empty(self.n_values), np.empty(3)
         N.call("prsp_bsc_gpu_get_stats", self._h, _p(s), _p(ssT), _p(ysT), _p(vc), _p(sc))
         return SuffStats(s, ssT, ysT, vc, float(sc[0]), float(sc[1]), int(sc[2]))
 
@@ -254,6 +293,13 @@ class BscGpuModel:
         key = (y.__array_interface__["data"][0], y.shape)
         if key != self._data_key:
             self.load(y)
+
+
+class BscGpuModel(LinearDiscreteGpuModel):
+    """BSC truncated-EM on one B200: a drop-in for LinearDiscreteModel(kBsc)."""
+
+    def __init__(self, dim: int, latents: int, trunc: TruncationConfig, device: int = 0):
+        super().__init__("bsc", dim, latents, trunc, None, device)
 
 
 # ------------------------------------------------------------------ fixtures

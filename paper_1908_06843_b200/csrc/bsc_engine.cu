@@ -12,36 +12,15 @@
 #include "bsc_kernels.cuh"
 #include "dgemm.cuh"
 #include "mstep_kernels.cuh"
+#include "engine_util.hpp"
+#include "sched_builder.hpp"
 
 namespace bscgpu {
 
 namespace {
 
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw Error(kInternal, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
-}
+using namespace util;
 
-template <class T>
-T* dalloc(size_t count, const char* what) {
-  void* p = nullptr;
-  ck(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), what);
-  ck(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), what);
-  return static_cast<T*>(p);
-}
-
-void dfree(void* p) {
-  if (p) cudaFree(p);
-}
-
-int round_up(int x, int m) { return (x + m - 1) / m * m; }
-
-// Register-resident unit slots per lane (H ≤ 32·MAXJ).
-int maxj_for(uint32_t h) {
-  const int need = static_cast<int>((h + 31) / 32);
-  for (int m : {1, 2, 4, 6, 8, 10, 12, 16, 24, 32})
-    if (need <= m) return m;
-  return 32;
-}
 template <bool STAGED>
 const void* enum_fn_t(int maxj) {
   switch (maxj) {
@@ -59,8 +38,6 @@ const void* enum_fn_t(int maxj) {
 }
 const void* enum_fn(int maxj, bool staged) { return staged ? enum_fn_t<true>(maxj) : enum_fn_t<false>(maxj); }
 
-constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
-
 // Tile configurations (see dgemm.cuh).
 // GEMM1  B = Y·W:     M = points, N = Hp, K = Dp.
 #define GEMM1_CFG 128, 64, 16, 32, 32, true, true, 3
@@ -77,7 +54,46 @@ constexpr double kLog2Pi = 1.8378770664093454836;  // linear_discrete.cpp:24
 
 BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
                      int device)
-    : D_(dim), H_(latents), hprime_(hprime), gamma_(gamma), cap_(state_cap), device_(device) {
+    : alphabet_{0.0, 1.0}, values_{1.0}, D_(dim), H_(latents), hprime_(hprime), gamma_(gamma), cap_(state_cap),
+      device_(device) {
+  init(device);
+}
+
+// LinearDiscreteModel ctor (linear_discrete.cpp:32-61) and value_table
+// (:71-97): bsc {1}, tsc {−1, +1}, dsc the sorted alphabet without 0.
+BscEngine::BscEngine(int family, uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma,
+                     uint64_t state_cap, const double* alphabet, uint32_t n_alpha, int device)
+    : family_(family), D_(dim), H_(latents), hprime_(hprime), gamma_(gamma), cap_(state_cap), device_(device) {
+  switch (family) {
+    case kBsc:
+      alphabet_ = {0.0, 1.0};
+      break;
+    case kTsc:
+      alphabet_ = {-1.0, 0.0, 1.0};
+      break;
+    case kDsc: {
+      if (!alphabet || n_alpha < 2) throw Error(kConfig, "dsc: alphabet needs at least two values");
+      alphabet_.assign(alphabet, alphabet + n_alpha);
+      for (double v : alphabet_)
+        if (!std::isfinite(v)) throw Error(kConfig, "dsc: alphabet values must be finite");
+      std::sort(alphabet_.begin(), alphabet_.end());
+      if (std::adjacent_find(alphabet_.begin(), alphabet_.end()) != alphabet_.end())
+        throw Error(kConfig, "dsc: alphabet values must be distinct");
+      if (std::find(alphabet_.begin(), alphabet_.end(), 0.0) == alphabet_.end())
+        throw Error(kConfig, "dsc: alphabet must contain 0");
+      break;
+    }
+    default:
+      throw Error(kConfig, "linear model: unknown family");
+  }
+  for (double v : alphabet_)
+    if (v != 0.0) values_.push_back(v);
+  if (values_.size() > 8) throw Error(kConfig, "gpu: more than 8 non-zero latent values are not supported");
+  if (family_ == kDsc) probs_.assign(alphabet_.size(), 1.0 / alphabet_.size());
+  init(device);
+}
+
+void BscEngine::init(int device) {
   if (D_ == 0 || H_ == 0) throw Error(kConfig, "linear model: dim and latents must be >= 1");
   // TruncationConfig::validate, truncation.cpp:23-30
   if (hprime_ == 0 || hprime_ > H_) throw Error(kConfig, "truncation: hprime must satisfy 1 <= hprime <= latents");
@@ -96,8 +112,11 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   own_stream_ = true;
   Dp_ = round_up(static_cast<int>(D_), 8);
   Hp_ = round_up(static_cast<int>(H_), 8);
-  lay_ = StatsLayout{static_cast<long long>(D_), static_cast<long long>(H_)};
-  build_template();
+  lay_ = StatsLayout{static_cast<long long>(D_), static_cast<long long>(H_), static_cast<long long>(values_.size())};
+  if (vpath())
+    build_template_v();
+  else
+    build_template();
   if (const char* e = std::getenv("BSC_ENUM_PROFILE")) prof_on_ = e[0] == '1';
   // posterior-weight path (tests and A/B runs): 0 auto, 1 multiplicative after the
   // exact maximum, 2 exp per state
@@ -115,7 +134,7 @@ BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t g
   d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
   d_msc_ = dalloc<MstepScalars>(1, "mstep scalars");
   ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
-  ck(cudaMallocHost(&h_tail_, 4 * sizeof(double)), "pinned");
+  ck(cudaMallocHost(&h_tail_, (values_.size() + 3) * sizeof(double)), "pinned");
   ck(cudaMallocHost(&h_err_, sizeof(int)), "pinned");
   cudaStream_t cs;
   ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
@@ -138,7 +157,8 @@ BscEngine::~BscEngine() {
                   d_sched_split_, (void*)d_y_, (void*)d_y2_,
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
-                  (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_})
+                  (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
+                  (void*)d_vpart_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -300,107 +320,16 @@ void BscEngine::build_template() {
     lists[q].push_back(i);
     for (size_t a = 0; a + 1 < S.size(); ++a) lists[pair_index(S[a], q)].push_back(i);
   }
-  // Balanced lane schedules (see SchedDesc): the lists of every output are
-  // concatenated in output order and cut into 32 equal runs. An output whose
-  // list lies inside one run is written directly by that lane; one that spans
-  // runs leaves a partial per run in consecutive slots, summed afterwards.
-  std::vector<SchedDesc> sched;
-  std::vector<uint32_t> ent;  // packed: src/8 | (int16 dst code) << 16
-  std::vector<int4> splits;
-  constexpr int R = kSchedRuns;
-  constexpr int kSlots = 2 * kSchedRuns;  // ≤ R−1 split outputs, ≤ 2R−2 partials
+  // Balanced lane schedules (see SchedDesc and ScheduleBuilder).
   const EnumSmem L1 = EnumSmem::make(hp, n_tab, n_coup, kSlots, n_out_, 0);
   if (L1.tab != L0.tab || L1.coup != L0.coup) throw Error(kInternal, "state template layout mismatch");
-  auto add_schedule = [&](const std::vector<std::vector<int>>& ls, const std::vector<int>& targets) {
-    std::vector<std::pair<int, int>> seq;  // (byte offset, output)
-    for (size_t o = 0; o < ls.size(); ++o) {
-      if (ls[o].empty()) seq.emplace_back(tab_off(n_tab), static_cast<int>(o));  // writes 0
-      for (int v : ls[o]) seq.emplace_back(v, static_cast<int>(o));
-    }
-    const int T = static_cast<int>(seq.size());
-    const int iters = (T + R - 1) / R;
-    std::vector<int> first_lane(ls.size(), 1 << 30), last_lane(ls.size(), -1);
-    for (int j = 0; j < T; ++j) {
-      const int o = seq[j].second, l = j / iters;
-      first_lane[o] = std::min(first_lane[o], l);
-      last_lane[o] = std::max(last_lane[o], l);
-    }
-    // dst: ≥ 0 output byte offset, −1 continue, ≤ −2 split slot −dst−2 (see seg_flush)
-    auto pack = [&](int src, int dst) {
-      uint32_t code = 0xffffu;
-      if (dst >= 0) code = w16(dst);
-      else if (dst <= -2) code = 0x8000u | static_cast<uint32_t>(L1.part + (-dst - 2));
-      if (dst != -1 && (code & 0x7fffu) >= 0x7fffu) throw Error(kConfig, "gpu: schedule destination out of range");
-      if (dst >= 0 && code > 0x7fffu) throw Error(kConfig, "gpu: schedule destination out of range");
-      return w16(src) | (code << 16);
-    };
-    // runs → list segments (the entries of one output inside one run)
-    struct Seg {
-      std::vector<int> src;
-      int dst;
-    };
-    std::vector<std::vector<Seg>> runs(R);
-    std::vector<int> slot_begin(ls.size(), -1);
-    int slot = 0;
-    for (int l = 0; l < R; ++l) {
-      const int b = l * iters, e = std::min(T, b + iters);
-      for (int j = b; j < e; ++j) {
-        const int o = seq[j].second;
-        if (j == b || seq[j - 1].second != o) runs[l].push_back(Seg{{}, -1});
-        runs[l].back().src.push_back(seq[j].first);
-        if (j + 1 == e || seq[j + 1].second != o) {
-          if (first_lane[o] == last_lane[o]) {
-            runs[l].back().dst = targets[o];
-          } else {
-            if (slot_begin[o] < 0) slot_begin[o] = slot;
-            runs[l].back().dst = -(slot + 2);
-            ++slot;
-          }
-        }
-      }
-    }
-    // Emit one entry per run per iteration. Within a segment the order is
-    // free (it is a sum), so each half-warp's 16 loads of one instruction are
-    // picked greedily to fall in distinct 8-byte shared-memory banks.
-    std::vector<uint32_t> rows(static_cast<size_t>(iters) * R, pack(tab_off(n_tab), -1));
-    std::vector<size_t> cur(R, 0);
-    std::vector<std::vector<int>> rem(R);
-    for (int l = 0; l < R; ++l)
-      if (!runs[l].empty()) rem[l] = runs[l][0].src;
-    for (int it = 0; it < iters; ++it)
-      for (int u = 0; u < R / 32; ++u)
-        for (int half = 0; half < 2; ++half) {
-          unsigned used = 0;
-          for (int k = 0; k < 16; ++k) {
-            const int l = 32 * u + 16 * half + k;
-            if (cur[l] >= runs[l].size()) continue;
-            auto& r = rem[l];
-            size_t pick = 0;
-            for (size_t q = 0; q < r.size(); ++q)
-              if (!((used >> ((r[q] / 8) & 15)) & 1u)) {
-                pick = q;
-                break;
-              }
-            const int src = r[pick];
-            used |= 1u << ((src / 8) & 15);
-            r[pick] = r.back();
-            r.pop_back();
-            const int dst = r.empty() ? runs[l][cur[l]].dst : -1;
-            rows[static_cast<size_t>(it) * R + l] = pack(src, dst);
-            if (r.empty() && ++cur[l] < runs[l].size()) r = runs[l][cur[l]].src;
-          }
-        }
-    SchedDesc sd{iters, static_cast<int>(ent.size() / R), 0, static_cast<int>(splits.size())};
-    for (size_t o = 0; o < ls.size(); ++o)
-      if (first_lane[o] != last_lane[o]) {
-        const int nparts = last_lane[o] - first_lane[o] + 1;
-        splits.push_back(int4{targets[o], slot_begin[o], slot_begin[o] + nparts, 0});
-        ++sd.n_split;
-      }
-    if (sd.n_split >= R || slot > kSlots) throw Error(kInternal, "state template: schedule split overflow");
-    ent.insert(ent.end(), rows.begin(), rows.end());
-    sched.push_back(sd);
-  };
+  ScheduleBuilder sb;
+  sb.zero_off = tab_off(n_tab);
+  sb.part_base = L1.part;
+  auto add_schedule = [&](const std::vector<std::vector<int>>& ls, const std::vector<int>& tg) { sb.add(ls, tg); };
+  auto& sched = sb.sched;
+  auto& ent = sb.ent;
+  auto& splits = sb.splits;
   // subtree sums, level γ−1 down to 1: sub(A) = q(A) + Σ_{children} sub(c)
   for (int k = static_cast<int>(gamma_) - 1; k >= 1; --k) {
     std::vector<std::vector<int>> ls;
@@ -472,8 +401,10 @@ void BscEngine::ensure_work(uint64_t n) {
   d_part_ = dalloc<double>((size_t)splits_ * part_stride_, "splitK partials");
 
   // enumerator launch shape: per-warp shared region, as many warps as fit
-  const EnumSmem L = EnumSmem::make(hprime_, n_tab_, n_coup_, n_slots_, n_out_, static_cast<int>(H_));
-  const int per_warp = L.total * 8;
+  const int V = static_cast<int>(values_.size());
+  const int per_warp =
+      vpath() ? ldv_per_warp_bytes()
+              : 8 * EnumSmem::make(hprime_, n_tab_, n_coup_, n_slots_, n_out_, static_cast<int>(H_)).total;
   if (per_warp > 200 * 1024)
     throw Error(kConfig, "gpu: state template too large for shared memory (" + std::to_string(n_multi_) + " states)");
   // Pick (warps per CTA, staged tables) maximising resident warps per SM
@@ -498,7 +429,7 @@ void BscEngine::ensure_work(uint64_t n) {
   enum_block_ = warps * 32;
   enum_smem_ = warps * per_warp + (stage_tables_ ? table_bytes : 0);
   const int maxj = maxj_for(H_);
-  const void* fn = enum_fn(maxj, stage_tables_);
+  const void* fn = vpath() ? ldv_kernel_fn(maxj, stage_tables_) : enum_fn(maxj, stage_tables_);
   ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "enum smem attr");
   int per_sm = 0;
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, enum_block_, enum_smem_), "occupancy");
@@ -510,6 +441,12 @@ void BscEngine::ensure_work(uint64_t n) {
   d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
   d_warp_sc_ = dalloc<double>((size_t)enum_ctas_ * 2, "cta_scalars");
   colsum_chunks_ = 1;
+  if (vpath()) {
+    dfree(d_vpart_);
+    vpart_stride_ = (static_cast<int>(H_) + V + 2 + 1) & ~1;
+    d_vpart_ = dalloc<double>((size_t)enum_ctas_ * vpart_stride_, "cta partials");
+    vpart_chunks_ = 1;
+  }
 }
 
 void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
@@ -552,11 +489,28 @@ double BscEngine::step_streamed(const double* y_host, uint64_t n, double tempera
 }
 
 void BscEngine::set_params(const double* w, double pi, double sigma2) {
-  // LinearDiscreteModel::validate, linear_discrete.cpp:99-127 (BSC)
+  if (family_ == kDsc) throw Error(kConfig, "dsc: parameters need the value probabilities (set_params_ex)");
+  set_params_ex(w, pi, sigma2, nullptr, 0);
+}
+
+// LinearDiscreteModel::validate, linear_discrete.cpp:99-127.
+void BscEngine::set_params_ex(const double* w, double pi, double sigma2, const double* probs, uint32_t n_probs) {
+  const char* nm = family_ == kBsc ? "bsc" : family_ == kTsc ? "tsc" : "dsc";
   for (size_t i = 0; i < (size_t)D_ * H_; ++i)
-    if (!std::isfinite(w[i])) throw Error(kNumeric, "bsc: non-finite dictionary");
-  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) throw Error(kConfig, "bsc: sigma2 must be positive");
-  if (!(pi > 0.0 && pi < 1.0)) throw Error(kConfig, "bsc: pi must lie in (0,1)");
+    if (!std::isfinite(w[i])) throw Error(kNumeric, std::string(nm) + ": non-finite dictionary");
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) throw Error(kConfig, std::string(nm) + ": sigma2 must be positive");
+  if (family_ == kDsc) {
+    if (!probs || n_probs != alphabet_.size()) throw Error(kConfig, "dsc: values/probs size mismatch");
+    double total = 0.0;
+    for (uint32_t i = 0; i < n_probs; ++i) {
+      if (!(probs[i] > 0.0)) throw Error(kConfig, "dsc: probabilities must be positive");
+      total += probs[i];
+    }
+    if (std::abs(total - 1.0) > 1e-6) throw Error(kConfig, "dsc: probabilities must sum to 1");
+    probs_.assign(probs, probs + n_probs);
+  } else if (!(pi > 0.0 && pi < 1.0)) {
+    throw Error(kConfig, std::string(nm) + ": pi must lie in (0,1)");
+  }
   ck(cudaSetDevice(device_), "set device");
   ck(cudaMemcpy2DAsync(d_w_, (size_t)Hp_ * 8, w, (size_t)H_ * 8, (size_t)H_ * 8, D_, cudaMemcpyHostToDevice,
                        static_cast<cudaStream_t>(stream_)),
@@ -565,6 +519,11 @@ void BscEngine::set_params(const double* w, double pi, double sigma2) {
   sigma2_ = sigma2;
   have_params_ = true;
   gram_fresh_ = false;
+}
+
+void BscEngine::get_params_ex(double* w, double* pi, double* sigma2, double* probs) {
+  get_params(w, pi, sigma2);
+  if (probs && family_ == kDsc) std::memcpy(probs, probs_.data(), probs_.size() * 8);
 }
 
 void BscEngine::get_params(double* w, double* pi, double* sigma2) {
@@ -594,17 +553,17 @@ void BscEngine::enqueue_gram(void* stream) {
   launches_ += 2;
 }
 
-void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
-                                 int chunk) {
+// The fields both enumerators share (EnumArgs, bsc_kernels.cuh): shapes, the
+// resident buffers of this chunk, the state tables and the per-shard
+// constants of linear_discrete.cpp:219-227 (host libm, as the reference).
+void BscEngine::fill_enum_args(void* out, double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
+                               int chunk, double log_p0) {
+  (void)chunk;
   auto s = static_cast<cudaStream_t>(stream_);
-  // value_table (:71-97, BSC :75-79) and the per-shard constants (:219-227),
-  // computed on the host with the same libm as the reference.
-  const double log_p1 = std::log(pi_), log_p0 = std::log(1.0 - pi_);
+  EnumArgs& a = *static_cast<EnumArgs*>(out);
   const double inv2s = 1.0 / (2.0 * sigma2_);
   const double norm_const = -0.5 * static_cast<double>(D_) * (kLog2Pi + std::log(sigma2_));
   const double zero_prior = static_cast<double>(H_) * log_p0;
-
-  EnumArgs a{};
   a.N = static_cast<int>(rows);
   a.D = D_;
   a.H = H_;
@@ -621,7 +580,6 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   a.y2 = d_y2_ + off;
   a.ES = d_es_ + off * Hp_;
   a.ssT = d_stats_ + lay_.off_ssT();
-  a.warp_scalars = d_warp_sc_ + (size_t)chunk * enum_ctas_ * 2;
   a.cand_out = cands ? d_cand_ + off * hprime_ : nullptr;
   a.map_mass = infer ? d_map_mass_ + off : nullptr;
   a.map_state = infer ? d_map_state_ + off : nullptr;
@@ -644,14 +602,28 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   a.sched_split = static_cast<const int4*>(d_sched_split_);
   a.n_slots = n_slots_;
   a.n_out = n_out_;
-  a.log_pi = log_p1;
-  a.dlp = log_p1 - log_p0;
   a.inv2s = inv2s;
   a.base0 = zero_prior + norm_const;
   a.inv_T = 1.0 / temperature;
   a.weight_mode = weight_mode_;
   a.eps_dot = 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
+}
 
+void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
+                                 int chunk) {
+  if (vpath()) {
+    launch_enumerate_v(temperature, cands, infer, off, rows, chunk);
+    return;
+  }
+  auto s = static_cast<cudaStream_t>(stream_);
+  // value_table (:71-97, BSC :75-79) and the per-shard constants (:219-227),
+  // computed on the host with the same libm as the reference.
+  const double log_p1 = std::log(pi_), log_p0 = std::log(1.0 - pi_);
+  EnumArgs a{};
+  fill_enum_args(&a, temperature, cands, infer, off, rows, chunk, log_p0);
+  a.log_pi = log_p1;
+  a.dlp = log_p1 - log_p0;
+  a.warp_scalars = d_warp_sc_ + (size_t)chunk * enum_ctas_ * 2;
   const int maxj = maxj_for(H_);
   void* args[] = {&a};
   ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s), "enumerate launch");
@@ -692,6 +664,11 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     d_warp_es_ = dalloc<double>((size_t)nchunks * splits_ * Hp_, "split-K column sums");
     d_warp_sc_ = dalloc<double>((size_t)nchunks * enum_ctas_ * 2, "cta scalars");
     colsum_chunks_ = nchunks;
+  }
+  if (vpath() && nchunks > vpart_chunks_) {
+    dfree(d_vpart_);
+    d_vpart_ = dalloc<double>((size_t)nchunks * enum_ctas_ * vpart_stride_, "cta partials");
+    vpart_chunks_ = nchunks;
   }
   launches_ = 0;
   ev(0);
@@ -745,12 +722,17 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   const long long DH = (long long)D_ * H_;
   reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
                                                            part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),
-                                                           lay_.off_ssT());
-  finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
-      nchunks * enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
-  counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
+                                                           vpath() ? -1 : lay_.off_ssT());
+  if (vpath()) {
+    finalize_v(nchunks * enum_ctas_, n);
+    launches_ += 2;
+  } else {
+    finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
+        nchunks * enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
+    counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
+    launches_ += 3;
+  }
   ck(cudaGetLastError(), "finalize");
-  launches_ += 3;
   ev(5);
 }
 
@@ -850,7 +832,8 @@ void BscEngine::enqueue_mstep(void* stream) {
   enqueue_gram(s);
   mstep_traces_kernel<<<kTraceCtas, 256, 0, s>>>(d_w_, Hp_, d_g_, Hp_, d_stats_, lay_.off_ssT(), D, H,
                                                   d_trace_part_);
-  mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, d_trace_part_, sc);
+  mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, static_cast<int>(values_.size()),
+                                       d_trace_part_, sc);
   ck(cudaGetLastError(), "mstep scalars");
   launches_ += 3;
 }
@@ -863,16 +846,45 @@ void BscEngine::finish_mstep() {
   // one synchronisation per iteration: new π, σ², the (all-reduced) F and the
   // E-step error flag come back together
   ck(cudaMemcpyAsync(h_msc_, sc, sizeof(MstepScalars), cudaMemcpyDeviceToHost, s), "mstep scalars D2H");
-  ck(cudaMemcpyAsync(h_tail_, d_stats_ + lay_.off_tail(), 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "F D2H");
+  const size_t V = values_.size();
+  ck(cudaMemcpyAsync(h_tail_, d_stats_ + lay_.off_tail(), (V + 3) * sizeof(double), cudaMemcpyDeviceToHost, s),
+     "F D2H");
   ck(cudaMemcpyAsync(h_err_, d_err_, sizeof(int), cudaMemcpyDeviceToHost, s), "err D2H");
   sync();
   const int err = *static_cast<int*>(h_err_);
   if (err & kErrNonFiniteScore) throw Error(kConfig, "select_candidates: scores must be finite");
   if (err & kErrNonFiniteLogJoint) throw Error(kNumeric, "log_sum_exp: empty support");
   const auto* h = static_cast<const MstepScalars*>(h_msc_);
-  pi_ = h->pi;
+  const double* tail = static_cast<const double*>(h_tail_);
   sigma2_ = h->sigma2;
-  last_F_ = static_cast<const double*>(h_tail_)[2];
+  last_F_ = tail[V + 1];
+  if (family_ == kDsc) {
+    // linear_discrete.cpp:382-404: probs of the non-zero values from the
+    // counts, the rest on 0, floored at 1e-9 (model.hpp:34) and renormalised
+    const double nh = tail[V + 2] * static_cast<double>(H_);
+    double nonzero = 0.0;
+    size_t k = 0;
+    for (size_t i = 0; i < alphabet_.size(); ++i) {
+      if (alphabet_[i] == 0.0) continue;
+      probs_[i] = tail[k++] / nh;
+      nonzero += probs_[i];
+    }
+    for (size_t i = 0; i < alphabet_.size(); ++i)
+      if (alphabet_[i] == 0.0) probs_[i] = 1.0 - nonzero;
+    bool floored = false;
+    for (double& q : probs_)
+      if (q < 1e-9) {
+        q = 1e-9;
+        floored = true;
+      }
+    if (floored) {
+      double tot = 0.0;
+      for (double q : probs_) tot += q;
+      for (double& q : probs_) q /= tot;
+    }
+  } else {
+    pi_ = h->pi;
+  }
   if (timing_) {
     auto el = [&](int a, int b) {
       float ms = 0;
@@ -903,11 +915,12 @@ void BscEngine::get_stats(double* sum_s, double* sum_ssT, double* sum_y_sT, doub
   if (sum_s) std::memcpy(sum_s, h.data() + lay_.off_s(), (size_t)H_ * 8);
   if (sum_ssT) std::memcpy(sum_ssT, h.data() + lay_.off_ssT(), (size_t)H_ * H_ * 8);
   const double* t = h.data() + lay_.off_tail();
-  if (value_counts) value_counts[0] = t[0];
+  const size_t V = values_.size();
+  if (value_counts) std::memcpy(value_counts, t, V * 8);
   if (scalars) {
-    scalars[0] = t[1];
-    scalars[1] = t[2];
-    scalars[2] = t[3];
+    scalars[0] = t[V];
+    scalars[1] = t[V + 1];
+    scalars[2] = t[V + 2];
   }
 }
 
@@ -918,11 +931,12 @@ void BscEngine::set_stats(const double* sum_s, const double* sum_ssT, const doub
   std::memcpy(h.data() + lay_.off_s(), sum_s, (size_t)H_ * 8);
   std::memcpy(h.data() + lay_.off_ssT(), sum_ssT, (size_t)H_ * H_ * 8);
   double* t = h.data() + lay_.off_tail();
-  t[0] = value_counts[0];
-  t[1] = scalars[0];
-  t[2] = scalars[1];
-  t[3] = scalars[2];
-  if (!(t[3] >= 1.0)) throw Error(kConfig, "bsc: mstep without data");
+  const size_t V = values_.size();
+  std::memcpy(t, value_counts, V * 8);
+  t[V] = scalars[0];
+  t[V + 1] = scalars[1];
+  t[V + 2] = scalars[2];
+  if (!(t[V + 2] >= 1.0)) throw Error(kConfig, "linear model: mstep without data");
   ck(cudaMemcpyAsync(d_stats_, h.data(), h.size() * 8, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream_)),
      "stats H2D");
   sync();
@@ -957,6 +971,20 @@ void BscEngine::inference(double* map_states, double* map_mass, double* expected
   check_err();
   const std::vector<uint64_t>& masks = dfs_masks_;
   std::memset(map_states, 0, n_ * H_ * 8);
+  if (vpath()) {  // index → (unit, value) lists: zero, (h, v) h-major, then DFS patterns
+    const uint64_t V = values_.size();
+    for (uint64_t n = 0; n < n_; ++n) {
+      const uint64_t i = static_cast<uint64_t>(st[n]);
+      double* row = map_states + n * H_;
+      if (i == 0) continue;
+      if (i <= H_ * V) {
+        row[(i - 1) / V] = values_[(i - 1) % V];
+        continue;
+      }
+      for (const auto& pv : dfs_patterns_[i - 1 - H_ * V]) row[cand[n * hprime_ + pv.first]] = values_[pv.second];
+    }
+    return;
+  }
   for (uint64_t n = 0; n < n_; ++n) {
     const int i = st[n];
     double* row = map_states + n * H_;

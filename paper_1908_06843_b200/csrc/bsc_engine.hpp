@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace bscgpu {
@@ -18,14 +19,23 @@ struct Error : std::runtime_error {
 };
 inline constexpr int kConfig = 2, kData = 3, kNumeric = 4, kInternal = 5;
 
+// Packed statistics buffer (the all-reduce payload): [Σy⟨s⟩ᵀ D·H | Σ⟨s⟩ H |
+// Σ⟨ssᵀ⟩ H·H | value_counts V | Σ‖y‖² | Σ log Z | N] (SuffStats fields,
+// linear_discrete.cpp:211-217; V = number of non-zero values).
 struct StatsLayout {
-  long long D, H;
+  long long D, H, V = 1;
   long long off_ysT() const { return 0; }
   long long off_s() const { return D * H; }
   long long off_ssT() const { return D * H + H; }
-  long long off_tail() const { return D * H + H + H * H; }  // counts, y2, logZ, points
-  long long count() const { return off_tail() + 4; }
+  long long off_tail() const { return D * H + H + H * H; }  // counts[V], y2, logZ, points
+  long long count() const { return off_tail() + V + 3; }
 };
+
+// Linear discrete families (LinearDiscreteModel, linear_discrete.hpp:31-87).
+enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
+
+// The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
+const void* ldv_kernel_fn(int maxj, bool staged);
 
 struct EngineTimings {
   float gram_ms, gemm1_ms, enum_ms, gemm2_ms, finalize_ms, mstep_ms;
@@ -34,6 +44,9 @@ struct EngineTimings {
 class BscEngine {
  public:
   BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap, int device);
+  // family kTsc / kDsc (dsc: `alphabet` of n_alpha distinct values containing 0)
+  BscEngine(int family, uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
+            const double* alphabet, uint32_t n_alpha, int device);
   ~BscEngine();
   BscEngine(const BscEngine&) = delete;
   BscEngine& operator=(const BscEngine&) = delete;
@@ -47,6 +60,13 @@ class BscEngine {
 
   void set_params(const double* w_host, double pi, double sigma2);
   void get_params(double* w_host, double* pi, double* sigma2);
+  // dsc: probabilities aligned with the sorted alphabet (pi unused)
+  void set_params_ex(const double* w_host, double pi, double sigma2, const double* probs, uint32_t n_probs);
+  void get_params_ex(double* w_host, double* pi, double* sigma2, double* probs);
+  int family() const { return family_; }
+  uint32_t num_values() const { return static_cast<uint32_t>(values_.size()); }  // non-zero values
+  uint32_t alphabet_size() const { return static_cast<uint32_t>(alphabet_.size()); }
+  const std::vector<double>& alphabet() const { return alphabet_; }
 
   // E-step over the resident shard at temperature T → device stats buffer.
   void estep(double temperature, bool want_candidates = false);
@@ -71,7 +91,7 @@ class BscEngine {
   uint32_t latents() const { return H_; }
   uint32_t hprime() const { return hprime_; }
   uint32_t gamma() const { return gamma_; }
-  uint64_t states_per_point() const { return 1 + H_ + n_multi_; }
+  uint64_t states_per_point() const { return 1 + (uint64_t)H_ * values_.size() + n_multi_; }
   int enum_launch_ctas() const { return enum_ctas_; }
   int enum_warps() const { return enum_warps_total_; }
   const EngineTimings& timings() const { return t_; }
@@ -83,7 +103,15 @@ class BscEngine {
   void sync();
 
  private:
+  void init(int device);
   void build_template();
+  void build_template_v();  // multi-valued families (ldv_engine.cu)
+  void launch_enumerate_v(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows, int chunk);
+  void fill_enum_args(void* enum_args, double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
+                      int chunk, double log_p0);
+  bool vpath() const { return family_ != kBsc; }
+  int ldv_per_warp_bytes() const;
+  void finalize_v(int nparts, uint64_t n);
   void ensure_work(uint64_t n);
   void refresh_gram();
   void launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows, int chunk);
@@ -93,6 +121,10 @@ class BscEngine {
   void enqueue_gram(void* stream);
   void finish_mstep();
 
+  int family_ = kBsc;
+  std::vector<double> alphabet_;  // dsc: sorted alphabet with 0; bsc {0,1}; tsc {-1,0,1}
+  std::vector<double> values_;    // the non-zero values, ascending
+  std::vector<double> probs_;     // dsc probabilities (aligned with alphabet_)
   uint32_t D_, H_, hprime_, gamma_;
   uint64_t cap_;
   int device_;
@@ -110,6 +142,9 @@ class BscEngine {
   int desc_bytes_ = 0, ent_bytes_ = 0;  // table sizes (16-byte multiples)
   bool stage_tables_ = false;           // staged into shared memory per CTA
   std::vector<uint64_t> dfs_masks_;  // multi-active supports in reference order
+  std::vector<std::vector<std::pair<uint8_t, uint8_t>>> dfs_patterns_;  // V path: (position, value index)
+  double* d_vpart_ = nullptr;        // V path: per-CTA partials [chunks][ctas][vpart_stride_]
+  int vpart_stride_ = 0, vpart_chunks_ = 0;
   void* d_desc_ = nullptr;
   int* d_dfs_ = nullptr;
   int* d_level_off_ = nullptr;

@@ -46,7 +46,7 @@ __device__ __forceinline__ bool ranks_before(double v1, int i1, double v2, int i
 // acc += w·w over d, separately rounded) — the selection scores use it, so it
 // must match bit for bit — plus column norms for the selection error bound.
 // The off-diagonal Gram (pairwise log-joint terms, t3) comes from the DMMA GEMM.
-__global__ void gram_diag_exact_kernel(const double* __restrict__ W, int D, int H, int ldw,
+static __global__ void gram_diag_exact_kernel(const double* __restrict__ W, int D, int H, int ldw,
                                        double* __restrict__ G, int ldg, double* __restrict__ wnorm,
                                        double* __restrict__ gdiag) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -102,7 +102,7 @@ __device__ __forceinline__ double exp_nonpos(double x) {
 
 // ‖y_n‖² per data point (linear_discrete.cpp:242), once per resident dataset:
 // one warp per row.
-__global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int D, int ldy,
+static __global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int D, int ldy,
                                   double* __restrict__ y2) {
   const long long n = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
 // statistics [ysT D·H | s H | ssT H·H | counts | y2 | logZ | points]:
 // Σ y⟨s⟩ᵀ from the GEMM partials, Σ⟨s⟩ (= diag Σ⟨ssᵀ⟩, v = 1) from its
 // fused column sums.
-__global__ void reduce_ysT_kernel(const double* __restrict__ part, const double* __restrict__ colsum, int splits,
+static __global__ void reduce_ysT_kernel(const double* __restrict__ part, const double* __restrict__ colsum, int splits,
                                   int colsum_rows, long long split_stride, int D, int H, int ldp,
                                   double* __restrict__ stats, long long off_s, long long off_ssT) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -936,12 +936,12 @@ __global__ void reduce_ysT_kernel(const double* __restrict__ part, const double*
     double s = 0.0;
     for (int z = 0; z < colsum_rows; ++z) s += colsum[(long long)z * ldp + h];
     stats[off_s + h] = s;
-    stats[off_ssT + (long long)h * H + h] = s;
+    if (off_ssT >= 0) stats[off_ssT + (long long)h * H + h] = s;  // BSC: ⟨s_h²⟩ = ⟨s_h⟩
   }
 }
 
 // Mirror of the upper triangle of Σ⟨ssᵀ⟩ and the scalars.
-__global__ void finalize_stats_kernel(int nctas, const double* __restrict__ cta_scalars, int H, long long npoints,
+static __global__ void finalize_stats_kernel(int nctas, const double* __restrict__ cta_scalars, int H, long long npoints,
                                       double* __restrict__ stats, long long off_ssT, long long off_tail) {
   double* ssT = stats + off_ssT;
   const long long HH = (long long)H * H;
@@ -966,7 +966,7 @@ __global__ void finalize_stats_kernel(int nctas, const double* __restrict__ cta_
 }
 
 // value_counts = Σ_h Σ⟨s⟩_h (every active unit carries value 1)
-__global__ void counts_kernel(double* stats, long long off_s, int H, long long off_tail) {
+static __global__ void counts_kernel(double* stats, long long off_s, int H, long long off_tail) {
   double acc = 0.0;
   for (int h = threadIdx.x; h < H; h += 32) acc += stats[off_s + h];
   acc = warp_sum(acc);

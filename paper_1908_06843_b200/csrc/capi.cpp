@@ -17,6 +17,9 @@
 struct prsp_bsc_gpu {
   bscgpu::BscEngine engine;
   prsp_bsc_gpu(uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, int dev) : engine(d, h, hp, g, cap, dev) {}
+  prsp_bsc_gpu(int fam, uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, const double* vals, uint32_t nv,
+               int dev)
+      : engine(fam, d, h, hp, g, cap, vals, nv, dev) {}
 };
 
 namespace {
@@ -66,6 +69,34 @@ int prsp_bsc_gpu_create(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_
   });
 }
 
+int prsp_bsc_gpu_create_model(const char* model, uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma,
+                              uint64_t state_cap, const double* values, uint32_t n_values, int device,
+                              prsp_bsc_gpu** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(model, "model");
+    const std::string m(model);
+    int fam = -1;
+    if (m == "bsc") fam = bscgpu::kBsc;
+    if (m == "tsc") fam = bscgpu::kTsc;
+    if (m == "dsc") fam = bscgpu::kDsc;
+    if (fam < 0) throw bscgpu::Error(bscgpu::kConfig, "unknown model '" + m + "' (gpu: bsc, tsc, dsc)");
+    *out = new prsp_bsc_gpu(fam, dim, latents, hprime, gamma, state_cap, values, n_values, device);
+  });
+}
+
+int prsp_bsc_gpu_model_info(const prsp_bsc_gpu* ctx, int* family, uint32_t* n_values, uint32_t* alphabet_size,
+                            double* alphabet_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    const auto& e = ctx->engine;
+    if (family) *family = e.family();
+    if (n_values) *n_values = e.num_values();
+    if (alphabet_size) *alphabet_size = e.alphabet_size();
+    if (alphabet_out) std::memcpy(alphabet_out, e.alphabet().data(), e.alphabet().size() * sizeof(double));
+  });
+}
+
 void prsp_bsc_gpu_free(prsp_bsc_gpu* ctx) { delete ctx; }
 
 int prsp_bsc_gpu_set_stream(prsp_bsc_gpu* ctx, void* stream) {
@@ -112,6 +143,23 @@ int prsp_bsc_gpu_set_params(prsp_bsc_gpu* ctx, const double* w, double pi, doubl
     need(w, "w");
     ctx->engine.set_params(w, pi, sigma2);
     ctx->engine.sync();
+  });
+}
+
+int prsp_bsc_gpu_set_params_ex(prsp_bsc_gpu* ctx, const double* w, double pi, double sigma2, const double* probs,
+                               uint32_t n_probs) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(w, "w");
+    ctx->engine.set_params_ex(w, pi, sigma2, probs, n_probs);
+    ctx->engine.sync();
+  });
+}
+
+int prsp_bsc_gpu_get_params_ex(prsp_bsc_gpu* ctx, double* w, double* pi, double* sigma2, double* probs) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.get_params_ex(w, pi, sigma2, probs);
   });
 }
 

@@ -196,8 +196,11 @@ __global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const
   }
 }
 
-// σ²' = max((t1 − 2t2 + t3)/(N·D), 1e-12), π' = clip(counts/(N·H), 1e-6, 1−1e-6)
-__global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long off_tail, int D, int H,
+// σ²' = max((t1 − 2t2 + t3)/(N·D), 1e-12) and, for bsc / tsc,
+// π' = clip(Σ_v counts_v/(N·H), 1e-6, 1−1e-6) (linear_discrete.cpp:369-381:
+// bsc counts(0,0), tsc counts(0,0) + counts(0,1)); dsc probabilities are
+// finished on the host from the counts. Tail layout: counts[V], y2, logZ, N.
+__global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long off_tail, int D, int H, int V,
                                      const double* __restrict__ partial, MstepScalars* sc) {
   double t2 = 0.0, t3 = 0.0;
   for (int c = 0; c < kTraceCtas; ++c) {
@@ -206,11 +209,13 @@ __global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long
   }
   sc->t2 = t2;
   sc->t3 = t3;
-  const double n = stats[off_tail + 3];
-  const double t1 = stats[off_tail + 1];
+  const double n = stats[off_tail + V + 2];
+  const double t1 = stats[off_tail + V];
   const double s2 = (t1 - 2.0 * sc->t2 + sc->t3) / (n * static_cast<double>(D));
   sc->sigma2 = s2 < 1e-12 ? 1e-12 : s2;
-  double p = stats[off_tail] / (n * static_cast<double>(H));
+  double cnt = stats[off_tail];
+  for (int k = 1; k < V; ++k) cnt += stats[off_tail + k];
+  double p = cnt / (n * static_cast<double>(H));
   p = p < 1e-6 ? 1e-6 : p;
   p = (1.0 - 1e-6) < p ? (1.0 - 1e-6) : p;
   sc->pi = p;
