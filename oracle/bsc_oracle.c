@@ -1306,3 +1306,523 @@ int ld_generate(uint32_t family, const double* alpha, const double* probs, uint3
   free(s);
   return OK;
 }
+
+/* ============================================================ max causes */
+/* MaxCausesModel (max_causes.cpp): binary latents, the data mean at each
+ * dimension is the dictionary entry of the winning active unit (largest W, or
+ * largest |W| in absmax mode; ties keep the lowest unit). mode 0 = mca (kMax),
+ * 1 = mmca (kAbsMax). */
+#define K_MIN_MCA_WEIGHT 1e-8 /* model.hpp:36 */
+#define K_EVIDENCE_FLOOR 1e-9 /* model.hpp:37 */
+
+typedef struct {
+  uint32_t mode;
+  double rho; /* soft winner exponent (mca only), 0 = hard winners */
+} mca_cfg_t;
+
+/* winner_at, max_causes.cpp:27-41 */
+static uint32_t mca_winner(const double* w, uint32_t h, size_t d, const uint32_t* act, uint32_t k,
+                           uint32_t mode) {
+  uint32_t best = act[0];
+  double best_key = mode == 0 ? w[d * h + act[0]] : fabs(w[d * h + act[0]]);
+  for (uint32_t i = 1; i < k; ++i) {
+    const double key = mode == 0 ? w[d * h + act[i]] : fabs(w[d * h + act[i]]);
+    if (key > best_key) {
+      best_key = key;
+      best = act[i];
+    }
+  }
+  return best;
+}
+
+static int mca_validate(uint32_t d, uint32_t h, const double* w, double pi, double sigma2, uint32_t mode) {
+  const char* nm = mode == 0 ? "mca" : "mmca";
+  for (size_t i = 0; i < (size_t)d * h; ++i)
+    if (!isfinite(w[i])) return fail(E_NUMERIC, "%s: non-finite dictionary", nm);
+  if (mode == 0)
+    for (size_t i = 0; i < (size_t)d * h; ++i)
+      if (w[i] < K_MIN_MCA_WEIGHT) return fail(E_CONFIG, "mca: dictionary entries must be >= the weight floor");
+  if (!(pi > 0.0 && pi < 1.0)) return fail(E_CONFIG, "%s: pi must lie in (0,1)", nm);
+  if (!(sigma2 > 0.0)) return fail(E_CONFIG, "%s: sigma2 must be positive", nm);
+  return OK;
+}
+
+/* selection scores, max_causes.cpp:174-176: (2 w_h·y − ‖w_h‖²)·inv2s */
+static void mca_scores(const double* wt, uint32_t d, uint32_t h, const double* y, double inv2s, double* scores) {
+  for (uint32_t u = 0; u < h; ++u) {
+    const double* col = wt + (size_t)u * d;
+    double dot = 0.0, sq = 0.0;
+    for (uint32_t t = 0; t < d; ++t) dot += col[t] * y[t];
+    for (uint32_t t = 0; t < d; ++t) sq += col[t] * col[t];
+    scores[u] = (2.0 * dot - sq) * inv2s;
+  }
+}
+
+typedef struct {
+  double *num, *den; /* winner_num, winner_den (D×H) */
+  double sum_act, log_partition;
+  uint64_t points;
+  double residual; /* residual pass */
+} mca_stats_t;
+
+/* Per-point states, log-joints (and winners) under W: the shared core of
+ * estep_impl (:180-250) and residual_impl (:283-350). */
+static int mca_point(const double* w, const double* wt, uint32_t d, uint32_t h, uint32_t hprime,
+                     const tmpl_t* tmpl, uint32_t mode, double pi, double sigma2, const double* y,
+                     states_t* s, uint32_t* cand, double* scores, keyed_t* scratch, double* lj,
+                     uint32_t* winners, double* resid_out) {
+  const double lp1 = log(pi), lp0 = log(1.0 - pi);
+  const double norm_const = -0.5 * (double)d * (K_LOG_2PI + log(sigma2));
+  const double inv2s = 1.0 / (2.0 * sigma2);
+  mca_scores(wt, d, h, y, inv2s, scores);
+  int rc = select_cands(scores, h, hprime, cand, scratch);
+  if (rc) return rc;
+  instantiate(tmpl, h, cand, s);
+  for (size_t i = 0; i < s->n; ++i) {
+    const uint32_t k = s->len[i];
+    const uint32_t* act = s->act + i * s->stride;
+    double resid = 0.0;
+    if (k == 0) {
+      for (uint32_t t = 0; t < d; ++t) resid += y[t] * y[t];
+    } else {
+      for (uint32_t t = 0; t < d; ++t) {
+        const uint32_t win = mca_winner(w, h, t, act, k, mode);
+        if (winners) winners[i * d + t] = win;
+        const double r = y[t] - w[(size_t)t * h + win];
+        resid += r * r;
+      }
+    }
+    if (resid_out) resid_out[i] = resid;
+    const double kk = (double)k;
+    lj[i] = kk * lp1 + ((double)h - kk) * lp0 + norm_const - resid * inv2s;
+  }
+  return OK;
+}
+
+typedef struct {
+  uint32_t d, h, hprime, gamma, mode;
+  double rho, pi, sigma2, temperature;
+  const double *w, *wt, *y;
+  const double *w_new; /* residual pass: the updated dictionary (NULL in the E pass) */
+  const tmpl_t* tmpl;
+} mca_ctx_t;
+
+static int mca_rows(const mca_ctx_t* c, uint64_t rb, uint64_t re, mca_stats_t* st, double* map_states,
+                    double* map_mass, double* expected) {
+  const uint32_t d = c->d, h = c->h;
+  const size_t total = 1 + h + c->tmpl->count;
+  states_t s;
+  states_alloc(&s, total, c->gamma);
+  double* scores = malloc(h * sizeof(double));
+  double* lj = malloc(total * sizeof(double));
+  double* q = malloc(total * sizeof(double));
+  double* es = malloc(h * sizeof(double));
+  double* rnew = malloc(total * sizeof(double));
+  uint32_t* winners = malloc(total * d * sizeof(uint32_t));
+  uint32_t* cand = malloc(c->hprime * sizeof(uint32_t));
+  keyed_t* scratch = malloc(h * sizeof(keyed_t));
+  int rc = OK;
+  for (uint64_t n = rb; n < re && !rc; ++n) {
+    const double* y = c->y + n * d;
+    rc = mca_point(c->w, c->wt, d, h, c->hprime, c->tmpl, c->mode, c->pi, c->sigma2, y, &s, cand, scores,
+                   scratch, lj, c->w_new ? NULL : winners, NULL);
+    if (rc) break;
+    if (c->w_new) { /* residual_impl :315-349: q at T (max/sum), resid under W' */
+      for (size_t i = 0; i < s.n; ++i) {
+        const uint32_t k = s.len[i];
+        const uint32_t* act = s.act + i * s.stride;
+        double r = 0.0;
+        if (k == 0) {
+          for (uint32_t t = 0; t < d; ++t) r += y[t] * y[t];
+        } else {
+          for (uint32_t t = 0; t < d; ++t) {
+            const double b = y[t] - c->w_new[(size_t)t * h + mca_winner(c->w_new, h, t, act, k, c->mode)];
+            r += b * b;
+          }
+        }
+        rnew[i] = r;
+      }
+      double m = lj[0];
+      for (size_t i = 0; i < s.n; ++i) m = dmax(m, lj[i]);
+      double acc = 0.0;
+      for (size_t i = 0; i < s.n; ++i) {
+        q[i] = exp((lj[i] - m) / c->temperature);
+        acc += q[i];
+      }
+      double pr = 0.0;
+      for (size_t i = 0; i < s.n; ++i) pr += q[i] / acc * rnew[i];
+      st->residual += pr;
+      st->points++;
+      continue;
+    }
+    double lse1;
+    rc = lse(lj, s.n, &lse1);
+    if (rc) break;
+    if (c->temperature == 1.0) {
+      for (size_t i = 0; i < s.n; ++i) q[i] = exp(lj[i] - lse1);
+    } else {
+      double m = lj[0];
+      for (size_t i = 0; i < s.n; ++i) m = dmax(m, lj[i]);
+      double acc = 0.0;
+      for (size_t i = 0; i < s.n; ++i) {
+        q[i] = exp((lj[i] - m) / c->temperature);
+        acc += q[i];
+      }
+      for (size_t i = 0; i < s.n; ++i) q[i] /= acc;
+    }
+    for (uint32_t j = 0; j < h; ++j) es[j] = 0.0; /* :226-259 */
+    for (size_t i = 0; i < s.n; ++i) {
+      const double qi = q[i];
+      const uint32_t k = s.len[i];
+      const uint32_t* act = s.act + i * s.stride;
+      if (k == 0) continue;
+      st->sum_act += qi * (double)k;
+      for (uint32_t a = 0; a < k; ++a) es[act[a]] += qi;
+      if (c->rho > 0.0) {
+        for (uint32_t t = 0; t < d; ++t) {
+          double wmax = 0.0;
+          for (uint32_t a = 0; a < k; ++a) wmax = dmax(wmax, c->w[(size_t)t * h + act[a]]);
+          double tot = 0.0;
+          for (uint32_t a = 0; a < k; ++a) tot += pow(c->w[(size_t)t * h + act[a]] / wmax, c->rho);
+          for (uint32_t a = 0; a < k; ++a) {
+            const double share = pow(c->w[(size_t)t * h + act[a]] / wmax, c->rho) / tot;
+            st->num[(size_t)t * h + act[a]] += qi * share * y[t];
+            st->den[(size_t)t * h + act[a]] += qi * share;
+          }
+        }
+      } else {
+        for (uint32_t t = 0; t < d; ++t) {
+          const uint32_t win = winners[i * d + t];
+          st->num[(size_t)t * h + win] += qi * y[t];
+          st->den[(size_t)t * h + win] += qi;
+        }
+      }
+    }
+    st->log_partition += lse1;
+    st->points++;
+    if (map_states) {
+      size_t best = 0;
+      for (size_t i = 1; i < s.n; ++i)
+        if (q[i] > q[best]) best = i;
+      map_mass[n] = q[best];
+      for (uint32_t a = 0; a < s.len[best]; ++a) map_states[n * h + s.act[best * s.stride + a]] = 1.0;
+      for (uint32_t j = 0; j < h; ++j) expected[n * h + j] = es[j];
+    }
+  }
+  states_free(&s);
+  free(scores);
+  free(lj);
+  free(q);
+  free(es);
+  free(rnew);
+  free(winners);
+  free(cand);
+  free(scratch);
+  return rc;
+}
+
+static int mca_ctx_init(mca_ctx_t* c, tmpl_t* t, uint32_t mode, double rho, uint32_t d, uint32_t h,
+                        uint32_t hprime, uint32_t gamma, const double* w, double pi, double sigma2,
+                        double temperature, const double* y) {
+  int rc = mca_validate(d, h, w, pi, sigma2, mode);
+  if (rc) return rc;
+  if (rho < 0.0) return fail(E_CONFIG, "%s: soft winner exponent must be >= 0", mode == 0 ? "mca" : "mmca");
+  if (rho > 0.0 && mode != 0) return fail(E_CONFIG, "soft winners require the non-negative max mode");
+  rc = tmpl_build(t, h, hprime, gamma, 1, 1000000);
+  if (rc) return rc;
+  double* wt = malloc((size_t)d * h * sizeof(double));
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j) wt[(size_t)j * d + i] = w[(size_t)i * h + j];
+  *c = (mca_ctx_t){d, h, hprime, gamma, mode, rho, pi, sigma2, temperature, w, wt, y, NULL, t};
+  return OK;
+}
+
+/* MaxCausesModel::estep_stats (:384-391). scalars = {sum_act, log_partition, points}. */
+int mca_estep_stats(uint32_t mode, double rho, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                    const double* w, double pi, double sigma2, double temperature, const double* y, uint64_t n,
+                    uint64_t row_begin, uint64_t row_end, double* winner_num, double* winner_den,
+                    double* scalars) {
+  if (row_end < row_begin || row_end > n) return fail(E_CONFIG, "bad row range");
+  mca_ctx_t c;
+  tmpl_t t;
+  int rc = mca_ctx_init(&c, &t, mode, rho, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
+  if (rc) return rc;
+  mca_stats_t st = {calloc((size_t)d * h, 8), calloc((size_t)d * h, 8), 0.0, 0.0, 0, 0.0};
+  rc = mca_rows(&c, row_begin, row_end, &st, NULL, NULL, NULL);
+  if (!rc) {
+    memcpy(winner_num, st.num, (size_t)d * h * 8);
+    memcpy(winner_den, st.den, (size_t)d * h * 8);
+    scalars[0] = st.sum_act;
+    scalars[1] = st.log_partition;
+    scalars[2] = (double)st.points;
+  }
+  free(st.num);
+  free(st.den);
+  free((void*)c.wt);
+  tmpl_free(&t);
+  return rc;
+}
+
+/* MaxCausesModel::mstep_fixedpoint (:393-414). */
+int mca_mstep_fixedpoint(uint32_t mode, uint32_t d, uint32_t h, const double* w_prev, const double* winner_num,
+                         const double* winner_den, const double* scalars, double* w_out, double* pi_out) {
+  const uint64_t points = (uint64_t)scalars[2];
+  if (points == 0) return fail(E_CONFIG, "%s: mstep without data", mode == 0 ? "mca" : "mmca");
+  const double nh = (double)points * (double)h;
+  if (w_out != w_prev) memcpy(w_out, w_prev, (size_t)d * h * 8);
+  for (size_t i = 0; i < (size_t)d * h; ++i)
+    if (winner_den[i] >= K_EVIDENCE_FLOOR) {
+      double v = winner_num[i] / winner_den[i];
+      if (mode == 0) v = dmax(v, K_MIN_MCA_WEIGHT);
+      w_out[i] = v;
+    }
+  *pi_out = dmin(dmax(scalars[0] / nh, K_MIN_PI), 1.0 - K_MIN_PI);
+  return OK;
+}
+
+/* ------------- map_reduce for the two passes of MaxCausesModel::step */
+typedef struct {
+  const mca_ctx_t* c;
+  uint64_t n, shards;
+  mca_stats_t* partial;
+  int* rc;
+  char (*err)[512];
+  uint64_t next;
+  pthread_mutex_t mu;
+} mca_pool_t;
+
+static void* mca_worker(void* arg) {
+  mca_pool_t* p = arg;
+  for (;;) {
+    pthread_mutex_lock(&p->mu);
+    const uint64_t i = p->next++;
+    pthread_mutex_unlock(&p->mu);
+    if (i >= p->shards) return NULL;
+    uint64_t b, e;
+    shard_range(p->n, p->shards, i, &b, &e);
+    p->rc[i] = mca_rows(p->c, b, e, &p->partial[i], NULL, NULL, NULL);
+    if (p->rc[i]) snprintf(p->err[i], 512, "shard %llu: %s", (unsigned long long)i, g_err);
+  }
+}
+
+static int mca_map_reduce(const mca_ctx_t* c, uint64_t n, uint32_t shards, uint32_t workers, mca_stats_t* tot) {
+  mca_pool_t p;
+  p.c = c;
+  p.n = n;
+  p.shards = shards;
+  p.partial = malloc(shards * sizeof(mca_stats_t));
+  p.rc = calloc(shards, sizeof(int));
+  p.err = calloc(shards, 512);
+  p.next = 0;
+  pthread_mutex_init(&p.mu, NULL);
+  const size_t dh = (size_t)c->d * c->h;
+  for (uint32_t i = 0; i < shards; ++i)
+    p.partial[i] = (mca_stats_t){calloc(dh, 8), calloc(dh, 8), 0.0, 0.0, 0, 0.0};
+  const uint32_t threads = workers < shards ? workers : shards;
+  if (threads <= 1) {
+    mca_worker(&p);
+  } else {
+    pthread_t* th = malloc(threads * sizeof(pthread_t));
+    for (uint32_t i = 0; i < threads; ++i) pthread_create(&th[i], NULL, mca_worker, &p);
+    for (uint32_t i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+  }
+  int rc = OK;
+  for (uint32_t i = 0; i < shards && !rc; ++i)
+    if (p.rc[i]) rc = fail(p.rc[i], "%s", p.err[i]);
+  if (!rc) { /* SuffStats::combine: ordered fold, fields in insertion order */
+    *tot = p.partial[0];
+    p.partial[0].num = p.partial[0].den = NULL;
+    for (uint32_t i = 1; i < shards; ++i) {
+      const mca_stats_t* o = &p.partial[i];
+      for (size_t j = 0; j < dh; ++j) tot->num[j] += o->num[j];
+      for (size_t j = 0; j < dh; ++j) tot->den[j] += o->den[j];
+      tot->sum_act += o->sum_act;
+      tot->log_partition += o->log_partition;
+      tot->residual += o->residual;
+      tot->points += o->points;
+    }
+  }
+  for (uint32_t i = 0; i < shards; ++i) {
+    free(p.partial[i].num);
+    free(p.partial[i].den);
+  }
+  free(p.partial);
+  free(p.rc);
+  free(p.err);
+  pthread_mutex_destroy(&p.mu);
+  return rc;
+}
+
+/* MaxCausesModel::step (:416-446): E pass, fixed-point M-step, then the
+ * residual pass for sigma2 (posterior held at the incoming params). */
+int mca_step(uint32_t mode, double rho, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+             const double* w, double pi, double sigma2, double temperature, const double* y, uint64_t n,
+             uint32_t shards, uint32_t workers, double* w_out, double* pi_out, double* sigma2_out,
+             double* free_energy) {
+  if (shards == 0 || workers == 0) return fail(E_CONFIG, "shard plan: shards and workers must be >= 1");
+  mca_ctx_t c;
+  tmpl_t t;
+  int rc = mca_ctx_init(&c, &t, mode, rho, d, h, hprime, gamma, w, pi, sigma2, temperature, y);
+  if (rc) return rc;
+  mca_stats_t st = {0};
+  rc = mca_map_reduce(&c, n, shards, workers, &st);
+  double* wn = malloc((size_t)d * h * 8);
+  double pin = pi;
+  if (!rc) {
+    double sc[3] = {st.sum_act, st.log_partition, (double)st.points};
+    rc = mca_mstep_fixedpoint(mode, d, h, w, st.num, st.den, sc, wn, &pin);
+  }
+  if (!rc) {
+    mca_ctx_t c2 = c;
+    c2.w_new = wn;
+    mca_stats_t rs = {0};
+    rc = mca_map_reduce(&c2, n, shards, workers, &rs);
+    if (!rc) {
+      memcpy(w_out, wn, (size_t)d * h * 8);
+      *pi_out = pin;
+      *sigma2_out = dmax(rs.residual / ((double)st.points * (double)d), K_MIN_SIGMA2);
+      *free_energy = st.log_partition;
+    }
+    free(rs.num);
+    free(rs.den);
+  }
+  free(wn);
+  free(st.num);
+  free(st.den);
+  free((void*)c.wt);
+  tmpl_free(&t);
+  return rc;
+}
+
+int mca_candidates(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, const double* w, double pi,
+                   double sigma2, const double* y, uint64_t n, uint32_t* out) {
+  int rc = mca_validate(d, h, w, pi, sigma2, mode);
+  if (rc) return rc;
+  double* wt = malloc((size_t)d * h * 8);
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j) wt[(size_t)j * d + i] = w[(size_t)i * h + j];
+  double* scores = malloc(h * 8);
+  keyed_t* scratch = malloc(h * sizeof(keyed_t));
+  for (uint64_t i = 0; i < n && !rc; ++i) {
+    mca_scores(wt, d, h, y + i * d, 1.0 / (2.0 * sigma2), scores);
+    rc = select_cands(scores, h, hprime, out + i * hprime, scratch);
+  }
+  free(wt);
+  free(scores);
+  free(scratch);
+  return rc;
+}
+
+/* MaxCausesModel::inference (:448-468). */
+int mca_inference(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma, const double* w,
+                  double pi, double sigma2, const double* y, uint64_t n, double* map_states, double* map_mass,
+                  double* expected) {
+  mca_ctx_t c;
+  tmpl_t t;
+  int rc = mca_ctx_init(&c, &t, mode, 0.0, d, h, hprime, gamma, w, pi, sigma2, 1.0, y);
+  if (rc) return rc;
+  memset(map_states, 0, n * h * 8);
+  mca_stats_t st = {calloc((size_t)d * h, 8), calloc((size_t)d * h, 8), 0.0, 0.0, 0, 0.0};
+  rc = mca_rows(&c, 0, n, &st, map_states, map_mass, expected);
+  free(st.num);
+  free(st.den);
+  free((void*)c.wt);
+  tmpl_free(&t);
+  return rc;
+}
+
+/* MaxCausesModel::log_joint (:132-153). */
+int mca_log_joint(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2,
+                  const double* y, const double* s, double* out) {
+  uint32_t* act = malloc((h ? h : 1) * sizeof(uint32_t));
+  uint32_t k = 0;
+  for (uint32_t j = 0; j < h; ++j) {
+    if (s[j] == 1.0)
+      act[k++] = j;
+    else if (s[j] != 0.0) {
+      free(act);
+      return fail(E_CONFIG, "max causes: latent configuration must be binary");
+    }
+  }
+  double resid = 0.0;
+  for (uint32_t t = 0; t < d; ++t) {
+    const double wb = k ? w[(size_t)t * h + mca_winner(w, h, t, act, k, mode)] : 0.0;
+    const double r = y[t] - wb;
+    resid += r * r;
+  }
+  free(act);
+  const double prior = (double)k * log(pi) + (double)(h - k) * log(1.0 - pi);
+  *out = prior - 0.5 * (double)d * (K_LOG_2PI + log(sigma2)) - resid / (2.0 * sigma2);
+  return OK;
+}
+
+/* MaxCausesModel::exact_log_likelihood (:454-474): all 2^H masks. */
+int mca_exact_log_likelihood(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2,
+                             const double* y, uint64_t n, double* out) {
+  int rc = mca_validate(d, h, w, pi, sigma2, mode);
+  if (rc) return rc;
+  if (h > 22) return fail(E_CONFIG, "%s: state space too large for exact evaluation", mode == 0 ? "mca" : "mmca");
+  const uint64_t ns = 1ull << h;
+  double* lj = malloc(ns * 8);
+  double* s = malloc(h * 8);
+  double total = 0.0;
+  for (uint64_t i = 0; i < n && !rc; ++i) {
+    for (uint64_t m = 0; m < ns && !rc; ++m) {
+      for (uint32_t j = 0; j < h; ++j) s[j] = (m >> j) & 1 ? 1.0 : 0.0;
+      rc = mca_log_joint(mode, d, h, w, pi, sigma2, y + i * d, s, &lj[m]);
+    }
+    double l;
+    if (!rc) rc = lse(lj, ns, &l);
+    if (!rc) total += l;
+  }
+  *out = total;
+  free(lj);
+  free(s);
+  return rc;
+}
+
+/* MaxCausesModel::generate (:430-452). */
+int mca_generate(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2, uint64_t n,
+                 uint64_t seed, double* y_out) {
+  int rc = mca_validate(d, h, w, pi, sigma2, mode);
+  if (rc) return rc;
+  const double noise_std = sqrt(sigma2);
+  uint32_t* act = malloc((h ? h : 1) * sizeof(uint32_t));
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t k = 0;
+    for (uint32_t j = 0; j < h; ++j)
+      if (rng_bernoulli(&r, pi)) act[k++] = j;
+    for (uint32_t t = 0; t < d; ++t) {
+      const double wb = k ? w[(size_t)t * h + mca_winner(w, h, t, act, k, mode)] : 0.0;
+      y_out[i * d + t] = wb + noise_std * rng_normal(&r);
+    }
+  }
+  free(act);
+  return OK;
+}
+
+/* MaxCausesModel::standard_init (:121-130) with detail::init_weights
+ * (model.cpp:201-220, take_abs in mca mode). */
+int mca_standard_init(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, const double* y, uint64_t n,
+                      uint64_t seed, double* w_out, double* pi_out, double* sigma2_out) {
+  if (n < 2) return fail(E_DATA, "standard_init requires at least two data points");
+  double* m = malloc(d * sizeof(double));
+  column_means(y, n, d, m);
+  const double var = mean_variance(y, n, d, m);
+  const double sd = var > 0.0 ? sqrt(var / h) : 0.0;
+  rng_t r;
+  rng_seed(&r, seed);
+  for (uint32_t i = 0; i < d; ++i)
+    for (uint32_t j = 0; j < h; ++j) {
+      double v = m[i] + sd * rng_normal(&r);
+      if (mode == 0) v = dmax(fabs(v), K_MIN_MCA_WEIGHT);
+      w_out[(size_t)i * h + j] = v;
+    }
+  *sigma2_out = dmax(var, K_MIN_SIGMA2);
+  *pi_out = (double)(hprime < h ? hprime : h) / (2.0 * (double)h);
+  free(m);
+  return OK;
+}

@@ -114,6 +114,33 @@ int ld_generate(uint32_t family, const double* alpha, const double* probs, uint3
                 double pi, uint32_t d, uint32_t h, const double* w, double sigma2, uint64_t n,
                 uint64_t seed, double* y_out);
 
+/* Max causes (max_causes.cpp): mode 0 = mca (max), 1 = mmca (absmax); rho =
+ * soft winner exponent (mca only). estep scalars = {sum_act, log_partition,
+ * points}; winner_num / winner_den are D×H. */
+int mca_estep_stats(uint32_t mode, double rho, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+                    const double* w, double pi, double sigma2, double temperature, const double* y, uint64_t n,
+                    uint64_t row_begin, uint64_t row_end, double* winner_num, double* winner_den,
+                    double* scalars);
+int mca_mstep_fixedpoint(uint32_t mode, uint32_t d, uint32_t h, const double* w_prev, const double* winner_num,
+                         const double* winner_den, const double* scalars, double* w_out, double* pi_out);
+int mca_step(uint32_t mode, double rho, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma,
+             const double* w, double pi, double sigma2, double temperature, const double* y, uint64_t n,
+             uint32_t shards, uint32_t workers, double* w_out, double* pi_out, double* sigma2_out,
+             double* free_energy);
+int mca_candidates(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, const double* w, double pi,
+                   double sigma2, const double* y, uint64_t n, uint32_t* out);
+int mca_inference(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, uint32_t gamma, const double* w,
+                  double pi, double sigma2, const double* y, uint64_t n, double* map_states, double* map_mass,
+                  double* expected);
+int mca_log_joint(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2,
+                  const double* y, const double* s, double* out);
+int mca_exact_log_likelihood(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2,
+                             const double* y, uint64_t n, double* out);
+int mca_generate(uint32_t mode, uint32_t d, uint32_t h, const double* w, double pi, double sigma2, uint64_t n,
+                 uint64_t seed, double* y_out);
+int mca_standard_init(uint32_t mode, uint32_t d, uint32_t h, uint32_t hprime, const double* y, uint64_t n,
+                      uint64_t seed, double* w_out, double* pi_out, double* sigma2_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,9 @@ class Oracle:
     def available(kind: str) -> bool:
         return os.path.exists(PORT_LIB if kind == "port" else REF_LIB)
 
+    def _mcall(self, name, *args):
+        self._call(name, *args, pre="mca_" if self.kind == "port" else "ref_mca_")
+
     def _lcall(self, name, *args):
         self._call(("ld_" if self.kind == "ref" else "") + name, *args, pre="ld_" if self.kind == "port" else None)
 
@@ -350,6 +353,98 @@ class Oracle:
         self._lcall("exact_log_likelihood", *prior.args(), _u32(w.shape[0]), _u32(w.shape[1]), _p(w),
                     _dbl(sigma2), _p(y), _u64(y.shape[0]), C.byref(out))
         return out.value
+
+
+
+    # ----------------------------------------------------------- max causes
+    # mode "mca" (max) or "mmca" (absmax); rho = soft winner exponent
+    @staticmethod
+    def _mode(mode):
+        return _u32({"mca": 0, "mmca": 1}[mode])
+
+    def mca_estep_stats(self, mode, w, pi, sigma2, y, hprime, gamma, temperature=1.0, rows=None, rho=0.0):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        b, e = (0, n) if rows is None else rows
+        num, den, sc = np.empty((d, h)), np.empty((d, h)), np.empty(3)
+        self._mcall("estep_stats", self._mode(mode), _dbl(rho), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w),
+                    _dbl(pi), _dbl(sigma2), _dbl(temperature), _p(y), _u64(n), _u64(b), _u64(e), _p(num), _p(den),
+                    _p(sc))
+        return dict(winner_num=num, winner_den=den, sum_act=sc[0], log_partition=sc[1], points=int(sc[2]))
+
+    def mca_mstep_fixedpoint(self, mode, stats, w_prev, pi_prev, sigma2_prev):
+        w_prev = _f64(w_prev)
+        d, h = w_prev.shape
+        w, pi = np.empty((d, h)), _dbl()
+        sc = np.array([stats["sum_act"], stats["log_partition"], float(stats["points"])])
+        num, den = _f64(stats["winner_num"]), _f64(stats["winner_den"])
+        if self.kind == "port":
+            self._mcall("mstep_fixedpoint", self._mode(mode), _u32(d), _u32(h), _p(w_prev), _p(num), _p(den), _p(sc),
+                        _p(w), C.byref(pi))
+        else:
+            self._mcall("mstep_fixedpoint", self._mode(mode), _u32(d), _u32(h), _p(w_prev), _dbl(pi_prev),
+                        _dbl(sigma2_prev), _p(num), _p(den), _p(sc), _p(w), C.byref(pi))
+        return w, pi.value
+
+    def mca_step(self, mode, w, pi, sigma2, y, hprime, gamma, temperature=1.0, shards=1, workers=1, rho=0.0):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        wo = np.empty((d, h))
+        pio, s2o, f = _dbl(), _dbl(), _dbl()
+        self._mcall("step", self._mode(mode), _dbl(rho), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w),
+                    _dbl(pi), _dbl(sigma2), _dbl(temperature), _p(y), _u64(y.shape[0]), _u32(shards), _u32(workers),
+                    _p(wo), C.byref(pio), C.byref(s2o), C.byref(f))
+        return wo, pio.value, s2o.value, f.value
+
+    def mca_candidates(self, mode, w, pi, sigma2, y, hprime):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        out = np.empty((y.shape[0], hprime), np.uint32)
+        self._mcall("candidates", self._mode(mode), _u32(d), _u32(h), _u32(hprime), _p(w), _dbl(pi), _dbl(sigma2),
+                    _p(y), _u64(y.shape[0]), _p(out))
+        return out
+
+    def mca_inference(self, mode, w, pi, sigma2, y, hprime, gamma):
+        w, y = _f64(w), _f64(y)
+        d, h = w.shape
+        n = y.shape[0]
+        ms, mm, ex = np.empty((n, h)), np.empty(n), np.empty((n, h))
+        extra = [] if self.kind == "port" else [_u32(1)]
+        self._mcall("inference", self._mode(mode), _u32(d), _u32(h), _u32(hprime), _u32(gamma), _p(w), _dbl(pi),
+                    _dbl(sigma2), _p(y), _u64(n), *extra, _p(ms), _p(mm), _p(ex))
+        return ms, mm, ex
+
+    def mca_log_joint(self, mode, w, pi, sigma2, y, s):
+        w, y, s = _f64(w), _f64(y), _f64(s)
+        out = _dbl()
+        self._mcall("log_joint", self._mode(mode), _u32(w.shape[0]), _u32(w.shape[1]), _p(w), _dbl(pi),
+                    _dbl(sigma2), _p(y), _p(s), C.byref(out))
+        return out.value
+
+    def mca_exact_log_likelihood(self, mode, w, pi, sigma2, y):
+        w, y = _f64(w), _f64(y)
+        out = _dbl()
+        self._mcall("exact_log_likelihood", self._mode(mode), _u32(w.shape[0]), _u32(w.shape[1]), _p(w), _dbl(pi),
+                    _dbl(sigma2), _p(y), _u64(y.shape[0]), C.byref(out))
+        return out.value
+
+    def mca_generate(self, mode, w, pi, sigma2, n, seed):
+        w = _f64(w)
+        d, h = w.shape
+        y = np.empty((n, d))
+        self._mcall("generate", self._mode(mode), _u32(d), _u32(h), _p(w), _dbl(pi), _dbl(sigma2), _u64(n),
+                    _u64(seed), _p(y))
+        return y
+
+    def mca_standard_init(self, mode, y, h, hprime, seed):
+        y = _f64(y)
+        n, d = y.shape
+        w = np.empty((d, h))
+        pi, s2 = _dbl(), _dbl()
+        self._mcall("standard_init", self._mode(mode), _u32(d), _u32(h), _u32(hprime), _p(y), _u64(n), _u64(seed),
+                    _p(w), C.byref(pi), C.byref(s2))
+        return w, pi.value, s2.value
 
 
 

@@ -16,6 +16,7 @@
 #include "bars.hpp"
 #include "core.hpp"
 #include "linear_discrete.hpp"
+#include "max_causes.hpp"
 #include "model.hpp"
 #include "parallel.hpp"
 #include "truncation.hpp"
@@ -87,6 +88,20 @@ LinearDiscreteParams ld_params(std::uint32_t family, std::uint32_t d, std::uint3
     p.values.assign(alpha, alpha + nalpha);
     p.probs.assign(probs, probs + nalpha);
   }
+  return p;
+}
+
+MaxCausesModel mca_model(std::uint32_t mode, std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
+                         std::uint32_t gamma, double rho) {
+  return MaxCausesModel(mode == 0 ? MaxMode::kMax : MaxMode::kAbsMax, d, h,
+                        TruncationConfig{h, hprime, gamma, 1000000}, rho);
+}
+
+McaParams mca_params(std::uint32_t d, std::uint32_t h, const double* w, double pi, double sigma2) {
+  McaParams p;
+  p.w = DenseMatrix(d, h, std::vector<double>(w, w + std::size_t(d) * h));
+  p.pi = pi;
+  p.sigma2 = sigma2;
   return p;
 }
 
@@ -530,6 +545,129 @@ int ref_ld_state_count(std::uint32_t h, std::uint32_t hprime, std::uint32_t gamm
     TruncationConfig cfg{h, hprime, gamma, 1000000};
     cfg.validate();
     *out = truncated_state_count(cfg, nv);
+  });
+}
+
+// ---- max causes (mode 0 mca, 1 mmca; rho = soft winner exponent)
+int ref_mca_estep_stats(std::uint32_t mode, double rho, std::uint32_t d, std::uint32_t h,
+                        std::uint32_t hprime, std::uint32_t gamma, const double* w, double pi,
+                        double sigma2, double temperature, const double* y, std::uint64_t n,
+                        std::uint64_t row_begin, std::uint64_t row_end, double* winner_num,
+                        double* winner_den, double* scalars) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, hprime, gamma, rho);
+    SuffStats s = m.estep_stats(mca_params(d, h, w, pi, sigma2), wrap_data(y, n, d),
+                                RowRange{row_begin, row_end}, temperature);
+    std::memcpy(winner_num, s.at("winner_num").data(), std::size_t(d) * h * sizeof(double));
+    std::memcpy(winner_den, s.at("winner_den").data(), std::size_t(d) * h * sizeof(double));
+    scalars[0] = s.scalar("sum_act");
+    scalars[1] = s.scalar("log_partition");
+    scalars[2] = static_cast<double>(s.points);
+  });
+}
+
+int ref_mca_mstep_fixedpoint(std::uint32_t mode, std::uint32_t d, std::uint32_t h,
+                             const double* w_prev, double pi_prev, double sigma2_prev,
+                             const double* winner_num, const double* winner_den,
+                             const double* scalars, double* w_out, double* pi_out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, h, 1, 0.0);
+    SuffStats s;
+    std::memcpy(s.field("winner_num", d, h).data(), winner_num, std::size_t(d) * h * sizeof(double));
+    std::memcpy(s.field("winner_den", d, h).data(), winner_den, std::size_t(d) * h * sizeof(double));
+    s.scalar("sum_act") = scalars[0];
+    s.scalar("log_partition") = scalars[1];
+    s.points = static_cast<std::uint64_t>(scalars[2]);
+    ModelParams out = m.mstep_fixedpoint(s, mca_params(d, h, w_prev, pi_prev, sigma2_prev));
+    const auto& p = std::get<McaParams>(out);
+    std::memcpy(w_out, p.w.data(), p.w.size() * sizeof(double));
+    *pi_out = p.pi;
+  });
+}
+
+int ref_mca_step(std::uint32_t mode, double rho, std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
+                 std::uint32_t gamma, const double* w, double pi, double sigma2, double temperature,
+                 const double* y, std::uint64_t n, std::uint32_t shards, std::uint32_t workers,
+                 double* w_out, double* pi_out, double* sigma2_out, double* free_energy) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, hprime, gamma, rho);
+    AnnealState st;
+    st.temperature = temperature;
+    StepResult r = m.step(mca_params(d, h, w, pi, sigma2), st, wrap_data(y, n, d),
+                          ShardPlan::with_shards(n, shards, workers));
+    const auto& p = std::get<McaParams>(r.params);
+    std::memcpy(w_out, p.w.data(), p.w.size() * sizeof(double));
+    *pi_out = p.pi;
+    *sigma2_out = p.sigma2;
+    *free_energy = r.free_energy;
+  });
+}
+
+int ref_mca_candidates(std::uint32_t mode, std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
+                       const double* w, double pi, double sigma2, const double* y, std::uint64_t n,
+                       std::uint32_t* out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, hprime, 1, 0.0);
+    const McaParams p = mca_params(d, h, w, pi, sigma2);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      auto c = select_candidates(m.selection_scores(p, std::span<const double>(y + i * d, d)), hprime);
+      std::memcpy(out + i * hprime, c.data(), hprime * sizeof(std::uint32_t));
+    }
+  });
+}
+
+int ref_mca_inference(std::uint32_t mode, std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
+                      std::uint32_t gamma, const double* w, double pi, double sigma2, const double* y,
+                      std::uint64_t n, std::uint32_t shards, double* map_states, double* map_mass,
+                      double* expected) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, hprime, gamma, 0.0);
+    InferenceResult r = m.inference(mca_params(d, h, w, pi, sigma2), wrap_data(y, n, d),
+                                    ShardPlan::with_shards(n, shards, shards));
+    std::memcpy(map_states, r.map_states.data(), r.map_states.size() * sizeof(double));
+    std::memcpy(map_mass, r.map_mass.data(), r.map_mass.size() * sizeof(double));
+    std::memcpy(expected, r.expected_states.data(), r.expected_states.size() * sizeof(double));
+  });
+}
+
+int ref_mca_log_joint(std::uint32_t mode, std::uint32_t d, std::uint32_t h, const double* w, double pi,
+                      double sigma2, const double* y, const double* s, double* out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, h, 1, 0.0);
+    *out = m.log_joint(mca_params(d, h, w, pi, sigma2), std::span<const double>(y, d),
+                       std::span<const double>(s, h));
+  });
+}
+
+int ref_mca_exact_log_likelihood(std::uint32_t mode, std::uint32_t d, std::uint32_t h, const double* w,
+                                 double pi, double sigma2, const double* y, std::uint64_t n, double* out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, h, h, 0.0);
+    *out = m.exact_log_likelihood(mca_params(d, h, w, pi, sigma2), wrap_data(y, n, d));
+  });
+}
+
+int ref_mca_generate(std::uint32_t mode, std::uint32_t d, std::uint32_t h, const double* w, double pi,
+                     double sigma2, std::uint64_t n, std::uint64_t seed, double* y_out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, h, 1, 0.0);
+    RngStream rng(seed);
+    DataSet ds = m.generate(mca_params(d, h, w, pi, sigma2), n, rng);
+    std::memcpy(y_out, ds.y.data(), ds.y.size() * sizeof(double));
+  });
+}
+
+int ref_mca_standard_init(std::uint32_t mode, std::uint32_t d, std::uint32_t h, std::uint32_t hprime,
+                          const double* y, std::uint64_t n, std::uint64_t seed, double* w_out,
+                          double* pi_out, double* sigma2_out) {
+  return guarded([&] {
+    auto m = mca_model(mode, d, h, hprime, 1, 0.0);
+    RngStream rng(seed);
+    ModelParams p = m.standard_init(wrap_data(y, n, d), rng);
+    const auto& mp = std::get<McaParams>(p);
+    std::memcpy(w_out, mp.w.data(), mp.w.size() * sizeof(double));
+    *pi_out = mp.pi;
+    *sigma2_out = mp.sigma2;
   });
 }
 

@@ -9,10 +9,14 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and not f.startswith("ld_"))
+GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN)
+                      if f.endswith(".npz") and not f.startswith(("ld_", "mca_")))
 # linear discrete families other than BSC (tsc / dsc), SURVEY.md §8(f) row 2
 LD_GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f.startswith("ld_"))
 FAMILY_NAMES = {0: "bsc", 1: "tsc", 2: "dsc"}
+# max causes (mca / mmca), SURVEY.md §8(f) row 3
+MCA_GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f.startswith("mca_"))
+MCA_MODES = {0: "mca", 1: "mmca"}
 
 
 def golden_prior(g, pi_key="pi0", probs_key="probs0"):

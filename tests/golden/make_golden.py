@@ -73,6 +73,32 @@ def ld_case(name, prior, y, w0, s20, hprime, gamma, iters=3, temperature=1.0):
     print(name, {k: np.shape(v) for k, v in out.items()})
 
 
+def mca_case(name, mode, y, w0, pi0, s20, hprime, gamma, iters=3, temperature=1.0, rho=0.0):
+    """A max-causes case (max_causes.cpp): E pass stats, one step (fixed-point
+    W/π then the residual pass for σ²), a trajectory and the inference readout."""
+    d, h = w0.shape
+    out = dict(y=y, W0=w0, mode=0 if mode == "mca" else 1, rho=rho, pi0=pi0, sigma2_0=s20, hprime=hprime,
+               gamma=gamma, temperature=temperature)
+    out["candidates"] = R.mca_candidates(mode, w0, pi0, s20, y, hprime)
+    st = R.mca_estep_stats(mode, w0, pi0, s20, y, hprime, gamma, temperature, rho=rho)
+    for k, v in st.items():
+        out["stats_" + k] = np.asarray(v)
+    w1, p1, s1, f = R.mca_step(mode, w0, pi0, s20, y, hprime, gamma, temperature, shards=3, workers=2, rho=rho)
+    out.update(W1=w1, pi1=p1, sigma2_1=s1, F0=f)
+    ws, ps, ss, fs = [], [], [], []
+    w, p, s = w0, pi0, s20
+    for _ in range(iters):
+        w, p, s, f = R.mca_step(mode, w, p, s, y, hprime, gamma, 1.0, rho=rho)
+        ws.append(w), ps.append(p), ss.append(s), fs.append(f)
+    out.update(traj_W=np.array(ws), traj_pi=np.array(ps), traj_sigma2=np.array(ss), traj_F=np.array(fs))
+    ms, mm, ex = R.mca_inference(mode, w0, pi0, s20, y, hprime, gamma)
+    out.update(map_states=ms, map_mass=mm, expected=ex)
+    if h <= 10:
+        out["exact_ll0"] = R.mca_exact_log_likelihood(mode, w0, pi0, s20, y)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
 def baseline_init(y, h, seed):
     # BASELINE.json's init recipe is not reference code (SURVEY.md §8(d) pins
     # it); the C restatement computes it. The reference then runs from it.
@@ -117,3 +143,12 @@ if __name__ == "__main__":
     y = R.ld_generate(dsc, wt, 0.3, 160, 17)
     w, _, s = baseline_init(y, 10, 17)
     ld_case("ld_dsc_d16_h10_hp5_g3", Prior("dsc", alpha=dsc.alpha, probs=[0.1, 0.7, 0.1, 0.1]), y, w, s, 5, 3)
+    # max causes: max-superposition bars and an absmax dictionary
+    y, truth = R.make_bars(4, 150, max_mode=True, noise=1.0, seed=31)
+    w, p, s = R.mca_standard_init("mca", y, 8, 6, 31)
+    mca_case("mca_bars4_h8_hp6_g3", "mca", y, w, p, s, 6, 3)
+    mca_case("mca_bars4_h8_hp6_g3_soft", "mca", y, w, p, s, 6, 3, iters=2, rho=2.0)
+    wt = Oracle("port").random_dictionary(12, 10, 33, 3.0)
+    y = R.mca_generate("mmca", wt, 0.2, 0.3, 120, 33)
+    w, p, s = R.mca_standard_init("mmca", y, 10, 5, 33)
+    mca_case("mca_mmca_d12_h10_hp5_g3_T2", "mmca", y, w, p, s, 5, 3, iters=2, temperature=2.0)
