@@ -131,6 +131,37 @@ int prsp_bsc_baseline_init(uint32_t dim, uint32_t latents, const double* y, uint
 int prsp_bsc_standard_init(uint32_t dim, uint32_t latents, uint32_t hprime, const double* y, uint64_t n,
                            uint64_t seed, double* w_out, double* pi_out, double* sigma2_out);
 
+/* ---- max causes ----------------------------------
+ * MaxCausesModel (max_causes.cpp): mca (max) / mmca (absmax) superposition.
+ *   prsp_mca_gpu_create      MaxCausesModel ctor (max_causes.cpp:83-99); model "mca" | "mmca",
+ *                            soft_winner_rho >= 0 (mca only)
+ *   prsp_mca_gpu_step        MaxCausesModel::step (:416-446): E pass, fixed-point M-step,
+ *                            residual pass for sigma2; *free_energy at the incoming params
+ *   prsp_mca_gpu_estep       MaxCausesModel::estep_stats (:384-391) over the resident shard;
+ *                            stats [winner_num D·H | winner_den D·H | sum_act | log_partition | points]
+ *   prsp_mca_gpu_mstep_fixedpoint  MaxCausesModel::mstep_fixedpoint (:393-414) from the device stats
+ *   prsp_mca_gpu_residual_commit   the residual pass of step (:423-436) and the update of W, pi, sigma2
+ *   prsp_mca_gpu_inference / _candidates   inference (:448-468) / selection as estep_impl (:205-207)
+ */
+typedef struct prsp_mca_gpu prsp_mca_gpu;
+int prsp_mca_gpu_create(const char* model, double soft_winner_rho, uint32_t dim, uint32_t latents, uint32_t hprime,
+                        uint32_t gamma, uint64_t state_cap, int device, prsp_mca_gpu** out);
+void prsp_mca_gpu_free(prsp_mca_gpu* ctx);
+int prsp_mca_gpu_states_per_point(const prsp_mca_gpu* ctx, uint64_t* out);
+int prsp_mca_gpu_load_data(prsp_mca_gpu* ctx, const double* y_host, uint64_t n);
+int prsp_mca_gpu_set_params(prsp_mca_gpu* ctx, const double* w, double pi, double sigma2);
+int prsp_mca_gpu_get_params(prsp_mca_gpu* ctx, double* w, double* pi, double* sigma2);
+int prsp_mca_gpu_step(prsp_mca_gpu* ctx, double temperature, double* free_energy);
+int prsp_mca_gpu_estep(prsp_mca_gpu* ctx, double temperature);
+int prsp_mca_gpu_stats_buffer(prsp_mca_gpu* ctx, double** device_ptr, uint64_t* count);
+int prsp_mca_gpu_get_stats(prsp_mca_gpu* ctx, double* winner_num, double* winner_den, double* scalars);
+int prsp_mca_gpu_set_stats(prsp_mca_gpu* ctx, const double* winner_num, const double* winner_den,
+                           const double* scalars);
+int prsp_mca_gpu_mstep_fixedpoint(prsp_mca_gpu* ctx, double* w_out, double* pi_out);
+int prsp_mca_gpu_residual_commit(prsp_mca_gpu* ctx, double temperature, double* residual_out);
+int prsp_mca_gpu_candidates(prsp_mca_gpu* ctx, uint32_t* out);
+int prsp_mca_gpu_inference(prsp_mca_gpu* ctx, double* map_states, double* map_mass, double* expected);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,21 @@ SIGNATURES = {
     "prsp_bsc_gpu_timings": [_ptr, _ptr],
     "prsp_bsc_gpu_launches": [_ptr, C.POINTER(_int)],
     "prsp_bsc_gpu_enum_phase_cycles": [_ptr, _ptr],
+    "prsp_mca_gpu_create": [C.c_char_p, _dbl, _u32, _u32, _u32, _u32, _u64, _int, C.POINTER(_ptr)],
+    "prsp_mca_gpu_free": [_ptr],
+    "prsp_mca_gpu_states_per_point": [_ptr, C.POINTER(_u64)],
+    "prsp_mca_gpu_load_data": [_ptr, _ptr, _u64],
+    "prsp_mca_gpu_set_params": [_ptr, _ptr, _dbl, _dbl],
+    "prsp_mca_gpu_get_params": [_ptr, _ptr, _dp, _dp],
+    "prsp_mca_gpu_step": [_ptr, _dbl, _dp],
+    "prsp_mca_gpu_estep": [_ptr, _dbl],
+    "prsp_mca_gpu_stats_buffer": [_ptr, C.POINTER(_ptr), C.POINTER(_u64)],
+    "prsp_mca_gpu_get_stats": [_ptr, _ptr, _ptr, _ptr],
+    "prsp_mca_gpu_set_stats": [_ptr, _ptr, _ptr, _ptr],
+    "prsp_mca_gpu_mstep_fixedpoint": [_ptr, _ptr, _dp],
+    "prsp_mca_gpu_residual_commit": [_ptr, _dbl, _dp],
+    "prsp_mca_gpu_candidates": [_ptr, _ptr],
+    "prsp_mca_gpu_inference": [_ptr, _ptr, _ptr, _ptr],
     "prsp_bsc_bars_generate": [_u32, _u64, _dbl, _dbl, _dbl, _int, _u64, _ptr, _ptr],
     "prsp_bsc_generate": [_u32, _u32, _ptr, _dbl, _dbl, _u64, _u64, _ptr],
     "prsp_bsc_random_dictionary": [_u32, _u32, _u64, _dbl, _ptr],
@@ -59,6 +74,7 @@ _RESTYPES = {
     "prsp_bsc_gpu_version": C.c_char_p,
     "prsp_bsc_gpu_last_error": C.c_char_p,
     "prsp_bsc_gpu_free": None,
+    "prsp_mca_gpu_free": None,
 }
 
 STATUS = {0: "PRSP_OK", 2: "PRSP_ERR_CONFIG", 3: "PRSP_ERR_DATA", 4: "PRSP_ERR_NUMERIC", 5: "PRSP_ERR_INTERNAL"}

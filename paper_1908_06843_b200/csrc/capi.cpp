@@ -13,6 +13,7 @@
 
 #include "bsc_engine.hpp"
 #include "fixtures.hpp"
+#include "mca_engine.hpp"
 
 struct prsp_bsc_gpu {
   bscgpu::BscEngine engine;
@@ -20,6 +21,12 @@ struct prsp_bsc_gpu {
   prsp_bsc_gpu(int fam, uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, const double* vals, uint32_t nv,
                int dev)
       : engine(fam, d, h, hp, g, cap, vals, nv, dev) {}
+};
+
+struct prsp_mca_gpu {
+  bscgpu::McaEngine engine;
+  prsp_mca_gpu(int mode, double rho, uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, int dev)
+      : engine(mode, rho, d, h, hp, g, cap, dev) {}
 };
 
 namespace {
@@ -339,6 +346,124 @@ int prsp_bsc_standard_init(uint32_t dim, uint32_t latents, uint32_t hprime, cons
   return guarded([&] {
     need(y, "y");
     bscgpu::standard_init(dim, latents, hprime, y, n, seed, w_out, pi_out, sigma2_out);
+  });
+}
+
+int prsp_mca_gpu_create(const char* model, double rho, uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma,
+                        uint64_t state_cap, int device, prsp_mca_gpu** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(model, "model");
+    const std::string m(model);
+    if (m != "mca" && m != "mmca") throw bscgpu::Error(bscgpu::kConfig, "unknown model '" + m + "' (mca, mmca)");
+    *out = new prsp_mca_gpu(m == "mca" ? 0 : 1, rho, dim, latents, hprime, gamma, state_cap, device);
+  });
+}
+
+void prsp_mca_gpu_free(prsp_mca_gpu* ctx) { delete ctx; }
+
+int prsp_mca_gpu_states_per_point(const prsp_mca_gpu* ctx, uint64_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    *out = ctx->engine.states_per_point();
+  });
+}
+
+int prsp_mca_gpu_load_data(prsp_mca_gpu* ctx, const double* y, uint64_t n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(y, "y");
+    ctx->engine.load_data(y, n);
+  });
+}
+
+int prsp_mca_gpu_set_params(prsp_mca_gpu* ctx, const double* w, double pi, double sigma2) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(w, "w");
+    ctx->engine.set_params(w, pi, sigma2);
+  });
+}
+
+int prsp_mca_gpu_get_params(prsp_mca_gpu* ctx, double* w, double* pi, double* sigma2) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.get_params(w, pi, sigma2);
+  });
+}
+
+int prsp_mca_gpu_step(prsp_mca_gpu* ctx, double temperature, double* free_energy) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    const double f = ctx->engine.step(temperature);
+    if (free_energy) *free_energy = f;
+  });
+}
+
+int prsp_mca_gpu_estep(prsp_mca_gpu* ctx, double temperature) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.estep(temperature);
+  });
+}
+
+int prsp_mca_gpu_stats_buffer(prsp_mca_gpu* ctx, double** ptr, uint64_t* count) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    *ptr = ctx->engine.stats_device();
+    *count = ctx->engine.stats_count();
+  });
+}
+
+int prsp_mca_gpu_get_stats(prsp_mca_gpu* ctx, double* num, double* den, double* scalars) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.get_stats(num, den, scalars);
+  });
+}
+
+int prsp_mca_gpu_set_stats(prsp_mca_gpu* ctx, const double* num, const double* den, const double* scalars) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(num, "winner_num");
+    need(den, "winner_den");
+    need(scalars, "scalars");
+    ctx->engine.set_stats(num, den, scalars);
+  });
+}
+
+int prsp_mca_gpu_mstep_fixedpoint(prsp_mca_gpu* ctx, double* w_out, double* pi_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.mstep_fixedpoint();
+    ctx->engine.get_updated(w_out, pi_out);
+  });
+}
+
+int prsp_mca_gpu_residual_commit(prsp_mca_gpu* ctx, double temperature, double* residual_out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.residual_and_commit(temperature);
+    if (residual_out) *residual_out = ctx->engine.residual_device_sum();
+  });
+}
+
+int prsp_mca_gpu_candidates(prsp_mca_gpu* ctx, uint32_t* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->engine.candidates(out);
+  });
+}
+
+int prsp_mca_gpu_inference(prsp_mca_gpu* ctx, double* map_states, double* map_mass, double* expected) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(map_states, "map_states");
+    need(map_mass, "map_mass");
+    need(expected, "expected");
+    ctx->engine.inference(map_states, map_mass, expected);
   });
 }
 

@@ -22,6 +22,7 @@
 // warp in shared memory and reduced per CTA in fixed order.
 #pragma once
 #include "bsc_kernels.cuh"
+#include "warp_select.cuh"
 
 namespace bscgpu {
 
@@ -159,65 +160,19 @@ __global__ void __launch_bounds__(256, 2) ldv_enumerate_kernel(LdvArgs la) {
     const double eps = 2.5 * a.inv2s * la.vmax * a.eps_dot * bound * sqrt(y2) * 1.0001 + 0x1.0p-46 * mag;
 
     // ---- top-H' (truncation.cpp:38-57), exact re-rank of the near-tie band
-    if (HP < H) {
-      double t, nv;
-      top_k<MAXJ>(f, removed, HP, H, lane, pool_v, pool_i, scand, t, nv);
-      if (!(t - nv > 2.0 * eps)) {
-        uint32_t rem2 = 0;
-#pragma unroll
-        for (int j = 0; j < MAXJ; ++j) {
-          const int h = lane + 32 * j;
-          if (h >= H) {
-            rem2 |= 1u << j;
-          } else if (f[j] > t + 2.0 * eps) {
-            f[j] = INFINITY;
-          } else if (f[j] < t - 2.0 * eps) {
-            f[j] = -INFINITY;
-          } else {
-            double acc = 0.0;
-            for (int d = 0; d < a.D; ++d) acc = __dadd_rn(acc, __dmul_rn(a.W[(long long)d * a.Hp + h], y[d]));
-            const double g = a.gdiag[h];
-            double best = -INFINITY;
-            for (int k = 0; k < V; ++k) {
-              const double v = la.values[k];
-              const double sc = __dadd_rn(
-                  la.logp[k], __dmul_rn(__dsub_rn(__dmul_rn(2.0 * v, acc), __dmul_rn(__dmul_rn(v, v), g)), a.inv2s));
-              best = best < sc ? sc : best;
-            }
-            f[j] = best;
-          }
-        }
-        for (int r = 0; r < HP; ++r) {
-          double wv;
-          int wi;
-          select_round<MAXJ>(f, rem2, lane, wv, wi);
-          if ((wi & 31) == lane) rem2 |= 1u << (wi >> 5);
-          if (lane == 0) scand[r] = static_cast<uint32_t>(wi);
-        }
+    warp_select<MAXJ>(f, removed, eps, H, HP, lane, pool_v, pool_i, scand, [&](int h) {
+      double acc = 0.0;
+      for (int d = 0; d < a.D; ++d) acc = __dadd_rn(acc, __dmul_rn(a.W[(long long)d * a.Hp + h], y[d]));
+      const double g = a.gdiag[h];
+      double best = -INFINITY;
+      for (int k = 0; k < V; ++k) {
+        const double v = la.values[k];
+        const double sc =
+            __dadd_rn(la.logp[k], __dmul_rn(__dsub_rn(__dmul_rn(2.0 * v, acc), __dmul_rn(__dmul_rn(v, v), g)), a.inv2s));
+        best = best < sc ? sc : best;
       }
-    } else {
-      for (int p = lane; p < HP; p += 32) scand[p] = static_cast<uint32_t>(p);
-    }
-    __syncwarp();
-    {  // candidates ascending (truncation.cpp:55)
-      uint32_t mine[2] = {0xffffffffu, 0xffffffffu};
-      int pos[2] = {-1, -1};
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int p = lane + 32 * s;
-        if (p < HP) {
-          mine[s] = scand[p];
-          int rk = 0;
-          for (int q = 0; q < HP; ++q) rk += scand[q] < mine[s];
-          pos[s] = rk;
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-        if (pos[s] >= 0) scand[pos[s]] = mine[s];
-      __syncwarp();
-    }
+      return best;
+    });
     if (a.cand_out)
       for (int p = lane; p < HP; p += 32) a.cand_out[(long long)n * HP + p] = scand[p];
 
