@@ -162,6 +162,62 @@ int prsp_mca_gpu_residual_commit(prsp_mca_gpu* ctx, double temperature, double* 
 int prsp_mca_gpu_candidates(prsp_mca_gpu* ctx, uint32_t* out);
 int prsp_mca_gpu_inference(prsp_mca_gpu* ctx, double* map_states, double* map_mass, double* expected);
 
+/* ---- run I/O and the training driver ----------------
+ *   prsp_gpu_array_save / _load   save_array / load_array, PRSPAR01 (array_io.cpp:53-95);
+ *                                 prsp_matrix_save / prsp_matrix_load (prsp.h:71-72)
+ *   prsp_gpu_dataset_load         load_dataset: PRSPAR01 by magic, else headerless CSV
+ *                                 (array_io.cpp:97-153); prsp_dataset_load (prsp.h:60)
+ *   prsp_gpu_sha256[_file]        sha256_hex / sha256_hex_file (sha256.hpp), the manifest data hash
+ *   prsp_gpu_format_double        format_double (array_io.cpp:159-164)
+ *   prsp_gpu_train                train_run (run_io.cpp:196-230) + run (em.cpp:27-77) with every EM
+ *                                 step on the GPU; out_dir (nullable) receives free_energy.csv,
+ *                                 checkpoint_*.prsp (cadence of run_io.cpp:150-151), final_*.prsp and
+ *                                 manifest.json (prsp-manifest-1); prsp_train (prsp.h:117-118)
+ *   prsp_gpu_result_*             prsp_result_iterations / _trace / _param (prsp.h:120-127)
+ *   prsp_gpu_run_open / _infer    load_run (run_io.cpp:165-194) / prsp_infer (capi.cpp:389-407)
+ * Array loads are two-call: with out == NULL only the shape is returned.
+ * Schedules are piecewise linear over the fraction of the iteration budget
+ * (annealing.cpp); NULL / 0 anchors mean constant T = 1 and no weight noise. */
+typedef struct {
+  const char* model; /* "bsc" | "tsc" | "dsc" | "mca" | "mmca" */
+  uint32_t latents, hprime, gamma; /* hprime 0 → latents, gamma 0 → hprime */
+  const double* values; /* dsc alphabet */
+  uint32_t n_values;
+  uint64_t iterations, seed;
+  uint32_t workers, shards; /* recorded in the manifest */
+  int has_tolerance;
+  double tolerance;
+  const double* temperature_pos;
+  const double* temperature_val;
+  uint32_t n_temperature;
+  const double* w_noise_pos;
+  const double* w_noise_val;
+  uint32_t n_w_noise;
+  double soft_winner_rho; /* mca */
+  int device;
+} prsp_gpu_train_config;
+typedef struct prsp_gpu_result prsp_gpu_result;
+typedef struct prsp_gpu_run prsp_gpu_run;
+
+int prsp_gpu_array_save(const char* path, const double* data, uint64_t rows, uint64_t cols);
+int prsp_gpu_array_load(const char* path, uint64_t* rows, uint64_t* cols, double* out);
+int prsp_gpu_dataset_load(const char* path, uint64_t* rows, uint64_t* cols, double* out);
+int prsp_gpu_sha256(const void* data, uint64_t bytes, char* hex65);
+int prsp_gpu_sha256_file(const char* path, char* hex65);
+int prsp_gpu_format_double(double v, char* out, uint32_t capacity);
+int prsp_gpu_train(const prsp_gpu_train_config* config, const double* y, uint64_t n, uint64_t d,
+                   const char* data_file, const char* out_dir, prsp_gpu_result** out);
+int prsp_gpu_result_iterations(const prsp_gpu_result* r, uint64_t* out);
+int prsp_gpu_result_trace(const prsp_gpu_result* r, double* free_energy);
+int prsp_gpu_result_param(const prsp_gpu_result* r, const char* name, uint64_t* rows, uint64_t* cols, double* out);
+void prsp_gpu_result_free(prsp_gpu_result* r);
+int prsp_gpu_run_open(const char* dir, prsp_gpu_run** out);
+int prsp_gpu_run_info(const prsp_gpu_run* run, char* model, uint32_t capacity, uint32_t* dim, uint32_t* latents);
+int prsp_gpu_run_param(const prsp_gpu_run* run, const char* name, uint64_t* rows, uint64_t* cols, double* out);
+int prsp_gpu_run_infer(const prsp_gpu_run* run, const double* y, uint64_t n, uint64_t d, int device,
+                       double* map_states, double* map_mass, double* expected);
+void prsp_gpu_run_free(prsp_gpu_run* run);
+
 #ifdef __cplusplus
 }
 #endif

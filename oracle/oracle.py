@@ -448,6 +448,53 @@ class Oracle:
 
 
 
+    # ---------------------------------------- run I/O + EM driver (ref only)
+    def save_array(self, path, a):
+        a = _f64(np.atleast_2d(a))
+        self._call("save_array", str(path).encode(), _p(a), _u64(a.shape[0]), _u64(a.shape[1]))
+
+    def load_dataset(self, path):
+        r, c = _u64(), _u64()
+        self._call("load_dataset", str(path).encode(), C.byref(r), C.byref(c), None)
+        out = np.empty((r.value, c.value))
+        self._call("load_dataset", str(path).encode(), C.byref(r), C.byref(c), _p(out))
+        return out
+
+    def sha256(self, data: bytes):
+        buf = C.create_string_buffer(65)
+        src = C.create_string_buffer(data, len(data)) if data else None
+        self._call("sha256", None if src is None else C.cast(src, _ptr), _u64(len(data)), buf)
+        return buf.value.decode()
+
+    def sha256_file(self, path):
+        buf = C.create_string_buffer(65)
+        self._call("sha256_file", str(path).encode(), buf)
+        return buf.value.decode()
+
+    def format_double(self, v):
+        buf = C.create_string_buffer(32)
+        self._call("format_double", _dbl(v), buf, _u32(32))
+        return buf.value.decode()
+
+    def train(self, model, y, latents, hprime, gamma, iterations, seed, values=None, shards=1, workers=1, tol=None,
+              temperature=((0.0, 1.0),), w_noise=((0.0, 0.0),)):
+        """em.cpp run() after train_run's setup; → (trace, W, pi, sigma2, probs)."""
+        y = _f64(y)
+        n, d = y.shape
+        vals = _f64(values if values is not None else np.zeros(0))
+        tp, tv = (_f64(x) for x in zip(*temperature))
+        npos, nval = (_f64(x) for x in zip(*w_noise))
+        trace, it = np.empty(iterations), _u64()
+        w, pi, s2 = np.empty((d, latents)), _dbl(), _dbl()
+        probs = np.empty(max(len(vals), 1))
+        self._call("train", model.encode(), _p(vals), _u32(len(vals)), _u32(d), _u32(latents), _u32(hprime),
+                   _u32(gamma), _u64(iterations), _u64(seed), _u32(shards), _u32(workers), _int(tol is not None),
+                   _dbl(tol or 0.0), _p(tp), _p(tv), _u32(len(tp)), _p(npos), _p(nval), _u32(len(npos)), _p(y),
+                   _u64(n), _p(trace), C.byref(it), _p(w), C.byref(pi), C.byref(s2), _p(probs))
+        return trace[:it.value], w, pi.value, s2.value, (probs[:len(vals)] if len(vals) else None)
+
+
+
 class RefSession:
     """The reference's ``LinearDiscreteModel::step`` over a resident dataset,
     for timing (bench.py ``--impl reference``)."""

@@ -13,7 +13,11 @@
 #include <string>
 #include <vector>
 
+#include "array_io.hpp"
 #include "bars.hpp"
+#include "em.hpp"
+#include "annealing.hpp"
+#include "sha256.hpp"
 #include "core.hpp"
 #include "linear_discrete.hpp"
 #include "max_causes.hpp"
@@ -668,6 +672,81 @@ int ref_mca_standard_init(std::uint32_t mode, std::uint32_t d, std::uint32_t h, 
     std::memcpy(w_out, mp.w.data(), mp.w.size() * sizeof(double));
     *pi_out = mp.pi;
     *sigma2_out = mp.sigma2;
+  });
+}
+
+// ---- run I/O and the EM driver (array_io.cpp, sha256.cpp, em.cpp, annealing.cpp)
+int ref_save_array(const char* path, const double* data, std::uint64_t rows, std::uint64_t cols) {
+  return guarded([&] { save_array(path, DenseMatrix(rows, cols, std::vector<double>(data, data + rows * cols))); });
+}
+
+int ref_load_dataset(const char* path, std::uint64_t* rows, std::uint64_t* cols, double* out) {
+  return guarded([&] {
+    DataSet ds = load_dataset(path);
+    *rows = ds.size();
+    *cols = ds.dim();
+    if (out) std::memcpy(out, ds.y.data(), ds.y.size() * sizeof(double));
+  });
+}
+
+int ref_sha256(const void* data, std::uint64_t bytes, char* hex65) {
+  return guarded([&] {
+    const std::string h = sha256_hex({static_cast<const std::uint8_t*>(data), static_cast<std::size_t>(bytes)});
+    std::memcpy(hex65, h.c_str(), 65);
+  });
+}
+
+int ref_sha256_file(const char* path, char* hex65) {
+  return guarded([&] { std::memcpy(hex65, sha256_hex_file(path).c_str(), 65); });
+}
+
+int ref_format_double(double v, char* out, std::uint32_t cap) {
+  return guarded([&] {
+    const std::string s = format_double(v);
+    if (s.size() + 1 > cap) throw ConfigError("buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
+// train_run's model setup and EM loop (run_io.cpp:196-230, em.cpp:27-77)
+// without the directory logger: standard_init from RngStream::derived(seed,
+// "init"), LinearAnnealing over the schedules, TrainOptions{tol, seed}.
+int ref_train(const char* model, const double* values, std::uint32_t n_values, std::uint32_t d,
+              std::uint32_t h, std::uint32_t hprime, std::uint32_t gamma, std::uint64_t iterations,
+              std::uint64_t seed, std::uint32_t shards, std::uint32_t workers, int has_tol, double tol,
+              const double* tpos, const double* tval, std::uint32_t nt, const double* npos,
+              const double* nval, std::uint32_t nn, const double* y, std::uint64_t n, double* trace,
+              std::uint64_t* iters, double* w_out, double* pi_out, double* sigma2_out, double* probs_out) {
+  return guarded([&] {
+    std::vector<double> vals(values, values + n_values);
+    auto m = make_model(model, d, h, TruncationConfig{h, hprime, gamma}, vals);
+    DataSet ds = wrap_data(y, n, d);
+    RngStream init_rng = RngStream::derived(seed, 0x696e6974);
+    ModelParams params = m->standard_init(ds, init_rng);
+    auto sched = [](const double* p, const double* v, std::uint32_t k, double dflt) {
+      if (!p || k == 0) return Schedule::constant(dflt);
+      std::vector<std::pair<double, double>> a;
+      for (std::uint32_t i = 0; i < k; ++i) a.emplace_back(p[i], v[i]);
+      return Schedule(a);
+    };
+    LinearAnnealing ann(iterations, sched(tpos, tval, nt, 1.0), sched(npos, nval, nn, 0.0));
+    TrainOptions opt;
+    if (has_tol) opt.tol = tol;
+    opt.noise_seed = seed;
+    TrainResult r = run(*m, std::move(params), ds, ann, ShardPlan::with_shards(n, shards, workers), nullptr, opt);
+    *iters = r.free_energy_trace.size();
+    std::memcpy(trace, r.free_energy_trace.data(), r.free_energy_trace.size() * sizeof(double));
+    if (const auto* p = std::get_if<LinearDiscreteParams>(&r.final_params)) {
+      std::memcpy(w_out, p->w.data(), p->w.size() * sizeof(double));
+      *pi_out = p->pi;
+      *sigma2_out = p->sigma2;
+      if (probs_out && !p->probs.empty()) std::memcpy(probs_out, p->probs.data(), p->probs.size() * sizeof(double));
+    } else {
+      const auto& q = std::get<McaParams>(r.final_params);
+      std::memcpy(w_out, q.w.data(), q.w.size() * sizeof(double));
+      *pi_out = q.pi;
+      *sigma2_out = q.sigma2;
+    }
   });
 }
 

@@ -64,6 +64,22 @@ SIGNATURES = {
     "prsp_mca_gpu_residual_commit": [_ptr, _dbl, _dp],
     "prsp_mca_gpu_candidates": [_ptr, _ptr],
     "prsp_mca_gpu_inference": [_ptr, _ptr, _ptr, _ptr],
+    "prsp_gpu_array_save": [C.c_char_p, _ptr, _u64, _u64],
+    "prsp_gpu_array_load": [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), _ptr],
+    "prsp_gpu_dataset_load": [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), _ptr],
+    "prsp_gpu_sha256": [_ptr, _u64, C.c_char_p],
+    "prsp_gpu_sha256_file": [C.c_char_p, C.c_char_p],
+    "prsp_gpu_format_double": [_dbl, C.c_char_p, _u32],
+    "prsp_gpu_train": [_ptr, _ptr, _u64, _u64, C.c_char_p, C.c_char_p, C.POINTER(_ptr)],
+    "prsp_gpu_result_iterations": [_ptr, C.POINTER(_u64)],
+    "prsp_gpu_result_trace": [_ptr, _ptr],
+    "prsp_gpu_result_param": [_ptr, C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), _ptr],
+    "prsp_gpu_result_free": [_ptr],
+    "prsp_gpu_run_open": [C.c_char_p, C.POINTER(_ptr)],
+    "prsp_gpu_run_info": [_ptr, C.c_char_p, _u32, C.POINTER(_u32), C.POINTER(_u32)],
+    "prsp_gpu_run_param": [_ptr, C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), _ptr],
+    "prsp_gpu_run_infer": [_ptr, _ptr, _u64, _u64, _int, _ptr, _ptr, _ptr],
+    "prsp_gpu_run_free": [_ptr],
     "prsp_bsc_bars_generate": [_u32, _u64, _dbl, _dbl, _dbl, _int, _u64, _ptr, _ptr],
     "prsp_bsc_generate": [_u32, _u32, _ptr, _dbl, _dbl, _u64, _u64, _ptr],
     "prsp_bsc_random_dictionary": [_u32, _u32, _u64, _dbl, _ptr],
@@ -75,6 +91,8 @@ _RESTYPES = {
     "prsp_bsc_gpu_last_error": C.c_char_p,
     "prsp_bsc_gpu_free": None,
     "prsp_mca_gpu_free": None,
+    "prsp_gpu_result_free": None,
+    "prsp_gpu_run_free": None,
 }
 
 STATUS = {0: "PRSP_OK", 2: "PRSP_ERR_CONFIG", 3: "PRSP_ERR_DATA", 4: "PRSP_ERR_NUMERIC", 5: "PRSP_ERR_INTERNAL"}

@@ -14,6 +14,7 @@
 #include "bsc_engine.hpp"
 #include "fixtures.hpp"
 #include "mca_engine.hpp"
+#include "run_io.hpp"
 
 struct prsp_bsc_gpu {
   bscgpu::BscEngine engine;
@@ -27,6 +28,13 @@ struct prsp_mca_gpu {
   bscgpu::McaEngine engine;
   prsp_mca_gpu(int mode, double rho, uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, int dev)
       : engine(mode, rho, d, h, hp, g, cap, dev) {}
+};
+
+struct prsp_gpu_result {
+  bscgpu::TrainResult r;
+};
+struct prsp_gpu_run {
+  bscgpu::TrainedRun run;
 };
 
 namespace {
@@ -466,5 +474,169 @@ int prsp_mca_gpu_inference(prsp_mca_gpu* ctx, double* map_states, double* map_ma
     ctx->engine.inference(map_states, map_mass, expected);
   });
 }
+
+int prsp_gpu_array_save(const char* path, const double* data, uint64_t rows, uint64_t cols) {
+  return guarded([&] {
+    need(path, "path");
+    if (rows * cols) need(data, "data");
+    bscgpu::save_array(path, data, rows, cols);
+  });
+}
+
+static int load_into(const bscgpu::Array& a, uint64_t* rows, uint64_t* cols, double* out) {
+  if (rows) *rows = a.rows;
+  if (cols) *cols = a.cols;
+  if (out && !a.data.empty()) std::memcpy(out, a.data.data(), a.data.size() * sizeof(double));
+  return 0;
+}
+
+int prsp_gpu_array_load(const char* path, uint64_t* rows, uint64_t* cols, double* out) {
+  return guarded([&] {
+    need(path, "path");
+    load_into(bscgpu::load_array(path), rows, cols, out);
+  });
+}
+
+int prsp_gpu_dataset_load(const char* path, uint64_t* rows, uint64_t* cols, double* out) {
+  return guarded([&] {
+    need(path, "path");
+    load_into(bscgpu::load_dataset(path), rows, cols, out);
+  });
+}
+
+int prsp_gpu_sha256(const void* data, uint64_t bytes, char* hex65) {
+  return guarded([&] {
+    need(hex65, "hex65");
+    if (bytes) need(data, "data");
+    std::memcpy(hex65, bscgpu::sha256_hex(data, bytes).c_str(), 65);
+  });
+}
+
+int prsp_gpu_sha256_file(const char* path, char* hex65) {
+  return guarded([&] {
+    need(path, "path");
+    need(hex65, "hex65");
+    std::memcpy(hex65, bscgpu::sha256_hex_file(path).c_str(), 65);
+  });
+}
+
+int prsp_gpu_format_double(double v, char* out, uint32_t capacity) {
+  return guarded([&] {
+    need(out, "out");
+    const std::string s = bscgpu::format_double(v);
+    if (s.size() + 1 > capacity) throw bscgpu::Error(bscgpu::kConfig, "format_double: buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+
+int prsp_gpu_train(const prsp_gpu_train_config* c, const double* y, uint64_t n, uint64_t d, const char* data_file,
+                   const char* out_dir, prsp_gpu_result** out) {
+  return guarded([&] {
+    need(c, "config");
+    need(c->model, "model");
+    need(y, "y");
+    need(out, "out");
+    bscgpu::RunConfig rc;
+    rc.model = c->model;
+    rc.latents = c->latents;
+    rc.hprime = c->hprime;
+    rc.gamma = c->gamma;
+    if (c->values && c->n_values) rc.values.assign(c->values, c->values + c->n_values);
+    rc.iterations = c->iterations;
+    rc.seed = c->seed;
+    rc.workers = c->workers;
+    rc.shards = c->shards;
+    if (c->has_tolerance) rc.tolerance = c->tolerance;
+    auto sched = [](const double* pos, const double* val, uint32_t k, double dflt) {
+      bscgpu::Schedule s;
+      if (!pos || !val || k == 0) {
+        s.anchors = {{0.0, dflt}};
+      } else {
+        for (uint32_t i = 0; i < k; ++i) s.anchors.emplace_back(pos[i], val[i]);
+      }
+      return s;
+    };
+    rc.temperature = sched(c->temperature_pos, c->temperature_val, c->n_temperature, 1.0);
+    rc.w_noise = sched(c->w_noise_pos, c->w_noise_val, c->n_w_noise, 0.0);
+    rc.soft_winner_rho = c->soft_winner_rho;
+    rc.device = c->device;
+    auto* r = new prsp_gpu_result{bscgpu::train_run(rc, y, n, d, data_file ? data_file : "", out_dir ? out_dir : "")};
+    *out = r;
+  });
+}
+
+int prsp_gpu_result_iterations(const prsp_gpu_result* r, uint64_t* out) {
+  return guarded([&] {
+    need(r, "result");
+    need(out, "out");
+    *out = r->r.trace.size();
+  });
+}
+
+int prsp_gpu_result_trace(const prsp_gpu_result* r, double* f) {
+  return guarded([&] {
+    need(r, "result");
+    need(f, "free_energy");
+    std::memcpy(f, r->r.trace.data(), r->r.trace.size() * sizeof(double));
+  });
+}
+
+static const bscgpu::Array& named(const std::vector<bscgpu::NamedArray>& v, const char* name) {
+  for (const auto& p : v)
+    if (p.name == name) return p.a;
+  throw bscgpu::Error(bscgpu::kConfig, std::string("no parameter array named ") + name);
+}
+
+int prsp_gpu_result_param(const prsp_gpu_result* r, const char* name, uint64_t* rows, uint64_t* cols, double* out) {
+  return guarded([&] {
+    need(r, "result");
+    need(name, "name");
+    load_into(named(r->r.params, name), rows, cols, out);
+  });
+}
+
+void prsp_gpu_result_free(prsp_gpu_result* r) { delete r; }
+
+int prsp_gpu_run_open(const char* dir, prsp_gpu_run** out) {
+  return guarded([&] {
+    need(dir, "dir");
+    need(out, "out");
+    *out = new prsp_gpu_run{bscgpu::load_run(dir)};
+  });
+}
+
+int prsp_gpu_run_info(const prsp_gpu_run* run, char* model, uint32_t capacity, uint32_t* dim, uint32_t* latents) {
+  return guarded([&] {
+    need(run, "run");
+    const auto& c = run->run.config;
+    if (model) {
+      if (c.model.size() + 1 > capacity) throw bscgpu::Error(bscgpu::kConfig, "run_info: buffer too small");
+      std::memcpy(model, c.model.c_str(), c.model.size() + 1);
+    }
+    if (dim) *dim = c.dim;
+    if (latents) *latents = c.latents;
+  });
+}
+
+int prsp_gpu_run_param(const prsp_gpu_run* run, const char* name, uint64_t* rows, uint64_t* cols, double* out) {
+  return guarded([&] {
+    need(run, "run");
+    need(name, "name");
+    load_into(named(run->run.params, name), rows, cols, out);
+  });
+}
+
+int prsp_gpu_run_infer(const prsp_gpu_run* run, const double* y, uint64_t n, uint64_t d, int device,
+                       double* map_states, double* map_mass, double* expected) {
+  return guarded([&] {
+    need(run, "run");
+    need(y, "y");
+    need(map_states, "map_states");
+    need(map_mass, "map_mass");
+    bscgpu::infer_run(run->run, y, n, d, map_states, map_mass, expected, device);
+  });
+}
+
+void prsp_gpu_run_free(prsp_gpu_run* run) { delete run; }
 
 }  // extern "C"

@@ -9,37 +9,11 @@
 #include <random>
 
 #include "bsc_engine.hpp"
+#include "rng_stream.hpp"
 
 namespace bscgpu {
 
 namespace {
-
-// splitmix64 (core.cpp:50-57)
-uint64_t mix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
-}
-
-// RngStream (core.hpp:129-150, core.cpp:59-79): mt19937_64, 53-bit uniforms,
-// Box-Muller normals.
-class Stream {
- public:
-  explicit Stream(uint64_t seed) : eng_(seed) {}
-  static Stream derived(uint64_t base, uint64_t index) { return Stream(mix64(mix64(base) ^ mix64(index + 1))); }
-  double uniform01() { return static_cast<double>(eng_() >> 11) * 0x1.0p-53; }
-  double normal() {
-    double u1 = uniform01();
-    while (u1 <= 0.0) u1 = uniform01();
-    const double u2 = uniform01();
-    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
-  }
-  bool bernoulli(double p) { return uniform01() < p; }
-
- private:
-  std::mt19937_64 eng_;
-};
 
 void column_means(const double* y, uint64_t n, uint32_t d, std::vector<double>& m) {
   m.assign(d, 0.0);
