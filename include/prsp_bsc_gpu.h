@@ -159,6 +159,8 @@ int prsp_mca_gpu_set_stats(prsp_mca_gpu* ctx, const double* winner_num, const do
                            const double* scalars);
 int prsp_mca_gpu_mstep_fixedpoint(prsp_mca_gpu* ctx, double* w_out, double* pi_out);
 int prsp_mca_gpu_residual_commit(prsp_mca_gpu* ctx, double temperature, double* residual_out);
+/* Multi-rank σ²: after summing residual_out across ranks, σ² = max(Σ/(N·D), 1e-12) (:431-436). */
+int prsp_mca_gpu_set_sigma2(prsp_mca_gpu* ctx, double sigma2);
 int prsp_mca_gpu_candidates(prsp_mca_gpu* ctx, uint32_t* out);
 int prsp_mca_gpu_inference(prsp_mca_gpu* ctx, double* map_states, double* map_mass, double* expected);
 

@@ -63,6 +63,7 @@ SIGNATURES = {
     "prsp_mca_gpu_mstep_fixedpoint": [_ptr, _ptr, _dp],
     "prsp_mca_gpu_residual_commit": [_ptr, _dbl, _dp],
     "prsp_mca_gpu_candidates": [_ptr, _ptr],
+    "prsp_mca_gpu_set_sigma2": [_ptr, _dbl],
     "prsp_mca_gpu_inference": [_ptr, _ptr, _ptr, _ptr],
     "prsp_gpu_array_save": [C.c_char_p, _ptr, _u64, _u64],
     "prsp_gpu_array_load": [C.c_char_p, C.POINTER(_u64), C.POINTER(_u64), _ptr],

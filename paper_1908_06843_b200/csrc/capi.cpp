@@ -457,6 +457,13 @@ int prsp_mca_gpu_residual_commit(prsp_mca_gpu* ctx, double temperature, double* 
   });
 }
 
+int prsp_mca_gpu_set_sigma2(prsp_mca_gpu* ctx, double sigma2) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->engine.set_sigma2(sigma2);
+  });
+}
+
 int prsp_mca_gpu_candidates(prsp_mca_gpu* ctx, uint32_t* out) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -35,6 +35,10 @@ class McaEngine {
   // residual pass (posterior at the current params, residual under W'), then W ← W', π, σ²
   void residual_and_commit(double temperature);
   double step(double temperature);  // returns F = Σ log Z at the incoming params
+  void set_sigma2(double s2) {
+    if (!(s2 > 0.0)) throw Error(kConfig, "max causes: sigma2 must be positive");
+    sigma2_ = s2;
+  }
   void candidates(uint32_t* out);
   void inference(double* map_states, double* map_mass, double* expected);
   double* stats_device() { return d_stats_; }

@@ -22,14 +22,15 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
-def stats_count(d: int, h: int) -> int:
-    return d * h + h + h * h + 4
+def stats_count(d: int, h: int, nv: int = 1) -> int:
+    return d * h + h + h * h + nv + 3
 
 
 def pack_stats(st: dict, d: int, h: int) -> np.ndarray:
     """Host copy of the device layout [sum_y_sT D·H | sum_s H | sum_ssT H·H |
-    value_counts | sum_y2 | log_partition | points] (bsc_engine.hpp StatsLayout)."""
-    out = np.empty(stats_count(d, h))
+    value_counts V | sum_y2 | log_partition | points] (bsc_engine.hpp StatsLayout)."""
+    vc = np.atleast_1d(np.asarray(st["value_counts"], float))
+    out = np.empty(stats_count(d, h, len(vc)))
     o = 0
     out[o:o + d * h] = np.asarray(st["sum_y_sT"]).ravel()
     o += d * h
@@ -37,12 +38,13 @@ def pack_stats(st: dict, d: int, h: int) -> np.ndarray:
     o += h
     out[o:o + h * h] = np.asarray(st["sum_ssT"]).ravel()
     o += h * h
-    out[o:o + 4] = [float(np.atleast_1d(st["value_counts"])[0]), st["sum_y2"], st["log_partition"],
-                    float(st["points"])]
+    out[o:o + len(vc)] = vc
+    o += len(vc)
+    out[o:o + 3] = [st["sum_y2"], st["log_partition"], float(st["points"])]
     return out
 
 
-def unpack_stats(buf: np.ndarray, d: int, h: int) -> dict:
+def unpack_stats(buf: np.ndarray, d: int, h: int, nv: int = 1) -> dict:
     o = 0
     ysT = buf[o:o + d * h].reshape(d, h).copy()
     o += d * h
@@ -50,9 +52,10 @@ def unpack_stats(buf: np.ndarray, d: int, h: int) -> dict:
     o += h
     ssT = buf[o:o + h * h].reshape(h, h).copy()
     o += h * h
-    t = buf[o:o + 4]
-    return dict(sum_s=s, sum_ssT=ssT, sum_y_sT=ysT, value_counts=np.array([t[0]]), sum_y2=float(t[1]),
-                log_partition=float(t[2]), points=int(round(t[3])))
+    vc = buf[o:o + nv].copy()
+    t = buf[o + nv:o + nv + 3]
+    return dict(sum_s=s, sum_ssT=ssT, sum_y_sT=ysT, value_counts=vc, sum_y2=float(t[0]),
+                log_partition=float(t[1]), points=int(round(t[2])))
 
 
 class _CudaArray:
@@ -72,8 +75,9 @@ def stats_tensor(model):
 
 
 def distributed_step(model, stats_view, temperature: float = 1.0, group=None) -> None:
-    """One EM iteration across ranks: local E-step → all-reduce(Σ stats) → M-step.
-    The model must run on torch's current stream (``model.set_stream``)."""
+    """One EM iteration across ranks (any linear discrete family): local E-step →
+    all-reduce(Σ stats) → M-step. The model must run on torch's current stream
+    (``model.set_stream``)."""
     import torch.distributed as dist
 
     from . import _native as N
@@ -82,3 +86,36 @@ def distributed_step(model, stats_view, temperature: float = 1.0, group=None) ->
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(stats_view, op=dist.ReduceOp.SUM, group=group)
     model.mstep_device()
+
+
+def mca_distributed_step(model, temperature: float = 1.0, group=None) -> float:
+    """One max-causes iteration across ranks (MaxCausesModel::step,
+    max_causes.cpp:416-446): local E pass → all-reduce(Σ winner statistics) →
+    replicated fixed-point M-step → local residual pass under W′ → all-reduce(Σ
+    residual) → σ² = max(Σ residual / (N·D), 1e-12). Returns F."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    multi = dist.is_initialized() and dist.get_world_size() > 1
+    N.call("prsp_mca_gpu_estep", model._h, float(temperature))
+    p, n = C.c_void_p(), C.c_uint64()
+    N.call("prsp_mca_gpu_stats_buffer", model._h, C.byref(p), C.byref(n))
+    if multi:
+        view = torch.as_tensor(_CudaArray(p.value, n.value), device=f"cuda:{torch.cuda.current_device()}")
+        dist.all_reduce(view, op=dist.ReduceOp.SUM, group=group)
+        torch.cuda.synchronize()
+    st = model.get_stats()
+    N.call("prsp_mca_gpu_mstep_fixedpoint", model._h, None, None)
+    r = C.c_double()
+    N.call("prsp_mca_gpu_residual_commit", model._h, float(temperature), C.byref(r))
+    if multi:
+        t = torch.tensor([r.value], dtype=torch.float64, device=f"cuda:{torch.cuda.current_device()}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        total = float(t.item())
+        s2 = max(total / (st.points * model.dim), 1e-12)
+        N.call("prsp_mca_gpu_set_sigma2", model._h, s2)
+    return st.log_partition

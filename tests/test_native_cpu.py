@@ -101,6 +101,16 @@ def test_pack_unpack_roundtrip(port):
     back = unpack_stats(buf, 16, 8)
     for k in st:
         assert np.array_equal(np.asarray(back[k]), np.asarray(st[k])), k
+    # multi-valued families: value_counts has one entry per non-zero value
+    from oracle.oracle import Prior
+
+    pr = Prior("dsc", 0.0, [-1.0, 0.0, 1.0, 2.0], [0.1, 0.7, 0.1, 0.1])
+    st = port.ld_estep_stats(pr, w, s2, y, 5, 3)
+    buf = pack_stats(st, 16, 8)
+    assert buf.shape == (stats_count(16, 8, 3),)
+    back = unpack_stats(buf, 16, 8, 3)
+    for k in st:
+        assert np.array_equal(np.asarray(back[k]), np.asarray(st[k])), k
 
 
 def test_flop_convention_matches_survey():
