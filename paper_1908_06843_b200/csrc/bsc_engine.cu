@@ -38,6 +38,24 @@ const void* enum_fn_t(int maxj) {
 }
 const void* enum_fn(int maxj, bool staged) { return staged ? enum_fn_t<true>(maxj) : enum_fn_t<false>(maxj); }
 
+using SolveFn = void (*)(const double*, int, int, double*, int, int, int);
+template <bool FWD>
+SolveFn solve_rows_t(int s) {
+  switch (s) {
+    case 1: return solve_rows_kernel<1, FWD>;
+    case 2: return solve_rows_kernel<2, FWD>;
+    case 4: return solve_rows_kernel<4, FWD>;
+    case 6: return solve_rows_kernel<6, FWD>;
+    case 8: return solve_rows_kernel<8, FWD>;
+    case 10: return solve_rows_kernel<10, FWD>;
+    case 12: return solve_rows_kernel<12, FWD>;
+    case 16: return solve_rows_kernel<16, FWD>;
+    case 24: return solve_rows_kernel<24, FWD>;
+    default: return solve_rows_kernel<32, FWD>;
+  }
+}
+SolveFn solve_rows_fn(int s, bool fwd) { return fwd ? solve_rows_t<true>(s) : solve_rows_t<false>(s); }
+
 // Tile configurations (see dgemm.cuh).
 // GEMM1  B = Y·W:     M = points, N = Hp, K = Dp.
 #define GEMM1_CFG 128, 64, 16, 32, 32, true, true, 3
@@ -131,6 +149,7 @@ void BscEngine::init(int device) {
   d_smulti_ = dalloc<double>(H_, "s_multi");
   d_err_ = dalloc<int>(1, "err");
   d_bm_ = dalloc<double>((size_t)H_ * Hp_, "Bm");
+  d_u_ = dalloc<double>((size_t)H_ * Hp_, "U");
   d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
   d_msc_ = dalloc<MstepScalars>(1, "mstep scalars");
   ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
@@ -158,7 +177,7 @@ BscEngine::~BscEngine() {
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
-                  (void*)d_vpart_})
+                  (void*)d_vpart_, (void*)d_u_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -548,7 +567,7 @@ void BscEngine::enqueue_gram(void* stream) {
   const int H = static_cast<int>(H_);
   GemmArgs g{H, H, Dp_, d_w_, Hp_, d_w_, Hp_, d_g_, Hp_, 1.0, 0.0, Dp_, 0};
   ck(launch_dgemm<GRAM_CFG>(g, 1, s), "gram gemm");
-  gram_diag_exact_kernel<<<(H_ + 127) / 128, 128, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, Hp_, d_wnorm_, d_gdiag_);
+  gram_diag_exact_kernel<<<(H_ + 31) / 32, 32, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, Hp_, d_wnorm_, d_gdiag_);
   ck(cudaGetLastError(), "gram");
   launches_ += 2;
 }
@@ -792,9 +811,8 @@ void BscEngine::enqueue_mstep(void* stream) {
     potrf_diag_kernel<<<1, 256, 0, s>>>(d_bm_, Hp_, k0, kb, sc);
     ++launches_;
     if (k1 < H) {
-      const int rows = H - k1, tpb = 32;
-      trsm_rows_kernel<true><<<(rows + tpb - 1) / tpb, tpb, 0, s>>>(d_bm_, Hp_, k0, kb, d_bm_, Hp_,
-                                                                                   k1, rows, k0);
+      const int rows = H - k1;
+      trsm_panel_warp_kernel<<<(rows + 7) / 8, 256, 0, s>>>(d_bm_, Hp_, k0, kb, k1, rows);
       GemmArgs g{rows, rows, kb, d_bm_ + (long long)k1 * Hp_ + k0, Hp_, d_bm_ + (long long)k1 * Hp_ + k0, Hp_,
                  d_bm_ + (long long)k1 * Hp_ + k1, Hp_, -1.0, 1.0, kb, 0};
       ck(launch_dgemm<SYRK_CFG>(g, 1, s), "syrk");
@@ -802,30 +820,23 @@ void BscEngine::enqueue_mstep(void* stream) {
     }
   }
   ck(cudaGetLastError(), "cholesky");
-  // X·L·Lᵀ = Σy⟨s⟩ᵀ: forward (Z·Lᵀ = R) then backward (X·L = Z), column blocks
-  const int tpb = 32, nblk = (D + tpb - 1) / tpb;
-  for (int j0 = 0; j0 < H; j0 += kCholNb) {
-    const int kb = std::min(kCholNb, H - j0);
-    if (j0 > 0) {
-      GemmArgs g{D, kb, j0, d_x_, Hp_, d_bm_ + (long long)j0 * Hp_, Hp_, d_x_ + j0, Hp_, -1.0, 1.0, j0, 0};
-      ck(launch_dgemm<SYRK_CFG>(g, 1, s), "solve fwd gemm");
-      ++launches_;
+  // X·L·Lᵀ = Σy⟨s⟩ᵀ: forward (Z·Lᵀ = R, against U = Lᵀ) then backward (X·L = Z),
+  // one warp per row of X over the full width
+  transpose_lower_kernel<<<dim3((H + 31) / 32, (Hp_ + 31) / 32), dim3(32, 8), 0, s>>>(d_bm_, Hp_, H, d_u_);
+  {
+    // 4 rows per CTA; pivot rows staged in blocks of rb (double-buffered)
+    const unsigned blocks = static_cast<unsigned>((D + 3) / 4);
+    const int rb = std::max(1, std::min(32, (160 * 1024) / (2 * Hp_ * 8)));
+    const size_t smem = (static_cast<size_t>((H + 1) & ~1) + 2ull * rb * Hp_) * sizeof(double);
+    for (bool fwd : {true, false}) {
+      auto fn = solve_rows_fn(maxj_for(H_), fwd);
+      ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)),
+         "solve smem");
+      fn<<<blocks, 128, smem, s>>>(fwd ? d_u_ : d_bm_, Hp_, H, d_x_, Hp_, D, rb);
     }
-    trsm_rows_kernel<true><<<nblk, tpb, 0, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
-    ++launches_;
   }
-  const int last0 = (H - 1) / kCholNb * kCholNb;
-  for (int j0 = last0; j0 >= 0; j0 -= kCholNb) {
-    const int kb = std::min(kCholNb, H - j0), j1 = j0 + kb;
-    if (j1 < H) {
-      GemmArgs g{D, kb, H - j1, d_x_ + j1, Hp_, d_bm_ + (long long)j1 * Hp_ + j0, Hp_, d_x_ + j0, Hp_, -1.0, 1.0,
-                 H - j1, 0};
-      ck(launch_dgemm<SOLVE_CFG>(g, 1, s), "solve bwd gemm");
-      ++launches_;
-    }
-    trsm_rows_kernel<false><<<nblk, tpb, 0, s>>>(d_bm_, Hp_, j0, kb, d_x_, Hp_, 0, D, j0);
-    ++launches_;
-  }
+  launches_ += 3;
   ck(cudaGetLastError(), "solve");
   commit_w_kernel<<<64, 256, 0, s>>>(d_x_, Hp_, d_w_, Hp_, D, H, sc);
   // Gram of W' (the next E-step's G; exact diagonal) also feeds t3

@@ -166,7 +166,7 @@ class BscEngine {
   double* d_map_mass_ = nullptr;
   int* d_err_ = nullptr;
   // M-step workspace
-  double *d_bm_ = nullptr, *d_x_ = nullptr, *d_trace_part_ = nullptr;
+  double *d_bm_ = nullptr, *d_x_ = nullptr, *d_trace_part_ = nullptr, *d_u_ = nullptr;
   void* d_msc_ = nullptr;
   void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // pinned
   double last_F_ = 0.0;

@@ -51,8 +51,17 @@ static __global__ void gram_diag_exact_kernel(const double* __restrict__ W, int 
                                        double* __restrict__ gdiag) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   if (h >= H) return;
+  // loads batched 16 ahead (the adds stay strictly sequential)
   double acc = 0.0;
-  for (int d = 0; d < D; ++d) {
+  int d = 0;
+  for (; d + 16 <= D; d += 16) {
+    double a[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) a[u] = W[(long long)(d + u) * ldw + h];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, __dmul_rn(a[u], a[u]));
+  }
+  for (; d < D; ++d) {
     const double a = W[(long long)d * ldw + h];
     acc = __dadd_rn(acc, __dmul_rn(a, a));
   }

@@ -218,7 +218,7 @@ void McaEngine::get_params(double* w, double* pi, double* sigma2) {
 void McaEngine::refresh(const double* w, double* wt, double* gdiag, double* wnorm, double* b) {
   auto s = static_cast<cudaStream_t>(stream_);
   transpose_w_kernel<<<dim3((H_ + 31) / 32, (Dp_ + 31) / 32), dim3(32, 8), 0, s>>>(w, D_, H_, Hp_, wt, Dp_);
-  gram_diag_exact_kernel<<<(H_ + 127) / 128, 128, 0, s>>>(w, D_, H_, Hp_, d_g_, Hp_, wnorm, gdiag);
+  gram_diag_exact_kernel<<<(H_ + 31) / 32, 32, 0, s>>>(w, D_, H_, Hp_, d_g_, Hp_, wnorm, gdiag);
   GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, w, Hp_, b, Hp_, 1.0, 0.0, Dp_, 0};
   ck(launch_dgemm<MCA_GEMM1_CFG>(g, 1, s), "gemm Y·W");
 }

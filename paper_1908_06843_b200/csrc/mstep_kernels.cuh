@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "dgemm.cuh"
+
 namespace bscgpu {
 
 constexpr int kCholNb = 64;
@@ -105,49 +107,152 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
   if (tid == 0 && fail) sc->chol_failed = 1;
 }
 
-// Row-wise triangular solves against the kb×kb lower block Lkk stored at
-// (k0,k0) of L (leading dim ldl), applied to rows [r0, r0+nrows) of X at
-// columns [c0, c0+kb); one thread per row, the row held in registers (the
-// 64-wide block is fully unrolled, padded with the identity past kb):
-//   FWD_T:  x · Lkkᵀ = x_in  (forward substitution)   — Cholesky panel / Z = R·L⁻ᵀ
-//   BWD  :  x · Lkk  = x_in  (backward substitution)  — X = Z·L⁻¹
-template <bool FWD_T>
-__global__ void __launch_bounds__(128) trsm_rows_kernel(const double* __restrict__ Lm, int ldl, int k0, int kb,
-                                                        double* __restrict__ X, int ldx, int r0, int nrows, int c0) {
-  __shared__ double L[kCholNb][kCholNb + 1];
+// Warp-per-row triangular solves (right-looking, one column per step, the
+// pivot broadcast by a shuffle): lane l holds entries l + 32·s of its row.
+// Same operation order as the column-by-column substitution, so a row solve
+// costs ~n dependent shuffle+FMA steps instead of n² serial FMAs per thread.
+
+// Cholesky panel: rows [r0, r0+nrows) of Bm at columns [k0, k0+kb) ← X·L_kk⁻ᵀ.
+// L_kk is staged per CTA in shared memory, transposed (U = L_kkᵀ).
+__global__ void __launch_bounds__(256) trsm_panel_warp_kernel(double* __restrict__ Bm, int ldb, int k0, int kb, int r0,
+                                                              int nrows) {
+  __shared__ double U[kCholNb][kCholNb + 1];
   __shared__ double rinv[kCholNb];
-  const int tid = threadIdx.x;
-  for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
-    const int i = e / kCholNb, j = e % kCholNb;
-    L[i][j] = (i < kb && j < kb) ? Lm[(long long)(k0 + i) * ldl + k0 + j] : (i == j ? 1.0 : 0.0);
+  for (int e = threadIdx.x; e < kCholNb * kCholNb; e += blockDim.x) {
+    const int c = e / kCholNb, t = e % kCholNb;  // U[c][t] = L[t][c]
+    U[c][t] = (c < kb && t < kb && t >= c) ? Bm[(long long)(k0 + t) * ldb + k0 + c] : 0.0;
   }
   __syncthreads();
-  for (int c = tid; c < kCholNb; c += blockDim.x) rinv[c] = 1.0 / L[c][c];
+  for (int c = threadIdx.x; c < kb; c += blockDim.x) rinv[c] = 1.0 / U[c][c];
   __syncthreads();
-  const int row = r0 + blockIdx.x * blockDim.x + tid;
+  const int lane = threadIdx.x & 31;
+  const int row = r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= r0 + nrows) return;
-  double* xr = X + (long long)row * ldx + c0;
-  double x[kCholNb];
+  double* xr = Bm + (long long)row * ldb + k0;
+  double x0 = lane < kb ? xr[lane] : 0.0, x1 = lane + 32 < kb ? xr[lane + 32] : 0.0;
+  for (int c = 0; c < kb; ++c) {
+    double xc;
+    if (c < 32) {
+      if (lane == c) x0 *= rinv[c];
+      xc = __shfl_sync(0xffffffffu, x0, c);
+      if (lane > c) x0 -= xc * U[c][lane];
+      x1 -= xc * U[c][lane + 32];
+    } else {
+      if (lane == c - 32) x1 *= rinv[c];
+      xc = __shfl_sync(0xffffffffu, x1, c - 32);
+      if (lane + 32 > c) x1 -= xc * U[c][lane + 32];
+    }
+  }
+  if (lane < kb) xr[lane] = x0;
+  if (lane + 32 < kb) xr[lane + 32] = x1;
+}
+
+// U = Lᵀ (lower factor in Bm → upper rows, zeros elsewhere).
+__global__ void transpose_lower_kernel(const double* __restrict__ Bm, int ldb, int H, double* __restrict__ U) {
+  __shared__ double tile[32][33];
+  const int c0 = blockIdx.x * 32, t0 = blockIdx.y * 32;  // U[c][t] = L[t][c], t ≥ c
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int t = t0 + r, c = c0 + threadIdx.x;
+    tile[r][threadIdx.x] = (t < H && c < H && t >= c) ? Bm[(long long)t * ldb + c] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int c = c0 + r, t = t0 + threadIdx.x;
+    if (c < H && t < ldb) U[(long long)c * ldb + t] = t < H ? tile[threadIdx.x][r] : 0.0;
+  }
+}
+
+// Rows of X (nrows × n, leading dim ldx) against the full factor:
+//   FWD: X·Lᵀ = X with T = U = Lᵀ (row c of T = column c of L)
+//   BWD: X·L  = X with T = L
+// S = register slots per lane (n ≤ 32·S). The rows of T are consumed in
+// order by every warp of the CTA: blocks of `rb` rows are staged in shared
+// memory with cp.async, double-buffered, so each step reads the pivot row at
+// shared-memory latency. Shared layout: rinv[n (padded)] | buf[2][rb·ldt].
+template <int S, bool FWD>
+__global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restrict__ T, int ldt, int n,
+                                                         double* __restrict__ X, int ldx, int nrows, int rb) {
+  extern __shared__ __align__(16) double msm[];
+  const int npad = (n + 1) & ~1;
+  double* rinv = msm;
+  double* buf0 = msm + npad;
+  double* buf1 = buf0 + (size_t)rb * ldt;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) rinv[c] = 1.0 / T[(long long)c * ldt + c];
+  const int nblk = (n + rb - 1) / rb;
+  auto stage = [&](int blk, double* dst) {  // rows of block blk (in consumption order)
+    const int b = FWD ? blk : nblk - 1 - blk;
+    const int r0 = b * rb, rows = (r0 + rb <= n ? rb : n - r0);
+    const int vec = ldt / 2;  // 16-byte chunks per row
+    for (int e = threadIdx.x; e < rows * vec; e += blockDim.x) {
+      const int r = e / vec, q = e - r * vec;
+      cp_async16(dst + (size_t)r * ldt + 2 * q, T + (long long)(r0 + r) * ldt + 2 * q, true);
+    }
+    cp_async_commit();
+  };
+  stage(0, buf0);
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const bool active = row < nrows;
+  double* xr = X + (long long)(active ? row : 0) * ldx;
+  double x[S];
 #pragma unroll
-  for (int c = 0; c < kCholNb; ++c) x[c] = c < kb ? xr[c] : 0.0;
-  if (FWD_T) {
+  for (int s = 0; s < S; ++s) x[s] = (active && lane + 32 * s < n) ? xr[lane + 32 * s] : 0.0;
+  int blk = 0, cur_r0 = FWD ? 0 : (nblk - 1) * rb;
+  double* cur = buf0;
+  double* nxt = buf1;
+  int blk_end = FWD ? -1 : 0x7fffffff;  // first c beyond the staged block (FWD) / below it (BWD)
+  auto advance = [&](int c) {
+    // make the block holding row c current (c leaves the staged range)
+    if (blk > 0) {
+      double* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (blk + 1 < nblk) stage(blk + 1, nxt);
+    const int b = FWD ? blk : nblk - 1 - blk;
+    cur_r0 = b * rb;
+    blk_end = FWD ? cur_r0 + rb : cur_r0 - 1;
+    ++blk;
+  };
+  if (FWD) {
 #pragma unroll
-    for (int c = 0; c < kCholNb; ++c) {
-      x[c] *= rinv[c];
+    for (int s = 0; s < S; ++s) {
+      const int cend = n - 32 * s < 32 ? n - 32 * s : 32;
+      for (int cc = 0; cc < cend; ++cc) {
+        const int c = 32 * s + cc;
+        if (c >= blk_end) advance(c);
+        const double* tr = cur + (size_t)(c - cur_r0) * ldt;
+        if (lane == cc) x[s] *= rinv[c];
+        const double xc = __shfl_sync(0xffffffffu, x[s], cc);
+        if (lane > cc && lane < cend) x[s] -= xc * tr[lane + 32 * s];
 #pragma unroll
-      for (int t = c + 1; t < kCholNb; ++t) x[t] -= x[c] * L[t][c];
+        for (int s2 = s + 1; s2 < S; ++s2)
+          if (lane + 32 * s2 < n) x[s2] -= xc * tr[lane + 32 * s2];
+      }
     }
   } else {
 #pragma unroll
-    for (int c = kCholNb - 1; c >= 0; --c) {
-      x[c] *= rinv[c];
+    for (int s = S - 1; s >= 0; --s) {
+      const int cend = n - 32 * s < 32 ? n - 32 * s : 32;
+      for (int cc = cend - 1; cc >= 0; --cc) {
+        const int c = 32 * s + cc;
+        if (c <= blk_end) advance(c);
+        const double* tr = cur + (size_t)(c - cur_r0) * ldt;
+        if (lane == cc) x[s] *= rinv[c];
+        const double xc = __shfl_sync(0xffffffffu, x[s], cc);
+        if (lane < cc) x[s] -= xc * tr[lane + 32 * s];
 #pragma unroll
-      for (int t = 0; t < c; ++t) x[t] -= x[c] * L[c][t];
+        for (int s2 = 0; s2 < s; ++s2) x[s2] -= xc * tr[lane + 32 * s2];
+      }
     }
   }
+  if (active) {
 #pragma unroll
-  for (int c = 0; c < kCholNb; ++c)
-    if (c < kb) xr[c] = x[c];
+    for (int s = 0; s < S; ++s)
+      if (lane + 32 * s < n) xr[lane + 32 * s] = x[s];
+  }
 }
 
 // W ← X unless the factorisation failed (then the previous W is kept).
