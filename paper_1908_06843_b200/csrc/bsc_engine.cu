@@ -695,7 +695,6 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   ev(1);
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
-  ck(cudaMemsetAsync(d_part_, 0, (size_t)splits_ * part_stride_ * 8, s), "zero partials");
   ck(cudaMemsetAsync(d_warp_es_, 0, (size_t)nchunks * splits_ * Hp_ * 8, s), "zero colsums");
   auto cs = static_cast<cudaStream_t>(copy_stream_);
   if (host_y) {
@@ -731,8 +730,14 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       int kchunk = (krows + splits_ - 1) / splits_;
       kchunk = (kchunk + 1) & ~1;
       const int splits = (krows + kchunk - 1) / kchunk;
-      GemmArgs g{Dp_, Hp_, krows, d_y_ + off * Dp_, Dp_, d_es_ + off * Hp_, Hp_, d_part_, Hp_, 1.0, 1.0, kchunk,
-                 part_stride_, d_warp_es_ + (size_t)c * splits_ * Hp_};
+      // the first chunk overwrites its partial slots (β = 0; the largest chunk, so
+      // later chunks accumulate into slots it wrote); slots it leaves unused are cleared
+      if (c == 0 && splits < splits_)
+        ck(cudaMemsetAsync(d_part_ + (size_t)splits * part_stride_, 0,
+                           (size_t)(splits_ - splits) * part_stride_ * 8, s),
+           "zero partials");
+      GemmArgs g{Dp_, Hp_, krows, d_y_ + off * Dp_, Dp_, d_es_ + off * Hp_, Hp_, d_part_, Hp_, 1.0,
+                 c == 0 ? 0.0 : 1.0, kchunk, part_stride_, d_warp_es_ + (size_t)c * splits_ * Hp_};
       ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
       ++launches_;
     }
