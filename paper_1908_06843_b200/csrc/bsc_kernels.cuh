@@ -79,7 +79,8 @@ __device__ __forceinline__ double small_exp(double x) {
   return static_cast<double>(r);
 }
 
-// e^x for x ≤ 0 in fp64 (the posterior weights exp(lj − max)): Cody–Waite
+// e^x for x ≤ 0 (and, exactly as well, for 0 < x ≤ 709) in fp64 (the
+// posterior weights exp(lj − max) and the guarded factors e^u, e^P): Cody–Waite
 // reduction x = k·ln2 + r, |r| ≤ ln2/2, Taylor polynomial of degree 13
 // (truncation < 5e-18 relative), and 2^k applied as two exact power-of-two
 // factors so gradual underflow rounds once (x < −745.2 gives 0). About 1 ulp;
@@ -641,6 +642,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // here (the MAP and moment passes recompute single_q from B) so the state
     // passes below run with MAXJ more registers of ILP
     const double mxs = mx;
+    double* esrow = a.ES + (long long)n * a.Hp;
     double zs1 = lane == 0 ? exp_nonpos(-mxs) : 0.0;
     double zsT = lane == 0 && !t1 ? exp_nonpos(-mxs * a.inv_T) : 0.0;
 #pragma unroll
@@ -718,9 +720,9 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         for (int p = lane; p < HP; p += 32) {
           tab[p] = exp_nonpos(tab[p] - mx);  // level-1 nodes {p}
           sqs[p] = tab[p];
-          su[p] = exp(su[p]);
+          su[p] = exp_nonpos(su[p]);  // |u| ≤ 300: the reduction + two scale factors are exact here too
         }
-        for (int e = lane; e < npairs; e += 32) sP[e] = exp(sP[e]);
+        for (int e = lane; e < npairs; e += 32) sP[e] = exp_nonpos(sP[e]);
         __syncwarp();
         for (int k = 2; k <= GM; ++k) {
           const int e = a.level_off[k];
@@ -884,7 +886,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // ---- ⟨s_n⟩ row: singleton mass for every unit; candidates then take their
     // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
     // Yᵀ⟨S⟩ GEMM from these rows.
-    double* esrow = a.ES + (long long)n * a.Hp;
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const int h = lane + 32 * j;
