@@ -127,3 +127,28 @@ def test_family_errors(pkg):
     with pytest.raises(P.ConfigError):
         t.set_params(P.LinearDiscreteParams(np.ones((4, 6)), 1.0, pi=1.5))
     t.close()
+
+
+@pytest.mark.parametrize("family,alpha,probs,d,h,hp,g,n", [
+    ("tsc", None, None, 10, 9, 9, 1, 60),                 # γ = 1: singletons only
+    ("tsc", None, None, 8, 6, 6, 6, 50),                  # exact mode H' = γ = H
+    ("dsc", [0.0, 0.5, 3.0], [0.8, 0.15, 0.05], 12, 20, 4, 4, 80),   # γ = H', positive alphabet
+])
+def test_family_edges(pkg, port, family, alpha, probs, d, h, hp, g, n):
+    from oracle.oracle import Prior
+
+    pr = Prior(family, 0.2, alpha, probs)
+    wt = port.random_dictionary(d, h, 41, 2.0)
+    y = port.ld_generate(pr, wt, 0.3, n, 42)
+    w0, _, s20 = port.baseline_init(np.r_[y, y + 0.1], h, 43)
+    m = gpu_model(pkg, pr, d, h, hp, g)
+    m.load(y)
+    p0 = gpu_params(pkg, pr, w0, s20)
+    assert np.array_equal(m.candidates(p0), port.ld_candidates(pr, w0, s20, y, hp))
+    check_stats(m.estep_stats(p0), port.ld_estep_stats(pr, w0, s20, y, hp, g))
+    wo, pio, qo, s2o, fo = port.ld_step(pr, w0, s20, y, hp, g)
+    check_step(pr, m.step(p0), wo, pio, qo, s2o, fo)
+    if hp == h == g:  # exact mode: F is the exact log-likelihood
+        ll = port.ld_exact_log_likelihood(pr, w0, s20, y)
+        assert abs(fo - ll) <= 1e-10 * abs(ll)
+    m.close()

@@ -105,3 +105,24 @@ def test_mca_errors(pkg):
     with pytest.raises(P.NumericError):
         m.set_params(P.McaParams(np.full((4, 6), np.nan), 0.2, 1.0))
     m.close()
+
+
+@pytest.mark.parametrize("mode,d,h,hp,g,n", [
+    ("mca", 9, 7, 7, 1, 50),     # γ = 1
+    ("mmca", 8, 6, 6, 6, 40),    # exact mode H' = γ = H
+])
+def test_mca_edges(pkg, port, mode, d, h, hp, g, n):
+    rng = np.random.default_rng(h * 7 + g)
+    wt = np.abs(rng.normal(size=(d, h))) + 0.1 if mode == "mca" else rng.normal(size=(d, h))
+    y = port.mca_generate(mode, wt, 0.25, 0.3, n, 5)
+    w0, pi0, s20 = port.mca_standard_init(mode, y, h, hp, 6)
+    m = pkg.McaGpuModel(mode, d, h, pkg.TruncationConfig(h, hp, g))
+    m.load(y)
+    p0 = pkg.McaParams(w0, pi0, s20)
+    check_stats(m.estep_stats(p0), port.mca_estep_stats(mode, w0, pi0, s20, y, hp, g))
+    wo, pio, s2o, fo = port.mca_step(mode, w0, pi0, s20, y, hp, g)
+    check_step(m.step(p0), wo, pio, s2o, fo)
+    if hp == h == g:
+        ll = port.mca_exact_log_likelihood(mode, w0, pi0, s20, y)
+        assert abs(fo - ll) <= 1e-10 * abs(ll)
+    m.close()

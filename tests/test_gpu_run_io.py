@@ -96,3 +96,24 @@ def test_run_directory_and_reload(rio, port, tmp_path):
     assert np.array_equal(ex, inf.expected_states)
     g.close()
     run.close()
+
+
+@pytest.mark.parametrize("model,values", [("dsc", [-1.0, 0.0, 2.0]), ("mca", None)])
+def test_run_directory_other_models(rio, port, tmp_path, model, values):
+    y = bars(port, seed=13)
+    out = tmp_path / model
+    cfg = rio.TrainConfig(model=model, latents=8, hprime=5, gamma=3, values=values, iterations=2, seed=4,
+                          tolerance=1e-9, w_noise=[(0.0, 0.1), (1.0, 0.0)])
+    r = rio.train(cfg, y, out_dir=str(out))
+    m = json.load(open(out / "manifest.json"))
+    names = ["W", "sigma2", "values", "probs"] if model == "dsc" else ["W", "sigma2", "pi"]
+    assert m["parameters"] == [f"final_{n}.prsp" for n in names]
+    assert m["tolerance"] == 1e-9 and m["w_noise"] == [[0.0, 0.1], [1.0, 0.0]]
+    if model == "dsc":
+        assert m["values"] == values
+    run = rio.Run(str(out))
+    for n in names:
+        assert np.array_equal(run.param(n), r.params[n])
+    ms, mm, ex = run.infer(y[:20])
+    assert ms.shape == (20, 8) and np.all(mm > 0) and np.all(mm <= 1)
+    run.close()
