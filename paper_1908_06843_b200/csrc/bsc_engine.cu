@@ -177,7 +177,7 @@ BscEngine::~BscEngine() {
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
-                  (void*)d_vpart_, (void*)d_u_})
+                  (void*)d_vpart_, (void*)d_u_, d_chunk_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -254,9 +254,7 @@ void BscEngine::build_template() {
   // level-lexicographic table: level 1 = {p}, then combinations of size k
   const int hp = static_cast<int>(hprime_);
   std::vector<std::vector<int>> sets;  // sorted member lists
-  std::vector<int> level_off{0};
   for (int p = 0; p < hp; ++p) sets.push_back({p});
-  level_off.push_back(hp);
   std::vector<int> comb;
   for (uint32_t k = 2; k <= gamma_; ++k) {
     comb.assign(k, 0);
@@ -269,108 +267,167 @@ void BscEngine::build_template() {
       ++comb[i];
       for (uint32_t j = i + 1; j < k; ++j) comb[j] = comb[j - 1] + 1;
     }
-    level_off.push_back(static_cast<int>(sets.size()));
   }
-  const int n_tab = static_cast<int>(sets.size());
-  if (n_tab != hp + n_multi_) throw Error(kInternal, "state template size mismatch");
+  if (static_cast<int>(sets.size()) != hp + n_multi_) throw Error(kInternal, "state template size mismatch");
   auto key = [](const std::vector<int>& v) {
     uint64_t m = 0;
     for (int p : v) m |= 1ull << p;
     return m;
   };
-  std::unordered_map<uint64_t, int> index_of, dfs_of;
-  for (int i = 0; i < n_tab; ++i) index_of[key(sets[i])] = i;
+  std::unordered_map<uint64_t, int> dfs_of;
   for (int i = 0; i < n_multi_; ++i) dfs_of[masks[i]] = i;
-  const int n_coup = gamma_ >= 3 ? level_off[gamma_ - 1] - hp : 0;
-  // byte offsets into a warp's shared region (the tab/coup/P/u part of the
-  // layout does not depend on the gather sizes)
-  const EnumSmem L0 = EnumSmem::make(hp, n_tab, n_coup, 0, 0, 0);
-  auto tab_off = [&](int i) { return (L0.tab + i) * 8; };
-  // packed {parent rel | sibling coup << 16, P[x][z] | u[z] << 16}, offsets / 8
-  auto w16 = [](int byte_off) {
-    if (byte_off < 0 || byte_off / 8 > 0xffff) throw Error(kConfig, "gpu: state template exceeds the 16-bit table range");
-    return static_cast<unsigned>(byte_off / 8);
-  };
-  std::vector<uint2> desc(n_tab, uint2{0, 0});
-  std::vector<int> dfs_idx(n_tab, -1);
-  std::vector<int2> child(hp + n_coup, int2{0, 0});
-  for (int i = hp; i < n_tab; ++i) {
-    const auto& S = sets[i];
-    const int z = S.back();
-    std::vector<int> A(S.begin(), S.end() - 1);
-    const int x = A.back();
-    std::vector<int> sib(A.begin(), A.end() - 1);
-    sib.push_back(z);
-    const int si = index_of.at(key(sib));
-    const int par_off = tab_off(index_of.at(key(A)));
-    const int sib_off = si < hp ? tab_off(n_tab) : (L0.coup + si - hp) * 8;
-    const int p_off = (L0.P + x * (2 * hp - x - 1) / 2 + (z - x - 1)) * 8;  // strict upper triangle
-    const int u_off = (L0.u + z) * 8;
-    desc[i] = uint2{w16(par_off) | (w16(sib_off) << 16), w16(p_off) | (w16(u_off) << 16)};
-    dfs_idx[i] = dfs_of.at(key(S));
-  }
-  for (int i = 0; i < hp + n_coup; ++i) {
-    const auto& A = sets[i];
-    const int nc = hp - 1 - A.back();
-    if (nc > 0 && A.size() < gamma_) {
-      std::vector<int> c0 = A;
-      c0.push_back(A.back() + 1);
-      const int fc = index_of.at(key(c0));
-      for (int c = 0; c < nc; ++c) {  // children contiguous in the next level
-        std::vector<int> cc = A;
-        cc.push_back(A.back() + 1 + c);
-        if (index_of.at(key(cc)) != fc + c) throw Error(kInternal, "state template: children not contiguous");
-      }
-      child[i] = int2{fc, nc};
-    }
-  }
-  n_tab_ = n_tab;
-  n_coup_ = n_coup;
 
-  // gather lists: ⟨s_p⟩ ← nodes with max p; ⟨s_p s_q⟩ ← nodes with max q containing p
+  // Chunks of consecutive roots (root = smallest member): a state's parent and
+  // sibling share its root, so chunks are independent tables run one after the
+  // other per point through one per-warp region. One chunk when the whole
+  // table leaves room for 16 warps per SM, else groups no larger than needed
+  // (never below the largest root's subtree).
+  std::vector<int> root_size(hp, 0), root_coup(hp, 0);
+  for (const auto& S : sets) {
+    ++root_size[S[0]];
+    if (S.size() >= 2 && S.size() + 1 <= gamma_) ++root_coup[S[0]];  // levels 2..γ−1
+  }
+  const int total_rows = static_cast<int>(sets.size());
+  auto make_groups = [&](int cap) {
+    std::vector<std::pair<int, int>> g;  // [first root, end root)
+    for (int r = 0; r < hp;) {
+      int e = r, rows = 0;
+      while (e < hp && (e == r || rows + root_size[e] <= cap)) rows += root_size[e++];
+      g.emplace_back(r, e);
+      r = e;
+    }
+    return g;
+  };
+  auto per_warp_bytes = [&](const std::vector<std::pair<int, int>>& g) {
+    int rows = 0, coup = 0;
+    for (const auto& [r0, r1] : g) {
+      int a = 0, b = 0;
+      for (int r = r0; r < r1; ++r) {
+        a += root_size[r];
+        b += root_coup[r];
+      }
+      rows = std::max(rows, a);
+      coup = std::max(coup, b);
+    }
+    return 8 * EnumSmem::make(hp, rows, coup, kSlots, hp + hp * (hp - 1) / 2, static_cast<int>(H_)).total;
+  };
+  const int budget = (228 * 1024 - 2 * 1024) / 16;  // per warp at 16 warps/SM
+  int cap_rows = total_rows;
+  const int min_cap = *std::max_element(root_size.begin(), root_size.end());
+  while (cap_rows > min_cap && per_warp_bytes(make_groups(cap_rows)) > budget)
+    cap_rows = std::max(min_cap, cap_rows * 7 / 8);
+  const auto groups = make_groups(cap_rows);
+
+  // per-chunk tables: rows in level-lexicographic order restricted to the chunk
+  std::vector<uint2> desc;
+  std::vector<int> dfs_idx, level_off_all;
+  std::vector<int4> chunk_info;
+  struct ChunkRows {
+    std::vector<int> rows;  // global set indices, chunk order
+    std::vector<int> lo;    // level offsets (γ+1)
+    int n_coup;
+  };
+  std::vector<ChunkRows> chunks;
+  int max_rows = 0, max_coup = 0;
+  for (const auto& [r0, r1] : groups) {
+    ChunkRows cr;
+    cr.lo.assign(gamma_ + 1, 0);
+    for (uint32_t k = 1; k <= gamma_; ++k) {
+      for (int i = 0; i < total_rows; ++i)
+        if (sets[i].size() == k && sets[i][0] >= r0 && sets[i][0] < r1) cr.rows.push_back(i);
+      cr.lo[k] = static_cast<int>(cr.rows.size());
+    }
+    cr.n_coup = gamma_ >= 3 ? cr.lo[gamma_ - 1] - cr.lo[1] : 0;
+    max_rows = std::max(max_rows, static_cast<int>(cr.rows.size()));
+    max_coup = std::max(max_coup, cr.n_coup);
+    chunks.push_back(std::move(cr));
+  }
+  n_tab_ = max_rows;
+  n_coup_ = max_coup;
+  n_chunks_ = static_cast<int>(chunks.size());
   n_out_ = hp + hp * (hp - 1) / 2;
+  const EnumSmem L1 = EnumSmem::make(hp, n_tab_, n_coup_, kSlots, n_out_, 0);
+  auto tab_off = [&](int i) { return (L1.tab + i) * 8; };
+  auto w16 = [](int byte_off) { return ScheduleBuilder::w16(byte_off); };
   auto pair_index = [hp](int p, int q) {  // row-major p < q
     return hp + p * (2 * hp - p - 1) / 2 + (q - p - 1);
   };
-  std::vector<std::vector<int>> lists(n_out_);
-  for (int i = 0; i < n_tab; ++i) {
-    const auto& S = sets[i];
-    const int q = S.back();
-    lists[q].push_back(i);
-    for (size_t a = 0; a + 1 < S.size(); ++a) lists[pair_index(S[a], q)].push_back(i);
-  }
-  // Balanced lane schedules (see SchedDesc and ScheduleBuilder).
-  const EnumSmem L1 = EnumSmem::make(hp, n_tab, n_coup, kSlots, n_out_, 0);
-  if (L1.tab != L0.tab || L1.coup != L0.coup) throw Error(kInternal, "state template layout mismatch");
   ScheduleBuilder sb;
-  sb.zero_off = tab_off(n_tab);
+  sb.zero_off = tab_off(n_tab_);
   sb.part_base = L1.part;
-  auto add_schedule = [&](const std::vector<std::vector<int>>& ls, const std::vector<int>& tg) { sb.add(ls, tg); };
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const auto& cr = chunks[c];
+    const int base = static_cast<int>(desc.size());
+    const int nl1 = cr.lo[1], nrows = static_cast<int>(cr.rows.size());
+    chunk_info.push_back(int4{base, nrows, nl1, groups[c].first});
+    level_off_all.insert(level_off_all.end(), cr.lo.begin(), cr.lo.end());
+    std::unordered_map<uint64_t, int> local;
+    for (int i = 0; i < nrows; ++i) local[key(sets[cr.rows[i]])] = i;
+    for (int i = 0; i < nrows; ++i) {
+      const auto& S = sets[cr.rows[i]];
+      if (S.size() == 1) {
+        desc.push_back(uint2{0, 0});
+        dfs_idx.push_back(-1);
+        continue;
+      }
+      const int z = S.back();
+      std::vector<int> A(S.begin(), S.end() - 1);
+      const int x = A.back();
+      std::vector<int> sib(A.begin(), A.end() - 1);
+      sib.push_back(z);
+      const int par_off = tab_off(local.at(key(A)));
+      const int sib_off = sib.size() == 1 ? tab_off(n_tab_) : (L1.coup + local.at(key(sib)) - nl1) * 8;
+      const int p_off = (L1.P + x * (2 * hp - x - 1) / 2 + (z - x - 1)) * 8;  // strict upper triangle
+      const int u_off = (L1.u + z) * 8;
+      desc.push_back(uint2{w16(par_off) | (w16(sib_off) << 16), w16(p_off) | (w16(u_off) << 16)});
+      dfs_idx.push_back(dfs_of.at(key(S)));
+    }
+    // subtree sums, level γ−1 down to 1: sub(A) = q(A) + Σ_{children} sub(c);
+    // children are contiguous in the next level of the chunk
+    for (int k = static_cast<int>(gamma_) - 1; k >= 1; --k) {
+      std::vector<std::vector<int>> ls;
+      std::vector<int> tg;
+      for (int i = cr.lo[k - 1]; i < cr.lo[k]; ++i) {
+        const auto& A = sets[cr.rows[i]];
+        std::vector<int> l{tab_off(i)};
+        for (int z = A.back() + 1; z < hp; ++z) {
+          std::vector<int> ch = A;
+          ch.push_back(z);
+          const int li = local.at(key(ch));
+          if (l.size() > 1 && li != l.back() / 8 - L1.tab + 1)
+            throw Error(kInternal, "state template: children not contiguous");
+          l.push_back(tab_off(li));
+        }
+        ls.push_back(l);
+        tg.push_back(tab_off(i));
+      }
+      sb.add(ls, tg);
+    }
+    {  // this chunk's share of the moments: ⟨s_p⟩ ← nodes with max p; ⟨s_p s_q⟩ ← max q, p ∈ S
+      std::vector<std::vector<int>> ls(n_out_);
+      std::vector<int> tg(n_out_);
+      for (int i = 0; i < nrows; ++i) {
+        const auto& S = sets[cr.rows[i]];
+        const int q = S.back();
+        ls[q].push_back(tab_off(i));
+        for (size_t m = 0; m + 1 < S.size(); ++m) ls[pair_index(S[m], q)].push_back(tab_off(i));
+      }
+      for (int o = 0; o < n_out_; ++o) tg[o] = (L1.outs + o) * 8;
+      // outputs with no state in this chunk stay out of its schedule
+      std::vector<std::vector<int>> ls2;
+      std::vector<int> tg2;
+      for (int o = 0; o < n_out_; ++o)
+        if (!ls[o].empty()) {
+          ls2.push_back(ls[o]);
+          tg2.push_back(tg[o]);
+        }
+      sb.add(ls2, tg2);
+    }
+  }
+  n_slots_ = kSlots;
   auto& sched = sb.sched;
   auto& ent = sb.ent;
   auto& splits = sb.splits;
-  // subtree sums, level γ−1 down to 1: sub(A) = q(A) + Σ_{children} sub(c)
-  for (int k = static_cast<int>(gamma_) - 1; k >= 1; --k) {
-    std::vector<std::vector<int>> ls;
-    std::vector<int> tg;
-    for (int i = level_off[k - 1]; i < level_off[k]; ++i) {
-      std::vector<int> l{tab_off(i)};
-      for (int c = 0; c < child[i].y; ++c) l.push_back(tab_off(child[i].x + c));
-      ls.push_back(l);
-      tg.push_back(tab_off(i));
-    }
-    add_schedule(ls, tg);
-  }
-  {  // moments into souts
-    std::vector<std::vector<int>> ls(lists.size());
-    std::vector<int> tg(lists.size());
-    for (size_t o = 0; o < lists.size(); ++o) {
-      for (int i : lists[o]) ls[o].push_back(tab_off(i));
-      tg[o] = (L1.outs + static_cast<int>(o)) * 8;
-    }
-    add_schedule(ls, tg);
-  }
-  n_slots_ = kSlots;
 
   // 16-byte multiples: the kernel stages both tables into shared memory as int4
   while ((desc.size() * sizeof(uint2)) % 16) desc.push_back(uint2{0, 0});
@@ -380,12 +437,14 @@ void BscEngine::build_template() {
   d_desc_ = dalloc<uint2>(desc.size(), "desc");
   d_dfs_ = dalloc<int>(dfs_idx.size(), "dfs");
   ck(cudaMemcpy(d_dfs_, dfs_idx.data(), dfs_idx.size() * 4, cudaMemcpyHostToDevice), "dfs");
-  d_level_off_ = dalloc<int>(level_off.size(), "level_off");
+  d_level_off_ = dalloc<int>(level_off_all.size(), "level_off");
+  d_chunk_ = dalloc<int4>(chunk_info.size(), "chunks");
   d_sched_ = dalloc<SchedDesc>(sched.size(), "schedules");
   d_sched_ent_ = dalloc<uint32_t>(ent.size(), "schedule entries");
   d_sched_split_ = dalloc<int4>(splits.size(), "schedule splits");
   ck(cudaMemcpy(d_desc_, desc.data(), desc_bytes_, cudaMemcpyHostToDevice), "desc");
-  ck(cudaMemcpy(d_level_off_, level_off.data(), level_off.size() * 4, cudaMemcpyHostToDevice), "level_off");
+  ck(cudaMemcpy(d_level_off_, level_off_all.data(), level_off_all.size() * 4, cudaMemcpyHostToDevice), "level_off");
+  ck(cudaMemcpy(d_chunk_, chunk_info.data(), chunk_info.size() * sizeof(int4), cudaMemcpyHostToDevice), "chunks");
   ck(cudaMemcpy(d_sched_, sched.data(), sched.size() * sizeof(SchedDesc), cudaMemcpyHostToDevice), "sched");
   if (!ent.empty()) ck(cudaMemcpy(d_sched_ent_, ent.data(), ent_bytes_, cudaMemcpyHostToDevice), "ent");
   if (!splits.empty())
@@ -613,6 +672,8 @@ void BscEngine::fill_enum_args(void* out, double temperature, bool cands, bool i
   a.stage_ent_bytes = stage_tables_ ? ent_bytes_ : 0;
   a.dfs = d_dfs_;
   a.level_off = d_level_off_;
+  a.chunk = static_cast<const int4*>(d_chunk_);
+  a.n_chunks = n_chunks_;
   a.n_multi = n_multi_;
   a.n_tab = n_tab_;
   a.n_coup = n_coup_;

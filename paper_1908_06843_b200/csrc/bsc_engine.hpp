@@ -139,6 +139,8 @@ class BscEngine {
 
   // template tables
   int n_multi_ = 0, n_tab_ = 0, n_coup_ = 0, n_slots_ = 0, n_out_ = 0;
+  int n_chunks_ = 1;          // BSC table chunks (consecutive roots); n_tab_ / n_coup_ are per chunk maxima
+  void* d_chunk_ = nullptr;   // int4 per chunk {row base, rows, level-1 rows, first root}
   int desc_bytes_ = 0, ent_bytes_ = 0;  // table sizes (16-byte multiples)
   bool stage_tables_ = false;           // staged into shared memory per CTA
   std::vector<uint64_t> dfs_masks_;  // multi-active supports in reference order

@@ -161,13 +161,22 @@ struct SchedDesc {
 // Packed entry (uint32): low 16 bits = source offset / 8; high 16 bits =
 // 0xffff continue, else segment end: bit 15 clear → store acc·scale at
 // offset (bits 0-14)·8 (an output), set → store acc unscaled (a split slot).
+// ACC: outputs accumulate (the moment gather of a chunked table) instead of
+// being overwritten; split slots are always overwritten.
+template <bool ACC = false>
 __device__ __forceinline__ void seg_flush(uint32_t v, double& acc, uint32_t sbase, double scale) {
   const uint32_t hi = v >> 16;
-  const double val = (hi & 0x8000u) ? acc : acc * scale;
+  double val = (hi & 0x8000u) ? acc : acc * scale;
+  const uint32_t addr = sbase + (hi & 0x7fffu) * 8;
+  if (ACC && hi < 0x8000u) {
+    double old;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(old) : "r"(addr) : "memory");
+    val += old;
+  }
   // predicated store (no branch): taken only at a segment end
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t@p st.shared.f64 [%1], %2;\n\t}" ::"r"(hi),
-      "r"(sbase + (hi & 0x7fffu) * 8), "d"(val)
+      "r"(addr), "d"(val)
       : "memory");
   acc = hi != 0xffffu ? 0.0 : acc;
 }
@@ -183,6 +192,7 @@ constexpr int kSchedRuns = 64;
 // this iteration's stores. Safe because a store only ever targets the node
 // (or slot) of a segment that has just ended in this lane, and no later entry
 // of the same schedule reads it.
+template <bool ACC = false>
 __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t* ent,
                                              const int4* __restrict__ split, char* smb, double* spart, double scale,
                                              int lane) {
@@ -202,8 +212,8 @@ __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t
       const double y0 = ent_src(smb, w0), y1 = ent_src(smb, w1);
       a0 += x0;
       a1 += x1;
-      seg_flush(v0, a0, sbase, scale);
-      seg_flush(v1, a1, sbase, scale);
+      seg_flush<ACC>(v0, a0, sbase, scale);
+      seg_flush<ACC>(v1, a1, sbase, scale);
       v0 = w0;
       v1 = w1;
       x0 = y0;
@@ -217,7 +227,8 @@ __device__ __forceinline__ void run_schedule(const SchedDesc& sd, const uint32_t
     if (lane + 32 * u < sd.n_split) {
       double s = 0.0;
       for (int j = sp.y; j < sp.z; ++j) s += spart[j];
-      *reinterpret_cast<double*>(smb + sp.x) = s * scale;
+      double* t = reinterpret_cast<double*>(smb + sp.x);
+      *t = ACC ? *t + s * scale : s * scale;
     }
   }
   __syncwarp();
@@ -244,11 +255,19 @@ struct EnumArgs {
   const uint2* sdesc;
   // shared-memory staging of sdesc / sched_ent per CTA (bytes, 0 = read global)
   int stage_desc_bytes, stage_ent_bytes;
-  const int* dfs;         // [n_tab] index of the state in the reference (DFS) order
-  const int* level_off;   // [gamma + 1]: level k occupies [level_off[k-1], level_off[k])
-  int n_multi, n_tab, n_coup;  // n_tab = hprime + n_multi; n_coup = states of levels 2..γ-1
-  // schedules: sched[0 .. γ−2] the subtree levels γ−1 … 1, sched[γ−1] the
-  // moment gather into souts (n_out = hprime + hprime·(hprime−1)/2 outputs)
+  // The state table is cut into chunks of consecutive roots (the smallest
+  // member of a state): parents and siblings never cross a chunk, so a point's
+  // chunks run one after the other through the same per-warp table region.
+  // chunk[c] = {first row of the chunk in sdesc/dfs, rows, level-1 rows (= its
+  // roots), first root}.
+  const int4* chunk;
+  int n_chunks;
+  const int* dfs;         // [rows] index of the state in the reference (DFS) order
+  const int* level_off;   // [c][gamma + 1]: level k of chunk c is [level_off[k-1], level_off[k]) (chunk rows)
+  int n_multi, n_tab, n_coup;  // n_tab / n_coup: the largest chunk's rows / rows of levels 2..γ-1
+  // schedules: sched[c][0 .. γ−2] the subtree levels γ−1 … 1 of chunk c,
+  // sched[c][γ−1] its part of the moment gather, accumulated into souts
+  // (n_out = hprime + hprime·(hprime−1)/2 outputs)
   const SchedDesc* sched;
   const uint32_t* sched_ent;  // packed entries [rows][kSchedRuns]
   const int4* sched_split;
@@ -261,13 +280,15 @@ struct EnumArgs {
 constexpr int kPoolCap = 64;
 
 struct EnumSmem {
-  // offsets (in doubles) of the per-warp region
+  // offsets (in doubles) of the per-warp region. n_tab / n_coup are the
+  // largest chunk's (see EnumArgs::chunk); the moment outputs persist across
+  // the chunks of a point and get their own region.
   int u, P, tab, coup, part, outs, qs, pool_v, pool_i, cand, total;
   __host__ __device__ static EnumSmem make(int hprime, int n_tab, int n_coup, int n_items, int n_out, int h) {
     EnumSmem s;
     s.u = 0;
     s.P = s.u + hprime;                           // strict upper triangle, row-major
-    s.qs = s.P + hprime * (hprime - 1) / 2 + 1;
+    s.qs = s.P + hprime * (hprime - 1) / 2 + 1;   // level-1 weights of all candidates
     s.cand = s.qs + hprime;                       // uint32 candidates packed 2 per double
     s.tab = s.cand + (hprime + 1) / 2 + 1;
     // the selection pool (values + indices) is dead before the table is filled
@@ -276,13 +297,14 @@ struct EnumSmem {
     int tab_end = s.tab + n_tab + 1;              // tab[n_tab] = 0: padding slot of the lists
     if (tab_end < s.pool_i + kPoolCap / 2 + 1) tab_end = s.pool_i + kPoolCap / 2 + 1;
     s.coup = tab_end;
-    // coup (rel pass), the exp compaction queue (n_tab ints) and the schedule
-    // slots + outputs (moment pass) are live one after the other: they overlay
+    // coup (weight pass), the exp compaction queue (n_tab ints) and the schedule
+    // slots (moment pass) are live one after the other within a chunk: they overlay
     s.part = s.coup;
-    s.outs = s.part + n_items;
+    int region = n_coup;
+    if (region < n_tab / 2 + 1) region = n_tab / 2 + 1;
+    if (region < n_items) region = n_items;
+    s.outs = s.coup + region;
     s.total = s.outs + n_out;
-    if (s.total < s.coup + n_coup) s.total = s.coup + n_coup;
-    if (s.total < s.coup + n_tab / 2 + 1) s.total = s.coup + n_tab / 2 + 1;
     if (s.total < h + 2) s.total = h + 2;  // end-of-kernel CTA reduction reuses the regions
     s.total = (s.total + 1) & ~1;
     return s;
@@ -567,7 +589,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       const uint32_t c = scand[p];
       const double v = a.dlp + a.inv2s * (2.0 * brow[c] - a.gdiag[c]);
       su[p] = v;
-      tab[p] = v;  // level-1 node {p}
     }
     // pairwise terms (strict upper triangle, row-major): the Gram gathers are
     // issued first and land while the singleton terms are computed
@@ -660,94 +681,117 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     const double ub = GM * fmax(umax, 0.0) + 0.5 * GM * (GM - 1) * fmax(pmax, 0.0);
     char* smb = reinterpret_cast<char*>(sm);
     const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
-    if (mult_ok && a.weight_mode == 0 && ub - mx <= 300.0) {
-      mx = fmax(mx, ub);
-    } else {
-    // multi-active states, level by level; table entries hold byte offsets
-    // into this warp's shared region (host-computed, EnumSmem layout)
-    // Four states per lane per iteration, all loads before any store (a
-    // level only reads earlier levels): four independent chains.
-    for (int k = 2; k <= GM; ++k) {
-      const int e = a.level_off[k];
-      const bool keep = k < GM;
-      for (int i0 = a.level_off[k - 1] + lane; i0 < e; i0 += 128) {
-        uint2 d[4];
+    const bool skip_rel = mult_ok && a.weight_mode == 0 && ub - mx <= 300.0;
+
+    // log-joints relative to the zero state of chunk c's multi-active states,
+    // level by level (table entries hold byte offsets into this warp's region):
+    //   coup(S) = coup(sibling) + P[x][z],  rel(S) = rel(parent) + u[z] + coup(S).
+    // Four states per lane per iteration, all loads before any store (a level
+    // only reads earlier levels): four independent chains.
+    auto rel_chunk = [&](int c) -> double {
+      const int4 ci = a.chunk[c];
+      const uint2* cdesc = sdesc + ci.x;
+      const int* lo = a.level_off + c * (GM + 1);
+      const int nl1 = ci.z;
+      for (int l = lane; l < nl1; l += 32) tab[l] = su[ci.w + l];  // level-1 nodes {r}
+      __syncwarp();
+      double m = -INFINITY;
+      for (int k = 2; k <= GM; ++k) {
+        const int e = lo[k];
+        const bool keep = k < GM;
+        for (int i0 = lo[k - 1] + lane; i0 < e; i0 += 128) {
+          uint2 d[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + 32 * u;
-          d[u] = i < e ? sdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
-        }
-        double c[4], r[4];
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u;
+            d[u] = i < e ? cdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
+          }
+          double cc[4], r[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // {parent rel | sibling coup, P[x][z] | u[z]} as offsets / 8
-          c[u] = *reinterpret_cast<const double*>(smb + (d[u].x >> 16) * 8) +
-                 *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
-          r[u] = *reinterpret_cast<const double*>(smb + (d[u].x & 0xffffu) * 8) +
-                 *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) + c[u];
-        }
+          for (int u = 0; u < 4; ++u) {  // {parent rel | sibling coup, P[x][z] | u[z]} as offsets / 8
+            cc[u] = *reinterpret_cast<const double*>(smb + (d[u].x >> 16) * 8) +
+                    *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
+            r[u] = *reinterpret_cast<const double*>(smb + (d[u].x & 0xffffu) * 8) +
+                   *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) + cc[u];
+          }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + 32 * u;
-          if (i < e) {
-            tab[i] = r[u];
-            if (keep) coup[i - HP] = c[u];
-            mx = fmax(mx, r[u]);
+          for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < e) {
+              tab[i] = r[u];
+              if (keep) coup[i - nl1] = cc[u];
+              m = fmax(m, r[u]);
+            }
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
-    }
-    mx = warp_max(mx);
-    if (!isfinite(mx)) {
-      if (lane == 0) atomicOr(a.err, kErrNonFiniteLogJoint);
-      continue;
-    }
+      return m;
+    };
+
+    if (skip_rel) {
+      mx = fmax(mx, ub);
+    } else {
+      for (int c = 0; c < a.n_chunks; ++c) mx = fmax(mx, rel_chunk(c));
+      mx = warp_max(mx);
+      if (!isfinite(mx)) {
+        if (lane == 0) atomicOr(a.err, kErrNonFiniteLogJoint);
+        continue;
+      }
     }
 
     ENUM_PHASE(3);
-    // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286)
-    double z1 = zs1 * exp_nonpos(mxs - mx), zt = 0.0;
-    if (t1) {
-      // q = exp_nonpos(rel − max). Terms below e^-32 of the largest state change no
-      // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
-      // (MUFU.EX2); the others — typically a few dozen — in fp64, compacted.
+    // log-sum-exp at T = 1 (core.cpp:36-45) and q at temperature T (:272-286);
+    // the moment outputs accumulate over the chunks, unnormalised
+    double z1 = zs1 * exp_nonpos(mxs - mx), zt = t1 ? 0.0 : zsT * exp_nonpos((mxs - mx) * a.inv_T);
+    for (int o = lane; o < a.n_out; o += 32) souts[o] = 0.0;  // outputs without states stay 0
+    if (mult_ok) {
+      // Multiplicative posterior weights: with |u| ≤ 300 and (γ−1)·|P| ≤ 300
+      // every factor and partial product stays inside fp64 range, and
+      //   q(S) = q(A) · e^{u_z} · e^{coup(S)},  e^{coup(S)} = e^{coup(sib)} · e^{P_xz},
+      // so a multi-active state costs three multiplications instead of an
+      // exp (a state whose parent underflowed is below e^-145 of the sum).
+      for (int p = lane; p < HP; p += 32) {
+        sqs[p] = exp_nonpos(su[p] - mx);  // level-1 nodes {p}
+        su[p] = exp_nonpos(su[p]);        // |u| ≤ 300: the reduction + two scale factors are exact here too
+      }
+      for (int e = lane; e < npairs; e += 32) sP[e] = exp_nonpos(sP[e]);
+      __syncwarp();
+    }
+    double bv = -1.0;  // running MAP candidate over the chunks (value, reference index)
+    int bi = 0x7fffffff;
+    for (int c = 0; c < a.n_chunks; ++c) {
+      const int4 ci = a.chunk[c];
+      const uint2* cdesc = sdesc + ci.x;
+      const int* lo = a.level_off + c * (GM + 1);
+      const int nl1 = ci.z, ntab = ci.y;
       if (mult_ok) {
-        // Multiplicative posterior weights: with |u| ≤ 300 and (γ−1)·|P| ≤ 300
-        // every factor and partial product stays inside fp64 range, and
-        //   q(S) = q(A) · e^{u_z} · e^{coup(S)},  e^{coup(S)} = e^{coup(sib)} · e^{P_xz},
-        // so a multi-active state costs three multiplications instead of an
-        // exp (a state whose parent underflowed is below e^-145 of the sum).
-        for (int p = lane; p < HP; p += 32) {
-          tab[p] = exp_nonpos(tab[p] - mx);  // level-1 nodes {p}
-          sqs[p] = tab[p];
-          su[p] = exp_nonpos(su[p]);  // |u| ≤ 300: the reduction + two scale factors are exact here too
-        }
-        for (int e = lane; e < npairs; e += 32) sP[e] = exp_nonpos(sP[e]);
+        for (int l = lane; l < nl1; l += 32) tab[l] = sqs[ci.w + l];
         __syncwarp();
         for (int k = 2; k <= GM; ++k) {
-          const int e = a.level_off[k];
+          const int e = lo[k];
           const bool keep = k < GM, first = k == 2;
-          for (int i0 = a.level_off[k - 1] + lane; i0 < e; i0 += 128) {
+          for (int i0 = lo[k - 1] + lane; i0 < e; i0 += 128) {
             uint2 d[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i = i0 + 32 * u;
-              d[u] = i < e ? sdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
+              d[u] = i < e ? cdesc[i] : make_uint2(zero_w | (zero_w << 16), zero_w | (zero_w << 16));
             }
-            double c[4], q[4];
+            double cc[4], q[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const double es = first ? 1.0 : *reinterpret_cast<const double*>(smb + (d[u].x >> 16) * 8);
-              c[u] = es * *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
+              cc[u] = es * *reinterpret_cast<const double*>(smb + (d[u].y & 0xffffu) * 8);
               q[u] = *reinterpret_cast<const double*>(smb + (d[u].x & 0xffffu) * 8) *
-                     *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) * c[u];
+                     *reinterpret_cast<const double*>(smb + (d[u].y >> 16) * 8) * cc[u];
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i = i0 + 32 * u;
               if (i < e) {
                 tab[i] = q[u];
-                if (keep) coup[i - HP] = c[u];
+                if (keep) coup[i - nl1] = cc[u];
                 z1 += q[u];
               }
             }
@@ -755,69 +799,82 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
           __syncwarp();
         }
       } else {
-      int* queue = reinterpret_cast<int*>(coup);  // coup/part/outs are free here
-      int nq = 0;
-      for (int b0 = 0; b0 < a.n_tab; b0 += 128) {
-        double x[4];
-        bool big[4];
+        if (a.n_chunks > 1) rel_chunk(c);  // one chunk: still in place from the max pass
+        if (t1) {
+          // q = exp_nonpos(rel − max). Terms below e^-32 of the largest state change no
+          // fp64 sum they enter (< 2^-46 relative each) and are evaluated in fp32
+          // (MUFU.EX2); the others — typically a few dozen — in fp64, compacted.
+          int* queue = reinterpret_cast<int*>(coup);  // coup/part are free here
+          int nq = 0;
+          for (int b0 = 0; b0 < ntab; b0 += 128) {
+            double x[4];
+            bool big[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = b0 + 32 * u + lane;
-          x[u] = i < a.n_tab ? tab[i] - mx : -INFINITY;
-          big[u] = x[u] >= -32.0;
-        }
+            for (int u = 0; u < 4; ++u) {
+              const int i = b0 + 32 * u + lane;
+              x[u] = i < ntab ? tab[i] - mx : -INFINITY;
+              big[u] = x[u] >= -32.0;
+            }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = b0 + 32 * u + lane;
-          if (i < a.n_tab) tab[i] = big[u] ? x[u] : small_exp(x[u]);
-          const unsigned bm = __ballot_sync(0xffffffffu, big[u]);
-          if (big[u]) queue[nq + __popc(bm & ((1u << lane) - 1u))] = i;
-          nq += __popc(bm);
-        }
-      }
-      __syncwarp();
-      for (int e0 = lane; e0 < nq; e0 += 128) {  // fp64 for the compacted terms, 4 chains
-        int idx[4];
-        double x[4];
+            for (int u = 0; u < 4; ++u) {
+              const int i = b0 + 32 * u + lane;
+              if (i < ntab) tab[i] = big[u] ? x[u] : small_exp(x[u]);
+              const unsigned bm = __ballot_sync(0xffffffffu, big[u]);
+              if (big[u]) queue[nq + __popc(bm & ((1u << lane) - 1u))] = i;
+              nq += __popc(bm);
+            }
+          }
+          __syncwarp();
+          for (int e0 = lane; e0 < nq; e0 += 128) {  // fp64 for the compacted terms, 4 chains
+            int idx[4];
+            double x[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + 32 * u;
-          idx[u] = e < nq ? queue[e] : -1;
-          x[u] = idx[u] >= 0 ? tab[idx[u]] : 0.0;
-        }
+            for (int u = 0; u < 4; ++u) {
+              const int e = e0 + 32 * u;
+              idx[u] = e < nq ? queue[e] : -1;
+              x[u] = idx[u] >= 0 ? tab[idx[u]] : 0.0;
+            }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = exp_nonpos(x[u]);
+            for (int u = 0; u < 4; ++u) x[u] = exp_nonpos(x[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (idx[u] >= 0) tab[idx[u]] = x[u];
-      }
-      __syncwarp();
-      for (int i = lane; i < a.n_tab; i += 32) {
-        const double v = tab[i];
-        if (i >= HP)
-          z1 += v;
-        else
-          sqs[i] = v;
-      }
-      }
-      z1 = warp_sum(z1);
-      zt = z1;
-    } else {
-      zt = zsT * exp_nonpos((mxs - mx) * a.inv_T);
-      for (int i = lane; i < a.n_tab; i += 32) {
-        const double r = tab[i] - mx;
-        const double et = exp_nonpos(r * a.inv_T);
-        tab[i] = et;
-        if (i >= HP) {
-          z1 += exp_nonpos(r);
-          zt += et;
+            for (int u = 0; u < 4; ++u)
+              if (idx[u] >= 0) tab[idx[u]] = x[u];
+          }
+          __syncwarp();
+          for (int i = nl1 + lane; i < ntab; i += 32) z1 += tab[i];
         } else {
-          sqs[i] = et;
+          for (int i = lane; i < ntab; i += 32) {
+            const double r = tab[i] - mx;
+            const double et = exp_nonpos(r * a.inv_T);
+            tab[i] = et;
+            if (i >= nl1) {
+              z1 += exp_nonpos(r);
+              zt += et;
+            }
+          }
         }
+        __syncwarp();
       }
-      z1 = warp_sum(z1);
-      zt = warp_sum(zt);
+      if (a.map_state)  // MAP candidates among this chunk's multi-active states (DFS order index)
+        for (int i = nl1 + lane; i < ntab; i += 32) {
+          const int ri = 1 + H + a.dfs[ci.x + i];
+          if (ranks_before(tab[i], ri, bv, bi)) {
+            bv = tab[i];
+            bi = ri;
+          }
+        }
+      // subtree sums, bottom-up (level γ nodes are leaves): sub(A) = q(A) + Σ
+      // children, one balanced schedule per level; then this chunk's share of
+      // ⟨s_p⟩ and ⟨s_p s_q⟩ as sums of subtree values, accumulated into souts
+      const SchedDesc* sc = a.sched + c * GM;
+      for (int k = 0; k < GM - 1; ++k) run_schedule(sc[k], sent, a.sched_split, smb, spart, 1.0, lane);
+      if (a.n_chunks == 1)  // a single table writes the outputs once
+        run_schedule<false>(sc[GM - 1], sent, a.sched_split, smb, spart, 1.0, lane);
+      else
+        run_schedule<true>(sc[GM - 1], sent, a.sched_split, smb, spart, 1.0, lane);
     }
+    z1 = warp_sum(z1);
+    zt = t1 ? z1 : warp_sum(zt);
     const double lse_rel = mx + log(z1);
     const double base = a.base0 - y2 * a.inv2s;
     const double inv_z = 1.0 / zt;
@@ -827,8 +884,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     __syncwarp();
 
-    // B row and Gram diagonal for the singleton weights of phases 4/6, loaded
-    // now so the loads land during the subtree pass
+    // B row and Gram diagonal for the singleton weights of phases 4/6
     double bb[MAXJ], gg[MAXJ];
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
@@ -842,8 +898,10 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     if (a.map_state) {
       // MAP state (linear_discrete.cpp:314-316: first maximum in reference
       // order: zero, singletons 0..H−1, then multi-active in DFS order)
-      double bv = lane == 0 ? exp(-mx * a.inv_T) : -1.0;
-      int bi = lane == 0 ? 0 : 0x7fffffff;
+      if (lane == 0 && ranks_before(exp(-mx * a.inv_T), 0, bv, bi)) {
+        bv = exp(-mx * a.inv_T);
+        bi = 0;
+      }
 #pragma unroll
       for (int j = 0; j < MAXJ; ++j) {
         const int h = lane + 32 * j;
@@ -851,13 +909,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         if (h < H && ranks_before(q, 1 + h, bv, bi)) {
           bv = q;
           bi = 1 + h;
-        }
-      }
-      for (int i = HP + lane; i < a.n_tab; i += 32) {
-        const int ri = 1 + H + a.dfs[i];
-        if (ranks_before(tab[i], ri, bv, bi)) {
-          bv = tab[i];
-          bi = ri;
         }
       }
 #pragma unroll
@@ -875,13 +926,6 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       }
     }
 
-    ENUM_PHASE(5);
-    // subtree sums, bottom-up (level γ nodes are leaves): sub(A) = q(A) + Σ
-    // children, one balanced schedule per level; then ⟨s_p⟩ and ⟨s_p s_q⟩ as
-    // sums of subtree values (the last schedule, scaled by 1/Z)
-    for (int k = 0; k < GM - 1; ++k) run_schedule(a.sched[k], sent, a.sched_split, smb, spart, 1.0, lane);
-    run_schedule(a.sched[GM - 1], sent, a.sched_split, smb, spart, inv_z, lane);
-
     ENUM_PHASE(6);
     // ---- ⟨s_n⟩ row: singleton mass for every unit; candidates then take their
     // full marginal (linear_discrete.cpp:288-304). Σ_n ⟨s_n⟩ is summed by the
@@ -892,7 +936,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       if (h < H) esrow[h] = single_qj(j) * inv_z;
     }
     __syncwarp();
-    for (int p = lane; p < HP; p += 32) esrow[scand[p]] = souts[p];
+    for (int p = lane; p < HP; p += 32) esrow[scand[p]] = souts[p] * inv_z;
     // candidate pairs (upper triangle: scand ascending ⇒ c_p < c_q)
     for (int o = HP + lane; o < a.n_out; o += 32) {
       // o − HP enumerates (p, q), p < q, row-major
@@ -902,7 +946,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
         ++p;
       }
       const int q = p + 1 + idx;
-      atomicAdd(a.ssT + (long long)scand[p] * H + scand[q], souts[o]);
+      atomicAdd(a.ssT + (long long)scand[p] * H + scand[q], souts[o] * inv_z);
     }
     __syncwarp();
   }
