@@ -884,15 +884,25 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     }
     __syncwarp();
 
-    // B row and Gram diagonal for the singleton weights of phases 4/6
-    double bb[MAXJ], gg[MAXJ];
+    // B row and Gram diagonal for the singleton weights of phases 4/6: held in
+    // registers when they are few (MAXJ ≤ 12), else re-read where used
+    constexpr bool kHold = MAXJ <= 12;
+    constexpr int NB = kHold ? MAXJ : 1;
+    double bb[NB], gg[NB];
+    if (kHold) {
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const int h = lane + 32 * j;
-      bb[j] = h < H ? brow[h] : 0.0;
-      gg[j] = h < H ? a.gdiag[h] : 0.0;
+      for (int j = 0; j < NB; ++j) {
+        const int h = lane + 32 * j;
+        bb[j] = h < H ? brow[h] : 0.0;
+        gg[j] = h < H ? a.gdiag[h] : 0.0;
+      }
     }
-    auto single_qj = [&](int j) { return exp_nonpos((a.dlp + a.inv2s * (2.0 * bb[j] - gg[j]) - mx) * a.inv_T); };
+    auto single_qj = [&](int j) {
+      const int h = lane + 32 * j;
+      const double b = kHold ? bb[kHold ? j : 0] : (h < H ? brow[h] : 0.0);
+      const double g = kHold ? gg[kHold ? j : 0] : (h < H ? a.gdiag[h] : 0.0);
+      return exp_nonpos((a.dlp + a.inv2s * (2.0 * b - g) - mx) * a.inv_T);
+    };
 
     ENUM_PHASE(4);
     if (a.map_state) {
