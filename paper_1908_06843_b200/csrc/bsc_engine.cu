@@ -61,6 +61,8 @@ SolveFn solve_rows_fn(int s, bool fwd) { return fwd ? solve_rows_t<true>(s) : so
 #define GEMM1_CFG 128, 64, 16, 32, 32, true, true, 3
 // GEMM2  Yᵀ·⟨S⟩:      M = Dp, N = Hp, K = points (split-K).
 #define GEMM2_CFG 128, 64, 16, 32, 32, false, true, 3
+// (64-row tiles when Dp is not a multiple of 128: no half-empty last row tile)
+#define GEMM2_CFG64 64, 64, 16, 32, 32, false, true, 4
 // M-step products (C −= A·Bᵀ and C −= A·B).
 // (32×32 tiles: these products are skinny — N = 64 — so small tiles give the CTAs)
 #define SYRK_CFG 32, 32, 16, 16, 16, true, false, 3
@@ -470,7 +472,8 @@ void BscEngine::ensure_work(uint64_t n) {
   cudaDeviceProp prop;
   ck(cudaGetDeviceProperties(&prop, device_), "props");
   // split-K for Yᵀ⟨S⟩: whole waves (2 resident CTAs per SM), never a ragged tail
-  const int tiles = ((Dp_ + 127) / 128) * ((Hp_ + 63) / 64);
+  const int bm = Dp_ % 128 == 0 ? 128 : 64;  // GEMM2 row tile (GEMM2_CFG / GEMM2_CFG64)
+  const int tiles = ((Dp_ + bm - 1) / bm) * ((Hp_ + 63) / 64);
   const int slots = 2 * prop.multiProcessorCount;
   int waves = 1;
   while (waves < 8 && (waves * slots) / tiles < 8) ++waves;  // ≥ 8 splits when the output is small
@@ -799,7 +802,8 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
            "zero partials");
       GemmArgs g{Dp_, Hp_, krows, d_y_ + off * Dp_, Dp_, d_es_ + off * Hp_, Hp_, d_part_, Hp_, 1.0,
                  c == 0 ? 0.0 : 1.0, kchunk, part_stride_, d_warp_es_ + (size_t)c * splits_ * Hp_};
-      ck(launch_dgemm<GEMM2_CFG>(g, splits, s), "gemm Yᵀ·ES");
+      ck(Dp_ % 128 == 0 ? launch_dgemm<GEMM2_CFG>(g, splits, s) : launch_dgemm<GEMM2_CFG64>(g, splits, s),
+         "gemm Yᵀ·ES");
       ++launches_;
     }
     if (c == 0) ev(4);
