@@ -291,9 +291,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            v, kind, dt = cpu_reference_rate(w, args.baseline_sample or n_local, threads)
+            # bounded sample: the whole c2 workload (~5 s on 16 threads), the same
+            # CPU work for the larger dictionaries (cost per point ∝ D·H)
+            sample = args.baseline_sample or min(n_local, max(2000, 200000 * 256 * 300 // (w.D * w.H)))
+            v, kind, dt = cpu_reference_rate(w, sample, threads)
             line["cpu_baseline"] = {"value": v, "unit": "points/s", "cores": threads, "kind": kind,
-                                    "sample": f"{args.baseline_sample or n_local} points of {w.name}, one full EM "
+                                    "sample": f"{sample} points of {w.name}, one full EM "
                                               f"step on all host threads ({dt:.1f} s)"}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
