@@ -54,25 +54,20 @@ int main() {
   cudaStreamCreate(&s);
   GemmArgs g1{M, Np, Kp, y, Kp, w, Np, b, Np, 1.0, 0.0, Kp, 0};
   RUN1("128x64x16 w32x32 s3", 128, 64, 16, 32, 32, true, true, 3);
-  RUN1("128x64x16 w32x32 s4", 128, 64, 16, 32, 32, true, true, 4);
-  RUN1("128x64x32 w32x32 s3", 128, 64, 32, 32, 32, true, true, 3);
-  RUN1("64x64x16 w32x32 s4", 64, 64, 16, 32, 32, true, true, 4);
-  RUN1("128x128x16 w32x64 s3", 128, 128, 16, 32, 64, true, true, 3);
-  RUN1("128x128x16 w64x32 s3", 128, 128, 16, 64, 32, true, true, 3);
-  RUN1("256x64x16 w64x32 s3", 256, 64, 16, 64, 32, true, true, 3);
-  RUN1("128x32x16 w32x32 s4", 128, 32, 16, 32, 32, true, true, 4);
-  RUN1("64x152? n/a -> 64x64x32 s3", 64, 64, 32, 32, 32, true, true, 3);
+  RUN1("128x64x16 w32x32 s2", 128, 64, 16, 32, 32, true, true, 2);
+  RUN1("64x64x16 w32x32 s2", 64, 64, 16, 32, 32, true, true, 2);
+  RUN1("64x64x16 w32x32 s3", 64, 64, 16, 32, 32, true, true, 3);
+  RUN1("64x128x16 w32x32 s3", 64, 128, 16, 32, 32, true, true, 3);
+  RUN1("128x64x16 w64x16 s3", 128, 64, 16, 64, 16, true, true, 3);
+  RUN1("128x64x16 w16x64 s3", 128, 64, 16, 16, 64, true, true, 3);
   const int krows = M;
   int kchunk = (krows + splits - 1) / splits;
   kchunk = (kchunk + 1) & ~1;
   GemmArgs g2{Kp, Np, krows, y, Kp, es, Np, part, Np, 1.0, 0.0, kchunk, (long long)Kp * Np, cs};
   RUN2("128x64x16 w32x32 s3", 128, 64, 16, 32, 32, false, true, 3);
-  RUN2("128x64x16 w32x32 s4", 128, 64, 16, 32, 32, false, true, 4);
-  RUN2("128x64x32 w32x32 s3", 128, 64, 32, 32, 32, false, true, 3);
-  RUN2("64x64x16 w32x32 s4", 64, 64, 16, 32, 32, false, true, 4);
-  RUN2("128x128x16 w32x64 s3", 128, 128, 16, 32, 64, false, true, 3);
-  RUN2("128x128x16 w64x32 s3", 128, 128, 16, 64, 32, false, true, 3);
-  RUN2("256x64x16 w64x32 s3", 256, 64, 16, 64, 32, false, true, 3);
-  RUN2("64x64x32 w32x32 s3", 64, 64, 32, 32, 32, false, true, 3);
+  RUN2("128x64x16 w32x32 s2", 128, 64, 16, 32, 32, false, true, 2);
+  RUN2("64x64x16 w32x32 s3", 64, 64, 16, 32, 32, false, true, 3);
+  RUN2("64x128x16 w32x32 s3", 64, 128, 16, 32, 32, false, true, 3);
+  RUN2("128x64x16 w64x16 s3", 128, 64, 16, 64, 16, false, true, 3);
   return 0;
 }
