@@ -58,8 +58,8 @@ SolveFn solve_rows_fn(int s, bool fwd) { return fwd ? solve_rows_t<true>(s) : so
 
 // Tile configurations (see dgemm.cuh).
 // GEMM1  B = Y·W:     M = points, N = Hp, K = Dp.
-// (tools/gemm_bench.cu sweep at c2 shapes: 64×64×16, 2 stages, 4 warps is the fastest)
-#define GEMM1_CFG 64, 64, 16, 32, 32, true, true, 2
+// (tools/gemm_bench.cu sweep at c2 shapes: 64×32 warp tiles, 2 stages, 4 warps is the fastest)
+#define GEMM1_CFG 128, 64, 16, 64, 32, true, true, 2
 // GEMM2  Yᵀ·⟨S⟩:      M = Dp, N = Hp, K = points (split-K).
 // (64×16 warp tiles: 1.09 ms against 1.13 ms for 32×32 in the sweep)
 #define GEMM2_CFG 128, 64, 16, 64, 16, false, true, 3

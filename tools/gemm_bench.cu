@@ -53,21 +53,24 @@ int main() {
   cudaStream_t s;
   cudaStreamCreate(&s);
   GemmArgs g1{M, Np, Kp, y, Kp, w, Np, b, Np, 1.0, 0.0, Kp, 0};
-  RUN1("128x64x16 w32x32 s3", 128, 64, 16, 32, 32, true, true, 3);
-  RUN1("128x64x16 w32x32 s2", 128, 64, 16, 32, 32, true, true, 2);
   RUN1("64x64x16 w32x32 s2", 64, 64, 16, 32, 32, true, true, 2);
-  RUN1("64x64x16 w32x32 s3", 64, 64, 16, 32, 32, true, true, 3);
-  RUN1("64x128x16 w32x32 s3", 64, 128, 16, 32, 32, true, true, 3);
-  RUN1("128x64x16 w64x16 s3", 128, 64, 16, 64, 16, true, true, 3);
-  RUN1("128x64x16 w16x64 s3", 128, 64, 16, 16, 64, true, true, 3);
+  RUN1("64x64x16 w64x16 s2", 64, 64, 16, 64, 16, true, true, 2);
+  RUN1("64x64x16 w16x64 s2", 64, 64, 16, 16, 64, true, true, 2);
+  RUN1("64x32x16 w32x32 s2", 64, 32, 16, 32, 32, true, true, 2);
+  RUN1("64x32x16 w32x32 s3", 64, 32, 16, 32, 32, true, true, 3);
+  RUN1("32x64x16 w32x32 s3", 32, 64, 16, 32, 32, true, true, 3);
+  RUN1("128x64x16 w64x32 s2", 128, 64, 16, 64, 32, true, true, 2);
+  RUN1("64x64x32 w32x32 s2", 64, 64, 32, 32, 32, true, true, 2);
   const int krows = M;
   int kchunk = (krows + splits - 1) / splits;
   kchunk = (kchunk + 1) & ~1;
   GemmArgs g2{Kp, Np, krows, y, Kp, es, Np, part, Np, 1.0, 0.0, kchunk, (long long)Kp * Np, cs};
-  RUN2("128x64x16 w32x32 s3", 128, 64, 16, 32, 32, false, true, 3);
-  RUN2("128x64x16 w32x32 s2", 128, 64, 16, 32, 32, false, true, 2);
-  RUN2("64x64x16 w32x32 s3", 64, 64, 16, 32, 32, false, true, 3);
-  RUN2("64x128x16 w32x32 s3", 64, 128, 16, 32, 32, false, true, 3);
   RUN2("128x64x16 w64x16 s3", 128, 64, 16, 64, 16, false, true, 3);
+  RUN2("128x64x16 w64x16 s2", 128, 64, 16, 64, 16, false, true, 2);
+  RUN2("128x64x16 w64x32 s3", 128, 64, 16, 64, 32, false, true, 3);
+  RUN2("128x64x16 w128x16 s3", 128, 64, 16, 128, 16, false, true, 3);
+  RUN2("128x32x16 w64x16 s3", 128, 32, 16, 64, 16, false, true, 3);
+  RUN2("64x64x16 w64x16 s3", 64, 64, 16, 64, 16, false, true, 3);
+  RUN2("128x64x32 w64x16 s2", 128, 64, 32, 64, 16, false, true, 2);
   return 0;
 }
