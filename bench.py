@@ -144,7 +144,7 @@ def run_reference(args, w, rank, world):
     line = {
         "impl": "reference", "metric": "BSC truncated-EM data points/sec per iteration", "value": value,
         "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": w.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {**w.describe(), "points_per_step": sample, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": kind,
                          "sample": f"{sample} points of {w.name}, one full EM step per timed step, "
@@ -191,8 +191,15 @@ def main():
     from paper_1908_06843_b200 import BscGpuModel, TruncationConfig, bsc
     from paper_1908_06843_b200 import dist as bdist
 
-    n_local = args.points or w.N
-    # weak scaling: every rank holds its own N-point shard (seeded per rank)
+    # weak scaling (c0–c3): every rank holds its own N-point shard; strong
+    # scaling (c4): the job's N points are sharded as ShardPlan::with_shards
+    # would (parallel.cpp:27-43). Shards are seeded per rank.
+    strong = w.scaling == "strong"
+    if strong:
+        b, e = bdist.shard_range(args.points or w.N, world, rank)
+        n_local = e - b
+    else:
+        n_local = args.points or w.N
     y = configs.data(w, n_local, seed_offset=1000 * rank)
     if world > 1:  # the same initial params on every rank (from rank 0's shard)
         y0 = y if rank == 0 else configs.data(w, n_local, seed_offset=0)
@@ -235,7 +242,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms = ms_total / args.steps
-    n_total = n_local * world
+    n_total = (args.points or w.N) if strong else n_local * world
     value = n_total / (ms / 1e3)
 
     # ---- end to end through the reference-facing C ABI with host buffers
@@ -273,7 +280,7 @@ def main():
     line = {
         "metric": "BSC truncated-EM data points/sec per iteration", "value": value, "unit": "points/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": w.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE.json recipe; random init of the stated architecture)",
         "config": {**w.describe(), "points_per_gpu": n_local, "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (Y 8·N·D = %.0f MB per GPU)" % (8 * n_local * w.D / 1e6)},

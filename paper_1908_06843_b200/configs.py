@@ -30,6 +30,7 @@ class Workload:
     pi_true: float = 0.0
     sigma2_true: float = 0.0
     dict_seed: int = 0
+    scaling: str = "weak"  # "strong": N is the job's total, sharded over the ranks
 
     def describe(self) -> dict:
         return dict(workload=self.name, D=self.D, H=self.H, hprime=self.hprime, gamma=self.gamma, N=self.N,
@@ -44,7 +45,7 @@ CONFIGS = {
     "c3": Workload("c3_random_D576_H1000", 576, 1000, 14, 5, 1_000_000, 10, 3, "random", pi_true=8 / 1000,
                    sigma2_true=0.25, dict_seed=3),
     "c4": Workload("c4_strong_D576_H1000_N4M", 576, 1000, 14, 5, 4_000_000, 10, 4, "random", pi_true=8 / 1000,
-                   sigma2_true=0.25, dict_seed=3),
+                   sigma2_true=0.25, dict_seed=3, scaling="strong"),
 }
 
 
