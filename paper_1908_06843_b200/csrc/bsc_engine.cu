@@ -10,6 +10,7 @@
 #include <unordered_map>
 
 #include "bsc_kernels.cuh"
+#include "lane_kernels.cuh"
 #include "dgemm.cuh"
 #include "mstep_kernels.cuh"
 #include "engine_util.hpp"
@@ -37,6 +38,28 @@ const void* enum_fn_t(int maxj) {
   }
 }
 const void* enum_fn(int maxj, bool staged) { return staged ? enum_fn_t<true>(maxj) : enum_fn_t<false>(maxj); }
+
+// the lane path's launches of enumerate_kernel: front half (unstaged, no state
+// tables) and the fallback over the points the front half marked
+template <int PASS, bool STAGED>
+const void* enum_pass_fn_t(int maxj) {
+  switch (maxj) {
+    case 1: return (const void*)enumerate_kernel<1, STAGED, PASS>;
+    case 2: return (const void*)enumerate_kernel<2, STAGED, PASS>;
+    case 4: return (const void*)enumerate_kernel<4, STAGED, PASS>;
+    case 6: return (const void*)enumerate_kernel<6, STAGED, PASS>;
+    case 8: return (const void*)enumerate_kernel<8, STAGED, PASS>;
+    case 10: return (const void*)enumerate_kernel<10, STAGED, PASS>;
+    case 12: return (const void*)enumerate_kernel<12, STAGED, PASS>;
+    case 16: return (const void*)enumerate_kernel<16, STAGED, PASS>;
+    case 24: return (const void*)enumerate_kernel<24, STAGED, PASS>;
+    default: return (const void*)enumerate_kernel<32, STAGED, PASS>;
+  }
+}
+const void* front_fn(int maxj) { return enum_pass_fn_t<kPassFront, false>(maxj); }
+const void* fallback_fn(int maxj, bool staged) {
+  return staged ? enum_pass_fn_t<kPassFallback, true>(maxj) : enum_pass_fn_t<kPassFallback, false>(maxj);
+}
 
 using SolveFn = void (*)(const double*, int, int, double*, int, int, int);
 template <bool FWD>
@@ -143,6 +166,9 @@ void BscEngine::init(int device) {
   // posterior-weight path (tests and A/B runs): 0 auto, 1 multiplicative after the
   // exact maximum, 2 exp per state
   if (const char* e = std::getenv("BSC_WEIGHT_MODE")) weight_mode_ = std::atoi(e);
+  // lane-per-point state pass (lane_kernels.cuh) for the shapes it is built for
+  lane_ok_ = !vpath() && gamma_ >= 2 && gamma_ <= 6 && hprime_ >= 2 && hprime_ <= 16;
+  if (const char* e = std::getenv("BSC_LANE")) lane_ok_ = lane_ok_ && e[0] != '0';
 
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
@@ -181,7 +207,7 @@ BscEngine::~BscEngine() {
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
-                  (void*)d_vpart_, (void*)d_u_, d_chunk_})
+                  (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -458,7 +484,8 @@ void BscEngine::build_template() {
 void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
   for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
-                  (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_})
+                  (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_rec_,
+                  (void*)d_lout_, (void*)d_pmode_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
   d_y_ = dalloc<double>(rows * Dp_, "Y");
@@ -521,8 +548,33 @@ void BscEngine::ensure_work(uint64_t n) {
   const uint64_t need = (n + warps - 1) / warps;
   enum_ctas_ = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(enum_ctas_, need)));
   enum_warps_total_ = enum_ctas_ * warps;
+  sc_ctas_ = enum_ctas_;
+  if (lane_ok_) {
+    // front half: no state tables, occupancy from its registers
+    front_smem_ = 8 * 8 * EnumSmem::make(hprime_, 0, 0, 0, 0, static_cast<int>(H_)).total;
+    const void* ff = front_fn(maxj);
+    ck(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem_), "front smem attr");
+    int fs = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs, ff, 256, front_smem_), "occupancy");
+    front_ctas_ = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)std::max(fs, 1) * prop.multiProcessorCount, (n + 7) / 8)));
+    const void* fb = fallback_fn(maxj, stage_tables_);
+    ck(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "fallback smem attr");
+    lane_smem_ = lane_smem_bytes(static_cast<int>(hprime_), static_cast<int>(gamma_));
+    ck(cudaFuncSetAttribute(lane_fn(gamma_, hprime_), cudaFuncAttributeMaxDynamicSharedMemorySize, lane_smem_),
+       "lane smem attr");
+    int fz = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fz, (const void*)lane_finish_kernel, 256, 0), "occupancy");
+    fin_ctas_ = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)std::max(fz, 1) * prop.multiProcessorCount, (n + 7) / 8)));
+    sc_ctas_ = std::max({enum_ctas_, front_ctas_, fin_ctas_});
+    const uint64_t tiles = (n + 31) / 32;
+    d_rec_ = dalloc<double>(tiles * 32 * lane_rec_fields(static_cast<int>(hprime_)), "lane records");
+    d_lout_ = dalloc<double>(tiles * 32 * lane_out_fields(static_cast<int>(hprime_)), "lane moments");
+    d_pmode_ = dalloc<int>(tiles * 32, "point modes");
+  }
   d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
-  d_warp_sc_ = dalloc<double>((size_t)enum_ctas_ * 2, "cta_scalars");
+  d_warp_sc_ = dalloc<double>((size_t)3 * sc_ctas_ * 2, "cta_scalars");
   colsum_chunks_ = 1;
   if (vpath()) {
     dfree(d_vpart_);
@@ -708,12 +760,51 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   fill_enum_args(&a, temperature, cands, infer, off, rows, chunk, log_p0);
   a.log_pi = log_p1;
   a.dlp = log_p1 - log_p0;
-  a.warp_scalars = d_warp_sc_ + (size_t)chunk * enum_ctas_ * 2;
+  // scalar partial regions of this chunk (see estep_chunked)
+  double* sc_front = d_warp_sc_ + ((size_t)0 * sc_chunks_ + chunk) * sc_ctas_ * 2;
+  double* sc_fin = d_warp_sc_ + ((size_t)1 * sc_chunks_ + chunk) * sc_ctas_ * 2;
+  double* sc_fb = d_warp_sc_ + ((size_t)2 * sc_chunks_ + chunk) * sc_ctas_ * 2;
+  a.warp_scalars = sc_front;
   const int maxj = maxj_for(H_);
   void* args[] = {&a};
-  ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s), "enumerate launch");
-  ck(cudaGetLastError(), "enumerate");
-  ++launches_;
+  const bool lane = lane_ok_ && !infer && temperature == 1.0 && weight_mode_ != 2;
+  if (!lane) {
+    ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s),
+       "enumerate launch");
+    ck(cudaGetLastError(), "enumerate");
+    ++launches_;
+    return;
+  }
+  // lane path: front half → lane-per-point states → fallback points → finish
+  a.rec = d_rec_;
+  a.pmode = d_pmode_;
+  a.cand_out = d_cand_ + off * hprime_;
+  ck(cudaLaunchKernel(front_fn(maxj), dim3(front_ctas_), dim3(256), args, front_smem_, s), "front launch");
+  LaneArgs la{static_cast<int>(rows), static_cast<int>(hprime_), d_rec_, d_lout_, d_pmode_};
+  void* largs[] = {&la};
+  ck(cudaLaunchKernel(lane_fn(gamma_, hprime_), dim3(static_cast<unsigned>((rows + 31) / 32)), dim3(32), largs, lane_smem_, s),
+     "lane states launch");
+  a.warp_scalars = sc_fb;
+  ck(cudaLaunchKernel(fallback_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s),
+     "fallback launch");
+  FinishArgs fa{};
+  fa.N = static_cast<int>(rows);
+  fa.H = H_;
+  fa.Hp = Hp_;
+  fa.hp = hprime_;
+  fa.rec = d_rec_;
+  fa.out = d_lout_;
+  fa.pmode = d_pmode_;
+  fa.cand = d_cand_ + off * hprime_;
+  fa.y2 = d_y2_ + off;
+  fa.ES = d_es_ + off * Hp_;
+  fa.ssT = d_stats_ + lay_.off_ssT();
+  fa.cta_scalars = sc_fin;
+  fa.base0 = a.base0;
+  fa.inv2s = a.inv2s;
+  lane_finish_kernel<<<fin_ctas_, 256, 0, s>>>(fa);
+  ck(cudaGetLastError(), "lane path");
+  launches_ += 4;
 }
 
 void BscEngine::estep(double temperature, bool want_candidates) {
@@ -747,7 +838,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     dfree(d_warp_es_);
     dfree(d_warp_sc_);
     d_warp_es_ = dalloc<double>((size_t)nchunks * splits_ * Hp_, "split-K column sums");
-    d_warp_sc_ = dalloc<double>((size_t)nchunks * enum_ctas_ * 2, "cta scalars");
+    d_warp_sc_ = dalloc<double>((size_t)3 * nchunks * sc_ctas_ * 2, "cta scalars");
     colsum_chunks_ = nchunks;
   }
   if (vpath() && nchunks > vpart_chunks_) {
@@ -762,6 +853,9 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
   ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
   ck(cudaMemsetAsync(d_warp_es_, 0, (size_t)nchunks * splits_ * Hp_ * 8, s), "zero colsums");
+  // per-CTA scalar partials: [role: whole/front pass, lane finish, fallback][chunk][sc_ctas_]
+  ck(cudaMemsetAsync(d_warp_sc_, 0, (size_t)3 * nchunks * sc_ctas_ * 2 * 8, s), "zero cta scalars");
+  sc_chunks_ = nchunks;
   auto cs = static_cast<cudaStream_t>(copy_stream_);
   if (host_y) {
     ck(cudaEventRecord(static_cast<cudaEvent_t>(chunk_ev_[kMaxChunks]), s), "event");
@@ -819,7 +913,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     launches_ += 2;
   } else {
     finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
-        nchunks * enum_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
+        3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
     counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
     launches_ += 3;
   }

@@ -34,6 +34,9 @@ struct StatsLayout {
 // Linear discrete families (LinearDiscreteModel, linear_discrete.hpp:31-87).
 enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
 
+// The lane-per-point state pass for (γ, H') (lane_engine.cu).
+const void* lane_fn(int gamma, int hprime);
+
 // The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
 const void* ldv_kernel_fn(int maxj, bool staged);
 
@@ -184,6 +187,12 @@ class BscEngine {
   bool timing_ = false;
   bool prof_on_ = false;
   int weight_mode_ = 0;
+  // lane-per-point state pass (lane_kernels.cuh)
+  bool lane_ok_ = false;
+  int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
+  int sc_ctas_ = 0, sc_chunks_ = 1;  // per-CTA scalar partial regions
+  double *d_rec_ = nullptr, *d_lout_ = nullptr;
+  int* d_pmode_ = nullptr;
   void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;

@@ -18,6 +18,10 @@ namespace bscgpu {
 
 constexpr int kMaxHprime = 64;  // candidate positions fit a uint64 mask
 
+// lane path (lane_kernels.cuh): record tile fields per point and point modes
+__host__ __device__ inline int lane_rec_fields(int hp) { return 4 + 2 * hp + hp * (hp - 1); }
+enum : int { kModeDone = 0, kModeShift = 1, kModeMax = 2, kModeFallback = 3 };
+
 // Error flags raised by device code (bit set in *err).
 enum : int { kErrNonFiniteScore = 1, kErrNonFiniteLogJoint = 2 };
 
@@ -273,6 +277,9 @@ struct EnumArgs {
   const int4* sched_split;
   int n_slots, n_out;
   int weight_mode;  // 0 auto, 1 multiplicative after the exact maximum, 2 exp per state
+  // lane path (lane_kernels.cuh): deferred-point records and per-point modes
+  double* rec;
+  int* pmode;
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
 };
@@ -422,16 +429,23 @@ __device__ __forceinline__ void top_k(const double (&f)[MAXJ], uint32_t removed,
   }
 }
 
+// Launch roles of enumerate_kernel: the whole per-point pass; the front half
+// of the lane path (selection + terms; points passing the multiplicative range
+// guard are deferred to lane_kernels.cuh, the rest marked for the fallback);
+// the whole pass over the points marked for the fallback only.
+enum : int { kPassFull = 0, kPassFront = 1, kPassFallback = 2 };
+
 // STAGED: the state descriptors and schedule entries are staged in shared
 // memory (compile-time, so every table access is an LDS, not a generic load)
-template <int MAXJ, bool STAGED>
+template <int MAXJ, bool STAGED, int PASS = kPassFull>
 __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   extern __shared__ __align__(16) double esm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
+  const EnumSmem L = PASS == kPassFront ? EnumSmem::make(a.hprime, 0, 0, 0, 0, a.H)
+                                         : EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
   // The state descriptors and schedule entries are the same for every point:
   // staged once per CTA in shared memory when they fit (else read from L1/L2).
   const uint2* sdesc = a.sdesc;
@@ -477,6 +491,12 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   }
 
   for (int n = gwarp; n < a.N; n += nwarps) {
+    if constexpr (PASS == kPassFallback) {
+      if (a.pmode[n] != kModeFallback) continue;
+    }
+    if constexpr (PASS == kPassFront) {
+      if (lane == 0) a.pmode[n] = kModeDone;  // stays so on an error (flagged in *err)
+    }
     ENUM_PHASE(7);
     const double* y = a.Y + (long long)n * a.Dp;
     const double* brow = a.B + (long long)n * a.Hp;
@@ -615,7 +635,8 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       }
       sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[p + 1 + idx]];
     }
-    if (lane == 0) tab[a.n_tab] = 0.0;  // zero slot (the selection pool overlays the table)
+    // zero slot (the selection pool overlays the table); the front pass has no table
+    if (PASS != kPassFront && lane == 0) tab[a.n_tab] = 0.0;
 
     ENUM_PHASE(2);
     // singletons over all H units and the zero state (rel = 0)
@@ -659,6 +680,13 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     pmax = warp_max(pmax);
     pabs = warp_max(pabs);
     const bool t1 = a.inv_T == 1.0;
+    // q(S) = q(A)·e^{u_z}·e^{coup(S)} keeps every factor and partial product in
+    // fp64 range when |u| ≤ 300 and (γ−1)|P| ≤ 300 (phase 3)
+    const bool mult_ok = t1 && a.weight_mode != 2 && uabs <= 300.0 && (GM - 1) * pabs <= 300.0;
+    // the multiplicative pass needs no maximum: any shift ≥ max rel works, and
+    // an upper bound within e^300 of the true maximum loses nothing to underflow
+    const double ub = GM * fmax(umax, 0.0) + 0.5 * GM * (GM - 1) * fmax(pmax, 0.0);
+    const bool skip_rel = mult_ok && a.weight_mode == 0 && ub - mx <= 300.0;
     // singleton weights, summed relative to the singleton maximum; rel1 dies
     // here (the MAP and moment passes recompute single_q from B) so the state
     // passes below run with MAXJ more registers of ILP
@@ -666,22 +694,47 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     double* esrow = a.ES + (long long)n * a.Hp;
     double zs1 = lane == 0 ? exp_nonpos(-mxs) : 0.0;
     double zsT = lane == 0 && !t1 ? exp_nonpos(-mxs * a.inv_T) : 0.0;
+    const bool defer = PASS == kPassFront && mult_ok;
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const double x = rel1[j] - mxs;  // −inf beyond H: exp_nonpos gives 0
-      zs1 += exp_nonpos(x);
+      const double e = exp_nonpos(x);
+      zs1 += e;
       if (!t1) zsT += exp_nonpos(x * a.inv_T);
+      // deferred points: the unnormalised singleton weights (lane_finish_kernel scales them)
+      if (PASS == kPassFront && defer && lane + 32 * j < H) esrow[lane + 32 * j] = e;
     }
     if (t1) zsT = zs1;
-    // q(S) = q(A)·e^{u_z}·e^{coup(S)} keeps every factor and partial product in
-    // fp64 range when |u| ≤ 300 and (γ−1)|P| ≤ 300 (phase 3)
-    const bool mult_ok = t1 && a.weight_mode != 2 && uabs <= 300.0 && (GM - 1) * pabs <= 300.0;
-    // the multiplicative pass needs no maximum: any shift ≥ max rel works, and
-    // an upper bound within e^300 of the true maximum loses nothing to underflow
-    const double ub = GM * fmax(umax, 0.0) + 0.5 * GM * (GM - 1) * fmax(pmax, 0.0);
+    if constexpr (PASS == kPassFront) {
+      if (defer) {
+        // record of the point for lane_states_kernel (layout: lane_kernels.cuh)
+        const int np = HP * (HP - 1) / 2;
+        double* rt = a.rec + (long long)(n >> 5) * lane_rec_fields(HP) * 32 + (n & 31);
+        zs1 = warp_sum(zs1);
+        if (lane == 0) {
+          rt[0] = fmax(mxs, ub);
+          rt[32] = zs1;
+          rt[64] = mxs;
+        }
+        for (int p = lane; p < HP; p += 32) {
+          const double u = su[p];
+          rt[(4 + p) * 32] = u;
+          rt[(4 + HP + p) * 32] = exp_nonpos(u);  // |u| ≤ 300: exact range of exp_nonpos
+        }
+        for (int e = lane; e < np; e += 32) {
+          const double v = sP[e];
+          rt[(4 + 2 * HP + e) * 32] = v;
+          rt[(4 + 2 * HP + np + e) * 32] = exp_nonpos(v);
+        }
+      }
+      if (lane == 0) {
+        a.pmode[n] = defer ? (skip_rel ? kModeShift : kModeMax) : kModeFallback;
+        y2_acc += y2;
+      }
+      continue;
+    }
     char* smb = reinterpret_cast<char*>(sm);
     const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
-    const bool skip_rel = mult_ok && a.weight_mode == 0 && ub - mx <= 300.0;
 
     // log-joints relative to the zero state of chunk c's multi-active states,
     // level by level (table entries hold byte offsets into this warp's region):
@@ -880,7 +933,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     const double inv_z = 1.0 / zt;
     if (lane == 0) {
       lse_acc += base + lse_rel;
-      y2_acc += y2;
+      if (PASS == kPassFull) y2_acc += y2;  // the fallback's points: counted by the front pass
     }
     __syncwarp();
 

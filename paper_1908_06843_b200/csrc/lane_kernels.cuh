@@ -1,0 +1,490 @@
+// Lane-per-point state pass of the BSC E-step (sm_100a).
+//
+// Reference: the per-state loop of LinearDiscreteModel::estep_impl
+// (linear_discrete.cpp:256-303) — log-joint, posterior q, ⟨s⟩ and ⟨s sᵀ⟩ over
+// the multi-active states of truncation.cpp:95-169 — for the points whose
+// log-joint terms pass the range guard of the multiplicative weights (the
+// common case; the rest keep the warp-per-point path of bsc_kernels.cuh).
+//
+// Split of the work (one E-step chunk):
+//   front   enumerate_kernel<…, kPassFront>: warp per point — scores, exact
+//           top-H', unary/pairwise terms u, P, singleton weights. A point that
+//           passes the guard is *deferred*: its u, e^u, P, e^P and scalars go to
+//           a record tile, its ⟨s⟩ row gets the unnormalised singleton weights.
+//           Anything else is marked for the fallback launch (kPassFallback).
+//   states  lane_states_kernel<γ>: one LANE per deferred point, 32 points per
+//           warp walking the same depth-first state tree in lockstep, so every
+//           index, loop bound and table offset is warp-uniform and all that is
+//           left per state is the arithmetic: q(A∪{z}) = q(A)·e^{u_z}·c(A,z),
+//           c(A∪{z},w) = c(A,w)·e^{P_zw}, subtree sums, and the moment updates.
+//           Per-point arrays live in shared memory as [slot][32 lanes] (one
+//           conflict-free 256-byte row per slot).
+//   finish  lane_finish_kernel: warp per point — log Z, the ⟨s⟩ row (scaled
+//           singletons, candidate marginals) and the candidate-pair RED.ADDs.
+//
+// Moments by subtree sums (post-order): sub(A) = q(A) + Σ_children sub(child);
+// ⟨s_p⟩ = Σ_{A: max A = p} sub(A), ⟨s_p s_q⟩ = Σ_{A: max A = q, p∈A} sub(A).
+// The depth-first order is the reference's prefix-first pattern order
+// (truncation.cpp:116-147), so the tree is exactly its state set.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "bsc_kernels.cuh"
+
+namespace bscgpu {
+
+// Record tile (per 32 consecutive points of a chunk), doubles [field][32]
+// (lane_rec_fields, bsc_kernels.cuh):
+//   0 shift (mode 1)   1 zs1 (zero + singleton weights relative to mxs)   2 mxs
+//   3 pad   4.. u[H']   .. e^u[H']   .. P[np]   .. e^P[np]      (np = H'(H'−1)/2)
+// Output tile: 0 shift   1 Σ multi-active weights   2.. M[nm]  (nm = H'(H'+1)/2,
+// upper triangle with diagonal, row-major: ⟨s_p⟩ on the diagonal)
+__host__ __device__ inline int lane_out_fields(int hp) { return 2 + hp * (hp + 1) / 2; }
+// shared memory per warp of lane_states_kernel<GM>
+__host__ __device__ inline int lane_smem_bytes(int hp, int gm) {
+  const int np = hp * (hp - 1) / 2, nm = hp * (hp + 1) / 2;
+  return (hp + np + (gm > 2 ? gm - 2 : 0) * hp + nm) * 256;
+}
+
+// point modes (EnumArgs::pmode): kModeDone / kModeShift (shift = the bound
+// in the record) / kModeMax (shift = exact maximum, computed here) /
+// kModeFallback (bsc_kernels.cuh)
+
+struct LaneArgs {
+  int N, hp;
+  const double* rec;
+  double* out;
+  const int* pmode;
+};
+
+// per-lane shared arrays: element i of the calling lane's array at byte offset i·256
+__device__ __forceinline__ double lds_(const char* p, int i) { return *reinterpret_cast<const double*>(p + i * 256); }
+__device__ __forceinline__ void sts_(char* p, int i, double v) { *reinterpret_cast<double*>(p + i * 256) = v; }
+
+// strict upper triangle (p < q): pidx = prow(p) + q;  with diagonal (p ≤ q): tri = mrow(p) + q
+__device__ __forceinline__ int prow_(int p, int hp) { return p * (2 * hp - p - 1) / 2 - p - 1; }
+__device__ __forceinline__ int mrow_(int p, int hp) { return p * (2 * hp - p + 1) / 2 - p; }
+
+// Weight pass below node A (|A| = K, max x, weight qA, members path[0..K)):
+// returns Σ_children sub(child) and adds every descendant's subtree sum into
+// the moment array M. c(A, w) is e^P row x for K = 1, else cv level K−2.
+template <int K, int GM>
+__device__ __forceinline__ double wnode(const char* eu, const char* eP, char* cv, char* M, int hp, double qA, int x,
+                                        int (&path)[8]) {
+  double ch = 0.0;
+  int mrow[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) mrow[i] = mrow_(path[i], hp);
+  const int px = prow_(x, hp);
+  if constexpr (K + 1 < GM) {
+    for (int z = x + 1; z < hp; ++z) {
+      const double c = K == 1 ? lds_(eP, px + z) : lds_(cv, (K - 2) * hp + z);
+      const double qz = qA * lds_(eu, z) * c;
+      const int pz = prow_(z, hp);
+      for (int w = z + 1; w < hp; ++w) {
+        const double cw = K == 1 ? lds_(eP, px + w) : lds_(cv, (K - 2) * hp + w);
+        sts_(cv, (K - 1) * hp + w, cw * lds_(eP, pz + w));
+      }
+      path[K] = z;
+      const double s = qz + wnode<K + 1, GM>(eu, eP, cv, M, hp, qz, z, path);
+      const int zz = mrow_(z, hp) + z;
+      double m[K + 1];
+      m[K] = lds_(M, zz);
+#pragma unroll
+      for (int i = 0; i < K; ++i) m[i] = lds_(M, mrow[i] + z);
+      sts_(M, zz, m[K] + s);
+#pragma unroll
+      for (int i = 0; i < K; ++i) sts_(M, mrow[i] + z, m[i] + s);
+      ch += s;
+    }
+  } else {
+    // leaves, two per iteration (their moment entries are distinct)
+    int z = x + 1;
+    for (; z + 1 < hp; z += 2) {
+      const double c0 = K == 1 ? lds_(eP, px + z) : lds_(cv, (K - 2) * hp + z);
+      const double c1 = K == 1 ? lds_(eP, px + z + 1) : lds_(cv, (K - 2) * hp + z + 1);
+      const double e0 = lds_(eu, z), e1 = lds_(eu, z + 1);
+      const int zz0 = mrow_(z, hp) + z, zz1 = mrow_(z + 1, hp) + z + 1;
+      double m0[K + 1], m1[K + 1];
+      m0[K] = lds_(M, zz0);
+      m1[K] = lds_(M, zz1);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        m0[i] = lds_(M, mrow[i] + z);
+        m1[i] = lds_(M, mrow[i] + z + 1);
+      }
+      const double s0 = qA * e0 * c0, s1 = qA * e1 * c1;
+      sts_(M, zz0, m0[K] + s0);
+      sts_(M, zz1, m1[K] + s1);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        sts_(M, mrow[i] + z, m0[i] + s0);
+        sts_(M, mrow[i] + z + 1, m1[i] + s1);
+      }
+      ch += s0 + s1;
+    }
+    if (z < hp) {
+      const double c0 = K == 1 ? lds_(eP, px + z) : lds_(cv, (K - 2) * hp + z);
+      const double s0 = qA * lds_(eu, z) * c0;
+      const int zz0 = mrow_(z, hp) + z;
+      sts_(M, zz0, lds_(M, zz0) + s0);
+#pragma unroll
+      for (int i = 0; i < K; ++i) sts_(M, mrow[i] + z, lds_(M, mrow[i] + z) + s0);
+      ch += s0;
+    }
+  }
+  return ch;
+}
+
+// Maximum log-joint (relative to the zero state) below node A: the additive
+// twin of wnode (rel(A∪{z}) = rel(A) + u_z + Σ_{a∈A} P_az), for the points
+// whose cheap upper bound was too loose to use as the shift (mode 2).
+template <int K, int GM>
+__device__ __forceinline__ double mnode(const char* U, const char* P, char* cv, int hp, double relA, int x) {
+  double m = -INFINITY;
+  const int px = prow_(x, hp);
+  for (int z = x + 1; z < hp; ++z) {
+    const double c = K == 1 ? lds_(P, px + z) : lds_(cv, (K - 2) * hp + z);
+    const double rz = relA + lds_(U, z) + c;
+    m = fmax(m, rz);
+    if constexpr (K + 1 < GM) {
+      const int pz = prow_(z, hp);
+      for (int w = z + 1; w < hp; ++w) {
+        const double cw = K == 1 ? lds_(P, px + w) : lds_(cv, (K - 2) * hp + w);
+        sts_(cv, (K - 1) * hp + w, cw + lds_(P, pz + w));
+      }
+      m = fmax(m, mnode<K + 1, GM>(U, P, cv, hp, rz, z));
+    }
+  }
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// Compile-time shapes (the BASELINE workloads' H', γ): the same tree walk with
+// every slot offset below the leaf-parent level a constant. Children lists of
+// a node are dispatched on its maximum x (a uniform switch), so the leaf loop
+// and the coupling-row build run fully unrolled with immediate shared-memory
+// offsets, their loads batched ahead of their stores (the targets of one batch
+// are distinct by construction).
+template <int HP, int GM>
+struct LaneShape {
+  static constexpr int NP = HP * (HP - 1) / 2, NM = HP * (HP + 1) / 2;
+  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + NP, O_M = O_CV + (GM > 2 ? GM - 2 : 0) * HP;
+  __host__ __device__ static constexpr int pidx(int p, int q) { return p * (2 * HP - p - 1) / 2 + (q - p - 1); }
+  __host__ __device__ static constexpr int tri(int p, int q) { return p * (2 * HP - p + 1) / 2 + (q - p); }
+};
+
+// lane-private slot i of the per-warp [slot][32] arrays (S = base + lane)
+#define LS(i) S[(i) * 32]
+
+// Leaves below node B (|B| = GM−1, max X): q(B∪{z}) = qB·e^{u_z}·c(B,z) for
+// z > X; each leaf adds its weight to M[z][z], M[X][z] and M[a][z] for the
+// other members a (runtime rows orow). c(B,·) = e^P row X when |B| = 1, else
+// coupling level GM−3. Returns Σ leaves.
+template <int HP, int GM, int X>
+__device__ __forceinline__ double leaf_block(double* S, double qB, const int* orow) {
+  using F = LaneShape<HP, GM>;
+  constexpr int NO = GM - 2 > 0 ? GM - 2 : 1;
+  double ch = 0.0;
+#pragma unroll
+  for (int z0 = X + 1; z0 < HP; z0 += 4) {
+    double c[4], e[4], md[4], mx[4], mo[NO][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int z = z0 + j;
+      if (z < HP) {
+        c[j] = GM == 2 ? LS(F::O_EP + F::pidx(X, z)) : LS(F::O_CV + (GM - 3) * HP + z);
+        e[j] = LS(F::O_EU + z);
+        md[j] = LS(F::O_M + F::tri(z, z));
+        mx[j] = LS(F::O_M + F::tri(X, z));
+#pragma unroll
+        for (int i = 0; i < GM - 2; ++i) mo[i][j] = LS(F::O_M + orow[i] + z);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int z = z0 + j;
+      if (z < HP) {
+        const double sv = qB * e[j] * c[j];
+        LS(F::O_M + F::tri(z, z)) = md[j] + sv;
+        LS(F::O_M + F::tri(X, z)) = mx[j] + sv;
+#pragma unroll
+        for (int i = 0; i < GM - 2; ++i) LS(F::O_M + orow[i] + z) = mo[i][j] + sv;
+        ch += sv;
+      }
+    }
+  }
+  return ch;
+}
+
+// Coupling row of child A∪{Z} (node A at depth K): cv[K−1][w] = c(A,w)·e^{P_Zw},
+// w > Z; c(A,·) = e^P row x (runtime, xrow) for K = 1, else cv[K−2].
+template <int HP, int GM, int K, int Z>
+__device__ __forceinline__ void cv_block(double* S, int xrow) {
+  using F = LaneShape<HP, GM>;
+  constexpr int NW = HP - 1 - Z > 0 ? HP - 1 - Z : 1;
+  double v[NW];
+#pragma unroll
+  for (int w = Z + 1; w < HP; ++w) {
+    const double cw = K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w);
+    v[w - Z - 1] = cw * LS(F::O_EP + F::pidx(Z, w));
+  }
+#pragma unroll
+  for (int w = Z + 1; w < HP; ++w) LS(F::O_CV + (K - 1) * HP + w) = v[w - Z - 1];
+}
+
+#define LANE_CASES(M_)                                                                                      \
+  M_(0) M_(1) M_(2) M_(3) M_(4) M_(5) M_(6) M_(7) M_(8) M_(9) M_(10) M_(11) M_(12) M_(13) M_(14) M_(15)
+
+template <int HP, int GM>
+__device__ __forceinline__ double leaf_dispatch(int x, double* S, double qB, const int* orow) {
+  double r = 0.0;
+  switch (x) {
+#define LANE_LEAF_CASE(v)                                                   \
+  case v:                                                                   \
+    if constexpr (v < HP - 1) r = leaf_block<HP, GM, (v < HP - 1 ? v : 0)>(S, qB, orow); \
+    break;
+    LANE_CASES(LANE_LEAF_CASE)
+#undef LANE_LEAF_CASE
+    default:
+      break;
+  }
+  return r;
+}
+
+template <int HP, int GM, int K>
+__device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
+  switch (z) {
+#define LANE_CV_CASE(v)                                                       \
+  case v:                                                                     \
+    if constexpr (v < HP - 1) cv_block<HP, GM, K, (v < HP - 1 ? v : 0)>(S, xrow); \
+    break;
+    LANE_CASES(LANE_CV_CASE)
+#undef LANE_CV_CASE
+    default:
+      break;
+  }
+}
+
+// Child A∪{Z} of a node A at depth K = GM−2 (a leaf parent), taken when Z > x:
+// its weight, coupling row, leaf block and moment entries (constant offsets
+// except the rows of A's members); then the next Z.
+template <int HP, int GM, int K, int Z>
+__device__ __forceinline__ void deep_child(double* S, double qA, int x, int xrow, const int* orow, const int* lrow,
+                                           double& ch) {
+  using F = LaneShape<HP, GM>;
+  if (Z > x) {
+    const double c = K == 1 ? S[(xrow + Z) * 32] : S[(F::O_CV + (K - 2) * HP + Z) * 32];
+    const double qz = qA * S[(F::O_EU + Z) * 32] * c;
+    double s = qz;
+    if constexpr (Z < HP - 1) {
+      cv_block<HP, GM, K, Z>(S, xrow);
+      s += leaf_block<HP, GM, Z>(S, qz, lrow);
+    }
+    constexpr int zz = F::O_M + F::tri(Z, Z);
+    double m[K + 1];
+    m[K] = S[zz * 32];
+#pragma unroll
+    for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + Z) * 32];
+    S[zz * 32] = m[K] + s;
+#pragma unroll
+    for (int i = 0; i < K; ++i) S[(orow[i] + Z) * 32] = m[i] + s;
+    ch += s;
+  }
+  if constexpr (Z + 1 < HP) deep_child<HP, GM, K, Z + 1>(S, qA, x, xrow, orow, lrow, ch);
+}
+
+// Node A (|A| = K ≤ GM−2, max x, weight qA, members path[0..K)): walks its
+// children, returns Σ_children sub(child). At the deepest such level
+// (K = GM−2: the children are leaf parents) the child loop is unrolled over
+// the child's maximum Z under a uniform predicate Z > x, so its coupling-row
+// build, its leaf block and its own moment entries all have constant offsets;
+// above it the loop runs over z at run time and dispatches the row build.
+template <int HP, int GM, int K>
+__device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)[8]) {
+  using F = LaneShape<HP, GM>;
+  int orow[K + 1];
+#pragma unroll
+  for (int i = 0; i < K; ++i) orow[i] = F::O_M + mrow_(path[i], HP);
+  const int xrow = F::O_EP + prow_(x, HP);
+  double ch = 0.0;
+  if constexpr (K == GM - 2) {
+    int lrow[K + 1];  // members' rows relative to O_M, for leaf_block
+#pragma unroll
+    for (int i = 0; i < K; ++i) lrow[i] = orow[i] - F::O_M;
+    deep_child<HP, GM, K, K>(S, qA, x, xrow, orow, lrow, ch);
+  } else {
+    for (int z = x + 1; z < HP; ++z) {
+      const double c = K == 1 ? S[(xrow + z) * 32] : S[(F::O_CV + (K - 2) * HP + z) * 32];
+      const double qz = qA * S[(F::O_EU + z) * 32] * c;
+      cv_dispatch<HP, GM, K>(z, S, xrow);
+      path[K] = z;
+      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, qz, z, path);
+      const int zz = F::O_M + mrow_(z, HP) + z;
+      double m[K + 1];
+      m[K] = S[zz * 32];
+#pragma unroll
+      for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
+      S[zz * 32] = m[K] + s;
+#pragma unroll
+      for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + s;
+      ch += s;
+    }
+  }
+  return ch;
+}
+
+// Root loop of the compile-time walk: Σ multi-active weights, M filled.
+template <int HP, int GM>
+__device__ __forceinline__ double fixed_walk(double* S, const double* ru, double shift, bool live) {
+  using F = LaneShape<HP, GM>;
+  int path[8];
+  double zm = 0.0;
+  double ur[HP];
+#pragma unroll
+  for (int r = 0; r < HP; ++r) ur[r] = live ? ru[r * 32] : 0.0;
+#pragma unroll 1
+  for (int r = 0; r < HP; ++r) {
+    double u = ur[0];
+#pragma unroll
+    for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
+    const double qr = live ? exp_nonpos(u - shift) : 0.0;
+    path[0] = r;
+    double ch;
+    if constexpr (GM == 2) {
+      ch = leaf_dispatch<HP, GM>(r, S, qr, path);
+    } else {
+      ch = fnode<HP, GM, 1>(S, qr, r, path);
+    }
+    const int rr = F::O_M + mrow_(r, HP) + r;
+    S[rr * 32] += qr + ch;
+    zm += ch;
+  }
+  return zm;
+}
+#undef LS
+
+// One warp per CTA, one tile of 32 consecutive points of the chunk; lane l
+// owns point 32·tile + l. HPF = 0: H' at run time (wnode), else the
+// compile-time walk for H' = HPF.
+template <int GM, int HPF>
+__global__ void __launch_bounds__(32) lane_states_kernel(LaneArgs a) {
+  extern __shared__ __align__(16) double lsm[];
+  const int lane = threadIdx.x;
+  const int hp = HPF ? HPF : a.hp, np = hp * (hp - 1) / 2, nm = hp * (hp + 1) / 2;
+  const long long tile = blockIdx.x;
+  const long long n = tile * 32 + lane;
+  const int mode = n < a.N ? a.pmode[n] : kModeDone;
+  const bool live = mode == kModeShift || mode == kModeMax;
+  if (!__any_sync(0xffffffffu, live)) return;
+  char* base = reinterpret_cast<char*>(lsm) + lane * 8;
+  char* eu = base;
+  char* eP = eu + hp * 256;
+  char* cv = eP + np * 256;
+  char* M = cv + (GM > 2 ? GM - 2 : 0) * hp * 256;
+  const double* rt = a.rec + tile * lane_rec_fields(hp) * 32 + lane;
+  const int fu = 4, feu = 4 + hp, fP = 4 + 2 * hp, feP = 4 + 2 * hp + np;
+  int path[8];
+
+  double shift = live ? rt[0] : 0.0;
+  if (__any_sync(0xffffffffu, mode == kModeMax)) {
+    // exact maximum over the multi-active states (u staged in the M region)
+    for (int p = 0; p < hp; ++p) sts_(M, p, live ? rt[(fu + p) * 32] : 0.0);
+    for (int e = 0; e < np; ++e) sts_(eP, e, live ? rt[(fP + e) * 32] : 0.0);
+    double m = -INFINITY;
+    for (int r = 0; r < hp; ++r) {
+      const double ur = lds_(M, r);
+      m = fmax(m, fmax(ur, mnode<1, GM>(M, eP, cv, hp, ur, r)));
+    }
+    if (mode == kModeMax) shift = fmax(rt[2 * 32], m);
+  }
+  for (int p = 0; p < hp; ++p) sts_(eu, p, live ? rt[(feu + p) * 32] : 0.0);
+  for (int e = 0; e < np; ++e) sts_(eP, e, live ? rt[(feP + e) * 32] : 0.0);
+  for (int i = 0; i < nm; ++i) sts_(M, i, 0.0);
+  double zm = 0.0;
+  if constexpr (HPF > 0) {
+    zm = fixed_walk<HPF, GM>(lsm + lane, rt + fu * 32, shift, live);
+  } else {
+    for (int r = 0; r < hp; ++r) {
+      const double qr = live ? exp_nonpos(rt[(fu + r) * 32] - shift) : 0.0;
+      path[0] = r;
+      const double ch = wnode<1, GM>(eu, eP, cv, M, hp, qr, r, path);
+      const int rr = mrow_(r, hp) + r;
+      sts_(M, rr, lds_(M, rr) + qr + ch);
+      zm += ch;
+    }
+  }
+  if (live) {
+    double* ot = a.out + tile * lane_out_fields(hp) * 32 + lane;
+    ot[0] = shift;
+    ot[32] = zm;
+    for (int i = 0; i < nm; ++i) ot[(2 + i) * 32] = lds_(M, i);
+  }
+}
+
+struct FinishArgs {
+  int N, H, Hp, hp;
+  const double* rec;
+  const double* out;
+  const int* pmode;
+  const uint32_t* cand;  // N × hp, ascending
+  const double* y2;
+  double* ES;
+  double* ssT;
+  double* cta_scalars;  // [gridDim.x][2] Σ log Z_n (deferred points), 0
+  double base0, inv2s;
+};
+
+// Warp per deferred point: log Z = base + shift + log(zs1·e^{mxs−shift} + Σ_multi q)
+// (core.cpp:36-45 at T = 1), the ⟨s_n⟩ row and the candidate pairs of Σ⟨ssᵀ⟩.
+static __global__ void __launch_bounds__(256) lane_finish_kernel(FinishArgs a) {
+  __shared__ double red[16];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int hp = a.hp, nm = hp * (hp + 1) / 2;
+  double lse_acc = 0.0;
+  for (int n = blockIdx.x * (blockDim.x >> 5) + wib; n < a.N; n += nwarps) {
+    const int mode = a.pmode[n];
+    if (mode != kModeShift && mode != kModeMax) continue;
+    const long long tile = n >> 5;
+    const double* rt = a.rec + tile * lane_rec_fields(hp) * 32 + (n & 31);
+    const double* ot = a.out + tile * lane_out_fields(hp) * 32 + (n & 31);
+    const double shift = ot[0], zm = ot[32];
+    const double zs1 = rt[32], mxs = rt[64];
+    const double es = exp_nonpos(mxs - shift);
+    const double z1 = zs1 * es + zm;
+    const double inv_z = 1.0 / z1;
+    if (lane == 0) lse_acc += (a.base0 - a.y2[n] * a.inv2s) + (shift + log(z1));
+    const double scale = es * inv_z;
+    double* esrow = a.ES + (long long)n * a.Hp;
+    for (int h = lane; h < a.H; h += 32) esrow[h] *= scale;
+    __syncwarp();
+    const uint32_t* cn = a.cand + (long long)n * hp;
+    // (p, q) of the moment entries this lane finishes: entries lane, lane+32, …
+    for (int o = lane; o < nm; o += 32) {
+      int idx = o, p = 0;
+      while (idx >= hp - p) {
+        idx -= hp - p;
+        ++p;
+      }
+      const int q = p + idx;
+      const double v = ot[(2 + o) * 32] * inv_z;
+      if (q == p)
+        esrow[cn[p]] = v;
+      else
+        atomicAdd(a.ssT + (long long)cn[p] * a.H + cn[q], v);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) red[wib] = lse_acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) l += red[w];
+    a.cta_scalars[2 * blockIdx.x] = l;
+    a.cta_scalars[2 * blockIdx.x + 1] = 0.0;
+  }
+}
+
+}  // namespace bscgpu
