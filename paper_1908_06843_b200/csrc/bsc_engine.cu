@@ -560,7 +560,7 @@ void BscEngine::ensure_work(uint64_t n) {
         1, std::min<uint64_t>((uint64_t)std::max(fs, 1) * prop.multiProcessorCount, (n + 7) / 8)));
     const void* fb = fallback_fn(maxj, stage_tables_);
     ck(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "fallback smem attr");
-    lane_smem_ = lane_smem_bytes(static_cast<int>(hprime_), static_cast<int>(gamma_));
+    lane_smem_ = lane_smem(static_cast<int>(gamma_), static_cast<int>(hprime_));
     ck(cudaFuncSetAttribute(lane_fn(gamma_, hprime_), cudaFuncAttributeMaxDynamicSharedMemorySize, lane_smem_),
        "lane smem attr");
     int fz = 0;

@@ -36,6 +36,7 @@ enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
 
 // The lane-per-point state pass for (γ, H') (lane_engine.cu).
 const void* lane_fn(int gamma, int hprime);
+int lane_smem(int gamma, int hprime);  // its dynamic shared memory per warp (bytes)
 
 // The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
 const void* ldv_kernel_fn(int maxj, bool staged);

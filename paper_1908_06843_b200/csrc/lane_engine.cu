@@ -8,16 +8,23 @@
 namespace bscgpu {
 
 const void* lane_fn(int gamma, int hprime) {
-  if (gamma == 4 && hprime == 10) return (const void*)lane_states_kernel<4, 10>;
-  if (gamma == 4 && hprime == 12) return (const void*)lane_states_kernel<4, 12>;
-  if (gamma == 5 && hprime == 14) return (const void*)lane_states_kernel<5, 14>;
+  if (gamma == 4 && hprime == 10) return (const void*)lane_states_fixed_kernel<4, 10>;
+  if (gamma == 4 && hprime == 12) return (const void*)lane_states_fixed_kernel<4, 12>;
+  if (gamma == 5 && hprime == 14) return (const void*)lane_states_fixed_kernel<5, 14>;
   switch (gamma) {
-    case 2: return (const void*)lane_states_kernel<2, 0>;
-    case 3: return (const void*)lane_states_kernel<3, 0>;
-    case 4: return (const void*)lane_states_kernel<4, 0>;
-    case 5: return (const void*)lane_states_kernel<5, 0>;
-    default: return (const void*)lane_states_kernel<6, 0>;
+    case 2: return (const void*)lane_states_kernel<2>;
+    case 3: return (const void*)lane_states_kernel<3>;
+    case 4: return (const void*)lane_states_kernel<4>;
+    case 5: return (const void*)lane_states_kernel<5>;
+    default: return (const void*)lane_states_kernel<6>;
   }
+}
+
+int lane_smem(int gamma, int hprime) {
+  if (gamma == 4 && hprime == 10) return LaneShape<10, 4>::SLOTS * 256;
+  if (gamma == 4 && hprime == 12) return LaneShape<12, 4>::SLOTS * 256;
+  if (gamma == 5 && hprime == 14) return LaneShape<14, 5>::SLOTS * 256;
+  return lane_smem_bytes(hprime, gamma);
 }
 
 }  // namespace bscgpu

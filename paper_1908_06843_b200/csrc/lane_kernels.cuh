@@ -161,16 +161,27 @@ __device__ __forceinline__ double mnode(const char* U, const char* P, char* cv, 
 }
 
 // ---------------------------------------------------------------------------
-// Compile-time shapes (the BASELINE workloads' H', γ): the same tree walk with
-// every slot offset below the leaf-parent level a constant. Children lists of
-// a node are dispatched on its maximum x (a uniform switch), so the leaf loop
-// and the coupling-row build run fully unrolled with immediate shared-memory
-// offsets, their loads batched ahead of their stores (the targets of one batch
-// are distinct by construction).
+// Compile-time shapes (the BASELINE workloads' H', γ ≥ 3): the same tree walk,
+// restructured so the deepest level runs out of registers with constant
+// shared-memory offsets.
+//
+// Node A at depth K = γ−2 (its children are the leaf parents), max x, members
+// a_1..a_K: with ce[w] = e^{u_w}·c(A,w) (a register vector, w > x)
+//   child  B = A∪{Z}:   q_B = q_A·ce[Z]
+//   leaf   B∪{w}, w>Z:  q = q_B·ce[w]·e^{P_Zw}
+// Every descendant of A contains all of A's members, so its contribution to
+// M[a_i][z] is the same for each i, and equals its contribution to M[z][z]
+// (z its maximum): one register accumulator R[z] per column collects them and
+// is flushed once per A into M[z][z] and the K member rows. Only the leaf-
+// parent row M[Z][w] is updated per leaf — at a constant offset. Levels above
+// run over z at run time (coupling rows built by a dispatched unrolled block).
 template <int HP, int GM>
 struct LaneShape {
+  static_assert(GM >= 3, "compile-time walk needs gamma >= 3");
   static constexpr int NP = HP * (HP - 1) / 2, NM = HP * (HP + 1) / 2;
-  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + NP, O_M = O_CV + (GM > 2 ? GM - 2 : 0) * HP;
+  static constexpr int CV_LEVELS = GM - 3;  // coupling rows of depths 2 .. γ−2
+  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + NP, O_M = O_CV + CV_LEVELS * HP;
+  static constexpr int SLOTS = O_M + NM;
   __host__ __device__ static constexpr int pidx(int p, int q) { return p * (2 * HP - p - 1) / 2 + (q - p - 1); }
   __host__ __device__ static constexpr int tri(int p, int q) { return p * (2 * HP - p + 1) / 2 + (q - p); }
 };
@@ -178,48 +189,8 @@ struct LaneShape {
 // lane-private slot i of the per-warp [slot][32] arrays (S = base + lane)
 #define LS(i) S[(i) * 32]
 
-// Leaves below node B (|B| = GM−1, max X): q(B∪{z}) = qB·e^{u_z}·c(B,z) for
-// z > X; each leaf adds its weight to M[z][z], M[X][z] and M[a][z] for the
-// other members a (runtime rows orow). c(B,·) = e^P row X when |B| = 1, else
-// coupling level GM−3. Returns Σ leaves.
-template <int HP, int GM, int X>
-__device__ __forceinline__ double leaf_block(double* S, double qB, const int* orow) {
-  using F = LaneShape<HP, GM>;
-  constexpr int NO = GM - 2 > 0 ? GM - 2 : 1;
-  double ch = 0.0;
-#pragma unroll
-  for (int z0 = X + 1; z0 < HP; z0 += 4) {
-    double c[4], e[4], md[4], mx[4], mo[NO][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int z = z0 + j;
-      if (z < HP) {
-        c[j] = GM == 2 ? LS(F::O_EP + F::pidx(X, z)) : LS(F::O_CV + (GM - 3) * HP + z);
-        e[j] = LS(F::O_EU + z);
-        md[j] = LS(F::O_M + F::tri(z, z));
-        mx[j] = LS(F::O_M + F::tri(X, z));
-#pragma unroll
-        for (int i = 0; i < GM - 2; ++i) mo[i][j] = LS(F::O_M + orow[i] + z);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int z = z0 + j;
-      if (z < HP) {
-        const double sv = qB * e[j] * c[j];
-        LS(F::O_M + F::tri(z, z)) = md[j] + sv;
-        LS(F::O_M + F::tri(X, z)) = mx[j] + sv;
-#pragma unroll
-        for (int i = 0; i < GM - 2; ++i) LS(F::O_M + orow[i] + z) = mo[i][j] + sv;
-        ch += sv;
-      }
-    }
-  }
-  return ch;
-}
-
-// Coupling row of child A∪{Z} (node A at depth K): cv[K−1][w] = c(A,w)·e^{P_Zw},
-// w > Z; c(A,·) = e^P row x (runtime, xrow) for K = 1, else cv[K−2].
+// Coupling row of child A∪{Z} (node A at depth K < γ−2): cv[K−1][w] =
+// c(A,w)·e^{P_Zw}, w > Z; c(A,·) = e^P row x (runtime, xrow) for K = 1, else cv[K−2].
 template <int HP, int GM, int K, int Z>
 __device__ __forceinline__ void cv_block(double* S, int xrow) {
   using F = LaneShape<HP, GM>;
@@ -237,22 +208,6 @@ __device__ __forceinline__ void cv_block(double* S, int xrow) {
 #define LANE_CASES(M_)                                                                                      \
   M_(0) M_(1) M_(2) M_(3) M_(4) M_(5) M_(6) M_(7) M_(8) M_(9) M_(10) M_(11) M_(12) M_(13) M_(14) M_(15)
 
-template <int HP, int GM>
-__device__ __forceinline__ double leaf_dispatch(int x, double* S, double qB, const int* orow) {
-  double r = 0.0;
-  switch (x) {
-#define LANE_LEAF_CASE(v)                                                   \
-  case v:                                                                   \
-    if constexpr (v < HP - 1) r = leaf_block<HP, GM, (v < HP - 1 ? v : 0)>(S, qB, orow); \
-    break;
-    LANE_CASES(LANE_LEAF_CASE)
-#undef LANE_LEAF_CASE
-    default:
-      break;
-  }
-  return r;
-}
-
 template <int HP, int GM, int K>
 __device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
   switch (z) {
@@ -267,40 +222,39 @@ __device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
   }
 }
 
-// Child A∪{Z} of a node A at depth K = GM−2 (a leaf parent), taken when Z > x:
-// its weight, coupling row, leaf block and moment entries (constant offsets
-// except the rows of A's members); then the next Z.
-template <int HP, int GM, int K, int Z>
-__device__ __forceinline__ void deep_child(double* S, double qA, int x, int xrow, const int* orow, const int* lrow,
+// Child A∪{Z} of the deepest node A (taken when Z > x) and its leaves.
+template <int HP, int GM, int Z>
+__device__ __forceinline__ void deep_child(double* S, double qA, int x, const double (&ce)[HP], double (&R)[HP],
                                            double& ch) {
   using F = LaneShape<HP, GM>;
   if (Z > x) {
-    const double c = K == 1 ? S[(xrow + Z) * 32] : S[(F::O_CV + (K - 2) * HP + Z) * 32];
-    const double qz = qA * S[(F::O_EU + Z) * 32] * c;
+    const double qz = qA * ce[Z];
     double s = qz;
     if constexpr (Z < HP - 1) {
-      cv_block<HP, GM, K, Z>(S, xrow);
-      s += leaf_block<HP, GM, Z>(S, qz, lrow);
+      constexpr int NW = HP - 1 - Z;
+      double q[NW], m[NW];
+#pragma unroll
+      for (int j = 0; j < NW; ++j) {
+        const int w = Z + 1 + j;
+        q[j] = qz * ce[w] * LS(F::O_EP + F::pidx(Z, w));
+        m[j] = LS(F::O_M + F::tri(Z, w));
+      }
+#pragma unroll
+      for (int j = 0; j < NW; ++j) {
+        const int w = Z + 1 + j;
+        LS(F::O_M + F::tri(Z, w)) = m[j] + q[j];
+        R[w] += q[j];
+        s += q[j];
+      }
     }
-    constexpr int zz = F::O_M + F::tri(Z, Z);
-    double m[K + 1];
-    m[K] = S[zz * 32];
-#pragma unroll
-    for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + Z) * 32];
-    S[zz * 32] = m[K] + s;
-#pragma unroll
-    for (int i = 0; i < K; ++i) S[(orow[i] + Z) * 32] = m[i] + s;
+    R[Z] += s;
     ch += s;
   }
-  if constexpr (Z + 1 < HP) deep_child<HP, GM, K, Z + 1>(S, qA, x, xrow, orow, lrow, ch);
+  if constexpr (Z + 1 < HP) deep_child<HP, GM, Z + 1>(S, qA, x, ce, R, ch);
 }
 
-// Node A (|A| = K ≤ GM−2, max x, weight qA, members path[0..K)): walks its
-// children, returns Σ_children sub(child). At the deepest such level
-// (K = GM−2: the children are leaf parents) the child loop is unrolled over
-// the child's maximum Z under a uniform predicate Z > x, so its coupling-row
-// build, its leaf block and its own moment entries all have constant offsets;
-// above it the loop runs over z at run time and dispatches the row build.
+// Node A (|A| = K ≤ γ−2, max x, weight qA, members path[0..K)): walks its
+// children, returns Σ_children sub(child).
 template <int HP, int GM, int K>
 __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)[8]) {
   using F = LaneShape<HP, GM>;
@@ -310,10 +264,30 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
   const int xrow = F::O_EP + prow_(x, HP);
   double ch = 0.0;
   if constexpr (K == GM - 2) {
-    int lrow[K + 1];  // members' rows relative to O_M, for leaf_block
+    double ce[HP], R[HP];
 #pragma unroll
-    for (int i = 0; i < K; ++i) lrow[i] = orow[i] - F::O_M;
-    deep_child<HP, GM, K, K>(S, qA, x, xrow, orow, lrow, ch);
+    for (int w = 0; w < HP; ++w) {
+      R[w] = 0.0;
+      ce[w] = 0.0;
+      if (w > x) {
+        const double c = K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w);
+        ce[w] = LS(F::O_EU + w) * c;
+      }
+    }
+    deep_child<HP, GM, (K < HP ? K : 0)>(S, qA, x, ce, R, ch);
+    // flush the column accumulators: M[z][z] and the members' rows
+#pragma unroll
+    for (int z = 0; z < HP; ++z) {
+      if (z > x) {
+        double m[K + 1];
+        m[K] = LS(F::O_M + F::tri(z, z));
+#pragma unroll
+        for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
+        LS(F::O_M + F::tri(z, z)) = m[K] + R[z];
+#pragma unroll
+        for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + R[z];
+      }
+    }
   } else {
     for (int z = x + 1; z < HP; ++z) {
       const double c = K == 1 ? S[(xrow + z) * 32] : S[(F::O_CV + (K - 2) * HP + z) * 32];
@@ -334,45 +308,15 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
   }
   return ch;
 }
-
-// Root loop of the compile-time walk: Σ multi-active weights, M filled.
-template <int HP, int GM>
-__device__ __forceinline__ double fixed_walk(double* S, const double* ru, double shift, bool live) {
-  using F = LaneShape<HP, GM>;
-  int path[8];
-  double zm = 0.0;
-  double ur[HP];
-#pragma unroll
-  for (int r = 0; r < HP; ++r) ur[r] = live ? ru[r * 32] : 0.0;
-#pragma unroll 1
-  for (int r = 0; r < HP; ++r) {
-    double u = ur[0];
-#pragma unroll
-    for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
-    const double qr = live ? exp_nonpos(u - shift) : 0.0;
-    path[0] = r;
-    double ch;
-    if constexpr (GM == 2) {
-      ch = leaf_dispatch<HP, GM>(r, S, qr, path);
-    } else {
-      ch = fnode<HP, GM, 1>(S, qr, r, path);
-    }
-    const int rr = F::O_M + mrow_(r, HP) + r;
-    S[rr * 32] += qr + ch;
-    zm += ch;
-  }
-  return zm;
-}
 #undef LS
 
 // One warp per CTA, one tile of 32 consecutive points of the chunk; lane l
-// owns point 32·tile + l. HPF = 0: H' at run time (wnode), else the
-// compile-time walk for H' = HPF.
-template <int GM, int HPF>
+// owns point 32·tile + l. Run-time H' (generic tree walk, wnode).
+template <int GM>
 __global__ void __launch_bounds__(32) lane_states_kernel(LaneArgs a) {
   extern __shared__ __align__(16) double lsm[];
   const int lane = threadIdx.x;
-  const int hp = HPF ? HPF : a.hp, np = hp * (hp - 1) / 2, nm = hp * (hp + 1) / 2;
+  const int hp = a.hp, np = hp * (hp - 1) / 2, nm = hp * (hp + 1) / 2;
   const long long tile = blockIdx.x;
   const long long n = tile * 32 + lane;
   const int mode = n < a.N ? a.pmode[n] : kModeDone;
@@ -403,23 +347,80 @@ __global__ void __launch_bounds__(32) lane_states_kernel(LaneArgs a) {
   for (int e = 0; e < np; ++e) sts_(eP, e, live ? rt[(feP + e) * 32] : 0.0);
   for (int i = 0; i < nm; ++i) sts_(M, i, 0.0);
   double zm = 0.0;
-  if constexpr (HPF > 0) {
-    zm = fixed_walk<HPF, GM>(lsm + lane, rt + fu * 32, shift, live);
-  } else {
-    for (int r = 0; r < hp; ++r) {
-      const double qr = live ? exp_nonpos(rt[(fu + r) * 32] - shift) : 0.0;
-      path[0] = r;
-      const double ch = wnode<1, GM>(eu, eP, cv, M, hp, qr, r, path);
-      const int rr = mrow_(r, hp) + r;
-      sts_(M, rr, lds_(M, rr) + qr + ch);
-      zm += ch;
-    }
+  for (int r = 0; r < hp; ++r) {
+    const double qr = live ? exp_nonpos(rt[(fu + r) * 32] - shift) : 0.0;
+    path[0] = r;
+    const double ch = wnode<1, GM>(eu, eP, cv, M, hp, qr, r, path);
+    const int rr = mrow_(r, hp) + r;
+    sts_(M, rr, lds_(M, rr) + qr + ch);
+    zm += ch;
   }
   if (live) {
     double* ot = a.out + tile * lane_out_fields(hp) * 32 + lane;
     ot[0] = shift;
     ot[32] = zm;
     for (int i = 0; i < nm; ++i) ot[(2 + i) * 32] = lds_(M, i);
+  }
+}
+
+// The compile-time walk for H' = HP, γ = GM (layout LaneShape<HP, GM>).
+template <int GM, int HP>
+__global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
+  using F = LaneShape<HP, GM>;
+  extern __shared__ __align__(16) double lsm[];
+  const int lane = threadIdx.x;
+  const long long tile = blockIdx.x;
+  const long long n = tile * 32 + lane;
+  const int mode = n < a.N ? a.pmode[n] : kModeDone;
+  const bool live = mode == kModeShift || mode == kModeMax;
+  if (!__any_sync(0xffffffffu, live)) return;
+  double* S = lsm + lane;
+  char* base = reinterpret_cast<char*>(lsm) + lane * 8;
+  const double* rt = a.rec + tile * lane_rec_fields(HP) * 32 + lane;
+  constexpr int fu = 4, feu = 4 + HP, fP = 4 + 2 * HP, feP = 4 + 2 * HP + F::NP;
+
+  double ur[HP];
+#pragma unroll
+  for (int r = 0; r < HP; ++r) ur[r] = live ? rt[(fu + r) * 32] : 0.0;
+  double shift = live ? rt[0] : 0.0;
+  if (__any_sync(0xffffffffu, mode == kModeMax)) {
+    // exact maximum: u and the coupling sums staged in the M region
+    char* U = base + F::O_M * 256;
+    char* cvm = U + HP * 256;
+    char* eP = base + F::O_EP * 256;
+#pragma unroll
+    for (int p = 0; p < HP; ++p) sts_(U, p, ur[p]);
+    for (int e = 0; e < F::NP; ++e) sts_(eP, e, live ? rt[(fP + e) * 32] : 0.0);
+    double m = -INFINITY;
+    for (int r = 0; r < HP; ++r) {
+      const double u = lds_(U, r);
+      m = fmax(m, fmax(u, mnode<1, GM>(U, eP, cvm, HP, u, r)));
+    }
+    if (mode == kModeMax) shift = fmax(rt[2 * 32], m);
+  }
+#pragma unroll
+  for (int p = 0; p < HP; ++p) S[(F::O_EU + p) * 32] = live ? rt[(feu + p) * 32] : 0.0;
+  for (int e = 0; e < F::NP; ++e) S[(F::O_EP + e) * 32] = live ? rt[(feP + e) * 32] : 0.0;
+  for (int i = 0; i < F::NM; ++i) S[(F::O_M + i) * 32] = 0.0;
+  int path[8];
+  double zm = 0.0;
+#pragma unroll 1
+  for (int r = 0; r < HP; ++r) {
+    double u = ur[0];
+#pragma unroll
+    for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
+    const double qr = live ? exp_nonpos(u - shift) : 0.0;
+    path[0] = r;
+    const double ch = fnode<HP, GM, 1>(S, qr, r, path);
+    const int rr = F::O_M + mrow_(r, HP) + r;
+    S[rr * 32] += qr + ch;
+    zm += ch;
+  }
+  if (live) {
+    double* ot = a.out + tile * lane_out_fields(HP) * 32 + lane;
+    ot[0] = shift;
+    ot[32] = zm;
+    for (int i = 0; i < F::NM; ++i) ot[(2 + i) * 32] = S[(F::O_M + i) * 32];
   }
 }
 
