@@ -551,7 +551,12 @@ void BscEngine::ensure_work(uint64_t n) {
   sc_ctas_ = enum_ctas_;
   if (lane_ok_) {
     // front half: no state tables, occupancy from its registers
-    front_smem_ = 8 * 8 * EnumSmem::make(hprime_, 0, 0, 0, 0, static_cast<int>(H_)).total;
+    {  // per warp: its region (+ two B-row buffers when two CTAs still fit); per CTA: diag(G)
+      const int tot = EnumSmem::make(hprime_, 0, 0, 0, 0, static_cast<int>(H_)).total;
+      const int gst = 8 * ((static_cast<int>(H_) + 1) & ~1);
+      front_stage_b_ = maxj <= 16 && 8 * 8 * (tot + 2 * Hp_) + gst <= (227 * 1024) / 2 - 1024;
+      front_smem_ = 8 * 8 * (tot + (front_stage_b_ ? 2 * Hp_ : 0)) + gst;
+    }
     const void* ff = front_fn(maxj);
     ck(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem_), "front smem attr");
     int fs = 0;
@@ -778,6 +783,7 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   // lane path: front half → lane-per-point states → fallback points → finish
   a.rec = d_rec_;
   a.pmode = d_pmode_;
+  a.stage_b = front_stage_b_ ? 1 : 0;
   a.cand_out = d_cand_ + off * hprime_;
   ck(cudaLaunchKernel(front_fn(maxj), dim3(front_ctas_), dim3(256), args, front_smem_, s), "front launch");
   LaneArgs la{static_cast<int>(rows), static_cast<int>(hprime_), d_rec_, d_lout_, d_pmode_};

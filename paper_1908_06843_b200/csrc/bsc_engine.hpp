@@ -189,7 +189,7 @@ class BscEngine {
   bool prof_on_ = false;
   int weight_mode_ = 0;
   // lane-per-point state pass (lane_kernels.cuh)
-  bool lane_ok_ = false;
+  bool lane_ok_ = false, front_stage_b_ = false;
   int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
   int sc_ctas_ = 0, sc_chunks_ = 1;  // per-CTA scalar partial regions
   double *d_rec_ = nullptr, *d_lout_ = nullptr;

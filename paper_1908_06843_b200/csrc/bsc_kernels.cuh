@@ -40,6 +40,26 @@ __device__ __forceinline__ int warp_isum(int v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Row p of entry e of a strict upper triangle stored row-major (H' columns):
+// start(p) = p(2H'−p−1)/2 ≤ e < start(p+1); closed form, corrected by one step.
+__device__ __forceinline__ int pair_row(int e, int hp) {
+  const float b = 2.0f * hp - 1.0f;
+  int p = static_cast<int>((b - sqrtf(fmaxf(b * b - 8.0f * e, 0.0f))) * 0.5f);
+  p = max(0, min(p, hp - 2));
+  if (p * (2 * hp - p - 1) / 2 > e)
+    --p;
+  else if ((p + 1) * (2 * hp - p - 2) / 2 <= e)
+    ++p;
+  return p;
+}
+
+// One row of `cnt16` 16-byte chunks global → shared by the warp (cp.async, L2 only).
+__device__ __forceinline__ void cp_async_row(double* dst, const double* src, int cnt16, int lane) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  for (int c = lane; c < cnt16; c += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + c * 16), "l"(src + 2 * c) : "memory");
+}
+
 // (value desc, index asc): true when (v1,i1) ranks before (v2,i2).
 __device__ __forceinline__ bool ranks_before(double v1, int i1, double v2, int i2) {
   return v1 > v2 || (v1 == v2 && i1 < i2);
@@ -280,6 +300,7 @@ struct EnumArgs {
   // lane path (lane_kernels.cuh): deferred-point records and per-point modes
   double* rec;
   int* pmode;
+  int stage_b;  // front pass: B rows double-buffered in shared memory by cp.async
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
 };
@@ -463,7 +484,18 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     sdesc = reinterpret_cast<const uint2*>(cta);
     sent = reinterpret_cast<const uint32_t*>(cta + a.stage_desc_bytes);
   }
-  double* sm = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + stage_bytes) + (long long)wib * L.total;
+  // front pass: diag(G) staged per CTA, and per warp two B-row buffers (when they fit)
+  const double* gdiag = a.gdiag;
+  int gstage = 0, wstride = L.total;
+  if constexpr (PASS == kPassFront) {
+    gstage = (a.H + 1) & ~1;
+    for (int i = threadIdx.x; i < a.H; i += blockDim.x) esm[i] = a.gdiag[i];
+    __syncthreads();
+    gdiag = esm;
+    if (MAXJ <= 16 && a.stage_b) wstride += 2 * a.Hp;
+  }
+  double* sm = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + stage_bytes) + gstage + (long long)wib * wstride;
+  double* bbuf = sm + L.total;  // front pass with stage_b: [2][Hp]
   double* su = sm + L.u;
   double* sP = sm + L.P;
   double* tab = sm + L.tab;
@@ -490,7 +522,14 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     t_last = t_;                                                                        \
   }
 
-  for (int n = gwarp; n < a.N; n += nwarps) {
+  // (compiled in for the register budget of MAXJ ≤ 16 only)
+  const bool stage_b = PASS == kPassFront && MAXJ <= 16 && a.stage_b;
+  if (stage_b && gwarp < a.N) {
+    cp_async_row(bbuf, a.B + (long long)gwarp * a.Hp, a.Hp / 2, lane);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int it = 0;
+  for (int n = gwarp; n < a.N; n += nwarps, ++it) {
     if constexpr (PASS == kPassFallback) {
       if (a.pmode[n] != kModeFallback) continue;
     }
@@ -500,7 +539,16 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     ENUM_PHASE(7);
     const double* y = a.Y + (long long)n * a.Dp;
     const double* brow = a.B + (long long)n * a.Hp;
-    {  // pull the B row two points ahead into L2 while this point is processed
+    if (stage_b) {
+      // the next point's row lands in the other buffer while this one is used
+      __syncwarp();
+      const long long nn = n + nwarps;
+      if (nn < a.N) cp_async_row(bbuf + ((it + 1) & 1) * a.Hp, a.B + nn * a.Hp, a.Hp / 2, lane);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp();
+      brow = bbuf + (it & 1) * a.Hp;
+    } else {  // pull the B row two points ahead into L2 while this point is processed
       const long long nn = n + 2LL * nwarps;
       if (nn < a.N)
         for (int l = lane; l < row_lines; l += 32)
@@ -524,7 +572,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     for (int j = 0; j < MAXJ; ++j) {
       const int h = lane + 32 * j;
       if (h < H) {
-        const double b = brow[h], g = a.gdiag[h];
+        const double b = brow[h], g = gdiag[h];
         f[j] = __dadd_rn(a.log_pi, __dmul_rn(__dsub_rn(__dmul_rn(2.0, b), g), a.inv2s));
         bad |= !isfinite(f[j]);
         mag = fmax(mag, fabs(f[j]) + a.inv2s * (2.0 * fabs(b) + g));
@@ -607,7 +655,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
     // lj(S) − base = Σ_a [dlp + inv2s(2b_a − G_aa)] + Σ_{a<c} (−2 inv2s G_ac)
     for (int p = lane; p < HP; p += 32) {
       const uint32_t c = scand[p];
-      const double v = a.dlp + a.inv2s * (2.0 * brow[c] - a.gdiag[c]);
+      const double v = a.dlp + a.inv2s * (2.0 * brow[c] - gdiag[c]);
       su[p] = v;
     }
     // pairwise terms (strict upper triangle, row-major): the Gram gathers are
@@ -619,21 +667,13 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       const int e = lane + 32 * u;
       gp[u] = 0.0;
       if (e < npairs) {
-        int idx = e, p = 0;
-        while (idx >= HP - 1 - p) {
-          idx -= HP - 1 - p;
-          ++p;
-        }
-        gp[u] = a.G[(long long)scand[p] * a.Hp + scand[p + 1 + idx]];
+        const int p = pair_row(e, HP), q = e - p * (2 * HP - p - 1) / 2 + p + 1;
+        gp[u] = a.G[(long long)scand[p] * a.Hp + scand[q]];
       }
     }
     for (int e = lane + 128; e < npairs; e += 32) {  // H' > 16
-      int idx = e, p = 0;
-      while (idx >= HP - 1 - p) {
-        idx -= HP - 1 - p;
-        ++p;
-      }
-      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[p + 1 + idx]];
+      const int p = pair_row(e, HP), q = e - p * (2 * HP - p - 1) / 2 + p + 1;
+      sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
     }
     // zero slot (the selection pool overlays the table); the front pass has no table
     if (PASS != kPassFront && lane == 0) tab[a.n_tab] = 0.0;
@@ -645,7 +685,7 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const int h = lane + 32 * j;
-      rel1[j] = h < H ? a.dlp + a.inv2s * (2.0 * brow[h] - a.gdiag[h]) : -INFINITY;
+      rel1[j] = h < H ? a.dlp + a.inv2s * (2.0 * brow[h] - gdiag[h]) : -INFINITY;
       mx = fmax(mx, rel1[j]);
     }
 #pragma unroll
@@ -698,7 +738,11 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const double x = rel1[j] - mxs;  // −inf beyond H: exp_nonpos gives 0
-      const double e = exp_nonpos(x);
+      double e;
+      if (PASS == kPassFront && MAXJ <= 16 && x < -32.0)
+        e = small_exp(x);  // below e^-32 of the largest term: invisible in the fp64 sums
+      else
+        e = exp_nonpos(x);
       zs1 += e;
       if (!t1) zsT += exp_nonpos(x * a.inv_T);
       // deferred points: the unnormalised singleton weights (lane_finish_kernel scales them)

@@ -222,36 +222,45 @@ __device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
   }
 }
 
-// Child A∪{Z} of the deepest node A (taken when Z > x) and its leaves.
+// Child A∪{Z} of the deepest node A and its leaves.
 template <int HP, int GM, int Z>
-__device__ __forceinline__ void deep_child(double* S, double qA, int x, const double (&ce)[HP], double (&R)[HP],
-                                           double& ch) {
+__device__ __forceinline__ void deep_child(double* S, double qA, const double (&ce)[HP], double (&R)[HP], double& ch) {
   using F = LaneShape<HP, GM>;
-  if (Z > x) {
-    const double qz = qA * ce[Z];
-    double s = qz;
-    if constexpr (Z < HP - 1) {
-      constexpr int NW = HP - 1 - Z;
-      double q[NW], m[NW];
+  const double qz = qA * ce[Z];
+  double s = qz;
+  if constexpr (Z < HP - 1) {
+    constexpr int NW = HP - 1 - Z;
+    double q[NW], m[NW];
 #pragma unroll
-      for (int j = 0; j < NW; ++j) {
-        const int w = Z + 1 + j;
-        q[j] = qz * ce[w] * LS(F::O_EP + F::pidx(Z, w));
-        m[j] = LS(F::O_M + F::tri(Z, w));
-      }
-#pragma unroll
-      for (int j = 0; j < NW; ++j) {
-        const int w = Z + 1 + j;
-        LS(F::O_M + F::tri(Z, w)) = m[j] + q[j];
-        R[w] += q[j];
-        s += q[j];
-      }
+    for (int j = 0; j < NW; ++j) {
+      const int w = Z + 1 + j;
+      q[j] = qz * ce[w] * LS(F::O_EP + F::pidx(Z, w));
+      m[j] = LS(F::O_M + F::tri(Z, w));
     }
-    R[Z] += s;
-    ch += s;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const int w = Z + 1 + j;
+      LS(F::O_M + F::tri(Z, w)) = m[j] + q[j];
+      R[w] += q[j];
+      s += q[j];
+    }
   }
-  if constexpr (Z + 1 < HP) deep_child<HP, GM, Z + 1>(S, qA, x, ce, R, ch);
+  R[Z] += s;
+  ch += s;
 }
+
+template <int HP, int GM, int Z>
+__device__ __forceinline__ void deep_pred(double* S, double qA, int x, const double (&ce)[HP], double (&R)[HP],
+                                          double& ch) {
+  if (Z > x) deep_child<HP, GM, Z>(S, qA, ce, R, ch);
+  if constexpr (Z + 1 < HP) deep_pred<HP, GM, Z + 1>(S, qA, x, ce, R, ch);
+}
+
+// Duff-style dispatch on the node maximum x: case x falls through the
+// unrolled blocks Z = x+1 … H'−1 (one uniform indirect branch per node).
+#define LANE_FT_CASES(BLOCK)                                                                                     \
+  BLOCK(0, 1) BLOCK(1, 2) BLOCK(2, 3) BLOCK(3, 4) BLOCK(4, 5) BLOCK(5, 6) BLOCK(6, 7) BLOCK(7, 8) BLOCK(8, 9)     \
+  BLOCK(9, 10) BLOCK(10, 11) BLOCK(11, 12) BLOCK(12, 13) BLOCK(13, 14) BLOCK(14, 15)
 
 // Node A (|A| = K ≤ γ−2, max x, weight qA, members path[0..K)): walks its
 // children, returns Σ_children sub(child).
@@ -266,26 +275,69 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
   if constexpr (K == GM - 2) {
     double ce[HP], R[HP];
 #pragma unroll
-    for (int w = 0; w < HP; ++w) {
-      R[w] = 0.0;
-      ce[w] = 0.0;
-      if (w > x) {
-        const double c = K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w);
-        ce[w] = LS(F::O_EU + w) * c;
+    for (int w = 0; w < HP; ++w) R[w] = 0.0;
+    if constexpr (GM < 5) {
+      // predicated unrolled blocks (fewer, shorter nodes: cheaper than the indirect branch)
+#pragma unroll
+      for (int w = 0; w < HP; ++w) {
+        ce[w] = 0.0;
+        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w));
       }
-    }
-    deep_child<HP, GM, (K < HP ? K : 0)>(S, qA, x, ce, R, ch);
-    // flush the column accumulators: M[z][z] and the members' rows
+      deep_pred<HP, GM, (K < HP ? K : 0)>(S, qA, x, ce, R, ch);
 #pragma unroll
-    for (int z = 0; z < HP; ++z) {
-      if (z > x) {
-        double m[K + 1];
-        m[K] = LS(F::O_M + F::tri(z, z));
+      for (int z = 0; z < HP; ++z) {
+        if (z > x) {
+          double m[K + 1];
+          m[K] = LS(F::O_M + F::tri(z, z));
 #pragma unroll
-        for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
-        LS(F::O_M + F::tri(z, z)) = m[K] + R[z];
+          for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
+          LS(F::O_M + F::tri(z, z)) = m[K] + R[z];
 #pragma unroll
-        for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + R[z];
+          for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + R[z];
+        }
+      }
+    } else {
+    // ce[w] = e^{u_w}·c(A,w), w > x
+      switch (x) {
+  #define LANE_CE(c_, Z_)                                                                        \
+    case c_:                                                                                     \
+      if constexpr (Z_ < HP) {                                                                   \
+        constexpr int Zc = Z_ < HP ? Z_ : 0;                                                     \
+        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? S[(xrow + Zc) * 32] : LS(F::O_CV + (K - 2) * HP + Zc)); \
+      }                                                                                          \
+      [[fallthrough]];
+        LANE_FT_CASES(LANE_CE)
+  #undef LANE_CE
+        default:
+          break;
+      }
+      switch (x) {
+  #define LANE_DC(c_, Z_)                                                     \
+    case c_:                                                                  \
+      if constexpr (Z_ < HP) deep_child<HP, GM, (Z_ < HP ? Z_ : 0)>(S, qA, ce, R, ch); \
+      [[fallthrough]];
+        LANE_FT_CASES(LANE_DC)
+  #undef LANE_DC
+        default:
+          break;
+      }
+      // flush the column accumulators: M[z][z] and the members' rows, z > x
+      switch (x) {
+  #define LANE_FL(c_, Z_)                                                           \
+    case c_:                                                                        \
+      if constexpr (Z_ < HP) {                                                      \
+        constexpr int Zc = Z_ < HP ? Z_ : 0;                                        \
+        double m[K + 1];                                                            \
+        m[K] = LS(F::O_M + F::tri(Zc, Zc));                                         \
+        _Pragma("unroll") for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + Zc) * 32]; \
+        LS(F::O_M + F::tri(Zc, Zc)) = m[K] + R[Zc];                                 \
+        _Pragma("unroll") for (int i = 0; i < K; ++i) S[(orow[i] + Zc) * 32] = m[i] + R[Zc]; \
+      }                                                                             \
+      [[fallthrough]];
+        LANE_FT_CASES(LANE_FL)
+  #undef LANE_FL
+        default:
+          break;
       }
     }
   } else {
