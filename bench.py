@@ -247,7 +247,7 @@ def main():
 
     # ---- end to end through the reference-facing C ABI with host buffers
     e2e = None
-    if world == 1:
+    if world == 1 and args.e2e_steps > 0:
         ypin = torch.empty((n_local, w.D), dtype=torch.float64, pin_memory=True)
         ypin.numpy()[:] = y
         e2e_model = model
