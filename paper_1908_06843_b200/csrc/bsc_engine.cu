@@ -12,6 +12,7 @@
 #include "bsc_kernels.cuh"
 #include "lane_kernels.cuh"
 #include "dgemm.cuh"
+#include "ozaki_gemm.cuh"
 #include "mstep_kernels.cuh"
 #include "engine_util.hpp"
 #include "sched_builder.hpp"
@@ -95,6 +96,17 @@ SolveFn solve_rows_fn(int s, bool fwd) { return fwd ? solve_rows_t<true>(s) : so
 // Gram WᵀW: M = N = H, K = Dp.
 #define GRAM_CFG 64, 64, 16, 32, 32, false, true, 3
 
+int oz_sms(int device) {
+  static int cache[64] = {};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
 }  // namespace
 
 BscEngine::BscEngine(uint32_t dim, uint32_t latents, uint32_t hprime, uint32_t gamma, uint64_t state_cap,
@@ -170,6 +182,20 @@ void BscEngine::init(int device) {
   lane_ok_ = !vpath() && gamma_ >= 2 && gamma_ <= 6 && hprime_ >= 2 && hprime_ <= 16;
   if (const char* e = std::getenv("BSC_LANE")) lane_ok_ = lane_ok_ && e[0] != '0';
 
+  // Y·W and Yᵀ⟨S⟩ on the integer tensor cores (ozaki_gemm.cuh) for the binary
+  // family (⟨s⟩ ∈ [0, 1] gives ⟨S⟩ a fixed slice scale); BSC_GEMM=dmma keeps them on DMMA
+  Kp_ = round_up(Dp_, 16);
+  oz_ = !vpath() && Kp_ <= oz::MAX_KJOB;
+  if (const char* e = std::getenv("BSC_GEMM")) oz_ = oz_ && std::strcmp(e, "dmma") != 0;
+  if (oz_) {
+    d_ws_ = dalloc<int8_t>((size_t)oz::S * Hp_ * Kp_, "W slices");
+    d_wsb_ = dalloc<double>(Hp_, "W slice scales");
+    d_two_ = dalloc<double>(Hp_, "ES slice scale");
+    d_ytsa_ = dalloc<double>((size_t)kMaxChunks * Dp_, "Yt slice scales");
+    d_ozmax_ = dalloc<unsigned long long>(Dp_ + Hp_, "column maxima");
+    std::vector<double> two(Hp_, 2.0);  // ⟨s⟩ ≤ 1 < 2
+    ck(cudaMemcpy(d_two_, two.data(), Hp_ * 8, cudaMemcpyHostToDevice), "ES scale");
+  }
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
   d_trace_part_ = dalloc<double>(2 * kTraceCtas, "trace partials");
@@ -207,7 +233,9 @@ BscEngine::~BscEngine() {
                   (void*)d_w_, (void*)d_g_, (void*)d_wnorm_, (void*)d_gdiag_, (void*)d_b_, (void*)d_es_, (void*)d_stats_,
                   (void*)d_smulti_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_part_, (void*)d_cand_,
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
-                  (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_})
+                  (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_,
+                  (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
+                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -485,9 +513,16 @@ void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
   for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
                   (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_rec_,
-                  (void*)d_lout_, (void*)d_pmode_})
+                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
+  if (oz_) {
+    oz_np_ = (static_cast<long long>(rows) + 127) / 128 * 128;
+    d_ys_ = dalloc<int8_t>((size_t)oz::S * rows * Kp_, "Y slices");
+    d_ysa_ = dalloc<double>(rows, "Y slice scales");
+    d_yts_ = dalloc<int8_t>((size_t)oz::S * Dp_ * oz_np_, "Yt slices");
+    d_ozcs_ = dalloc<double>((size_t)(oz_np_ / 128) * Hp_, "ES column sums");
+  }
   d_y_ = dalloc<double>(rows * Dp_, "Y");
   d_y2_ = dalloc<double>(rows, "y2");
   d_b_ = dalloc<double>(rows * Hp_, "B");
@@ -606,6 +641,43 @@ void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
                                                                        d_y2_);
   ck(cudaGetLastError(), "y2");
   n_ = n;
+  if (oz_) slice_y(0, n, 0, s);
+}
+
+// int8 slices of the resident Y for the two tensor-core products: rows with
+// per-point scales (A of Y·W) and columns with per-dimension scales over the
+// chunk (A of Yᵀ⟨S⟩, k = point index contiguous; scale vector `chunk`).
+void BscEngine::slice_y(uint64_t off, uint64_t rows, int chunk, void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  const long long cap_rows = static_cast<long long>((cap_n_ + 1) & ~1ull);
+  const double* y = d_y_ + off * Dp_;
+  oz::oz_slice_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
+      y, Dp_, static_cast<int>(rows), Dp_, Kp_, d_ys_ + off * Kp_, cap_rows * Kp_, d_ysa_ + off);
+  ck(cudaMemsetAsync(d_ozmax_ + Hp_, 0, (size_t)Dp_ * 8, s), "zero maxima");
+  const unsigned gy = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(256, rows / 512)));
+  oz::oz_colmax_kernel<<<dim3((Dp_ + 31) / 32, gy), 256, 0, s>>>(y, Dp_, static_cast<long long>(rows),
+                                                                 static_cast<int>(D_), d_ozmax_ + Hp_);
+  double* sc = d_ytsa_ + (size_t)chunk * Dp_;
+  oz::oz_scale_from_max_kernel<<<(Dp_ + 255) / 256, 256, 0, s>>>(d_ozmax_ + Hp_, static_cast<int>(D_), Dp_, 0.0, sc);
+  oz::oz_slice_cols_kernel<<<dim3((Dp_ + 31) / 32, static_cast<unsigned>((rows + 127) / 128)), 256, 0, s>>>(
+      y, Dp_, static_cast<long long>(rows), static_cast<int>(D_), Dp_, oz_np_, sc, d_yts_ + off,
+      static_cast<long long>(Dp_) * oz_np_, nullptr);
+  ck(cudaGetLastError(), "slice Y");
+  launches_ += 4;
+}
+
+// int8 slices of Wᵀ (rows h, k = d contiguous) with per-column scales.
+void BscEngine::slice_w(void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  ck(cudaMemsetAsync(d_ozmax_, 0, (size_t)Hp_ * 8, s), "zero maxima");
+  oz::oz_colmax_kernel<<<dim3((Hp_ + 31) / 32, 4), 256, 0, s>>>(d_w_, Hp_, static_cast<long long>(D_),
+                                                                static_cast<int>(H_), d_ozmax_);
+  oz::oz_scale_from_max_kernel<<<(Hp_ + 255) / 256, 256, 0, s>>>(d_ozmax_, static_cast<int>(H_), Hp_, 0.0, d_wsb_);
+  oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, (Kp_ + 127) / 128), 256, 0, s>>>(
+      d_w_, Hp_, static_cast<long long>(D_), static_cast<int>(H_), Hp_, Kp_, d_wsb_, d_ws_,
+      static_cast<long long>(Hp_) * Kp_, nullptr);
+  ck(cudaGetLastError(), "slice W");
+  launches_ += 3;
 }
 
 // Model::step with a host DataSet (the call em.cpp:39 makes): the data are
@@ -691,6 +763,7 @@ void BscEngine::enqueue_gram(void* stream) {
   gram_diag_exact_kernel<<<(H_ + 31) / 32, 32, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, Hp_, d_wnorm_, d_gdiag_);
   ck(cudaGetLastError(), "gram");
   launches_ += 2;
+  if (oz_) slice_w(stream);
 }
 
 // The fields both enumerators share (EnumArgs, bsc_kernels.cuh): shapes, the
@@ -748,7 +821,11 @@ void BscEngine::fill_enum_args(void* out, double temperature, bool cands, bool i
   a.base0 = zero_prior + norm_const;
   a.inv_T = 1.0 / temperature;
   a.weight_mode = weight_mode_;
-  a.eps_dot = 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
+  // |b_fast − b_oracle| ≤ eps_dot·‖W_h‖·‖y‖: DMMA (any order) and the oracle's
+  // left-to-right sum each within γ_D; the int8-sliced product within
+  // D·11·2⁻⁵⁶·s_y·s_h ≤ 5.5·D·2⁻⁵³‖y‖‖W_h‖ plus its fp64 group combine (ozaki_gemm.cuh)
+  a.eps_dot = (oz_ && !infer) ? (7.0 * static_cast<double>(Dp_) + 16.0) * 0x1.0p-53
+                              : 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
 }
 
 void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows,
@@ -838,6 +915,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   const uint64_t n = n_;
   chunk = std::max<uint64_t>(2, std::min<uint64_t>(n, chunk));
   chunk = (chunk + 1) & ~1ull;  // even row offsets (K4 reads K in pairs)
+  if (oz_ && chunk < n) chunk = std::min<uint64_t>(n, (chunk + 127) & ~127ull);  // 16-byte Yᵀ slice offsets
   const int nchunks = static_cast<int>((n + chunk - 1) / chunk);
   if (nchunks > kMaxChunks) throw Error(kConfig, "gpu: too many E-step chunks");
   if (nchunks > colsum_chunks_) {
@@ -862,6 +940,29 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   // per-CTA scalar partials: [role: whole/front pass, lane finish, fallback][chunk][sc_ctas_]
   ck(cudaMemsetAsync(d_warp_sc_, 0, (size_t)3 * nchunks * sc_ctas_ * 2 * 8, s), "zero cta scalars");
   sc_chunks_ = nchunks;
+  // Yᵀ⟨S⟩ on the integer tensor cores: k-splits sized on the first (largest) chunk
+  int oz_kchunk = 0, oz_splits0 = 0;
+  if (oz_) {
+    const long long npc = (static_cast<long long>(chunk) + 127) / 128 * 128;
+    if (npc * Hp_ * oz::S > oz_ess_bytes_) {
+      dfree(d_ess_);
+      d_ess_ = dalloc<int8_t>((size_t)npc * Hp_ * oz::S, "ES slices");
+      oz_ess_bytes_ = npc * Hp_ * oz::S;
+    }
+    oz_npc_ = npc;
+    int sms = 148;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "sms");
+    const int tiles = ((static_cast<int>(D_) + oz::BM - 1) / oz::BM) * ((static_cast<int>(H_) + oz::BN - 1) / oz::BN);
+    const long long want = std::max(1, sms / tiles);
+    const long long per = (static_cast<long long>(chunk) + want - 1) / want;
+    oz_kchunk = static_cast<int>(std::min<long long>(oz::MAX_KJOB, (per + oz::BK - 1) / oz::BK * oz::BK));
+    oz_splits0 = static_cast<int>((static_cast<long long>(chunk) + oz_kchunk - 1) / oz_kchunk);
+    if (oz_splits0 > oz_part_slots_) {
+      dfree(d_ozpart_);
+      d_ozpart_ = dalloc<double>((size_t)oz_splits0 * part_stride_, "Yt<S> partials");
+      oz_part_slots_ = oz_splits0;
+    }
+  }
   auto cs = static_cast<cudaStream_t>(copy_stream_);
   if (host_y) {
     ck(cudaEventRecord(static_cast<cudaEvent_t>(chunk_ev_[kMaxChunks]), s), "event");
@@ -882,7 +983,19 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
           d_y_ + off * Dp_, static_cast<long long>(rows), D_, Dp_, d_y2_ + off);
       ++launches_;
     }
-    {  // K1: B = Y·W
+    if (oz_ && (host_y || nchunks > 1)) slice_y(off, rows, c, s);
+    if (oz_) {  // K1: B = Y·W, int8 slices on tcgen05
+      const long long cap_rows = static_cast<long long>((cap_n_ + 1) & ~1ull);
+      oz::Args g{};
+      g.sa = d_ysa_ + off;
+      g.sb = d_wsb_;
+      g.C = d_b_ + off * Hp_;
+      g.ldc = Hp_;
+      ck(oz::launch_gemm(d_ys_ + off * Kp_, cap_rows * Kp_, Kp_, d_ws_, static_cast<long long>(Hp_) * Kp_, Kp_,
+                         static_cast<int>(rows), Hp_, Kp_, static_cast<int>(rows), Hp_, g, oz_sms(device_), s),
+         "oz gemm Y·W");
+      ++launches_;
+    } else {  // K1: B = Y·W
       GemmArgs g{static_cast<int>(rows), Hp_, Dp_, d_y_ + off * Dp_, Dp_, d_w_, Hp_, d_b_ + off * Hp_, Hp_,
                  1.0, 0.0, Dp_, 0};
       ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
@@ -891,7 +1004,26 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     if (c == 0) ev(2);
     launch_enumerate(temperature, want_candidates, false, off, rows, c);
     if (c == 0) ev(3);
-    {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES over this chunk (+ fused Σ⟨s⟩), split-K over its rows
+    if (oz_) {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES — ⟨S⟩ᵀ slices (+ column sums = Σ⟨s⟩ partials), then tcgen05
+      const unsigned kb = static_cast<unsigned>((rows + 127) / 128);
+      oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, kb), 256, 0, s>>>(
+          d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_, oz_npc_, d_two_, d_ess_,
+          static_cast<long long>(Hp_) * oz_npc_, d_ozcs_ + (off / 128) * Hp_);
+      ck(cudaGetLastError(), "slice ES");
+      oz::Args g{};
+      g.sa = d_ytsa_ + (size_t)((host_y || nchunks > 1) ? c : 0) * Dp_;
+      g.sb = d_two_;
+      g.C = d_ozpart_;
+      g.ldc = Hp_;
+      g.kchunk = oz_kchunk;
+      g.c_split_stride = part_stride_;
+      g.accumulate = c > 0;
+      ck(oz::launch_gemm(d_yts_ + off, static_cast<long long>(Dp_) * oz_np_, oz_np_, d_ess_,
+                         static_cast<long long>(Hp_) * oz_npc_, oz_npc_, static_cast<int>(D_), static_cast<int>(H_),
+                         static_cast<int>(rows), Dp_, Hp_, g, oz_sms(device_), s),
+         "oz gemm Yt·ES");
+      launches_ += 2;
+    } else {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES over this chunk (+ fused Σ⟨s⟩), split-K over its rows
       const int krows = static_cast<int>((rows + 1) & ~1ull);
       int kchunk = (krows + splits_ - 1) / splits_;
       kchunk = (kchunk + 1) & ~1;
@@ -911,9 +1043,14 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     if (c == 0) ev(4);
   }
   const long long DH = (long long)D_ * H_;
-  reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
-                                                           part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),
-                                                           vpath() ? -1 : lay_.off_ssT());
+  if (oz_)
+    reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_ozpart_, d_ozcs_, oz_splits0,
+                                                             static_cast<int>((n + 127) / 128), part_stride_, D_, H_,
+                                                             Hp_, d_stats_, lay_.off_s(), lay_.off_ssT());
+  else
+    reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
+                                                             part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),
+                                                             vpath() ? -1 : lay_.off_ssT());
   if (vpath()) {
     finalize_v(nchunks * enum_ctas_, n);
     launches_ += 2;

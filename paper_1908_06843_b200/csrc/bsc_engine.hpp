@@ -197,6 +197,19 @@ class BscEngine {
   void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;
+  // int8-sliced tcgen05 GEMMs (ozaki_gemm.cuh) for the binary family's Y·W and Yᵀ⟨S⟩
+  bool oz_ = false;
+  int Kp_ = 0;                          // Y / W slice row length (Dp_ rounded to 16)
+  long long oz_np_ = 0;                 // Yᵀ slice row length (resident rows rounded to 128)
+  long long oz_npc_ = 0;                // ⟨S⟩ᵀ slice row length (chunk rows rounded to 128)
+  int8_t *d_ys_ = nullptr, *d_yts_ = nullptr, *d_ws_ = nullptr, *d_ess_ = nullptr;
+  double *d_ysa_ = nullptr, *d_ytsa_ = nullptr, *d_wsb_ = nullptr, *d_two_ = nullptr;
+  double *d_ozpart_ = nullptr, *d_ozcs_ = nullptr;
+  unsigned long long* d_ozmax_ = nullptr;
+  int oz_part_slots_ = 0, oz_ytsa_chunks_ = 0;
+  long long oz_ess_bytes_ = 0;
+  void slice_y(uint64_t off, uint64_t rows, int chunk, void* stream);
+  void slice_w(void* stream);
   void* ev_[8] = {};
 };
 

@@ -1,0 +1,461 @@
+// fp64 GEMM on the sm_100a integer tensor cores (tcgen05.mma kind::i8) by
+// exact int8 slicing (the Ozaki scheme).
+//
+// Every row of A (and every column of B) is scaled by a power of two 2^e with
+// max|x| < 2^e and cut into S = 8 signed 7-bit slices:
+//     x = 2^e · Σ_{i<S} a_i · 2^{-7(i+1)} + r,   a_i ∈ [-127, 127],  |r| < 2^{e-56}
+// (truncation toward zero; every step is exact in fp64). The product is then
+//     A·B ≈ diag(sa) · Σ_{g<S} 2^{-7(g+2)} · (Σ_{i+j=g} A_i · B_j) · diag(sb)
+// where each inner sum is an exact int32 accumulation on the tensor cores
+// (|A_i B_j| ≤ 127² per term; ≤ 8·K_job·127² < 2^31 for K_job ≤ 16384) and the
+// eight group sums are combined in fp64 in the epilogue. Dropped terms
+// (i+j ≥ S) and the slicing remainders bound the error per output by
+//     |ΔC| ≤ K · 11·2^{-56} · sa_m · sb_n  ≤  K · 2^{-50.5} · max_k|a_mk| · max_k|b_kn|
+// which is of the order of (and never worse than K/u times) the rounding bound
+// of an fp64 DGEMM, γ_K Σ|a||b|.
+//
+// Kernel layout (one CTA per SM, persistent over jobs = (k-split, m-tile, n-tile)):
+//   warp 0: TMA producer — B tile (all S slices, 64 rows × 128 k) + A tiles
+//           (one slice, 128 rows × 128 k) through mbarrier rings;
+//   warp 1: TMEM allocation (512 columns = 8 group accumulators × 64) and the
+//           single-thread tcgen05.mma issue;
+//   warps 2-5: epilogue — tcgen05.ld of the 8 int32 groups, fp64 combine,
+//           scale, store (or accumulate) to C.
+// Operands are K-major int8, 128-byte swizzled (TMA SWIZZLE_128B ↔ UMMA
+// SWIZZLE_128B, SBO = 1024 B), K advanced by 32 bytes per MMA inside the row.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace bscgpu {
+namespace oz {
+
+constexpr int S = 8;                    // slices
+constexpr int BM = 128, BN = 64, BK = 128;
+constexpr int A_STAGES = 4, B_STAGES = 2;
+constexpr int A_BYTES = BM * BK;        // 16 KB
+constexpr int B_BYTES = S * BN * BK;    // 64 KB
+constexpr int SMEM_BYTES = A_STAGES * A_BYTES + B_STAGES * B_BYTES + 1024 + 256;
+constexpr int THREADS = 320;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
+constexpr int EPI_COLS = BN / 2;  // columns per epilogue thread
+constexpr int MAX_KJOB = 16384;         // int32 headroom per job (see above)
+
+struct Args {
+  int M, N;             // valid output rows / cols
+  int K;                // K extent (elements) of the whole product
+  int kchunk;           // K per job, a multiple of BK (≤ MAX_KJOB)
+  int m_tiles, n_tiles, k_splits;
+  const double* sa;     // row scales of A, [k_split][sa_stride]
+  long long sa_stride;  // 0: one vector for every split
+  const double* sb;     // column scales of B
+  long long sb_stride;
+  double* C;
+  long long ldc;
+  long long c_split_stride;  // partial slot stride per k-split
+  int accumulate;            // C += result (else C = result)
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// K-major operand, 128-byte swizzle, 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+// kind::i8: D s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24.
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                            (static_cast<uint32_t>(BM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- the GEMM
+__global__ void __launch_bounds__(THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_STAGES * A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + B_STAGES * B_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  const uint32_t full_a = smem_u32(bars), empty_a = full_a + 8 * A_STAGES;
+  const uint32_t full_b = empty_a + 8 * A_STAGES, empty_b = full_b + 8 * B_STAGES;
+  const uint32_t tfull = empty_b + 8 * B_STAGES, tempty = tfull + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < A_STAGES; ++i) mbar_init(full_a + 8 * i, 1), mbar_init(empty_a + 8 * i, 1);
+    for (int i = 0; i < B_STAGES; ++i) mbar_init(full_b + 8 * i, 1), mbar_init(empty_b + 8 * i, 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int per_split = a.m_tiles * a.n_tiles;
+  const int jobs = per_split * a.k_splits;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
+        const int nt = job % a.n_tiles, mt = (job / a.n_tiles) % a.m_tiles, ks = job / per_split;
+        const int k0 = ks * a.kchunk;
+        const int klen = min(a.kchunk, a.K - k0);
+        const int nkb = (klen + BK - 1) / BK;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(empty_b + 8 * bs, bph ^ 1);
+          mbar_expect_tx(full_b + 8 * bs, B_BYTES);
+          tma_load_3d(smem_u32(sB + bs * B_BYTES), &tb, k0 + kb * BK, nt * BN, 0, full_b + 8 * bs);
+          if (++bs == B_STAGES) bs = 0, bph ^= 1;
+          for (int i = 0; i < S; ++i) {
+            mbar_wait(empty_a + 8 * as, aph ^ 1);
+            mbar_expect_tx(full_a + 8 * as, A_BYTES);
+            tma_load_3d(smem_u32(sA + as * A_BYTES), &ta, k0 + kb * BK, mt * BM, i, full_a + 8 * as);
+            if (++as == A_STAGES) as = 0, aph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int as = 0, bs = 0, t = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int job = blockIdx.x; job < jobs; job += gridDim.x, ++t) {
+        const int ks = job / per_split;
+        const int k0 = ks * a.kchunk;
+        const int klen = min(a.kchunk, a.K - k0);
+        const int nkb = (klen + BK - 1) / BK;
+        if (t > 0) mbar_wait(tempty, (t - 1) & 1);  // the epilogue drained job t-1
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(full_b + 8 * bs, bph);
+          const uint32_t b_base = smem_u32(sB + bs * B_BYTES);
+          for (int i = 0; i < S; ++i) {
+            mbar_wait(full_a + 8 * as, aph);
+            tc_fence_after();
+            const uint64_t da = sdesc(smem_u32(sA + as * A_BYTES));
+            for (int j = 0; j < S - i; ++j) {
+              const uint64_t db = sdesc(b_base + j * BN * BK);
+              const uint32_t d = tmem + (i + j) * BN;
+#pragma unroll
+              for (int kk = 0; kk < BK / 32; ++kk)
+                mma_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb | i | kk) != 0);
+            }
+            tc_commit(empty_a + 8 * as);
+            if (++as == A_STAGES) as = 0, aph ^= 1;
+          }
+          tc_commit(empty_b + 8 * bs);
+          if (++bs == B_STAGES) bs = 0, bph ^= 1;
+        }
+        tc_commit(tfull);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;         // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;  // which half of the 64 columns
+    const int row = q * 32 + lane;
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * EPI_COLS;
+    int t = 0;
+    for (int job = blockIdx.x; job < jobs; job += gridDim.x, ++t) {
+      const int nt = job % a.n_tiles, mt = (job / a.n_tiles) % a.m_tiles, ks = job / per_split;
+      mbar_wait(tfull, t & 1);
+      tc_fence_after();
+      double acc[EPI_COLS];
+#pragma unroll
+      for (int c = 0; c < EPI_COLS; ++c) acc[c] = 0.0;
+#pragma unroll
+      for (int g = S - 1; g >= 0; --g) {
+        const double w = ldexp(1.0, -7 * (g + 2));
+        int v0[16], v1[16];
+        tmem_ld16(tbase + g * BN, v0);
+        tmem_ld16(tbase + g * BN + 16, v1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 16; ++x) {
+          acc[x] = fma(static_cast<double>(v0[x]), w, acc[x]);
+          acc[16 + x] = fma(static_cast<double>(v1[x]), w, acc[16 + x]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+      const int m = mt * BM + row;
+      if (m < a.M) {
+        const double sam = a.sa[ks * a.sa_stride + m];
+        const int c0 = nt * BN + half * EPI_COLS;
+        const double* sb = a.sb + ks * a.sb_stride + c0;
+        double* crow = a.C + ks * a.c_split_stride + static_cast<long long>(m) * a.ldc + c0;
+        const int nvalid = a.N - c0;
+        if (nvalid >= EPI_COLS && ((a.ldc | c0) & 1) == 0) {
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; c += 2) {
+            double2 v = make_double2(acc[c] * sam * sb[c], acc[c + 1] * sam * sb[c + 1]);
+            if (a.accumulate) {
+              const double2 o = *reinterpret_cast<const double2*>(crow + c);
+              v.x += o.x;
+              v.y += o.y;
+            }
+            *reinterpret_cast<double2*>(crow + c) = v;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; ++c) {
+            if (c < nvalid) {
+              const double v = acc[c] * sam * sb[c];
+              crow[c] = a.accumulate ? crow[c] + v : v;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------- slicing
+__device__ __forceinline__ double pow2_above(double m) {  // 2^e with m < 2^e (1 for m == 0)
+  return m > 0.0 ? ldexp(1.0, ilogb(m) + 1) : 1.0;
+}
+__device__ __forceinline__ void slice8(double x, double inv, int8_t (&o)[S]) {
+  double r = x * inv;  // |r| < 1, exact
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    r *= 128.0;
+    const double t = trunc(r);
+    o[i] = static_cast<int8_t>(t);
+    r -= t;
+  }
+}
+
+// Rows of X (R × K, row-major, ldx) → out[S][R][Kp] with a per-row scale
+// (one warp per row; columns K..Kp-1 written as zero; Kp % 4 == 0).
+__global__ void oz_slice_rows_kernel(const double* __restrict__ X, long long ldx, int R, int K, int Kp,
+                                     int8_t* __restrict__ out, long long slice_stride, double* __restrict__ scale) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= R) return;
+  const double* x = X + static_cast<long long>(row) * ldx;
+  double m = 0.0;
+  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(x[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const double sc = pow2_above(m), inv = 1.0 / sc;
+  if (lane == 0) scale[row] = sc;
+  for (int k = lane * 4; k < Kp; k += 128) {
+    uint32_t w[S] = {};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int8_t o[S];
+      slice8(k + e < K ? x[k + e] : 0.0, inv, o);
+#pragma unroll
+      for (int i = 0; i < S; ++i) w[i] |= static_cast<uint32_t>(static_cast<uint8_t>(o[i])) << (8 * e);
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+      *reinterpret_cast<uint32_t*>(out + i * slice_stride + static_cast<long long>(row) * Kp + k) = w[i];
+  }
+}
+
+// Column maxima of X (Krows × R, row-major): atomically folded into
+// colmax_bits[R] (non-negative doubles order like their bit patterns).
+__global__ void oz_colmax_kernel(const double* __restrict__ X, long long ldx, long long Krows, int R,
+                                 unsigned long long* __restrict__ colmax_bits) {
+  const int r = blockIdx.x * 32 + (threadIdx.x & 31);
+  double m = 0.0;
+  if (r < R)
+    for (long long k = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5); k < Krows;
+         k += static_cast<long long>(gridDim.y) * (blockDim.x >> 5))
+      m = fmax(m, fabs(X[k * ldx + r]));
+  __shared__ double sm[32][33];
+  sm[threadIdx.x >> 5][threadIdx.x & 31] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, sm[w][threadIdx.x]);
+    if (r < R) atomicMax(colmax_bits + r, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+__global__ void oz_scale_from_max_kernel(const unsigned long long* __restrict__ colmax_bits, int R, int Rp,
+                                         double fixed, double* __restrict__ scale) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < Rp) scale[r] = fixed > 0.0 ? fixed : (r < R ? pow2_above(__longlong_as_double(colmax_bits[r])) : 1.0);
+}
+
+// Columns of X (Krows × R, row-major, ldx) → out[S][Rp][Kp] (k contiguous)
+// with per-column scales scale[Rp]. Tile: 32 columns × 128 rows per CTA
+// (256 threads). Optionally writes the CTA's column sums of X to
+// colsum[blockIdx.y][Rp] (fixed order: 16 rows per thread, then 8 threads).
+__global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __restrict__ X, long long ldx,
+                                                           long long Krows, int R, int Rp, long long Kp,
+                                                           const double* __restrict__ scale,
+                                                           int8_t* __restrict__ out, long long slice_stride,
+                                                           double* __restrict__ colsum) {
+  __shared__ uint32_t sT[S][32][33];
+  __shared__ double ssum[8][33];
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + lane;
+  const long long k0 = static_cast<long long>(blockIdx.y) * 128;
+  const double inv = r < Rp ? 1.0 / scale[r] : 1.0;
+  double csum = 0.0;
+#pragma unroll
+  for (int w4 = 0; w4 < 4; ++w4) {  // 4 words = 16 rows per thread
+    uint32_t wd[S] = {};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const long long k = k0 + ty * 16 + w4 * 4 + e;
+      const double x = (r < R && k < Krows) ? X[k * ldx + r] : 0.0;
+      csum += x;
+      int8_t o[S];
+      slice8(x, inv, o);
+#pragma unroll
+      for (int i = 0; i < S; ++i) wd[i] |= static_cast<uint32_t>(static_cast<uint8_t>(o[i])) << (8 * e);
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) sT[i][lane][ty * 4 + w4] = wd[i];
+  }
+  ssum[ty][lane] = csum;
+  __syncthreads();
+  if (colsum && ty == 0 && r < R) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += ssum[w][lane];
+    colsum[static_cast<long long>(blockIdx.y) * Rp + r] = s;
+  }
+  // write: per slice, 32 rows × 32 words (128 B) — a warp writes one row
+  for (int idx = threadIdx.x; idx < S * 32 * 32; idx += 256) {
+    const int i = idx >> 10, rr = (idx >> 5) & 31, w = idx & 31;
+    const int orow = blockIdx.x * 32 + rr;
+    const long long k = k0 + w * 4;
+    if (orow < Rp && k < Kp)
+      *reinterpret_cast<uint32_t*>(out + i * slice_stride + static_cast<long long>(orow) * Kp + k) = sT[i][rr][w];
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// Slices [S][rows][Kp] int8 (k contiguous); K elements valid along k (TMA
+// zero-fills past K), box = 128 k × box_rows × box_slices.
+inline bool make_map(CUtensorMap* map, const int8_t* base, uint64_t K, uint64_t rows, uint64_t Kp,
+                     uint64_t slice_stride, uint32_t box_rows, uint32_t box_slices) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {K, rows, static_cast<cuuint64_t>(S)};
+  cuuint64_t strides[2] = {Kp, slice_stride};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), box_rows, box_slices};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// C (+)= A·B with A slices [S][M][KpA] (rows scaled by sa), B slices
+// [S][N][KpB] (rows of Bᵀ scaled by sb). K is split into jobs of kchunk.
+inline cudaError_t launch_gemm(const int8_t* As, long long a_slice_stride, long long KpA, const int8_t* Bs,
+                               long long b_slice_stride, long long KpB, int M, int N, int K, int Mrows_a,
+                               int Nrows_b, Args args, int num_sms, cudaStream_t s) {
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
+  }
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, As, K, Mrows_a, KpA, a_slice_stride, BM, 1) ||
+      !make_map(&tb, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S))
+    return cudaErrorInvalidValue;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.m_tiles = (M + BM - 1) / BM;
+  args.n_tiles = (N + BN - 1) / BN;
+  if (args.kchunk <= 0) args.kchunk = ((K + BK - 1) / BK) * BK;
+  args.k_splits = (K + args.kchunk - 1) / args.kchunk;
+  const int jobs = args.m_tiles * args.n_tiles * args.k_splits;
+  int grid = jobs < num_sms ? jobs : num_sms;
+  if (jobs > num_sms) {  // whole n-tile groups per CTA so neighbours share the A tile in L2
+    grid = (num_sms / args.n_tiles) * args.n_tiles;
+    if (grid <= 0) grid = num_sms;
+  }
+  oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, args);
+  return cudaGetLastError();
+}
+
+}  // namespace oz
+}  // namespace bscgpu
