@@ -1044,9 +1044,14 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   }
   const long long DH = (long long)D_ * H_;
   if (oz_)
-    reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_ozpart_, d_ozcs_, oz_splits0,
-                                                             static_cast<int>((n + 127) / 128), part_stride_, D_, H_,
-                                                             Hp_, d_stats_, lay_.off_s(), lay_.off_ssT());
+  {
+    reduce_ysT_kernel<<<(DH + 255) / 256, 256, 0, s>>>(d_ozpart_, d_ozcs_, oz_splits0, 0, part_stride_, D_, H_, Hp_,
+                                                        d_stats_, lay_.off_s(), lay_.off_ssT());
+    oz::oz_colsum_reduce_kernel<<<(H_ + 7) / 8, 256, 0, s>>>(d_ozcs_, static_cast<int>((n + 127) / 128), Hp_,
+                                                             static_cast<int>(H_), d_stats_ + lay_.off_s(),
+                                                             d_stats_ + lay_.off_ssT(), static_cast<int>(H_));
+    ++launches_;
+  }
   else
     reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
                                                              part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),

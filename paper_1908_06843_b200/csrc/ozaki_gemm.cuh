@@ -15,14 +15,19 @@
 // of an fp64 DGEMM, γ_K Σ|a||b|.
 //
 // Kernel layout (one CTA per SM, persistent over jobs = (k-split, m-tile, n-tile)):
-//   warp 0: TMA producer — B tile (all S slices, 64 rows × 128 k) + A tiles
-//           (one slice, 128 rows × 128 k) through mbarrier rings;
-//   warp 1: TMEM allocation (512 columns = 8 group accumulators × 64) and the
-//           single-thread tcgen05.mma issue;
-//   warps 2-5: epilogue — tcgen05.ld of the 8 int32 groups, fp64 combine,
-//           scale, store (or accumulate) to C.
-// Operands are K-major int8, 128-byte swizzled (TMA SWIZZLE_128B ↔ UMMA
-// SWIZZLE_128B, SBO = 1024 B), K advanced by 32 bytes per MMA inside the row.
+//   warp 0: TMA producer — B tile (S slices, 128 rows × 64 k) + A tiles
+//           (one slice, 128 rows × 64 k) through mbarrier rings;
+//   warp 1: TMEM allocation (512 columns = 4 group accumulators × 128) and the
+//           single-thread tcgen05.mma issue; each tile runs in two passes over
+//           K, groups 4-7 (26 slice products) then 0-3 (10 products);
+//   warps 2-9: epilogue — tcgen05.ld of the 4 int32 groups of a pass, fp64
+//           combine (smallest weights first) across both passes, scale, store
+//           (or accumulate) to C.
+// The 128-column tile matters: on B200 a kind::i8 M=128 K=32 MMA costs the same
+// ~80 cycles for N = 32, 64 or 128 (N = 256: 1.55×; tools/ozaki_test probes),
+// so N = 128 halves the issue time of N = 64 per output column.
+// Operands are K-major int8, 64-byte swizzled (TMA SWIZZLE_64B ↔ UMMA
+// SWIZZLE_64B, SBO = 512 B), K advanced by 32 bytes per MMA inside the row.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -32,14 +37,18 @@ namespace bscgpu {
 namespace oz {
 
 constexpr int S = 8;                    // slices
-constexpr int BM = 128, BN = 64, BK = 128;
-constexpr int A_STAGES = 4, B_STAGES = 2;
-constexpr int A_BYTES = BM * BK;        // 16 KB
-constexpr int B_BYTES = S * BN * BK;    // 64 KB
+constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int GPP = 4, NPASS = 2;       // 4 group accumulators × 128 TMEM columns per pass
+constexpr int A_STAGES = 10, B_STAGES = 2;
+constexpr int A_BYTES = BM * BK;        // 8 KB: one slice
+constexpr int B_BYTES = S * BN * BK;    // 64 KB: all slices
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 32 * (2 + EPI_WARPS);  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
+constexpr int EPI_COLS = BN / 2;        // columns per epilogue thread
 constexpr int SMEM_BYTES = A_STAGES * A_BYTES + B_STAGES * B_BYTES + 1024 + 256;
-constexpr int THREADS = 320;  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
-constexpr int EPI_COLS = BN / 2;  // columns per epilogue thread
 constexpr int MAX_KJOB = 16384;         // int32 headroom per job (see above)
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+static_assert(GPP * BN <= 512 && GPP * NPASS == S, "TMEM groups");
 
 struct Args {
   int M, N;             // valid output rows / cols
@@ -99,11 +108,12 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t da, uint64_t db
           d_tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
-// K-major operand, 128-byte swizzle, 8-row groups 1024 B apart (SBO), sm_100 descriptor version 1.
+// K-major operand, 64-byte swizzle (rows of BK = 64 int8), 8-row groups 512 B
+// apart (SBO), sm_100 descriptor version 1.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr & 0x3FFFF) >> 4) | (static_cast<uint64_t>(1) << 16) |
-         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
-         (static_cast<uint64_t>(2) << 61);
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(4) << 61);
 }
 // kind::i8: D s32 (bits 4-5 = 2), A/B signed (bits 7-9, 10-12 = 1), K-major, N>>3 at 17, M>>4 at 24.
 constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -116,17 +126,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------- the GEMM
 __global__ void __launch_bounds__(THREADS, 1)
-    oz_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, Args a) {
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb8,
+                   const __grid_constant__ CUtensorMap tb4, Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_STAGES * A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + B_STAGES * B_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * A_STAGES + 2 * B_STAGES + 2);
   const uint32_t full_a = smem_u32(bars), empty_a = full_a + 8 * A_STAGES;
   const uint32_t full_b = empty_a + 8 * A_STAGES, empty_b = full_b + 8 * B_STAGES;
   const uint32_t tfull = empty_b + 8 * B_STAGES, tempty = tfull + 8;
@@ -136,7 +157,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int i = 0; i < A_STAGES; ++i) mbar_init(full_a + 8 * i, 1), mbar_init(empty_a + 8 * i, 1);
     for (int i = 0; i < B_STAGES; ++i) mbar_init(full_b + 8 * i, 1), mbar_init(empty_b + 8 * i, 1);
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -158,86 +179,99 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
         const int nt = job % a.n_tiles, mt = (job / a.n_tiles) % a.m_tiles, ks = job / per_split;
         const int k0 = ks * a.kchunk;
-        const int klen = min(a.kchunk, a.K - k0);
-        const int nkb = (klen + BK - 1) / BK;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(empty_b + 8 * bs, bph ^ 1);
-          mbar_expect_tx(full_b + 8 * bs, B_BYTES);
-          tma_load_3d(smem_u32(sB + bs * B_BYTES), &tb, k0 + kb * BK, nt * BN, 0, full_b + 8 * bs);
-          if (++bs == B_STAGES) bs = 0, bph ^= 1;
-          for (int i = 0; i < S; ++i) {
-            mbar_wait(empty_a + 8 * as, aph ^ 1);
-            mbar_expect_tx(full_a + 8 * as, A_BYTES);
-            tma_load_3d(smem_u32(sA + as * A_BYTES), &ta, k0 + kb * BK, mt * BM, i, full_a + 8 * as);
-            if (++as == A_STAGES) as = 0, aph ^= 1;
+        const int nkb = (min(a.kchunk, a.K - k0) + BK - 1) / BK;
+        for (int p = 0; p < NPASS; ++p) {
+          const int gbase = (NPASS - 1 - p) * GPP;  // high groups first
+          const int nA = min(S, gbase + GPP);       // A slices 0 … nA−1 take part
+          const bool all_b = nA == S;               // B slices 0 … nA−1 likewise
+          for (int kb = 0; kb < nkb; ++kb) {
+            const int kc = k0 + kb * BK;
+            mbar_wait(empty_b + 8 * bs, bph ^ 1);
+            mbar_expect_tx(full_b + 8 * bs, all_b ? B_BYTES : B_BYTES / 2);
+            tma_load_3d(smem_u32(sB + bs * B_BYTES), all_b ? &tb8 : &tb4, kc, nt * BN, 0, full_b + 8 * bs);
+            if (++bs == B_STAGES) bs = 0, bph ^= 1;
+            for (int i = 0; i < nA; ++i) {
+              mbar_wait(empty_a + 8 * as, aph ^ 1);
+              mbar_expect_tx(full_a + 8 * as, A_BYTES);
+              tma_load_3d(smem_u32(sA + as * A_BYTES), &ta, kc, mt * BM, i, full_a + 8 * as);
+              if (++as == A_STAGES) as = 0, aph ^= 1;
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int as = 0, bs = 0, t = 0;
+      int as = 0, bs = 0, u = 0;
       uint32_t aph = 0, bph = 0;
-      for (int job = blockIdx.x; job < jobs; job += gridDim.x, ++t) {
+      for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
         const int ks = job / per_split;
         const int k0 = ks * a.kchunk;
-        const int klen = min(a.kchunk, a.K - k0);
-        const int nkb = (klen + BK - 1) / BK;
-        if (t > 0) mbar_wait(tempty, (t - 1) & 1);  // the epilogue drained job t-1
-        tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(full_b + 8 * bs, bph);
-          const uint32_t b_base = smem_u32(sB + bs * B_BYTES);
-          for (int i = 0; i < S; ++i) {
-            mbar_wait(full_a + 8 * as, aph);
-            tc_fence_after();
-            const uint64_t da = sdesc(smem_u32(sA + as * A_BYTES));
-            for (int j = 0; j < S - i; ++j) {
-              const uint64_t db = sdesc(b_base + j * BN * BK);
-              const uint32_t d = tmem + (i + j) * BN;
+        const int nkb = (min(a.kchunk, a.K - k0) + BK - 1) / BK;
+        for (int p = 0; p < NPASS; ++p, ++u) {
+          const int gbase = (NPASS - 1 - p) * GPP;
+          const int nA = min(S, gbase + GPP);
+          if (u > 0) mbar_wait(tempty, (u - 1) & 1);  // the epilogue drained the previous pass
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(full_b + 8 * bs, bph);
+            const uint32_t b_base = smem_u32(sB + bs * B_BYTES);
+            for (int i = 0; i < nA; ++i) {
+              mbar_wait(full_a + 8 * as, aph);
+              tc_fence_after();
+              const uint64_t da = sdesc(smem_u32(sA + as * A_BYTES));
+              // groups g = i + j in [gbase, gbase + GPP): i = 0 comes first and opens all of them
+              const int j0 = max(0, gbase - i), j1 = min(S - 1 - i, gbase + GPP - 1 - i);
+              for (int j = j0; j <= j1; ++j) {
+                const uint64_t db = sdesc(b_base + j * BN * BK);
+                const uint32_t d = tmem + (i + j - gbase) * BN;
 #pragma unroll
-              for (int kk = 0; kk < BK / 32; ++kk)
-                mma_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb | i | kk) != 0);
+                for (int kk = 0; kk < BK / 32; ++kk)
+                  mma_i8(d, da + 2 * kk, db + 2 * kk, kIdesc, (kb | i | kk) != 0);
+              }
+              tc_commit(empty_a + 8 * as);
+              if (++as == A_STAGES) as = 0, aph ^= 1;
             }
-            tc_commit(empty_a + 8 * as);
-            if (++as == A_STAGES) as = 0, aph ^= 1;
+            tc_commit(empty_b + 8 * bs);
+            if (++bs == B_STAGES) bs = 0, bph ^= 1;
           }
-          tc_commit(empty_b + 8 * bs);
-          if (++bs == B_STAGES) bs = 0, bph ^= 1;
+          tc_commit(tfull);
         }
-        tc_commit(tfull);
       }
     }
     __syncwarp();
   } else {
-    const int q = warp & 3;         // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) >> 2;  // which half of the 64 columns
+    const int q = warp & 3;                  // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;        // which half of the BN columns
     const int row = q * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * EPI_COLS;
-    int t = 0;
-    for (int job = blockIdx.x; job < jobs; job += gridDim.x, ++t) {
+    int u = 0;
+    for (int job = blockIdx.x; job < jobs; job += gridDim.x) {
       const int nt = job % a.n_tiles, mt = (job / a.n_tiles) % a.m_tiles, ks = job / per_split;
-      mbar_wait(tfull, t & 1);
-      tc_fence_after();
       double acc[EPI_COLS];
 #pragma unroll
       for (int c = 0; c < EPI_COLS; ++c) acc[c] = 0.0;
 #pragma unroll
-      for (int g = S - 1; g >= 0; --g) {
-        const double w = ldexp(1.0, -7 * (g + 2));
-        int v0[16], v1[16];
-        tmem_ld16(tbase + g * BN, v0);
-        tmem_ld16(tbase + g * BN + 16, v1);
-        tmem_wait_ld();
+      for (int p = 0; p < NPASS; ++p, ++u) {
+        const int gbase = (NPASS - 1 - p) * GPP;
+        mbar_wait(tfull, u & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int x = 0; x < 16; ++x) {
-          acc[x] = fma(static_cast<double>(v0[x]), w, acc[x]);
-          acc[16 + x] = fma(static_cast<double>(v1[x]), w, acc[16 + x]);
+        for (int gl = GPP - 1; gl >= 0; --gl) {  // smallest weights first
+          const double w = ldexp(1.0, -7 * (gbase + gl + 2));
+#pragma unroll
+          for (int h = 0; h < EPI_COLS / 32; ++h) {
+            int v[32];
+            tmem_ld32(tbase + gl * BN + h * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 32; ++x) acc[h * 32 + x] = fma(static_cast<double>(v[x]), w, acc[h * 32 + x]);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
       const int m = mt * BM + row;
       if (m < a.M) {
         const double sam = a.sa[ks * a.sa_stride + m];
@@ -318,6 +352,22 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ X, long long ldx
   }
 }
 
+// Σ over `rows` partial rows (stride ldp) per column h < H, one warp per
+// column: lane-strided sums then a shuffle tree (a fixed order).
+__global__ void oz_colsum_reduce_kernel(const double* __restrict__ part, int rows, int ldp, int H,
+                                        double* __restrict__ out, double* __restrict__ out_diag, int diag_ld) {
+  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (h >= H) return;
+  double s = 0.0;
+  for (int z = lane; z < rows; z += 32) s += part[static_cast<long long>(z) * ldp + h];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    out[h] = s;
+    if (out_diag) out_diag[static_cast<long long>(h) * diag_ld + h] = s;
+  }
+}
+
 // Column maxima of X (Krows × R, row-major): atomically folded into
 // colmax_bits[R] (non-negative doubles order like their bit patterns).
 __global__ void oz_colmax_kernel(const double* __restrict__ X, long long ldx, long long Krows, int R,
@@ -357,14 +407,19 @@ __global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __rest
   const int r = blockIdx.x * 32 + lane;
   const long long k0 = static_cast<long long>(blockIdx.y) * 128;
   const double inv = r < Rp ? 1.0 / scale[r] : 1.0;
+  double xv[16];  // all 16 loads in flight before any slicing
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const long long k = k0 + ty * 16 + e;
+    xv[e] = (r < R && k < Krows) ? __ldcs(X + k * ldx + r) : 0.0;
+  }
   double csum = 0.0;
 #pragma unroll
   for (int w4 = 0; w4 < 4; ++w4) {  // 4 words = 16 rows per thread
     uint32_t wd[S] = {};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const long long k = k0 + ty * 16 + w4 * 4 + e;
-      const double x = (r < R && k < Krows) ? X[k * ldx + r] : 0.0;
+      const double x = xv[w4 * 4 + e];
       csum += x;
       int8_t o[S];
       slice8(x, inv, o);
@@ -409,7 +464,7 @@ inline EncodeTiledFn encode_fn() {
 }
 
 // Slices [S][rows][Kp] int8 (k contiguous); K elements valid along k (TMA
-// zero-fills past K), box = 128 k × box_rows × box_slices.
+// zero-fills past K), box = BK k × box_rows × box_slices, 64-byte swizzle.
 inline bool make_map(CUtensorMap* map, const int8_t* base, uint64_t K, uint64_t rows, uint64_t Kp,
                      uint64_t slice_stride, uint32_t box_rows, uint32_t box_slices) {
   EncodeTiledFn fn = encode_fn();
@@ -419,7 +474,7 @@ inline bool make_map(CUtensorMap* map, const int8_t* base, uint64_t K, uint64_t 
   cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), box_rows, box_slices};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -436,9 +491,10 @@ inline cudaError_t launch_gemm(const int8_t* As, long long a_slice_stride, long 
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb8, tb4;
   if (!make_map(&ta, As, K, Mrows_a, KpA, a_slice_stride, BM, 1) ||
-      !make_map(&tb, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S))
+      !make_map(&tb8, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S) ||
+      !make_map(&tb4, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S / 2))
     return cudaErrorInvalidValue;
   args.M = M;
   args.N = N;
@@ -453,7 +509,7 @@ inline cudaError_t launch_gemm(const int8_t* As, long long a_slice_stride, long 
     grid = (num_sms / args.n_tiles) * args.n_tiles;
     if (grid <= 0) grid = num_sms;
   }
-  oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, args);
+  oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb8, tb4, args);
   return cudaGetLastError();
 }
 
