@@ -188,7 +188,7 @@ void BscEngine::init(int device) {
   oz_ = !vpath() && Kp_ <= oz::MAX_KJOB;
   if (const char* e = std::getenv("BSC_GEMM")) oz_ = oz_ && std::strcmp(e, "dmma") != 0;
   if (oz_) {
-    d_ws_ = dalloc<int8_t>((size_t)oz::S * Hp_ * Kp_, "W slices");
+    d_ws_ = dalloc<int8_t>((size_t)oz::S * Hp_ * round_up(Dp_, oz::BK), "W slices");
     d_wsb_ = dalloc<double>(Hp_, "W slice scales");
     d_two_ = dalloc<double>(Hp_, "ES slice scale");
     d_ytsa_ = dalloc<double>((size_t)kMaxChunks * Dp_, "Yt slice scales");
@@ -660,8 +660,8 @@ void BscEngine::slice_y(uint64_t off, uint64_t rows, int chunk, void* stream) {
   double* sc = d_ytsa_ + (size_t)chunk * Dp_;
   oz::oz_scale_from_max_kernel<<<(Dp_ + 255) / 256, 256, 0, s>>>(d_ozmax_ + Hp_, static_cast<int>(D_), Dp_, 0.0, sc);
   oz::oz_slice_cols_kernel<<<dim3((Dp_ + 31) / 32, static_cast<unsigned>((rows + 127) / 128)), 256, 0, s>>>(
-      y, Dp_, static_cast<long long>(rows), static_cast<int>(D_), Dp_, oz_np_, sc, d_yts_ + off,
-      static_cast<long long>(Dp_) * oz_np_, nullptr);
+      y, Dp_, static_cast<long long>(rows), static_cast<int>(D_), Dp_, (static_cast<long long>(rows) + 127) / 128 * 128,
+      sc, d_yts_ + (off / oz::BK) * Dp_ * oz::BK, static_cast<long long>(Dp_) * oz_np_, nullptr);
   ck(cudaGetLastError(), "slice Y");
   launches_ += 4;
 }
@@ -673,9 +673,10 @@ void BscEngine::slice_w(void* stream) {
   oz::oz_colmax_kernel<<<dim3((Hp_ + 31) / 32, 4), 256, 0, s>>>(d_w_, Hp_, static_cast<long long>(D_),
                                                                 static_cast<int>(H_), d_ozmax_);
   oz::oz_scale_from_max_kernel<<<(Hp_ + 255) / 256, 256, 0, s>>>(d_ozmax_, static_cast<int>(H_), Hp_, 0.0, d_wsb_);
-  oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, (Kp_ + 127) / 128), 256, 0, s>>>(
-      d_w_, Hp_, static_cast<long long>(D_), static_cast<int>(H_), Hp_, Kp_, d_wsb_, d_ws_,
-      static_cast<long long>(Hp_) * Kp_, nullptr);
+  const int kpw = round_up(Dp_, oz::BK);
+  oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, (kpw + 127) / 128), 256, 0, s>>>(
+      d_w_, Hp_, static_cast<long long>(D_), static_cast<int>(H_), Hp_, kpw, d_wsb_, d_ws_,
+      static_cast<long long>(Hp_) * kpw, nullptr);
   ck(cudaGetLastError(), "slice W");
   launches_ += 3;
 }
@@ -991,9 +992,9 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       g.sb = d_wsb_;
       g.C = d_b_ + off * Hp_;
       g.ldc = Hp_;
-      ck(oz::launch_gemm(d_ys_ + off * Kp_, cap_rows * Kp_, Kp_, d_ws_, static_cast<long long>(Hp_) * Kp_, Kp_,
-                         static_cast<int>(rows), Hp_, Kp_, static_cast<int>(rows), Hp_, g, oz_sms(device_), s),
-         "oz gemm Y·W");
+      const oz::Operand A{d_ys_ + off * Kp_, cap_rows * Kp_, Kp_, static_cast<int>(rows), 0};
+      const oz::Operand B{d_ws_, static_cast<long long>(Hp_) * round_up(Dp_, oz::BK), Hp_, Hp_, 1};
+      ck(oz::launch_gemm(A, B, static_cast<int>(rows), Hp_, Kp_, g, oz_sms(device_), s), "oz gemm Y·W");
       ++launches_;
     } else {  // K1: B = Y·W
       GemmArgs g{static_cast<int>(rows), Hp_, Dp_, d_y_ + off * Dp_, Dp_, d_w_, Hp_, d_b_ + off * Hp_, Hp_,
@@ -1007,8 +1008,9 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     if (oz_) {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES — ⟨S⟩ᵀ slices (+ column sums = Σ⟨s⟩ partials), then tcgen05
       const unsigned kb = static_cast<unsigned>((rows + 127) / 128);
       oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, kb), 256, 0, s>>>(
-          d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_, oz_npc_, d_two_, d_ess_,
-          static_cast<long long>(Hp_) * oz_npc_, d_ozcs_ + (off / 128) * Hp_);
+          d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_,
+          (static_cast<long long>(rows) + 127) / 128 * 128, d_two_, d_ess_, static_cast<long long>(Hp_) * oz_npc_,
+          d_ozcs_ + (off / 128) * Hp_);
       ck(cudaGetLastError(), "slice ES");
       oz::Args g{};
       g.sa = d_ytsa_ + (size_t)((host_y || nchunks > 1) ? c : 0) * Dp_;
@@ -1018,9 +1020,10 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       g.kchunk = oz_kchunk;
       g.c_split_stride = part_stride_;
       g.accumulate = c > 0;
-      ck(oz::launch_gemm(d_yts_ + off, static_cast<long long>(Dp_) * oz_np_, oz_np_, d_ess_,
-                         static_cast<long long>(Hp_) * oz_npc_, oz_npc_, static_cast<int>(D_), static_cast<int>(H_),
-                         static_cast<int>(rows), Dp_, Hp_, g, oz_sms(device_), s),
+      const oz::Operand A{d_yts_ + (off / oz::BK) * Dp_ * oz::BK, static_cast<long long>(Dp_) * oz_np_, Dp_, Dp_, 1};
+      const oz::Operand B{d_ess_, static_cast<long long>(Hp_) * oz_npc_, Hp_, Hp_, 1};
+      ck(oz::launch_gemm(A, B, static_cast<int>(D_), static_cast<int>(H_), static_cast<int>(rows), g, oz_sms(device_),
+                         s),
          "oz gemm Yt·ES");
       launches_ += 2;
     } else {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES over this chunk (+ fused Σ⟨s⟩), split-K over its rows

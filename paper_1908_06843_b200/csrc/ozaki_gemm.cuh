@@ -63,6 +63,20 @@ struct Args {
   long long ldc;
   long long c_split_stride;  // partial slot stride per k-split
   int accumulate;            // C += result (else C = result)
+  int blk_a, blk_b;          // operand layout: 0 rows [S][rows][ld], 1 K-blocked [S][k/BK][rows][BK]
+};
+
+// One sliced operand: slice s, row r, k at
+//   rows layout:      base + s·slice_stride + r·ld + k
+//   K-blocked layout: base + s·slice_stride + ((k / BK)·ld + r)·BK + k % BK   (ld = allocated rows)
+// The K-blocked layout keeps every TMA box (BK × rows) one contiguous run,
+// which matters when k is the point index (rows ~N bytes apart otherwise).
+struct Operand {
+  const int8_t* base;
+  long long slice_stride;
+  long long ld;
+  int rows;      // valid rows (TMA zero-fills past them)
+  int blocked;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -95,6 +109,21 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "[%5];\n" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_op(uint32_t dst, const CUtensorMap* map, bool blocked, int k, int row,
+                                            int slice, uint32_t bar) {
+  if (blocked)
+    tma_load_4d(dst, map, 0, row, k / BK, slice, bar);
+  else
+    tma_load_3d(dst, map, k, row, slice, bar);
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -188,12 +217,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int kc = k0 + kb * BK;
             mbar_wait(empty_b + 8 * bs, bph ^ 1);
             mbar_expect_tx(full_b + 8 * bs, all_b ? B_BYTES : B_BYTES / 2);
-            tma_load_3d(smem_u32(sB + bs * B_BYTES), all_b ? &tb8 : &tb4, kc, nt * BN, 0, full_b + 8 * bs);
+            tma_load_op(smem_u32(sB + bs * B_BYTES), all_b ? &tb8 : &tb4, a.blk_b, kc, nt * BN, 0, full_b + 8 * bs);
             if (++bs == B_STAGES) bs = 0, bph ^= 1;
             for (int i = 0; i < nA; ++i) {
               mbar_wait(empty_a + 8 * as, aph ^ 1);
               mbar_expect_tx(full_a + 8 * as, A_BYTES);
-              tma_load_3d(smem_u32(sA + as * A_BYTES), &ta, kc, mt * BM, i, full_a + 8 * as);
+              tma_load_op(smem_u32(sA + as * A_BYTES), &ta, a.blk_a, kc, mt * BM, i, full_a + 8 * as);
               if (++as == A_STAGES) as = 0, aph ^= 1;
             }
           }
@@ -392,7 +421,7 @@ __global__ void oz_scale_from_max_kernel(const unsigned long long* __restrict__ 
   if (r < Rp) scale[r] = fixed > 0.0 ? fixed : (r < R ? pow2_above(__longlong_as_double(colmax_bits[r])) : 1.0);
 }
 
-// Columns of X (Krows × R, row-major, ldx) → out[S][Rp][Kp] (k contiguous)
+// Columns of X (Krows × R, row-major, ldx) → out[S][Kp/BK][Rp][BK] (K-blocked, Kp % BK == 0)
 // with per-column scales scale[Rp]. Tile: 32 columns × 128 rows per CTA
 // (256 threads). Optionally writes the CTA's column sums of X to
 // colsum[blockIdx.y][Rp] (fixed order: 16 rows per thread, then 8 threads).
@@ -442,7 +471,7 @@ __global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __rest
     const int orow = blockIdx.x * 32 + rr;
     const long long k = k0 + w * 4;
     if (orow < Rp && k < Kp)
-      *reinterpret_cast<uint32_t*>(out + i * slice_stride + static_cast<long long>(orow) * Kp + k) = sT[i][rr][w];
+      *reinterpret_cast<uint32_t*>(out + i * slice_stride + ((k / BK) * Rp + orow) * BK + (k % BK)) = sT[i][rr][w];
   }
 }
 
@@ -463,26 +492,34 @@ inline EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Slices [S][rows][Kp] int8 (k contiguous); K elements valid along k (TMA
-// zero-fills past K), box = BK k × box_rows × box_slices, 64-byte swizzle.
-inline bool make_map(CUtensorMap* map, const int8_t* base, uint64_t K, uint64_t rows, uint64_t Kp,
-                     uint64_t slice_stride, uint32_t box_rows, uint32_t box_slices) {
+// TMA map of an operand: box = BK k × box_rows × box_slices, 64-byte swizzle;
+// K elements valid along k (TMA zero-fills past K and past the valid rows).
+inline bool make_map(CUtensorMap* map, const Operand& op, uint64_t K, uint32_t box_rows, uint32_t box_slices) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {K, rows, static_cast<cuuint64_t>(S)};
-  cuuint64_t strides[2] = {Kp, slice_stride};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (op.blocked) {
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(op.rows), (K + BK - 1) / BK,
+                          static_cast<cuuint64_t>(S)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(BK), static_cast<cuuint64_t>(op.ld) * BK,
+                             static_cast<cuuint64_t>(op.slice_stride)};
+    cuuint32_t box[4] = {static_cast<cuuint32_t>(BK), box_rows, 1, box_slices};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(op.base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  cuuint64_t dims[3] = {K, static_cast<cuuint64_t>(op.rows), static_cast<cuuint64_t>(S)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(op.ld), static_cast<cuuint64_t>(op.slice_stride)};
   cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), box_rows, box_slices};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(op.base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// C (+)= A·B with A slices [S][M][KpA] (rows scaled by sa), B slices
-// [S][N][KpB] (rows of Bᵀ scaled by sb). K is split into jobs of kchunk.
-inline cudaError_t launch_gemm(const int8_t* As, long long a_slice_stride, long long KpA, const int8_t* Bs,
-                               long long b_slice_stride, long long KpB, int M, int N, int K, int Mrows_a,
-                               int Nrows_b, Args args, int num_sms, cudaStream_t s) {
+// C (+)= A·B over K with A slices (rows scaled by sa) and B slices (rows of Bᵀ
+// scaled by sb); K is split into jobs of args.kchunk (multiple of BK).
+inline cudaError_t launch_gemm(const Operand& A, const Operand& B, int M, int N, int K, Args args, int num_sms,
+                               cudaStream_t s) {
   static bool attr[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -492,10 +529,10 @@ inline cudaError_t launch_gemm(const int8_t* As, long long a_slice_stride, long 
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   CUtensorMap ta, tb8, tb4;
-  if (!make_map(&ta, As, K, Mrows_a, KpA, a_slice_stride, BM, 1) ||
-      !make_map(&tb8, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S) ||
-      !make_map(&tb4, Bs, K, Nrows_b, KpB, b_slice_stride, BN, S / 2))
+  if (!make_map(&ta, A, K, BM, 1) || !make_map(&tb8, B, K, BN, S) || !make_map(&tb4, B, K, BN, S / 2))
     return cudaErrorInvalidValue;
+  args.blk_a = A.blocked;
+  args.blk_b = B.blocked;
   args.M = M;
   args.N = N;
   args.K = K;

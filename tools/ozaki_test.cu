@@ -48,7 +48,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&dsb, (size_t)Np * 8));
     CK(cudaMalloc(&dmax, (size_t)Np * 8));
     CK(cudaMalloc(&dYs, (size_t)oz::S * M * Kp));
-    CK(cudaMalloc(&dWs, (size_t)oz::S * Np * Kp));
+    CK(cudaMalloc(&dWs, (size_t)oz::S * Np * rup(K, 64)));
     CK(cudaMemcpy(dY, Y.data(), Y.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dW, W.data(), W.size() * 8, cudaMemcpyHostToDevice));
     CK(cudaMemset(dmax, 0, Np * 8));
@@ -63,8 +63,9 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms_slice, e0, e1);
     oz::oz_colmax_kernel<<<dim3((N + 31) / 32, 8), 256>>>(dW, N, K, N, dmax);
     oz::oz_scale_from_max_kernel<<<(Np + 255) / 256, 256>>>(dmax, N, (int)Np, 0.0, dsb);
-    oz::oz_slice_cols_kernel<<<dim3((Np + 31) / 32, (Kp + 127) / 128), 256>>>(dW, N, K, N, (int)Np, Kp, dsb, dWs,
-                                                                             Np * Kp, nullptr);
+    oz::oz_slice_cols_kernel<<<dim3((Np + 31) / 32, (rup(K, 64) + 127) / 128), 256>>>(dW, N, K, N, (int)Np, rup(K, 64),
+                                                                                      dsb, dWs, Np * rup(K, 64), nullptr);
+    const oz::Operand opA{dYs, (long long)M * Kp, Kp, M, 0}, opB{dWs, Np * rup(K, 64), Np, (int)Np, 1};
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     oz::Args a{};
@@ -72,7 +73,7 @@ int main(int argc, char** argv) {
     a.sb = dsb;
     a.C = dC;
     a.ldc = Np;
-    CK(oz::launch_gemm(dYs, (long long)M * Kp, Kp, dWs, Np * Kp, Kp, M, N, K, M, (int)Np, a, sms, 0));
+    CK(oz::launch_gemm(opA, opB, M, N, (int)Kp, a, sms, 0));
     CK(cudaDeviceSynchronize());
     std::vector<double> C((size_t)M * Np);
     CK(cudaMemcpy(C.data(), dC, C.size() * 8, cudaMemcpyDeviceToHost));
@@ -93,11 +94,11 @@ int main(int argc, char** argv) {
         worst_rel = fmax(worst_rel, err / (double)absum);
       }
     }
-    for (int it = 0; it < 3; ++it) CK(oz::launch_gemm(dYs, (long long)M * Kp, Kp, dWs, Np * Kp, Kp, M, N, K, M, (int)Np, a, sms, 0));
+    for (int it = 0; it < 3; ++it) CK(oz::launch_gemm(opA, opB, M, N, (int)Kp, a, sms, 0));
     cudaEventRecord(e0);
     const int reps = 10;
     for (int it = 0; it < reps; ++it)
-      CK(oz::launch_gemm(dYs, (long long)M * Kp, Kp, dWs, Np * Kp, Kp, M, N, K, M, (int)Np, a, sms, 0));
+      CK(oz::launch_gemm(opA, opB, M, N, (int)Kp, a, sms, 0));
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -146,7 +147,8 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
     float ms_slice;
     cudaEventElapsedTime(&ms_slice, e0, e1);
-    const int kchunk = 128 * (int)std::min<long long>(oz::MAX_KJOB / 128, (Pp / 128 + 13) / 14);
+    const int kchunk = 128 * (int)std::min<long long>(oz::MAX_KJOB / 128, (Pp / 128 + 23) / 24);
+    const oz::Operand opA{dYs, Dp * Pp, Dp, (int)Dp, 1}, opB{dEs, Hp * Pp, Hp, (int)Hp, 1};
     const int splits = (P + kchunk - 1) / kchunk;
     CK(cudaMalloc(&dC, (size_t)splits * Dp * Hp * 8));
     oz::Args a{};
@@ -156,7 +158,7 @@ int main(int argc, char** argv) {
     a.ldc = Hp;
     a.kchunk = kchunk;
     a.c_split_stride = Dp * Hp;
-    CK(oz::launch_gemm(dYs, Dp * Pp, Pp, dEs, Hp * Pp, Pp, D, H, P, (int)Dp, (int)Hp, a, sms, 0));
+    CK(oz::launch_gemm(opA, opB, D, H, P, a, sms, 0));
     CK(cudaDeviceSynchronize());
     std::vector<double> Cp((size_t)splits * Dp * Hp);
     CK(cudaMemcpy(Cp.data(), dC, Cp.size() * 8, cudaMemcpyDeviceToHost));
@@ -182,7 +184,7 @@ int main(int argc, char** argv) {
     cudaEventRecord(e0);
     const int reps = 10;
     for (int it = 0; it < reps; ++it)
-      CK(oz::launch_gemm(dYs, Dp * Pp, Pp, dEs, Hp * Pp, Pp, D, H, P, (int)Dp, (int)Hp, a, sms, 0));
+      CK(oz::launch_gemm(opA, opB, D, H, P, a, sms, 0));
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
