@@ -342,14 +342,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 __device__ __forceinline__ double pow2_above(double m) {  // 2^e with m < 2^e (1 for m == 0)
   return m > 0.0 ? ldexp(1.0, ilogb(m) + 1) : 1.0;
 }
-__device__ __forceinline__ void slice8(double x, double inv, int8_t (&o)[S]) {
-  double r = x * inv;  // |r| < 1, exact
+// The slices of x = scale·r (|r| < 1): a_i = sign(x)·⌊|r|·2^{7(i+1)}⌋ mod 2^7, i.e.
+// the base-128 digits of m = ⌊|r|·2⁵⁶⌋ (< 2⁵⁶) with x's sign — the same digits
+// as truncating r·2⁷ step by step, from one exact product and one conversion.
+// inv56 = 2⁵⁶ / scale (a power of two).
+__device__ __forceinline__ void slice8(double x, double inv56, int8_t (&o)[S]) {
+  const unsigned long long m = static_cast<unsigned long long>(fabs(x) * inv56);
+  const bool neg = x < 0.0;
 #pragma unroll
   for (int i = 0; i < S; ++i) {
-    r *= 128.0;
-    const double t = trunc(r);
-    o[i] = static_cast<int8_t>(t);
-    r -= t;
+    const int v = static_cast<int>((m >> (7 * (S - 1 - i))) & 127u);
+    o[i] = static_cast<int8_t>(neg ? -v : v);
   }
 }
 
@@ -364,7 +367,7 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ X, long long ldx
   for (int k = lane; k < K; k += 32) m = fmax(m, fabs(x[k]));
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const double sc = pow2_above(m), inv = 1.0 / sc;
+  const double sc = pow2_above(m), inv = ldexp(1.0 / sc, 56);
   if (lane == 0) scale[row] = sc;
   for (int k = lane * 4; k < Kp; k += 128) {
     uint32_t w[S] = {};
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __rest
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int r = blockIdx.x * 32 + lane;
   const long long k0 = static_cast<long long>(blockIdx.y) * 128;
-  const double inv = r < Rp ? 1.0 / scale[r] : 1.0;
+  const double inv = ldexp(r < Rp ? 1.0 / scale[r] : 1.0, 56);
   double xv[16];  // all 16 loads in flight before any slicing
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
