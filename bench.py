@@ -108,6 +108,15 @@ def fp64_peak():
     return 37.0, 37.0, "nominal B200 FP64 (no measurement found)"
 
 
+def int8_peak():
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) as f:
+            bf16 = json.load(f)["bf16_tflops"]
+        return round(2.0 * bf16, 1), "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense int8 = 2 x bf16)"
+    except Exception:
+        return 4500.0, "nominal B200 dense int8 (4.5 POPS)"
+
+
 def cpu_reference_rate(w, n_sample, threads, use_ref=True):
     """Reference (or C port) CPU EM step on a bounded sample: points/s."""
     from oracle import oracle as O
@@ -275,6 +284,20 @@ def main():
     achieved = fl / (tms / 1e3) / 1e12
     kernels = {k: {"ms": round(v[1], 4), "tflops": round(v[0] / (v[1] / 1e3) / 1e12, 3) if v[1] else None,
                    "frac": round(v[0] / (v[1] / 1e3) / 1e12 / v[2], 4) if v[1] else None} for k, v in rows.items()}
+    # Y·W and Yᵀ⟨S⟩ run on the int8 tensor cores by exact slicing (ozaki_gemm.cuh):
+    # 36 slice products of 2·N·D·H int8 ops each; "tflops"/"frac" above are the
+    # fp64-equivalent rate against the DMMA peak, these the int8 rate against
+    # the int8 dense peak (2× the measured bf16 peak, the B200 int8:bf16 ratio).
+    if os.environ.get("BSC_GEMM", "") != "dmma":
+        i8_peak, i8_src = int8_peak()
+        for k in ("gemm_yw", "gemm_ytes"):
+            t = kernels[k]["ms"]
+            if t:
+                tops = 36.0 * gemm_flops / (t / 1e3) / 1e12
+                kernels[k].update({"path": "int8 slices on tcgen05 (kind::i8)", "int8_tops": round(tops, 1),
+                                   "int8_frac": round(tops / i8_peak, 4), "int8_peak": i8_peak,
+                                   "int8_peak_source": i8_src})
+        kernels["gemm_ytes"]["includes"] = "⟨S⟩ slicing + column sums"
     kernels.update({k: {"ms": round(kern[k], 4)} for k in ("gram", "finalize", "mstep")})
     step_flops = (dense + state) * n_total
     line = {

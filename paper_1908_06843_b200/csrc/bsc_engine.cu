@@ -185,7 +185,7 @@ void BscEngine::init(int device) {
   // Y·W and Yᵀ⟨S⟩ on the integer tensor cores (ozaki_gemm.cuh) for the binary
   // family (⟨s⟩ ∈ [0, 1] gives ⟨S⟩ a fixed slice scale); BSC_GEMM=dmma keeps them on DMMA
   Kp_ = round_up(Dp_, 16);
-  oz_ = !vpath() && Kp_ <= oz::MAX_KJOB;
+  oz_ = !vpath() && Kp_ <= oz::MAX_KROW;
   if (const char* e = std::getenv("BSC_GEMM")) oz_ = oz_ && std::strcmp(e, "dmma") != 0;
   if (oz_) {
     d_ws_ = dalloc<int8_t>((size_t)oz::S * Hp_ * round_up(Dp_, oz::BK), "W slices");
@@ -651,8 +651,8 @@ void BscEngine::slice_y(uint64_t off, uint64_t rows, int chunk, void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
   const long long cap_rows = static_cast<long long>((cap_n_ + 1) & ~1ull);
   const double* y = d_y_ + off * Dp_;
-  oz::oz_slice_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
-      y, Dp_, static_cast<int>(rows), Dp_, Kp_, d_ys_ + off * Kp_, cap_rows * Kp_, d_ysa_ + off);
+  ck(oz::slice_rows(y, Dp_, static_cast<int>(rows), Dp_, Kp_, d_ys_ + off * Kp_, cap_rows * Kp_, d_ysa_ + off, s),
+     "slice Y rows");
   ck(cudaMemsetAsync(d_ozmax_ + Hp_, 0, (size_t)Dp_ * 8, s), "zero maxima");
   const unsigned gy = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(256, rows / 512)));
   oz::oz_colmax_kernel<<<dim3((Dp_ + 31) / 32, gy), 256, 0, s>>>(y, Dp_, static_cast<long long>(rows),

@@ -47,6 +47,7 @@ constexpr int THREADS = 32 * (2 + EPI_WARPS);  // producer, MMA, 8 epilogue warp
 constexpr int EPI_COLS = BN / 2;        // columns per epilogue thread
 constexpr int SMEM_BYTES = A_STAGES * A_BYTES + B_STAGES * B_BYTES + 1024 + 256;
 constexpr int MAX_KJOB = 16384;         // int32 headroom per job (see above)
+constexpr int MAX_KROW = 1024;          // longest row the row slicer holds in registers
 static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 static_assert(GPP * BN <= 512 && GPP * NPASS == S, "TMEM groups");
 
@@ -357,24 +358,46 @@ __device__ __forceinline__ void slice8(double x, double inv56, int8_t (&o)[S]) {
 }
 
 // Rows of X (R × K, row-major, ldx) → out[S][R][Kp] with a per-row scale
-// (one warp per row; columns K..Kp-1 written as zero; Kp % 4 == 0).
-__global__ void oz_slice_rows_kernel(const double* __restrict__ X, long long ldx, int R, int K, int Kp,
-                                     int8_t* __restrict__ out, long long slice_stride, double* __restrict__ scale) {
+// (one warp per row, the row read once into registers: NIT·128 ≥ Kp columns;
+// columns K..Kp-1 written as zero; Kp % 4 == 0, ldx even).
+template <int NIT>
+__global__ void __launch_bounds__(256) oz_slice_rows_kernel(const double* __restrict__ X, long long ldx, int R, int K,
+                                                            int Kp, int8_t* __restrict__ out, long long slice_stride,
+                                                            double* __restrict__ scale) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= R) return;
   const double* x = X + static_cast<long long>(row) * ldx;
+  double v[NIT][4];
   double m = 0.0;
-  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(x[k]));
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int k = it * 128 + lane * 4;
+#pragma unroll
+    for (int e = 0; e < 4; e += 2) {
+      double2 p = make_double2(0.0, 0.0);
+      if (k + e + 1 < K) {
+        p = __ldcs(reinterpret_cast<const double2*>(x + k + e));
+      } else if (k + e < K) {
+        p.x = x[k + e];
+      }
+      v[it][e] = p.x;
+      v[it][e + 1] = p.y;
+      m = fmax(m, fmax(fabs(p.x), fabs(p.y)));
+    }
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const double sc = pow2_above(m), inv = ldexp(1.0 / sc, 56);
   if (lane == 0) scale[row] = sc;
-  for (int k = lane * 4; k < Kp; k += 128) {
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int k = it * 128 + lane * 4;
+    if (k >= Kp) break;
     uint32_t w[S] = {};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       int8_t o[S];
-      slice8(k + e < K ? x[k + e] : 0.0, inv, o);
+      slice8(v[it][e], inv, o);
 #pragma unroll
       for (int i = 0; i < S; ++i) w[i] |= static_cast<uint32_t>(static_cast<uint8_t>(o[i])) << (8 * e);
     }
@@ -382,6 +405,23 @@ __global__ void oz_slice_rows_kernel(const double* __restrict__ X, long long ldx
     for (int i = 0; i < S; ++i)
       *reinterpret_cast<uint32_t*>(out + i * slice_stride + static_cast<long long>(row) * Kp + k) = w[i];
   }
+}
+
+inline cudaError_t slice_rows(const double* X, long long ldx, int R, int K, int Kp, int8_t* out,
+                              long long slice_stride, double* scale, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((R + 7) / 8);
+  switch ((Kp + 127) / 128) {
+    case 1: oz_slice_rows_kernel<1><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 2: oz_slice_rows_kernel<2><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 3: oz_slice_rows_kernel<3><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 4: oz_slice_rows_kernel<4><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 5: oz_slice_rows_kernel<5><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 6: oz_slice_rows_kernel<6><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 7: oz_slice_rows_kernel<7><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    case 8: oz_slice_rows_kernel<8><<<grid, 256, 0, s>>>(X, ldx, R, K, Kp, out, slice_stride, scale); break;
+    default: return cudaErrorInvalidValue;  // Kp > 1024: the engine keeps such shapes on DMMA
+  }
+  return cudaGetLastError();
 }
 
 // Σ over `rows` partial rows (stride ldp) per column h < H, one warp per
