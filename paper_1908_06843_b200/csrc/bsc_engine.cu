@@ -1063,7 +1063,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     finalize_v(nchunks * enum_ctas_, n);
     launches_ += 2;
   } else {
-    finalize_stats_kernel<<<std::max(1u, (H_ + 255) / 256), 256, 0, s>>>(
+    finalize_stats_kernel<<<std::max(1u, std::min(1024u, (H_ * H_ + 255) / 256)), 256, 0, s>>>(
         3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
     counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
     launches_ += 3;
