@@ -6,6 +6,7 @@
 #include <cuda_runtime_api.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -254,7 +255,9 @@ int prsp_bsc_gpu_step_host(prsp_bsc_gpu* ctx, const double* y, uint64_t n, const
     auto& e = ctx->engine;
     e.set_params(w, pi, sigma2);
     // ~8 chunks of ≥ 16k points: the H2D copy of chunk c+1 overlaps chunk c
-    const uint64_t chunk = std::max<uint64_t>(16384, (n + 7) / 8);
+    // (BSC_HOST_CHUNK overrides the chunk size in points, for tuning)
+    uint64_t chunk = std::max<uint64_t>(16384, (n + 7) / 8);
+    if (const char* v = std::getenv("BSC_HOST_CHUNK")) chunk = std::max<uint64_t>(128, std::strtoull(v, nullptr, 10));
     const double f = e.step_streamed(y, n, temperature, chunk);
     double p = 0, s2 = 0;
     e.get_params(w_out, &p, &s2);

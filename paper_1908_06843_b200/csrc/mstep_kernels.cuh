@@ -62,7 +62,6 @@ __global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int lda, int k0, int kb,
                                                          MstepScalars* sc) {
   __shared__ double L[kCholNb][kCholNb + 1];
-  __shared__ double rinv;
   __shared__ int fail;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   for (int e = tid; e < kCholNb * kCholNb; e += blockDim.x) {
@@ -71,26 +70,28 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
   }
   if (tid == 0) fail = sc->chol_failed;
   __syncthreads();
+  // Two barriers per column: every thread derives 1/√d itself and scales the
+  // column entries it needs on the fly (the same product the stored scaled
+  // entry holds), so each entry sees exactly the operations of the classic
+  // scale-then-update loop.
   for (int j = 0; j < kCholNb; ++j) {
-    if (tid == 0) {
-      double d = L[j][j];
-      if (!(d > 0.0) || !isfinite(d)) {
-        fail = 1;
-        d = 1.0;
-      }
-      d = sqrt(d);
-      L[j][j] = d;
-      rinv = 1.0 / d;
-    }
-    __syncthreads();
-    if (tid > j && tid < kCholNb) L[tid][j] *= rinv;
-    __syncthreads();
+    double d = L[j][j];
+    const bool bad = !(d > 0.0) || !isfinite(d);
+    if (bad) d = 1.0;
+    d = sqrt(d);
+    const double rinv = 1.0 / d;
     double li[4], lk[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      li[a] = L[ty + 16 * a][j];
-      lk[a] = L[tx + 16 * a][j];
+      li[a] = L[ty + 16 * a][j] * rinv;
+      lk[a] = L[tx + 16 * a][j] * rinv;
     }
+    __syncthreads();  // column j read by everyone before it is overwritten
+    if (tid == 0) {
+      if (bad) fail = 1;
+      L[j][j] = d;
+    }
+    if (tid > j && tid < kCholNb) L[tid][j] *= rinv;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
