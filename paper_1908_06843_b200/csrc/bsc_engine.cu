@@ -235,7 +235,7 @@ BscEngine::~BscEngine() {
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
                   (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_,
                   (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
-                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_})
+                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -513,7 +513,7 @@ void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
   for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
                   (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_rec_,
-                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_})
+                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_, (void*)d_pscale_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
   if (oz_) {
@@ -522,6 +522,7 @@ void BscEngine::ensure_work(uint64_t n) {
     d_ysa_ = dalloc<double>(rows, "Y slice scales");
     d_yts_ = dalloc<int8_t>((size_t)oz::S * Dp_ * oz_np_, "Yt slices");
     d_ozcs_ = dalloc<double>((size_t)(oz_np_ / 128) * Hp_, "ES column sums");
+    d_pscale_ = dalloc<double>(rows, "ES row scales");
   }
   d_y_ = dalloc<double>(rows * Dp_, "Y");
   d_y2_ = dalloc<double>(rows, "y2");
@@ -851,6 +852,8 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   const int maxj = maxj_for(H_);
   void* args[] = {&a};
   const bool lane = lane_ok_ && !infer && temperature == 1.0 && weight_mode_ != 2;
+  pscale_used_ = lane && oz_ && d_pscale_ != nullptr;
+  a.pscale = pscale_used_ ? d_pscale_ + off : nullptr;
   if (!lane) {
     ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s),
        "enumerate launch");
@@ -884,6 +887,7 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   fa.ES = d_es_ + off * Hp_;
   fa.ssT = d_stats_ + lay_.off_ssT();
   fa.cta_scalars = sc_fin;
+  fa.pscale = a.pscale;
   fa.base0 = a.base0;
   fa.inv2s = a.inv2s;
   lane_finish_kernel<<<fin_ctas_, 256, 0, s>>>(fa);
@@ -1010,7 +1014,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, kb), 256, 0, s>>>(
           d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_,
           (static_cast<long long>(rows) + 127) / 128 * 128, d_two_, d_ess_, static_cast<long long>(Hp_) * oz_npc_,
-          d_ozcs_ + (off / 128) * Hp_);
+          d_ozcs_ + (off / 128) * Hp_, pscale_used_ ? d_pscale_ + off : nullptr);
       ck(cudaGetLastError(), "slice ES");
       oz::Args g{};
       g.sa = d_ytsa_ + (size_t)((host_y || nchunks > 1) ? c : 0) * Dp_;

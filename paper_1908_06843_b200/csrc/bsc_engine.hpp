@@ -205,6 +205,8 @@ class BscEngine {
   int8_t *d_ys_ = nullptr, *d_yts_ = nullptr, *d_ws_ = nullptr, *d_ess_ = nullptr;
   double *d_ysa_ = nullptr, *d_ytsa_ = nullptr, *d_wsb_ = nullptr, *d_two_ = nullptr;
   double *d_ozpart_ = nullptr, *d_ozcs_ = nullptr;
+  double* d_pscale_ = nullptr;  // per-point ⟨s⟩-row scales deferred to the ⟨S⟩ slicer (lane path)
+  bool pscale_used_ = false;
   unsigned long long* d_ozmax_ = nullptr;
   int oz_part_slots_ = 0, oz_ytsa_chunks_ = 0;
   long long oz_ess_bytes_ = 0;

@@ -300,6 +300,7 @@ struct EnumArgs {
   // lane path (lane_kernels.cuh): deferred-point records and per-point modes
   double* rec;
   int* pmode;
+  double* pscale;  // front pass: 1 per point (the finish may defer its ⟨s⟩-row scale here)
   int stage_b;  // front pass: B rows double-buffered in shared memory by cp.async
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
@@ -534,7 +535,10 @@ __global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
       if (a.pmode[n] != kModeFallback) continue;
     }
     if constexpr (PASS == kPassFront) {
-      if (lane == 0) a.pmode[n] = kModeDone;  // stays so on an error (flagged in *err)
+      if (lane == 0) {
+        a.pmode[n] = kModeDone;  // stays so on an error (flagged in *err)
+        if (a.pscale) a.pscale[n] = 1.0;
+      }
     }
     ENUM_PHASE(7);
     const double* y = a.Y + (long long)n * a.Dp;

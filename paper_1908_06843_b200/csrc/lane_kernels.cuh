@@ -486,6 +486,7 @@ struct FinishArgs {
   double* ES;
   double* ssT;
   double* cta_scalars;  // [gridDim.x][2] Σ log Z_n (deferred points), 0
+  double* pscale;       // non-null: leave the singleton row unscaled, record the scale per point
   double base0, inv2s;
 };
 
@@ -511,7 +512,16 @@ static __global__ void __launch_bounds__(256) lane_finish_kernel(FinishArgs a) {
     if (lane == 0) lse_acc += (a.base0 - a.y2[n] * a.inv2s) + (shift + log(z1));
     const double scale = es * inv_z;
     double* esrow = a.ES + (long long)n * a.Hp;
-    for (int h = lane; h < a.H; h += 32) esrow[h] *= scale;
+    // With pscale the ⟨s⟩-row scale is applied by its consumer (the ⟨S⟩ slicer
+    // multiplies row n by pscale[n], the same single product) instead of a
+    // read-modify-write of the whole row here; the candidate entries are stored
+    // pre-divided so that product restores them (within an ulp).
+    const bool defer_row = a.pscale != nullptr && scale > 0x1.0p-1000 && scale < 0x1.0p1000;
+    if (defer_row) {
+      if (lane == 0) a.pscale[n] = scale;
+    } else {
+      for (int h = lane; h < a.H; h += 32) esrow[h] *= scale;
+    }
     __syncwarp();
     const uint32_t* cn = a.cand + (long long)n * hp;
     // (p, q) of the moment entries this lane finishes: entries lane, lane+32, …
@@ -524,7 +534,7 @@ static __global__ void __launch_bounds__(256) lane_finish_kernel(FinishArgs a) {
       const int q = p + idx;
       const double v = ot[(2 + o) * 32] * inv_z;
       if (q == p)
-        esrow[cn[p]] = v;
+        esrow[cn[p]] = defer_row ? v / scale : v;
       else
         atomicAdd(a.ssT + (long long)cn[p] * a.H + cn[q], v);
     }

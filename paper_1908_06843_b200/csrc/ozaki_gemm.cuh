@@ -472,7 +472,8 @@ __global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __rest
                                                            long long Krows, int R, int Rp, long long Kp,
                                                            const double* __restrict__ scale,
                                                            int8_t* __restrict__ out, long long slice_stride,
-                                                           double* __restrict__ colsum) {
+                                                           double* __restrict__ colsum,
+                                                           const double* __restrict__ rowscale = nullptr) {
   __shared__ uint32_t sT[S][32][33];
   __shared__ double ssum[8][33];
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -484,6 +485,13 @@ __global__ void __launch_bounds__(256) oz_slice_cols_kernel(const double* __rest
   for (int e = 0; e < 16; ++e) {
     const long long k = k0 + ty * 16 + e;
     xv[e] = (r < R && k < Krows) ? __ldcs(X + k * ldx + r) : 0.0;
+  }
+  if (rowscale) {  // per-row factors of this CTA's 128 rows, staged once
+    __shared__ double srs[128];
+    if (threadIdx.x < 128) srs[threadIdx.x] = k0 + threadIdx.x < Krows ? rowscale[k0 + threadIdx.x] : 1.0;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) xv[e] *= srs[ty * 16 + e];
   }
   double csum = 0.0;
 #pragma unroll
