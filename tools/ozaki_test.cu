@@ -1,7 +1,7 @@
 // Standalone check + timing of the int8-sliced tcgen05 fp64 GEMM (csrc/ozaki_gemm.cuh).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1908_06843_b200/csrc \
 //        tools/ozaki_test.cu -o tools/ozaki_test
-//   tools/ozaki_test [M N K]     (GEMM1 shape: C = Y·W;  GEMM2 shape: C = Yᵀ·E, split-K)
+//   tools/ozaki_test [M N K [P]]   (GEMM1 shape: C = Y·W;  GEMM2 shape: C = Yᵀ·E, split-K over P points)
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -111,7 +111,9 @@ int main(int argc, char** argv) {
   }
 
   // ---------------- GEMM2: C[D×H] = Yᵀ·E with Y [P×D], E [P×H] ∈ [0,1], split-K partials
-  for (int P : {20000, 200000}) {
+  const int P0 = argc > 4 ? atoi(argv[4]) : 0;  // one checked GEMM2 size (tests) instead of 20k + 200k
+  for (int P : {P0 ? P0 : 20000, P0 ? 0 : 200000}) {
+    if (P == 0) continue;
     const int D = K, H = N;
     const long long Dp = rup(D, 8), Hp = rup(H, 8), Pp = rup(P, 128);
     std::vector<double> Y((size_t)P * D), E((size_t)P * H);
