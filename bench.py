@@ -310,6 +310,11 @@ def main():
         "roofline": {"kernel": dom, "bound": "tensor" if dom.startswith("gemm") else "fp64", "pipe": pipe,
                      "achieved": round(achieved, 3), "peak": pk, "unit": "TFLOP/s", "frac": round(achieved / pk, 4),
                      "traffic": measured_traffic(w.name, dom, n_local), "peak_source": peak_src,
+                     "evidence": ("enumerate = front pass (issue-bound: 67% issue-active, IPC 2.69) + lane-per-point "
+                                  "state pass (latency-bound at 5 warps/SM: 24% issue-active) + finish; counted "
+                                  "F_state flops understate its work (selection, exps, gathers): "
+                                  "profiles/r01_front_c2_details.txt, r01_lane_c2_details.txt, r01_traffic.json")
+                     if dom == "enumerate" else None,
                      "algorithmic": "SURVEY.md §8(d): F_state=%d, F_dense=%d flops/point" % (state, dense)},
         "step_roofline": {"flops_per_step": step_flops, "tflops": round(step_flops / (ms / 1e3) / 1e12 / world, 3),
                           "frac_of_dmma_peak": round(step_flops / (ms / 1e3) / 1e12 / world / dmma_peak, 4)},
