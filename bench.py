@@ -299,6 +299,9 @@ def main():
                                    "int8_peak_source": i8_src})
         kernels["gemm_ytes"]["includes"] = "⟨S⟩ slicing + column sums"
     kernels.update({k: {"ms": round(kern[k], 4)} for k in ("gram", "finalize", "mstep")})
+    if kern.get("enum_front", 0.0) > 0.0:  # the lane path's launches inside "enumerate"
+        kernels["enumerate"]["parts_ms"] = {k[5:]: round(kern[k], 4)
+                                            for k in ("enum_front", "enum_states", "enum_fallback", "enum_finish")}
     step_flops = (dense + state) * n_total
     line = {
         "metric": "BSC truncated-EM data points/sec per iteration", "value": value, "unit": "points/s",

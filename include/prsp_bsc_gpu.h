@@ -112,6 +112,9 @@ int prsp_bsc_gpu_inference(prsp_bsc_gpu* ctx, double* map_states, double* map_ma
 /* Device timings of the last step (ms): gram, gemm Y·W, enumerate, gemm Yᵀ⟨S⟩, finalize, mstep. */
 int prsp_bsc_gpu_set_timing(prsp_bsc_gpu* ctx, int on);
 int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6);
+/* The same six, then the enumerator's lane-path launches (front pass, lane-per-point states,
+   fallback, finish; zeros when the single-kernel pass ran): the first min(n, 10) values. */
+int prsp_bsc_gpu_timings_ex(prsp_bsc_gpu* ctx, float* out, int n);
 int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out);
 /* Enumerator cycles per phase (summed over warps) of the last E-step when the
  * process runs with BSC_ENUM_PROFILE=1, else zeros: scores, selection, log-joint

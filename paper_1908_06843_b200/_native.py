@@ -47,6 +47,7 @@ SIGNATURES = {
     "prsp_bsc_gpu_inference": [_ptr, _ptr, _ptr, _ptr],
     "prsp_bsc_gpu_set_timing": [_ptr, _int],
     "prsp_bsc_gpu_timings": [_ptr, _ptr],
+    "prsp_bsc_gpu_timings_ex": [_ptr, _ptr, C.c_int],
     "prsp_bsc_gpu_launches": [_ptr, C.POINTER(_int)],
     "prsp_bsc_gpu_enum_phase_cycles": [_ptr, _ptr],
     "prsp_mca_gpu_create": [C.c_char_p, _dbl, _u32, _u32, _u32, _u32, _u64, _int, C.POINTER(_ptr)],

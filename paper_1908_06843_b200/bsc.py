@@ -279,9 +279,10 @@ class LinearDiscreteGpuModel:
         N.call("prsp_bsc_gpu_set_timing", self._h, int(on))
 
     def timings(self) -> dict:
-        t = np.zeros(6, np.float32)
-        N.call("prsp_bsc_gpu_timings", self._h, t.ctypes.data_as(C.c_void_p))
-        return dict(zip(["gram", "gemm_yw", "enumerate", "gemm_ytes", "finalize", "mstep"], map(float, t)))
+        t = np.zeros(10, np.float32)
+        N.call("prsp_bsc_gpu_timings_ex", self._h, t.ctypes.data_as(C.c_void_p), 10)
+        return dict(zip(["gram", "gemm_yw", "enumerate", "gemm_ytes", "finalize", "mstep",
+                         "enum_front", "enum_states", "enum_fallback", "enum_finish"], map(float, t)))
 
     def launches(self) -> int:
         v = C.c_int()

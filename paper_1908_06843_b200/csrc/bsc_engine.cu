@@ -866,14 +866,19 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   a.pmode = d_pmode_;
   a.stage_b = front_stage_b_ ? 1 : 0;
   a.cand_out = d_cand_ + off * hprime_;
+  const bool tm = timing_ && chunk == 0;
+  lane_timed_ = tm;
   ck(cudaLaunchKernel(front_fn(maxj), dim3(front_ctas_), dim3(256), args, front_smem_, s), "front launch");
+  if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[8]), s), "event");
   LaneArgs la{static_cast<int>(rows), static_cast<int>(hprime_), d_rec_, d_lout_, d_pmode_};
   void* largs[] = {&la};
   ck(cudaLaunchKernel(lane_fn(gamma_, hprime_), dim3(static_cast<unsigned>((rows + 31) / 32)), dim3(32), largs, lane_smem_, s),
      "lane states launch");
+  if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[9]), s), "event");
   a.warp_scalars = sc_fb;
   ck(cudaLaunchKernel(fallback_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s),
      "fallback launch");
+  if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[10]), s), "event");
   FinishArgs fa{};
   fa.N = static_cast<int>(rows);
   fa.H = H_;
@@ -1229,6 +1234,14 @@ void BscEngine::finish_mstep() {
     t_.gemm2_ms = el(3, 4);
     t_.finalize_ms = el(4, 5);
     t_.mstep_ms = el(5, 6);
+    if (lane_timed_) {
+      t_.front_ms = el(2, 8);
+      t_.states_ms = el(8, 9);
+      t_.fallback_ms = el(9, 10);
+      t_.finish_ms = el(10, 3);
+    } else {
+      t_.front_ms = t_.states_ms = t_.fallback_ms = t_.finish_ms = 0.f;
+    }
   }
 }
 

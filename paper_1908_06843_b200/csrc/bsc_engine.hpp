@@ -43,6 +43,8 @@ const void* ldv_kernel_fn(int maxj, bool staged);
 
 struct EngineTimings {
   float gram_ms, gemm1_ms, enum_ms, gemm2_ms, finalize_ms, mstep_ms;
+  // the enumerator's lane path, split (0 when the single-kernel pass ran)
+  float front_ms, states_ms, fallback_ms, finish_ms;
 };
 
 class BscEngine {
@@ -212,7 +214,8 @@ class BscEngine {
   long long oz_ess_bytes_ = 0;
   void slice_y(uint64_t off, uint64_t rows, int chunk, void* stream);
   void slice_w(void* stream);
-  void* ev_[8] = {};
+  void* ev_[12] = {};
+  bool lane_timed_ = false;
 };
 
 }  // namespace bscgpu

@@ -303,6 +303,17 @@ int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6) {
   });
 }
 
+int prsp_bsc_gpu_timings_ex(prsp_bsc_gpu* ctx, float* out, int n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    const auto& t = ctx->engine.timings();
+    const float v[10] = {t.gram_ms,  t.gemm1_ms,  t.enum_ms,     t.gemm2_ms,   t.finalize_ms,
+                         t.mstep_ms, t.front_ms,  t.states_ms,   t.fallback_ms, t.finish_ms};
+    std::memcpy(out, v, sizeof(float) * static_cast<size_t>(std::max(0, std::min(n, 10))));
+  });
+}
+
 int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out) {
   return guarded([&] {
     need(ctx, "ctx");
