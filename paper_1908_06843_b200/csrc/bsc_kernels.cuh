@@ -459,8 +459,13 @@ enum : int { kPassFull = 0, kPassFront = 1, kPassFallback = 2 };
 
 // STAGED: the state descriptors and schedule entries are staged in shared
 // memory (compile-time, so every table access is an LDS, not a generic load)
+#ifndef ENUM_FRONT_MINB
+// front pass CTAs per SM: 3 (80 registers) and 4 (64) were measured slower than 2 (c2 front
+// 0.95 -> 1.00 / 1.17 ms): the pass is issue-bound, not latency-bound
+#define ENUM_FRONT_MINB 2
+#endif
 template <int MAXJ, bool STAGED, int PASS = kPassFull>
-__global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
+__global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2) enumerate_kernel(EnumArgs a) {
   extern __shared__ __align__(16) double esm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
