@@ -180,7 +180,19 @@ struct LaneShape {
   static_assert(GM >= 3, "compile-time walk needs gamma >= 3");
   static constexpr int NP = HP * (HP - 1) / 2, NM = HP * (HP + 1) / 2;
   static constexpr int CV_LEVELS = GM - 3;  // coupling rows of depths 2 .. γ−2
-  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + NP, O_M = O_CV + CV_LEVELS * HP;
+  // e^P staged in shared memory, or (EP_GLOBAL) read from the record tile ([pair][32 lanes])
+  // through the read-only path, leaving the slots to e^u, the coupling rows and M. Measured:
+  // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) 5 -> 8 warps/SM but
+  // 0.45 -> 0.48 ms at c2 (the L2 reads cost more than the occupancy gains), so staged there.
+  static constexpr bool EP_GLOBAL = NP > 80;
+  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + (EP_GLOBAL ? 0 : NP), O_M = O_CV + CV_LEVELS * HP;
+  // element i of this lane's e^P (E: record tile or the staged slots, stride 32 doubles)
+  __device__ static __forceinline__ double ep(const double* E, int i) {
+    if constexpr (EP_GLOBAL)
+      return __ldg(E + i * 32);
+    else
+      return E[i * 32];
+  }
   static constexpr int SLOTS = O_M + NM;
   __host__ __device__ static constexpr int pidx(int p, int q) { return p * (2 * HP - p - 1) / 2 + (q - p - 1); }
   __host__ __device__ static constexpr int tri(int p, int q) { return p * (2 * HP - p + 1) / 2 + (q - p); }
@@ -192,14 +204,14 @@ struct LaneShape {
 // Coupling row of child A∪{Z} (node A at depth K < γ−2): cv[K−1][w] =
 // c(A,w)·e^{P_Zw}, w > Z; c(A,·) = e^P row x (runtime, xrow) for K = 1, else cv[K−2].
 template <int HP, int GM, int K, int Z>
-__device__ __forceinline__ void cv_block(double* S, int xrow) {
+__device__ __forceinline__ void cv_block(double* S, const double* __restrict__ E, int xrow) {
   using F = LaneShape<HP, GM>;
   constexpr int NW = HP - 1 - Z > 0 ? HP - 1 - Z : 1;
   double v[NW];
 #pragma unroll
   for (int w = Z + 1; w < HP; ++w) {
-    const double cw = K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w);
-    v[w - Z - 1] = cw * LS(F::O_EP + F::pidx(Z, w));
+    const double cw = K == 1 ? F::ep(E, xrow + w) : LS(F::O_CV + (K - 2) * HP + w);
+    v[w - Z - 1] = cw * F::ep(E, F::pidx(Z, w));
   }
 #pragma unroll
   for (int w = Z + 1; w < HP; ++w) LS(F::O_CV + (K - 1) * HP + w) = v[w - Z - 1];
@@ -209,11 +221,11 @@ __device__ __forceinline__ void cv_block(double* S, int xrow) {
   M_(0) M_(1) M_(2) M_(3) M_(4) M_(5) M_(6) M_(7) M_(8) M_(9) M_(10) M_(11) M_(12) M_(13) M_(14) M_(15)
 
 template <int HP, int GM, int K>
-__device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
+__device__ __forceinline__ void cv_dispatch(int z, double* S, const double* __restrict__ E, int xrow) {
   switch (z) {
 #define LANE_CV_CASE(v)                                                       \
   case v:                                                                     \
-    if constexpr (v < HP - 1) cv_block<HP, GM, K, (v < HP - 1 ? v : 0)>(S, xrow); \
+    if constexpr (v < HP - 1) cv_block<HP, GM, K, (v < HP - 1 ? v : 0)>(S, E, xrow); \
     break;
     LANE_CASES(LANE_CV_CASE)
 #undef LANE_CV_CASE
@@ -224,7 +236,7 @@ __device__ __forceinline__ void cv_dispatch(int z, double* S, int xrow) {
 
 // Child A∪{Z} of the deepest node A and its leaves.
 template <int HP, int GM, int Z>
-__device__ __forceinline__ void deep_child(double* S, double qA, const double (&ce)[HP], double (&R)[HP], double& ch) {
+__device__ __forceinline__ void deep_child(double* S, const double* __restrict__ E, double qA, const double (&ce)[HP], double (&R)[HP], double& ch) {
   using F = LaneShape<HP, GM>;
   const double qz = qA * ce[Z];
   double s = qz;
@@ -234,7 +246,7 @@ __device__ __forceinline__ void deep_child(double* S, double qA, const double (&
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
       const int w = Z + 1 + j;
-      q[j] = qz * ce[w] * LS(F::O_EP + F::pidx(Z, w));
+      q[j] = qz * ce[w] * F::ep(E, F::pidx(Z, w));
       m[j] = LS(F::O_M + F::tri(Z, w));
     }
 #pragma unroll
@@ -250,10 +262,10 @@ __device__ __forceinline__ void deep_child(double* S, double qA, const double (&
 }
 
 template <int HP, int GM, int Z>
-__device__ __forceinline__ void deep_pred(double* S, double qA, int x, const double (&ce)[HP], double (&R)[HP],
+__device__ __forceinline__ void deep_pred(double* S, const double* __restrict__ E, double qA, int x, const double (&ce)[HP], double (&R)[HP],
                                           double& ch) {
-  if (Z > x) deep_child<HP, GM, Z>(S, qA, ce, R, ch);
-  if constexpr (Z + 1 < HP) deep_pred<HP, GM, Z + 1>(S, qA, x, ce, R, ch);
+  if (Z > x) deep_child<HP, GM, Z>(S, E, qA, ce, R, ch);
+  if constexpr (Z + 1 < HP) deep_pred<HP, GM, Z + 1>(S, E, qA, x, ce, R, ch);
 }
 
 // Duff-style dispatch on the node maximum x: case x falls through the
@@ -265,12 +277,12 @@ __device__ __forceinline__ void deep_pred(double* S, double qA, int x, const dou
 // Node A (|A| = K ≤ γ−2, max x, weight qA, members path[0..K)): walks its
 // children, returns Σ_children sub(child).
 template <int HP, int GM, int K>
-__device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)[8]) {
+__device__ __forceinline__ double fnode(double* S, const double* __restrict__ E, double qA, int x, int (&path)[8]) {
   using F = LaneShape<HP, GM>;
   int orow[K + 1];
 #pragma unroll
   for (int i = 0; i < K; ++i) orow[i] = F::O_M + mrow_(path[i], HP);
-  const int xrow = F::O_EP + prow_(x, HP);
+  const int xrow = prow_(x, HP);
   double ch = 0.0;
   if constexpr (K == GM - 2) {
     double ce[HP], R[HP];
@@ -281,9 +293,9 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
 #pragma unroll
       for (int w = 0; w < HP; ++w) {
         ce[w] = 0.0;
-        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? S[(xrow + w) * 32] : LS(F::O_CV + (K - 2) * HP + w));
+        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(E, xrow + w) : LS(F::O_CV + (K - 2) * HP + w));
       }
-      deep_pred<HP, GM, (K < HP ? K : 0)>(S, qA, x, ce, R, ch);
+      deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, ch);
 #pragma unroll
       for (int z = 0; z < HP; ++z) {
         if (z > x) {
@@ -303,7 +315,7 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
     case c_:                                                                                     \
       if constexpr (Z_ < HP) {                                                                   \
         constexpr int Zc = Z_ < HP ? Z_ : 0;                                                     \
-        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? S[(xrow + Zc) * 32] : LS(F::O_CV + (K - 2) * HP + Zc)); \
+        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? F::ep(E, xrow + Zc) : LS(F::O_CV + (K - 2) * HP + Zc)); \
       }                                                                                          \
       [[fallthrough]];
         LANE_FT_CASES(LANE_CE)
@@ -314,7 +326,7 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
       switch (x) {
   #define LANE_DC(c_, Z_)                                                     \
     case c_:                                                                  \
-      if constexpr (Z_ < HP) deep_child<HP, GM, (Z_ < HP ? Z_ : 0)>(S, qA, ce, R, ch); \
+      if constexpr (Z_ < HP) deep_child<HP, GM, (Z_ < HP ? Z_ : 0)>(S, E, qA, ce, R, ch); \
       [[fallthrough]];
         LANE_FT_CASES(LANE_DC)
   #undef LANE_DC
@@ -342,11 +354,11 @@ __device__ __forceinline__ double fnode(double* S, double qA, int x, int (&path)
     }
   } else {
     for (int z = x + 1; z < HP; ++z) {
-      const double c = K == 1 ? S[(xrow + z) * 32] : S[(F::O_CV + (K - 2) * HP + z) * 32];
+      const double c = K == 1 ? F::ep(E, xrow + z) : S[(F::O_CV + (K - 2) * HP + z) * 32];
       const double qz = qA * S[(F::O_EU + z) * 32] * c;
-      cv_dispatch<HP, GM, K>(z, S, xrow);
+      cv_dispatch<HP, GM, K>(z, S, E, xrow);
       path[K] = z;
-      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, qz, z, path);
+      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, E, qz, z, path);
       const int zz = F::O_M + mrow_(z, HP) + z;
       double m[K + 1];
       m[K] = S[zz * 32];
@@ -439,10 +451,9 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
     // exact maximum: u and the coupling sums staged in the M region
     char* U = base + F::O_M * 256;
     char* cvm = U + HP * 256;
-    char* eP = base + F::O_EP * 256;
+    const char* eP = reinterpret_cast<const char*>(rt + fP * 32);  // P from the record tile
 #pragma unroll
     for (int p = 0; p < HP; ++p) sts_(U, p, ur[p]);
-    for (int e = 0; e < F::NP; ++e) sts_(eP, e, live ? rt[(fP + e) * 32] : 0.0);
     double m = -INFINITY;
     for (int r = 0; r < HP; ++r) {
       const double u = lds_(U, r);
@@ -452,7 +463,12 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
   }
 #pragma unroll
   for (int p = 0; p < HP; ++p) S[(F::O_EU + p) * 32] = live ? rt[(feu + p) * 32] : 0.0;
-  for (int e = 0; e < F::NP; ++e) S[(F::O_EP + e) * 32] = live ? rt[(feP + e) * 32] : 0.0;
+  // e^P of this lane's point (dead lanes: unused values)
+  const double* E = rt + feP * 32;
+  if constexpr (!F::EP_GLOBAL) {
+    for (int e = 0; e < F::NP; ++e) S[(F::O_EP + e) * 32] = live ? rt[(feP + e) * 32] : 0.0;
+    E = S + F::O_EP * 32;
+  }
   for (int i = 0; i < F::NM; ++i) S[(F::O_M + i) * 32] = 0.0;
   int path[8];
   double zm = 0.0;
@@ -463,7 +479,7 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
     for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
     const double qr = live ? exp_nonpos(u - shift) : 0.0;
     path[0] = r;
-    const double ch = fnode<HP, GM, 1>(S, qr, r, path);
+    const double ch = fnode<HP, GM, 1>(S, E, qr, r, path);
     const int rr = F::O_M + mrow_(r, HP) + r;
     S[rr * 32] += qr + ch;
     zm += ch;
