@@ -185,7 +185,13 @@ struct LaneShape {
   // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) 5 -> 8 warps/SM but
   // 0.45 -> 0.48 ms at c2 (the L2 reads cost more than the occupancy gains), so staged there.
   static constexpr bool EP_GLOBAL = NP > 80;
-  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + (EP_GLOBAL ? 0 : NP), O_M = O_CV + CV_LEVELS * HP;
+  static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + (EP_GLOBAL ? 0 : NP);
+  // coupling row c (written by depth-(c+1) nodes for their children) only ever holds
+  // w ≥ c + 2 (a depth-K node's child is ≥ K): rows packed without those slots, so
+  // (14, 5) fits 6 warps per SM. cvb(c) + w is the slot of entry w of row c.
+  __host__ __device__ static constexpr int cv_start(int c) { return c <= 0 ? O_CV : cv_start(c - 1) + HP - (c - 1) - 2; }
+  __host__ __device__ static constexpr int cvb(int c) { return cv_start(c) - (c + 2); }
+  static constexpr int O_M = cv_start(CV_LEVELS);
   // element i of this lane's e^P (E: record tile or the staged slots, stride 32 doubles)
   __device__ static __forceinline__ double ep(const double* E, int i) {
     if constexpr (EP_GLOBAL)
@@ -210,11 +216,11 @@ __device__ __forceinline__ void cv_block(double* S, const double* __restrict__ E
   double v[NW];
 #pragma unroll
   for (int w = Z + 1; w < HP; ++w) {
-    const double cw = K == 1 ? F::ep(E, xrow + w) : LS(F::O_CV + (K - 2) * HP + w);
+    const double cw = K == 1 ? F::ep(E, xrow + w) : LS(F::cvb(K - 2) + w);
     v[w - Z - 1] = cw * F::ep(E, F::pidx(Z, w));
   }
 #pragma unroll
-  for (int w = Z + 1; w < HP; ++w) LS(F::O_CV + (K - 1) * HP + w) = v[w - Z - 1];
+  for (int w = Z + 1; w < HP; ++w) LS(F::cvb(K - 1) + w) = v[w - Z - 1];
 }
 
 #define LANE_CASES(M_)                                                                                      \
@@ -293,7 +299,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
 #pragma unroll
       for (int w = 0; w < HP; ++w) {
         ce[w] = 0.0;
-        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(E, xrow + w) : LS(F::O_CV + (K - 2) * HP + w));
+        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(E, xrow + w) : LS(F::cvb(K - 2) + w));
       }
       deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, ch);
 #pragma unroll
@@ -315,7 +321,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
     case c_:                                                                                     \
       if constexpr (Z_ < HP) {                                                                   \
         constexpr int Zc = Z_ < HP ? Z_ : 0;                                                     \
-        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? F::ep(E, xrow + Zc) : LS(F::O_CV + (K - 2) * HP + Zc)); \
+        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? F::ep(E, xrow + Zc) : LS(F::cvb(K - 2) + Zc)); \
       }                                                                                          \
       [[fallthrough]];
         LANE_FT_CASES(LANE_CE)
@@ -354,7 +360,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
     }
   } else {
     for (int z = x + 1; z < HP; ++z) {
-      const double c = K == 1 ? F::ep(E, xrow + z) : S[(F::O_CV + (K - 2) * HP + z) * 32];
+      const double c = K == 1 ? F::ep(E, xrow + z) : S[(F::cvb(K - 2) + z) * 32];
       const double qz = qA * S[(F::O_EU + z) * 32] * c;
       cv_dispatch<HP, GM, K>(z, S, E, xrow);
       path[K] = z;
