@@ -604,6 +604,11 @@ void BscEngine::ensure_work(uint64_t n) {
     lane_smem_ = lane_smem(static_cast<int>(gamma_), static_cast<int>(hprime_));
     ck(cudaFuncSetAttribute(lane_fn(gamma_, hprime_), cudaFuncAttributeMaxDynamicSharedMemorySize, lane_smem_),
        "lane smem attr");
+    // shared-memory carveout of the lane state pass (percent of the SM's maximum; A/B runs:
+    // with e^P read through L1 the carveout trades resident warps against L1 hits)
+    if (const char* e = std::getenv("BSC_LANE_CARVEOUT"))
+      ck(cudaFuncSetAttribute(lane_fn(gamma_, hprime_), cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)),
+         "lane carveout");
     int fz = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fz, (const void*)lane_finish_kernel, 256, 0), "occupancy");
     fin_ctas_ = static_cast<int>(std::max<uint64_t>(

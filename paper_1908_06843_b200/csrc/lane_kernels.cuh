@@ -175,6 +175,9 @@ __device__ __forceinline__ double mnode(const char* U, const char* P, char* cv, 
 // is flushed once per A into M[z][z] and the K member rows. Only the leaf-
 // parent row M[Z][w] is updated per leaf — at a constant offset. Levels above
 // run over z at run time (coupling rows built by a dispatched unrolled block).
+#ifndef LANE_EPG_MIN_PAIRS
+#define LANE_EPG_MIN_PAIRS 80  // e^P read through L1 when H'(H'-1)/2 exceeds this
+#endif
 template <int HP, int GM>
 struct LaneShape {
   static_assert(GM >= 3, "compile-time walk needs gamma >= 3");
@@ -184,7 +187,7 @@ struct LaneShape {
   // through the read-only path, leaving the slots to e^u, the coupling rows and M. Measured:
   // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) 5 -> 8 warps/SM but
   // 0.45 -> 0.48 ms at c2 (the L2 reads cost more than the occupancy gains), so staged there.
-  static constexpr bool EP_GLOBAL = NP > 80;
+  static constexpr bool EP_GLOBAL = NP > LANE_EPG_MIN_PAIRS;
   static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + (EP_GLOBAL ? 0 : NP);
   // coupling row c (written by depth-(c+1) nodes for their children) only ever holds
   // w ≥ c + 2 (a depth-K node's child is ≥ K): rows packed without those slots, so
