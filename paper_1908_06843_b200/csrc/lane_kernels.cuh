@@ -175,6 +175,9 @@ __device__ __forceinline__ double mnode(const char* U, const char* P, char* cv, 
 // is flushed once per A into M[z][z] and the K member rows. Only the leaf-
 // parent row M[Z][w] is updated per leaf — at a constant offset. Levels above
 // run over z at run time (coupling rows built by a dispatched unrolled block).
+#ifndef LANE_EPS_ROW
+#define LANE_EPS_ROW 6  // first e^P row still staged when e^P is read through L1
+#endif
 #ifndef LANE_EPG_MIN_PAIRS
 #define LANE_EPG_MIN_PAIRS 80  // e^P read through L1 when H'(H'-1)/2 exceeds this
 #endif
@@ -194,11 +197,19 @@ struct LaneShape {
   // (14, 5) fits 6 warps per SM. cvb(c) + w is the slot of entry w of row c.
   __host__ __device__ static constexpr int cv_start(int c) { return c <= 0 ? O_CV : cv_start(c - 1) + HP - (c - 1) - 2; }
   __host__ __device__ static constexpr int cvb(int c) { return cv_start(c) - (c + 2); }
-  static constexpr int O_M = cv_start(CV_LEVELS);
-  // element i of this lane's e^P (E: record tile or the staged slots, stride 32 doubles)
-  __device__ static __forceinline__ double ep(const double* E, int i) {
+  // EP_GLOBAL: the e^P rows p ≥ EPS_ROW (pairs from EPS_FIRST on) are still staged. A
+  // deepest-level node with maximum x reads rows x+1 … H'−1, so row p is read by the C(p, γ−2)
+  // nodes below it: at (14, 5) rows 6-12 take 94 % of those reads in 28 slots (5 warps/SM).
+  static constexpr int EPS_ROW = EP_GLOBAL ? LANE_EPS_ROW : HP;
+  static constexpr int EPS_FIRST = EPS_ROW * (2 * HP - EPS_ROW - 1) / 2;
+  static constexpr int EPS_N = EP_GLOBAL ? NP - EPS_FIRST : 0;
+  static constexpr int O_EPS = cv_start(CV_LEVELS);
+  static constexpr int O_M = O_EPS + EPS_N;
+  // element i of this lane's e^P (E: record tile or the staged slots, stride 32 doubles;
+  // S: this lane's slot 0). i is warp-uniform, so the split branch never diverges.
+  __device__ static __forceinline__ double ep(const double* S, const double* E, int i) {
     if constexpr (EP_GLOBAL)
-      return __ldg(E + i * 32);
+      return i >= EPS_FIRST ? S[(O_EPS + i - EPS_FIRST) * 32] : __ldg(E + i * 32);
     else
       return E[i * 32];
   }
@@ -219,8 +230,8 @@ __device__ __forceinline__ void cv_block(double* S, const double* __restrict__ E
   double v[NW];
 #pragma unroll
   for (int w = Z + 1; w < HP; ++w) {
-    const double cw = K == 1 ? F::ep(E, xrow + w) : LS(F::cvb(K - 2) + w);
-    v[w - Z - 1] = cw * F::ep(E, F::pidx(Z, w));
+    const double cw = K == 1 ? F::ep(S, E, xrow + w) : LS(F::cvb(K - 2) + w);
+    v[w - Z - 1] = cw * F::ep(S, E, F::pidx(Z, w));
   }
 #pragma unroll
   for (int w = Z + 1; w < HP; ++w) LS(F::cvb(K - 1) + w) = v[w - Z - 1];
@@ -255,7 +266,7 @@ __device__ __forceinline__ void deep_child(double* S, const double* __restrict__
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
       const int w = Z + 1 + j;
-      q[j] = qz * ce[w] * F::ep(E, F::pidx(Z, w));
+      q[j] = qz * ce[w] * F::ep(S, E, F::pidx(Z, w));
       m[j] = LS(F::O_M + F::tri(Z, w));
     }
 #pragma unroll
@@ -302,7 +313,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
 #pragma unroll
       for (int w = 0; w < HP; ++w) {
         ce[w] = 0.0;
-        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(E, xrow + w) : LS(F::cvb(K - 2) + w));
+        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(S, E, xrow + w) : LS(F::cvb(K - 2) + w));
       }
       deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, ch);
 #pragma unroll
@@ -324,7 +335,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
     case c_:                                                                                     \
       if constexpr (Z_ < HP) {                                                                   \
         constexpr int Zc = Z_ < HP ? Z_ : 0;                                                     \
-        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? F::ep(E, xrow + Zc) : LS(F::cvb(K - 2) + Zc)); \
+        ce[Zc] = LS(F::O_EU + Zc) * (K == 1 ? F::ep(S, E, xrow + Zc) : LS(F::cvb(K - 2) + Zc)); \
       }                                                                                          \
       [[fallthrough]];
         LANE_FT_CASES(LANE_CE)
@@ -363,7 +374,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
     }
   } else {
     for (int z = x + 1; z < HP; ++z) {
-      const double c = K == 1 ? F::ep(E, xrow + z) : S[(F::cvb(K - 2) + z) * 32];
+      const double c = K == 1 ? F::ep(S, E, xrow + z) : S[(F::cvb(K - 2) + z) * 32];
       const double qz = qA * S[(F::O_EU + z) * 32] * c;
       cv_dispatch<HP, GM, K>(z, S, E, xrow);
       path[K] = z;
@@ -477,6 +488,8 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
   if constexpr (!F::EP_GLOBAL) {
     for (int e = 0; e < F::NP; ++e) S[(F::O_EP + e) * 32] = live ? rt[(feP + e) * 32] : 0.0;
     E = S + F::O_EP * 32;
+  } else {
+    for (int e = 0; e < F::EPS_N; ++e) S[(F::O_EPS + e) * 32] = live ? rt[(feP + F::EPS_FIRST + e) * 32] : 0.0;
   }
   for (int i = 0; i < F::NM; ++i) S[(F::O_M + i) * 32] = 0.0;
   int path[8];
