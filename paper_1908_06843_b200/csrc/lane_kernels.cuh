@@ -176,10 +176,10 @@ __device__ __forceinline__ double mnode(const char* U, const char* P, char* cv, 
 // parent row M[Z][w] is updated per leaf — at a constant offset. Levels above
 // run over z at run time (coupling rows built by a dispatched unrolled block).
 #ifndef LANE_EPS_ROW
-#define LANE_EPS_ROW 6  // first e^P row still staged when e^P is read through L1
+#define LANE_EPS_ROW (HP / 2 - 1)  // first e^P row still staged when e^P is read through L1
 #endif
 #ifndef LANE_EPG_MIN_PAIRS
-#define LANE_EPG_MIN_PAIRS 80  // e^P read through L1 when H'(H'-1)/2 exceeds this
+#define LANE_EPG_MIN_PAIRS 60  // e^P read through L1 when H'(H'-1)/2 exceeds this
 #endif
 template <int HP, int GM>
 struct LaneShape {
@@ -188,8 +188,9 @@ struct LaneShape {
   static constexpr int CV_LEVELS = GM - 3;  // coupling rows of depths 2 .. γ−2
   // e^P staged in shared memory, or (EP_GLOBAL) read from the record tile ([pair][32 lanes])
   // through the read-only path, leaving the slots to e^u, the coupling rows and M. Measured:
-  // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) 5 -> 8 warps/SM but
-  // 0.45 -> 0.48 ms at c2 (the L2 reads cost more than the occupancy gains), so staged there.
+  // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) fully unstaged reached
+  // 8 warps/SM but 0.45 -> 0.48 ms at c2. With the heavily read rows staged (EPS_ROW below):
+  // c3 10.6 ms, c2 0.423 ms (7 warps/SM); (10, 4) stays fully staged.
   static constexpr bool EP_GLOBAL = NP > LANE_EPG_MIN_PAIRS;
   static constexpr int O_EU = 0, O_EP = HP, O_CV = O_EP + (EP_GLOBAL ? 0 : NP);
   // coupling row c (written by depth-(c+1) nodes for their children) only ever holds
