@@ -241,12 +241,28 @@ class Oracle:
                    C.byref(pio), C.byref(s2o), C.byref(f))
         return wo, pio.value, s2o.value, f.value
 
-    def candidates(self, w, pi, sigma2, y, hprime):
+    def candidates(self, w, pi, sigma2, y, hprime, threads=1):
+        """Per-point candidate sets. ``threads`` > 1 splits the rows into blocks
+        computed concurrently (ctypes releases the GIL; every row is independent,
+        so the result is the same bytes as one call)."""
         w, y = _f64(w), _f64(y)
         d, h = w.shape
-        out = np.empty((y.shape[0], hprime), np.uint32)
-        self._call("candidates", _u32(d), _u32(h), _u32(hprime), _p(w), _dbl(pi), _dbl(sigma2), _p(y),
-                   _u64(y.shape[0]), _p(out))
+        n = y.shape[0]
+        out = np.empty((n, hprime), np.uint32)
+
+        def block(b, e):
+            if e > b:
+                self._call("candidates", _u32(d), _u32(h), _u32(hprime), _p(w), _dbl(pi), _dbl(sigma2),
+                           _p(y[b:e]), _u64(e - b), _p(out[b:e]))
+
+        if threads <= 1 or n < 2 * threads:
+            block(0, n)
+            return out
+        from concurrent.futures import ThreadPoolExecutor
+
+        cuts = np.linspace(0, n, 4 * threads + 1).astype(int)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda i: block(cuts[i], cuts[i + 1]), range(len(cuts) - 1)))
         return out
 
     def inference(self, w, pi, sigma2, y, hprime, gamma):

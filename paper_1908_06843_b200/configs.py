@@ -49,23 +49,82 @@ CONFIGS = {
 }
 
 
-def truth(w: Workload) -> np.ndarray:
+class _ProductGen:
+    """The package's own fixtures (csrc/fixtures.cpp, the reference's draw order)."""
+
+    @staticmethod
+    def random_dictionary(d, h, seed, scale):
+        return bsc.random_dictionary(d, h, seed, scale)
+
+    @staticmethod
+    def generate(w, pi, sigma2, n, seed):
+        return bsc.generate(bsc.BscParams(w, pi, sigma2), n, seed)
+
+    @staticmethod
+    def make_bars(size, n, seed):
+        return bsc.bars_generate(size, n, seed=seed)
+
+
+class OracleGen:
+    """The same fixtures from the oracle library (bit-identical draws), so that a
+    caller timing the reference never maps the product's library."""
+
+    def __init__(self, orc):
+        self.o = orc
+
+    def random_dictionary(self, d, h, seed, scale):
+        return self.o.random_dictionary(d, h, seed, scale)
+
+    def generate(self, w, pi, sigma2, n, seed):
+        return self.o.generate(w, pi, sigma2, n, seed)
+
+    def make_bars(self, size, n, seed):
+        return self.o.make_bars(size, n, seed=seed)
+
+
+# c4 (strong scaling) is generated in fixed blocks of BLOCK points, block b from
+# RngStream(block_seed(seed, b)): a rank can draw exactly its rows of the global
+# dataset, and every world size (1, 2, 4, 8) shards the same 4M points.
+BLOCK = 250_000
+
+
+def block_seed(seed: int, b: int) -> int:
+    return (seed << 20) | b
+
+
+def truth(w: Workload, gen=None) -> np.ndarray:
+    gen = gen or _ProductGen
     if w.kind == "bars":
-        _, t = bsc.bars_generate(w.bars_size, 1, seed=w.seed)
+        _, t = gen.make_bars(w.bars_size, 1, w.seed)
         return t
-    return bsc.random_dictionary(w.D, w.H, w.dict_seed, 5.0)
+    return gen.random_dictionary(w.D, w.H, w.dict_seed, 5.0)
 
 
-def data(w: Workload, n: int | None = None, seed_offset: int = 0) -> np.ndarray:
+def data(w: Workload, n: int | None = None, seed_offset: int = 0, gen=None, rows=None) -> np.ndarray:
     """The workload's data points (first ``n`` of the seeded stream for bars;
-    an independent seeded sample of size ``n`` for the random dictionaries)."""
+    an independent seeded sample of size ``n`` for the random dictionaries).
+    Strong-scaling workloads (c4) are blocked: ``rows=(b, e)`` returns global
+    rows [b, e) of the N-point dataset, identical whatever the sharding."""
+    gen = gen or _ProductGen
+    if w.scaling == "strong":
+        b, e = rows if rows is not None else (0, w.N if n is None else int(n))
+        wt = truth(w, gen)
+        parts = []
+        for blk in range(b // BLOCK, (e + BLOCK - 1) // BLOCK):
+            lo, hi = blk * BLOCK, (blk + 1) * BLOCK
+            y = gen.generate(wt, w.pi_true, w.sigma2_true, BLOCK, block_seed(w.seed, blk))
+            parts.append(y[max(b, lo) - lo:min(e, hi) - lo])
+        return np.ascontiguousarray(np.concatenate(parts)) if len(parts) > 1 else np.ascontiguousarray(parts[0])
     n = w.N if n is None else int(n)
     if w.kind == "bars":
-        y, _ = bsc.bars_generate(w.bars_size, n, seed=w.seed + seed_offset)
+        y, _ = gen.make_bars(w.bars_size, n, w.seed + seed_offset)
         return y
-    wt = truth(w)
-    return bsc.generate(bsc.BscParams(wt, w.pi_true, w.sigma2_true), n, w.seed + seed_offset)
+    wt = truth(w, gen)
+    return gen.generate(wt, w.pi_true, w.sigma2_true, n, w.seed + seed_offset)
 
 
-def init(w: Workload, y: np.ndarray) -> bsc.BscParams:
+def init(w: Workload, y: np.ndarray, gen_oracle=None) -> bsc.BscParams:
+    if gen_oracle is not None:
+        wi, pi, s2 = gen_oracle.baseline_init(y, w.H, w.seed)
+        return bsc.BscParams(wi, pi, s2)
     return bsc.baseline_init(y, w.H, w.seed)

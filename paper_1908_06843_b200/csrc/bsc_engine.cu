@@ -648,6 +648,7 @@ void BscEngine::load_data(const double* y, uint64_t n, bool device_ptr) {
   ck(cudaGetLastError(), "y2");
   n_ = n;
   if (oz_) slice_y(0, n, 0, s);
+  yts_whole_ = true;
 }
 
 // int8 slices of the resident Y for the two tensor-core products: rows with
@@ -999,6 +1000,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       ++launches_;
     }
     if (oz_ && (host_y || nchunks > 1)) slice_y(off, rows, c, s);
+    if (oz_ && c == 0 && !host_y && nchunks == 1 && !yts_whole_) slice_y(0, n, 0, s);  // after step_host
     if (oz_) {  // K1: B = Y·W, int8 slices on tcgen05
       const long long cap_rows = static_cast<long long>((cap_n_ + 1) & ~1ull);
       oz::Args g{};
@@ -1059,6 +1061,8 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     }
     if (c == 0) ev(4);
   }
+  // the Yᵀ slices now carry one column scale per chunk (d_ytsa_[c]) unless one chunk ran
+  if (oz_) yts_whole_ = nchunks == 1;
   const long long DH = (long long)D_ * H_;
   if (oz_)
   {

@@ -209,6 +209,7 @@ class BscEngine {
   double *d_ozpart_ = nullptr, *d_ozcs_ = nullptr;
   double* d_pscale_ = nullptr;  // per-point ⟨s⟩-row scales deferred to the ⟨S⟩ slicer (lane path)
   bool pscale_used_ = false;
+  bool yts_whole_ = true;  // Yᵀ slices scaled over the whole resident shard (false after a chunked step_host)
   unsigned long long* d_ozmax_ = nullptr;
   int oz_part_slots_ = 0, oz_ytsa_chunks_ = 0;
   long long oz_ess_bytes_ = 0;

@@ -6,6 +6,8 @@ free energy and one-step W, π, σ² within the tolerances below (north star:
 matrices). Small cases compare with the oracle directly; the full BASELINE
 sizes are checked through size-independent properties.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -232,7 +234,7 @@ def test_errors(pkg):
 
 # --------------------------------------------------- full-size properties
 def test_full_c2_properties(pkg, port):
-    """c2 at N = 200,000: candidates of a row sample bit-exact vs the oracle,
+    """c2 at N = 200,000: all candidate sets bit-exact vs the reference,
     shard additivity of the statistics, ⟨ssᵀ⟩ symmetry, Σ⟨s⟩ = value count,
     F = Σ log Z and EM monotone over a few iterations."""
     from paper_1908_06843_b200 import configs
@@ -243,8 +245,13 @@ def test_full_c2_properties(pkg, port):
     m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
     m.load(y)
     cand = m.candidates(p)
-    rows = np.random.default_rng(0).choice(len(y), 1500, replace=False)
-    assert np.array_equal(cand[rows], port.candidates(p.W, p.pi, p.sigma2, y[rows], w.hprime))
+    # every one of the 200,000 candidate sets, bit-exact against the reference build
+    # (oracle/_ref) when present, else the C port pinned to it
+    from oracle import oracle as O
+
+    orc = O.Oracle("ref") if O.Oracle.available("ref") else port
+    want = orc.candidates(p.W, p.pi, p.sigma2, y, w.hprime, threads=os.cpu_count() or 1)
+    assert np.array_equal(cand, want), int(np.count_nonzero(np.any(cand != want, axis=1)))
     st = m.estep_stats(p)
     assert np.allclose(st.sum_ssT, st.sum_ssT.T, rtol=0, atol=0)
     assert abs(st.value_counts[0] - st.sum_s.sum()) <= 1e-12 * st.value_counts[0]
@@ -281,6 +288,31 @@ def test_e2e_host_step_matches_resident(pkg):
     m2.load(y)
     b = m2.step(p)
     assert rel(a.params.W, b.params.W) < 1e-13 and abs(a.free_energy - b.free_energy) <= 1e-13 * abs(b.free_energy)
+    m.close()
+    m2.close()
+
+
+def test_resident_step_after_chunked_host_step(pkg):
+    """step_host slices Yᵀ per host chunk (one column scale per chunk); a later
+    resident step() on the same handle must not reuse those slices with chunk
+    0's scales (advisor finding, round 1). Chunks with different column maxima
+    (rows from 16384 on scaled ×4) make any mix-up visible."""
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c2"]
+    y = configs.data(w, 40_000)
+    y[16_384:] *= 4.0
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    a = m.step_host(p, y)  # 3 host chunks of ≤ 16384 points
+    b = m.step(p)  # resident data are the same rows
+    m2 = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m2.load(y)
+    c = m2.step(p)
+    for r in (a, b):
+        assert rel(r.params.W, c.params.W) < 1e-12, rel(r.params.W, c.params.W)
+        assert abs(r.free_energy - c.free_energy) <= 1e-12 * abs(c.free_energy)
+        assert abs(r.params.sigma2 - c.params.sigma2) <= 1e-12 * c.params.sigma2
     m.close()
     m2.close()
 

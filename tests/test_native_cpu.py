@@ -78,6 +78,27 @@ def test_fixtures_match_oracle(port):
     assert np.array_equal(configs.data(configs.CONFIGS["c1"], 64), port.make_bars(10, 64, seed=1)[0])
 
 
+def test_strong_scaling_data_is_sharding_invariant(port, monkeypatch):
+    """c4 is drawn in fixed blocks by global point index (configs.BLOCK): any
+    world size's shards concatenate to the same dataset, and the oracle-drawn
+    inputs of the reference arm are the same bytes as the package's."""
+    from dataclasses import replace
+
+    from paper_1908_06843_b200 import configs
+    from paper_1908_06843_b200.dist import shard_range
+
+    monkeypatch.setattr(configs, "BLOCK", 700)
+    w = replace(configs.CONFIGS["c4"], D=16, H=20, N=3000)
+    full = configs.data(w)
+    assert full.shape == (3000, 16)
+    for world in (1, 2, 3, 8):
+        parts = [configs.data(w, rows=shard_range(w.N, world, r)) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), full)
+    assert np.array_equal(configs.data(w, gen=configs.OracleGen(port)), full)
+    wc2 = configs.CONFIGS["c2"]
+    assert np.array_equal(configs.data(wc2, 300, gen=configs.OracleGen(port)), configs.data(wc2, 300))
+
+
 def test_shard_range_matches_shardplan():
     from paper_1908_06843_b200.dist import shard_range
 
