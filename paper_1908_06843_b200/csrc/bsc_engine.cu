@@ -57,7 +57,6 @@ const void* enum_pass_fn_t(int maxj) {
     default: return (const void*)enumerate_kernel<32, STAGED, PASS>;
   }
 }
-const void* front_fn(int maxj) { return enum_pass_fn_t<kPassFront, false>(maxj); }
 const void* fallback_fn(int maxj, bool staged) {
   return staged ? enum_pass_fn_t<kPassFallback, true>(maxj) : enum_pass_fn_t<kPassFallback, false>(maxj);
 }
@@ -586,19 +585,14 @@ void BscEngine::ensure_work(uint64_t n) {
   enum_warps_total_ = enum_ctas_ * warps;
   sc_ctas_ = enum_ctas_;
   if (lane_ok_) {
-    // front half: no state tables, occupancy from its registers
-    {  // per warp: its region (+ two B-row buffers when two CTAs still fit); per CTA: diag(G)
-      const int tot = EnumSmem::make(hprime_, 0, 0, 0, 0, static_cast<int>(H_)).total;
-      const int gst = 8 * ((static_cast<int>(H_) + 1) & ~1);
-      front_stage_b_ = maxj <= 16 && 8 * 8 * (tot + 2 * Hp_) + gst <= (227 * 1024) / 2 - 1024;
-      front_smem_ = 8 * 8 * (tot + (front_stage_b_ ? 2 * Hp_ : 0)) + gst;
-    }
-    const void* ff = front_fn(maxj);
-    ck(cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem_), "front smem attr");
+    // selection pass: thread per point, persistent over CTA tiles of 128 points
+    front_smem_ = select_smem(static_cast<int>(H_));
+    const void* sf = select_fn(static_cast<int>(hprime_));
+    ck(cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, front_smem_), "select smem attr");
     int fs = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs, ff, 256, front_smem_), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs, sf, 128, front_smem_), "occupancy");
     front_ctas_ = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)std::max(fs, 1) * prop.multiProcessorCount, (n + 7) / 8)));
+        1, std::min<uint64_t>((uint64_t)std::max(fs, 1) * prop.multiProcessorCount, (n + 127) / 128)));
     const void* fb = fallback_fn(maxj, stage_tables_);
     ck(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, enum_smem_), "fallback smem attr");
     lane_smem_ = lane_smem(static_cast<int>(gamma_), static_cast<int>(hprime_));
@@ -610,7 +604,7 @@ void BscEngine::ensure_work(uint64_t n) {
       ck(cudaFuncSetAttribute(lane_fn(gamma_, hprime_), cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)),
          "lane carveout");
     int fz = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fz, (const void*)lane_finish_kernel, 256, 0), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fz, finish_fn(maxj), 256, 0), "occupancy");
     fin_ctas_ = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)std::max(fz, 1) * prop.multiProcessorCount, (n + 7) / 8)));
     sc_ctas_ = std::max({enum_ctas_, front_ctas_, fin_ctas_});
@@ -832,6 +826,11 @@ void BscEngine::fill_enum_args(void* out, double temperature, bool cands, bool i
   // |b_fast − b_oracle| ≤ eps_dot·‖W_h‖·‖y‖: DMMA (any order) and the oracle's
   // left-to-right sum each within γ_D; the int8-sliced product within
   // D·11·2⁻⁵⁶·s_y·s_h ≤ 5.5·D·2⁻⁵³‖y‖‖W_h‖ plus its fp64 group combine (ozaki_gemm.cuh)
+  // fixed-point Σ⟨ssᵀ⟩ pairs: N contributions ≤ 1 per entry below 2^62
+  int kfx = 62;
+  for (uint64_t m = 1; m < std::max<uint64_t>(n_, 1) && kfx > 0; m <<= 1) --kfx;
+  fx_scale_ = std::ldexp(1.0, kfx);
+  a.fx_scale = fx_scale_;
   a.eps_dot = (oz_ && !infer) ? (7.0 * static_cast<double>(Dp_) + 16.0) * 0x1.0p-53
                               : 2.0 * (static_cast<double>(D_) + 2.0) * 0x1.0p-53;
 }
@@ -858,8 +857,8 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   const int maxj = maxj_for(H_);
   void* args[] = {&a};
   const bool lane = lane_ok_ && !infer && temperature == 1.0 && weight_mode_ != 2;
-  pscale_used_ = lane && oz_ && d_pscale_ != nullptr;
-  a.pscale = pscale_used_ ? d_pscale_ + off : nullptr;
+  pscale_used_ = false;
+  a.pscale = nullptr;
   if (!lane) {
     ck(cudaLaunchKernel(enum_fn(maxj, stage_tables_), dim3(enum_ctas_), dim3(enum_block_), args, enum_smem_, s),
        "enumerate launch");
@@ -867,14 +866,16 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
     ++launches_;
     return;
   }
-  // lane path: front half → lane-per-point states → fallback points → finish
+  // lane path: selection (thread per point) → lane-per-point states → fallback points → finish
   a.rec = d_rec_;
   a.pmode = d_pmode_;
-  a.stage_b = front_stage_b_ ? 1 : 0;
   a.cand_out = d_cand_ + off * hprime_;
+  a.pscale = nullptr;
+  pscale_used_ = false;
   const bool tm = timing_ && chunk == 0;
   lane_timed_ = tm;
-  ck(cudaLaunchKernel(front_fn(maxj), dim3(front_ctas_), dim3(256), args, front_smem_, s), "front launch");
+  ck(cudaLaunchKernel(select_fn(static_cast<int>(hprime_)), dim3(front_ctas_), dim3(128), args, front_smem_, s),
+     "select launch");
   if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[8]), s), "event");
   LaneArgs la{static_cast<int>(rows), static_cast<int>(hprime_), d_rec_, d_lout_, d_pmode_};
   void* largs[] = {&la};
@@ -890,18 +891,21 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   fa.H = H_;
   fa.Hp = Hp_;
   fa.hp = hprime_;
-  fa.rec = d_rec_;
   fa.out = d_lout_;
   fa.pmode = d_pmode_;
   fa.cand = d_cand_ + off * hprime_;
   fa.y2 = d_y2_ + off;
+  fa.B = d_b_ + off * Hp_;
+  fa.gdiag = d_gdiag_;
   fa.ES = d_es_ + off * Hp_;
   fa.ssT = d_stats_ + lay_.off_ssT();
   fa.cta_scalars = sc_fin;
-  fa.pscale = a.pscale;
   fa.base0 = a.base0;
   fa.inv2s = a.inv2s;
-  lane_finish_kernel<<<fin_ctas_, 256, 0, s>>>(fa);
+  fa.dlp = a.dlp;
+  fa.fx_scale = a.fx_scale;
+  void* fargs[] = {&fa};
+  ck(cudaLaunchKernel(finish_fn(maxj), dim3(fin_ctas_), dim3(256), fargs, 0, s), "finish launch");
   ck(cudaGetLastError(), "lane path");
   launches_ += 4;
 }
@@ -1082,7 +1086,8 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     launches_ += 2;
   } else {
     finalize_stats_kernel<<<std::max(1u, std::min(1024u, (H_ * H_ + 255) / 256)), 256, 0, s>>>(
-        3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail());
+        3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail(),
+        1.0 / fx_scale_);
     counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
     launches_ += 3;
   }

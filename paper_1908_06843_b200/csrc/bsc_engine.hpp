@@ -37,6 +37,9 @@ enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
 // The lane-per-point state pass for (γ, H') (lane_engine.cu).
 const void* lane_fn(int gamma, int hprime);
 int lane_smem(int gamma, int hprime);  // its dynamic shared memory per warp (bytes)
+const void* select_fn(int hprime);     // thread-per-point selection pass (select_kernels.cuh)
+int select_smem(int latents);          // its dynamic shared memory per CTA (bytes)
+const void* finish_fn(int maxj);       // lane_finish_kernel<MAXJ>
 
 // The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
 const void* ldv_kernel_fn(int maxj, bool staged);
@@ -209,7 +212,8 @@ class BscEngine {
   double *d_ozpart_ = nullptr, *d_ozcs_ = nullptr;
   double* d_pscale_ = nullptr;  // per-point ⟨s⟩-row scales deferred to the ⟨S⟩ slicer (lane path)
   bool pscale_used_ = false;
-  bool yts_whole_ = true;  // Yᵀ slices scaled over the whole resident shard (false after a chunked step_host)
+  bool yts_whole_ = true;
+  double fx_scale_ = 1.0;  // 2^k of the fixed-point Σ⟨ssᵀ⟩ pair accumulation (this E-step)  // Yᵀ slices scaled over the whole resident shard (false after a chunked step_host)
   unsigned long long* d_ozmax_ = nullptr;
   int oz_part_slots_ = 0, oz_ytsa_chunks_ = 0;
   long long oz_ess_bytes_ = 0;

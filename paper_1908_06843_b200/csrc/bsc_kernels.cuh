@@ -60,6 +60,17 @@ __device__ __forceinline__ void cp_async_row(double* dst, const double* src, int
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + c * 16), "l"(src + 2 * c) : "memory");
 }
 
+// Σ⟨ssᵀ⟩ candidate pairs in fixed point: each contribution v ∈ [0, 1] is added
+// as the integer rint(v·2^k) to the 64-bit image of its (strict upper) entry,
+// with 2^k chosen per E-step so that N·2^k < 2⁶³ (BscEngine::fx_scale). Integer
+// addition is associative, so the sum, unlike fp64 atomics, is the same bits
+// whatever order the points land in; the rounding (≤ 2^-(k+1) per term, 2.8e-14
+// at c2) is the order of one fp64 add into a running sum of 100-1000.
+// finalize_stats_kernel converts the triangle back to fp64 and mirrors it.
+__device__ __forceinline__ void pair_fx_add(double* entry, double v, double fx_scale) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(entry), __double2ull_rn(v * fx_scale));
+}
+
 // (value desc, index asc): true when (v1,i1) ranks before (v2,i2).
 __device__ __forceinline__ bool ranks_before(double v1, int i1, double v2, int i2) {
   return v1 > v2 || (v1 == v2 && i1 < i2);
@@ -304,6 +315,7 @@ struct EnumArgs {
   int stage_b;  // front pass: B rows double-buffered in shared memory by cp.async
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
+  double fx_scale;                          // 2^k of the fixed-point Σ⟨ssᵀ⟩ pairs (pair_fx_add)
 };
 
 constexpr int kPoolCap = 64;
@@ -1062,7 +1074,7 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
         ++p;
       }
       const int q = p + 1 + idx;
-      atomicAdd(a.ssT + (long long)scand[p] * H + scand[q], souts[o] * inv_z);
+      pair_fx_add(a.ssT + (long long)scand[p] * H + scand[q], souts[o] * inv_z, a.fx_scale);
     }
     __syncwarp();
   }
@@ -1110,14 +1122,21 @@ static __global__ void reduce_ysT_kernel(const double* __restrict__ part, const 
   }
 }
 
-// Mirror of the upper triangle of Σ⟨ssᵀ⟩ and the scalars.
+// Σ⟨ssᵀ⟩ off-diagonals: the fixed-point upper triangle (pair_fx_add) back to
+// fp64 (one rounding), mirrored; and the scalars.
 static __global__ void finalize_stats_kernel(int nctas, const double* __restrict__ cta_scalars, int H, long long npoints,
-                                      double* __restrict__ stats, long long off_ssT, long long off_tail) {
+                                      double* __restrict__ stats, long long off_ssT, long long off_tail,
+                                      double fx_inv) {
   double* ssT = stats + off_ssT;
   const long long HH = (long long)H * H;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < HH; e += (long long)gridDim.x * blockDim.x) {
     const int i = static_cast<int>(e / H), j = static_cast<int>(e % H);
-    if (i > j) ssT[e] = ssT[(long long)j * H + i];
+    if (i < j) {
+      const double v =
+          __ull2double_rn(static_cast<unsigned long long>(__double_as_longlong(ssT[e]))) * fx_inv;
+      ssT[e] = v;
+      ssT[(long long)j * H + i] = v;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     double l = 0.0, y2 = 0.0;

@@ -4,6 +4,7 @@
 // for every other shape with 2 ≤ γ ≤ 6, 2 ≤ H' ≤ 16.
 #include "bsc_engine.hpp"
 #include "lane_kernels.cuh"
+#include "select_kernels.cuh"
 
 namespace bscgpu {
 
@@ -17,6 +18,37 @@ const void* lane_fn(int gamma, int hprime) {
     case 4: return (const void*)lane_states_kernel<4>;
     case 5: return (const void*)lane_states_kernel<5>;
     default: return (const void*)lane_states_kernel<6>;
+  }
+}
+
+// the thread-per-point selection pass for H' (2 ≤ H' ≤ 16)
+const void* select_fn(int hprime) {
+  switch (hprime) {
+#define SEL_CASE(v) \
+  case v:           \
+    return (const void*)select_kernel<v>;
+    SEL_CASE(2) SEL_CASE(3) SEL_CASE(4) SEL_CASE(5) SEL_CASE(6) SEL_CASE(7) SEL_CASE(8) SEL_CASE(9)
+    SEL_CASE(10) SEL_CASE(11) SEL_CASE(12) SEL_CASE(13) SEL_CASE(14) SEL_CASE(15) SEL_CASE(16)
+#undef SEL_CASE
+    default:
+      return nullptr;
+  }
+}
+int select_smem(int latents) { return select_smem_bytes(latents); }
+
+// the finish pass with the singleton weights of MAXJ·32 ≥ H units in registers
+const void* finish_fn(int maxj) {
+  switch (maxj) {
+    case 1: return (const void*)lane_finish_kernel<1>;
+    case 2: return (const void*)lane_finish_kernel<2>;
+    case 4: return (const void*)lane_finish_kernel<4>;
+    case 6: return (const void*)lane_finish_kernel<6>;
+    case 8: return (const void*)lane_finish_kernel<8>;
+    case 10: return (const void*)lane_finish_kernel<10>;
+    case 12: return (const void*)lane_finish_kernel<12>;
+    case 16: return (const void*)lane_finish_kernel<16>;
+    case 24: return (const void*)lane_finish_kernel<24>;
+    default: return (const void*)lane_finish_kernel<32>;
   }
 }
 

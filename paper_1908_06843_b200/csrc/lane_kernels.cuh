@@ -517,65 +517,89 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
 
 struct FinishArgs {
   int N, H, Hp, hp;
-  const double* rec;
   const double* out;
   const int* pmode;
   const uint32_t* cand;  // N × hp, ascending
   const double* y2;
+  const double* B;       // N × Hp rows of Y·W (singleton terms)
+  const double* gdiag;   // diag(G)
   double* ES;
-  double* ssT;
-  double* cta_scalars;  // [gridDim.x][2] Σ log Z_n (deferred points), 0
-  double* pscale;       // non-null: leave the singleton row unscaled, record the scale per point
-  double base0, inv2s;
+  double* ssT;           // H × H; strict upper triangle accumulated as fixed point (pair_fx_add)
+  double* cta_scalars;   // [gridDim.x][2] Σ log Z_n (deferred points), 0
+  double base0, inv2s, dlp;
+  double fx_scale;       // 2^k of the fixed-point pair accumulation
 };
 
-// Warp per deferred point: log Z = base + shift + log(zs1·e^{mxs−shift} + Σ_multi q)
-// (core.cpp:36-45 at T = 1), the ⟨s_n⟩ row and the candidate pairs of Σ⟨ssᵀ⟩.
-static __global__ void __launch_bounds__(256) lane_finish_kernel(FinishArgs a) {
-  __shared__ double red[16];
+// Warp per deferred point (linear_discrete.cpp:272-304 at T = 1): the singleton
+// weights of all H units relative to the point's shift (recomputed from the B
+// row, as the selection pass leaves them), log Z = base + shift + log(z)
+// (core.cpp:36-45), the normalised ⟨s_n⟩ row (candidates take their marginals
+// from the state pass) and the candidate pairs of Σ⟨ssᵀ⟩ (fixed point:
+// order-independent, so the statistics are bitwise reproducible).
+template <int MAXJ>
+__global__ void __launch_bounds__(256) lane_finish_kernel(FinishArgs a) {
+  __shared__ double red[8];
+  __shared__ uint16_t pq[256];  // moment entry o → (p, q), p ≤ q (row-major upper triangle with diagonal)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int hp = a.hp, nm = hp * (hp + 1) / 2;
+  for (int o = threadIdx.x; o < nm; o += blockDim.x) {
+    int idx = o, p = 0;
+    while (idx >= hp - p) {
+      idx -= hp - p;
+      ++p;
+    }
+    pq[o] = static_cast<uint16_t>(p | ((p + idx) << 8));
+  }
+  __syncthreads();
+  const int row_lines = (a.Hp * 8 + 127) / 128;
   double lse_acc = 0.0;
   for (int n = blockIdx.x * (blockDim.x >> 5) + wib; n < a.N; n += nwarps) {
+    // the B rows of the next two points of this warp: into L2, and the next one into L1
+    if (n + 2 * nwarps < a.N)
+      for (int l = lane; l < row_lines; l += 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + (long long)(n + 2 * nwarps) * a.Hp + l * 16));
+    if (n + nwarps < a.N)
+      for (int l = lane; l < row_lines; l += 32)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.B + (long long)(n + nwarps) * a.Hp + l * 16));
     const int mode = a.pmode[n];
     if (mode != kModeShift && mode != kModeMax) continue;
     const long long tile = n >> 5;
-    const double* rt = a.rec + tile * lane_rec_fields(hp) * 32 + (n & 31);
     const double* ot = a.out + tile * lane_out_fields(hp) * 32 + (n & 31);
     const double shift = ot[0], zm = ot[32];
-    const double zs1 = rt[32], mxs = rt[64];
-    const double es = exp_nonpos(mxs - shift);
-    const double z1 = zs1 * es + zm;
+    const double* brow = a.B + (long long)n * a.Hp;
+    double e[MAXJ];
+    double zs = 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      e[j] = 0.0;
+      if (h < a.H) {
+        // rel = fma(inv2s, 2b − G_hh, dlp), the selection pass's rounding: shift ≥ rel
+        e[j] = exp_nonpos(__fma_rn(a.inv2s, __fma_rn(2.0, brow[h], -a.gdiag[h]), a.dlp) - shift);
+        zs += e[j];
+      }
+    }
+    zs = warp_sum(zs) + exp_nonpos(-shift);  // + the zero state
+    const double z1 = zs + zm;
     const double inv_z = 1.0 / z1;
     if (lane == 0) lse_acc += (a.base0 - a.y2[n] * a.inv2s) + (shift + log(z1));
-    const double scale = es * inv_z;
     double* esrow = a.ES + (long long)n * a.Hp;
-    // With pscale the ⟨s⟩-row scale is applied by its consumer (the ⟨S⟩ slicer
-    // multiplies row n by pscale[n], the same single product) instead of a
-    // read-modify-write of the whole row here; the candidate entries are stored
-    // pre-divided so that product restores them (within an ulp).
-    const bool defer_row = a.pscale != nullptr && scale > 0x1.0p-1000 && scale < 0x1.0p1000;
-    if (defer_row) {
-      if (lane == 0) a.pscale[n] = scale;
-    } else {
-      for (int h = lane; h < a.H; h += 32) esrow[h] *= scale;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int h = lane + 32 * j;
+      if (h < a.H) esrow[h] = e[j] * inv_z;
     }
     __syncwarp();
     const uint32_t* cn = a.cand + (long long)n * hp;
-    // (p, q) of the moment entries this lane finishes: entries lane, lane+32, …
+    // the moment entries this lane finishes: lane, lane + 32, …
     for (int o = lane; o < nm; o += 32) {
-      int idx = o, p = 0;
-      while (idx >= hp - p) {
-        idx -= hp - p;
-        ++p;
-      }
-      const int q = p + idx;
+      const int p = pq[o] & 0xff, q = pq[o] >> 8;
       const double v = ot[(2 + o) * 32] * inv_z;
       if (q == p)
-        esrow[cn[p]] = defer_row ? v / scale : v;
+        esrow[cn[p]] = v;
       else
-        atomicAdd(a.ssT + (long long)cn[p] * a.H + cn[q], v);
+        pair_fx_add(a.ssT + (long long)cn[p] * a.H + cn[q], v, a.fx_scale);
     }
     __syncwarp();
   }

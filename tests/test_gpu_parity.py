@@ -292,6 +292,30 @@ def test_e2e_host_step_matches_resident(pkg):
     m2.close()
 
 
+@pytest.mark.parametrize("cfg,n", [("c2", 60_000), ("c3", 6_000)])
+def test_bitwise_reproducible(pkg, cfg, n):
+    """Every reduction of the BSC E-step is order-fixed (split-K partials,
+    per-CTA partials, column sums) or order-independent (the Σ⟨ssᵀ⟩ candidate
+    pairs in fixed point), so repeated E-steps and steps give the same bits —
+    as the reference does at a fixed shard plan (parallel.hpp:35-37)."""
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS[cfg]
+    y = configs.data(w, n)
+    p = configs.init(w, y)
+    m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    m.load(y)
+    a, b = m.estep_stats(p), m.estep_stats(p)
+    for k in ["sum_s", "sum_ssT", "sum_y_sT", "value_counts"]:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    assert a.log_partition == b.log_partition and a.sum_y2 == b.sum_y2
+    r1, r2 = m.step(p), m.step(p)
+    assert np.array_equal(r1.params.W, r2.params.W)
+    assert r1.params.pi == r2.params.pi and r1.params.sigma2 == r2.params.sigma2
+    assert r1.free_energy == r2.free_energy
+    m.close()
+
+
 def test_resident_step_after_chunked_host_step(pkg):
     """step_host slices Yᵀ per host chunk (one column scale per chunk); a later
     resident step() on the same handle must not reuse those slices with chunk
