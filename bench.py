@@ -284,10 +284,18 @@ def main():
     model.set_stream(stream.cuda_stream)
     model.load(y)
     model.set_params(p0)
-    stats_view = bdist.stats_tensor(model)
+    if world > 1:
+        # the job's NCCL communicator inside the engine library: an iteration is one
+        # C call (E-step, ncclAllReduce of the packed statistics, replicated M-step)
+        bdist.init_native(model)
 
-    def one_step():
-        bdist.distributed_step(model, stats_view)
+        def one_step():
+            model.step_allreduce()
+    else:
+        stats_view = bdist.stats_tensor(model)
+
+        def one_step():
+            bdist.distributed_step(model, stats_view)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:  # sampled over warm-up + timed steps (≥ 0.2 s of load)

@@ -45,6 +45,16 @@
 extern "C" {
 #endif
 
+/* Return codes: the values of prsp_status (prsp.h:39-45), under names that do not
+ * clash with prsp.h when both are included. */
+enum {
+  PRSP_BSC_GPU_OK = 0,
+  PRSP_BSC_GPU_ERR_CONFIG = 2,
+  PRSP_BSC_GPU_ERR_DATA = 3,
+  PRSP_BSC_GPU_ERR_NUMERIC = 4,
+  PRSP_BSC_GPU_ERR_INTERNAL = 5
+};
+
 typedef struct prsp_bsc_gpu prsp_bsc_gpu; /* one device's engine + resident shard */
 
 const char* prsp_bsc_gpu_version(void);
@@ -96,6 +106,20 @@ int prsp_bsc_gpu_set_stats(prsp_bsc_gpu* ctx, const double* sum_s, const double*
 int prsp_bsc_gpu_mstep(prsp_bsc_gpu* ctx);
 /* estep + mstep on the resident shard; *free_energy = Σ_n log Z_n at the incoming params. */
 int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy);
+/* ---- multi-GPU: one process per GPU, each holding its row
+ * shard (ShardPlan::with_shards, parallel.cpp:27-43); the only exchange is the
+ * sum of the packed statistics, replacing map_reduce's ordered fold
+ * (parallel.cpp:109-158). NCCL is resolved at run time (dlopen libnccl.so.2).
+ *   prsp_bsc_gpu_nccl_unique_id   ncclGetUniqueId (root rank; send the 128 bytes to the others)
+ *   prsp_bsc_gpu_nccl_init        ncclCommInitRank on the context's device (owned by ctx)
+ *   prsp_bsc_gpu_nccl_attach      use a communicator the host owns (ncclComm_t, borrowed)
+ *   prsp_bsc_gpu_step_allreduce   LinearDiscreteModel::step over the job: local E-step,
+ *                                 ncclAllReduce(sum) of the statistics on the engine stream,
+ *                                 replicated M-step; F = the job's Σ log Z. */
+int prsp_bsc_gpu_nccl_unique_id(char* id128);
+int prsp_bsc_gpu_nccl_init(prsp_bsc_gpu* ctx, const char* id128, int nranks, int rank);
+int prsp_bsc_gpu_nccl_attach(prsp_bsc_gpu* ctx, void* nccl_comm);
+int prsp_bsc_gpu_step_allreduce(prsp_bsc_gpu* ctx, double temperature, double* free_energy);
 /* F = Σ_n log Z_n (all ranks, once the statistics were all-reduced) of the last M-step's input. */
 int prsp_bsc_gpu_free_energy(prsp_bsc_gpu* ctx, double* out);
 /* Reference-facing step: host Y and params in, host params and F out

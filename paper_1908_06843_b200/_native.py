@@ -42,6 +42,10 @@ SIGNATURES = {
     "prsp_bsc_gpu_mstep": [_ptr],
     "prsp_bsc_gpu_step": [_ptr, _dbl, _dp],
     "prsp_bsc_gpu_free_energy": [_ptr, _dp],
+    "prsp_bsc_gpu_nccl_unique_id": [_ptr],
+    "prsp_bsc_gpu_nccl_init": [_ptr, _ptr, _int, _int],
+    "prsp_bsc_gpu_nccl_attach": [_ptr, _ptr],
+    "prsp_bsc_gpu_step_allreduce": [_ptr, _dbl, _dp],
     "prsp_bsc_gpu_step_host": [_ptr, _ptr, _u64, _ptr, _dbl, _dbl, _dbl, _ptr, _dp, _dp, _dp],
     "prsp_bsc_gpu_candidates": [_ptr, _ptr],
     "prsp_bsc_gpu_inference": [_ptr, _ptr, _ptr, _ptr],

@@ -218,6 +218,24 @@ class LinearDiscreteGpuModel:
         p = BscParams(wo, pi.value, s2.value) if self.model == "bsc" else LinearDiscreteParams(wo, s2.value, pi.value)
         return StepResult(p, f.value)
 
+    # ------------------------------------------------ multi-GPU (native NCCL)
+    def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        """Join the job's NCCL communicator (ncclCommInitRank on this model's device);
+        ``unique_id`` is ``nccl_unique_id()`` of rank 0, sent to every rank."""
+        if len(unique_id) != 128:
+            raise N.ConfigError(2, "nccl: the unique id is 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        N.call("prsp_bsc_gpu_nccl_init", self._h, C.cast(buf, C.c_void_p), int(nranks), int(rank))
+
+    def step_allreduce(self, params: BscParams | None = None, temperature: float = 1.0) -> float:
+        """LinearDiscreteModel::step over the whole job: local E-step, NCCL sum of the
+        packed statistics, replicated M-step, all inside the library. Returns F."""
+        if params is not None:
+            self.set_params(params)
+        f = _dbl()
+        N.call("prsp_bsc_gpu_step_allreduce", self._h, float(temperature), C.byref(f))
+        return f.value
+
     def estep_stats(self, params: BscParams, data=None, temperature: float = 1.0) -> SuffStats:
         """LinearDiscreteModel::estep_stats (:327-334) over the resident shard."""
         if data is not None:
@@ -301,6 +319,13 @@ class BscGpuModel(LinearDiscreteGpuModel):
 
     def __init__(self, dim: int, latents: int, trunc: TruncationConfig, device: int = 0):
         super().__init__("bsc", dim, latents, trunc, None, device)
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the engine library (rank 0 of a job)."""
+    buf = C.create_string_buffer(128)
+    N.call("prsp_bsc_gpu_nccl_unique_id", C.cast(buf, C.c_void_p))
+    return buf.raw
 
 
 # ------------------------------------------------------------------ fixtures

@@ -61,6 +61,7 @@ class BscEngine {
   BscEngine& operator=(const BscEngine&) = delete;
 
   void set_stream(void* stream);
+  int device() const { return device_; }
   void* stream() const { return stream_; }
 
   // Data shard (row-major N×D, host or device pointer); stays resident.

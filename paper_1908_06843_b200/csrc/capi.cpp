@@ -15,10 +15,16 @@
 #include "bsc_engine.hpp"
 #include "fixtures.hpp"
 #include "mca_engine.hpp"
+#include "nccl_link.hpp"
 #include "run_io.hpp"
 
 struct prsp_bsc_gpu {
   bscgpu::BscEngine engine;
+  bscgpu::nccl::Comm comm = nullptr;  // the statistics all-reduce across ranks
+  bool own_comm = false;
+  ~prsp_bsc_gpu() {
+    if (comm && own_comm) bscgpu::nccl::api().comm_destroy(comm);
+  }
   prsp_bsc_gpu(uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, int dev) : engine(d, h, hp, g, cap, dev) {}
   prsp_bsc_gpu(int fam, uint32_t d, uint32_t h, uint32_t hp, uint32_t g, uint64_t cap, const double* vals, uint32_t nv,
                int dev)
@@ -234,6 +240,60 @@ int prsp_bsc_gpu_step(prsp_bsc_gpu* ctx, double temperature, double* free_energy
     need(ctx, "ctx");
     const double f = ctx->engine.step(temperature);
     if (free_energy) *free_energy = f;
+  });
+}
+
+int prsp_bsc_gpu_nccl_unique_id(char* id128) {
+  return guarded([&] {
+    need(id128, "id");
+    bscgpu::nccl::UniqueId id;
+    bscgpu::nccl::check(bscgpu::nccl::need().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(id128, id.internal, sizeof id.internal);
+  });
+}
+
+int prsp_bsc_gpu_nccl_init(prsp_bsc_gpu* ctx, const char* id128, int nranks, int rank) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(id128, "id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw bscgpu::Error(bscgpu::kConfig, "nccl: bad rank / nranks");
+    const auto& api = bscgpu::nccl::need();
+    bscgpu::nccl::UniqueId id;
+    std::memcpy(id.internal, id128, sizeof id.internal);
+    if (cudaSetDevice(ctx->engine.device()) != cudaSuccess) throw bscgpu::Error(bscgpu::kInternal, "cuda: set device");
+    bscgpu::nccl::Comm comm = nullptr;
+    bscgpu::nccl::check(api.comm_init_rank(&comm, nranks, id, rank), "ncclCommInitRank");
+    if (ctx->comm && ctx->own_comm) api.comm_destroy(ctx->comm);
+    ctx->comm = comm;
+    ctx->own_comm = true;
+  });
+}
+
+int prsp_bsc_gpu_nccl_attach(prsp_bsc_gpu* ctx, void* nccl_comm) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(nccl_comm, "comm");
+    bscgpu::nccl::need();
+    if (ctx->comm && ctx->own_comm) bscgpu::nccl::api().comm_destroy(ctx->comm);
+    ctx->comm = nccl_comm;
+    ctx->own_comm = false;
+  });
+}
+
+int prsp_bsc_gpu_step_allreduce(prsp_bsc_gpu* ctx, double temperature, double* free_energy) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (!ctx->comm) throw bscgpu::Error(bscgpu::kConfig, "nccl: no communicator (prsp_bsc_gpu_nccl_init / _attach)");
+    auto& e = ctx->engine;
+    e.estep(temperature);
+    // the packed statistics, summed in place over the ranks on the engine's stream:
+    // the M-step (replicated, deterministic) then reads the global sums
+    bscgpu::nccl::check(bscgpu::nccl::need().all_reduce(e.stats_device(), e.stats_device(), e.layout().count(),
+                                                        bscgpu::nccl::kFloat64, bscgpu::nccl::kSum, ctx->comm,
+                                                        static_cast<cudaStream_t>(e.stream())),
+                        "ncclAllReduce");
+    e.mstep();
+    if (free_energy) *free_energy = e.last_free_energy();
   });
 }
 

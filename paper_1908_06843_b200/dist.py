@@ -88,6 +88,21 @@ def distributed_step(model, stats_view, temperature: float = 1.0, group=None) ->
     model.mstep_device()
 
 
+def init_native(model, group=None) -> None:
+    """Give ``model`` the job's NCCL communicator through the engine library: rank
+    0's ncclGetUniqueId is broadcast over the torch.distributed group, then every
+    rank joins with ncclCommInitRank. After this, ``model.step_allreduce`` runs
+    the whole iteration (E-step, statistics all-reduce, M-step) in C++/CUDA."""
+    import torch.distributed as dist
+
+    from .bsc import nccl_unique_id
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    model.nccl_init(box[0], world, rank)
+
+
 def mca_distributed_step(model, temperature: float = 1.0, group=None) -> float:
     """One max-causes iteration across ranks (MaxCausesModel::step,
     max_causes.cpp:416-446): local E pass → all-reduce(Σ winner statistics) →

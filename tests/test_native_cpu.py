@@ -30,6 +30,17 @@ def test_library_exports_every_declared_symbol():
     assert set(syms) <= set(_native.SIGNATURES)
 
 
+def test_nccl_resolved_at_run_time():
+    """The statistics all-reduce uses NCCL through dlopen (nccl_link.hpp): the
+    library has no link-time NCCL dependency, and the bootstrap works here."""
+    from paper_1908_06843_b200 import _native
+    from paper_1908_06843_b200.bsc import nccl_unique_id
+
+    assert "libnccl" not in os.popen(f"ldd {_native.LIB_PATH}").read()
+    uid = nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+
+
 def test_library_is_sm100a():
     from paper_1908_06843_b200 import _native
 
