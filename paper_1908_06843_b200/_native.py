@@ -12,7 +12,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB_PATH = os.path.join(HERE, "_lib", "libprsp_bsc_b200.so")
+# PRSP_BSC_LIB: an alternative build of the same library (A/B runs of kernel variants)
+LIB_PATH = os.environ.get("PRSP_BSC_LIB") or os.path.join(HERE, "_lib", "libprsp_bsc_b200.so")
 
 _u32, _u64, _dbl, _int, _ptr = C.c_uint32, C.c_uint64, C.c_double, C.c_int, C.c_void_p
 _dp = C.POINTER(C.c_double)

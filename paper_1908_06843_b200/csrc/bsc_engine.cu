@@ -11,6 +11,7 @@
 
 #include "bsc_kernels.cuh"
 #include "lane_kernels.cuh"
+#include "finish_slice_kernels.cuh"
 #include "dgemm.cuh"
 #include "ozaki_gemm.cuh"
 #include "mstep_kernels.cuh"
@@ -202,7 +203,7 @@ void BscEngine::init(int device) {
   d_gdiag_ = dalloc<double>(H_, "gdiag");
   d_stats_ = dalloc<double>(lay_.count(), "stats");
   d_smulti_ = dalloc<double>(H_, "s_multi");
-  d_err_ = dalloc<int>(1, "err");
+  d_err_ = dalloc<int>(2, "err");  // error flags, fallback-point count
   d_bm_ = dalloc<double>((size_t)H_ * Hp_, "Bm");
   d_u_ = dalloc<double>((size_t)H_ * Hp_, "U");
   d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
@@ -607,7 +608,20 @@ void BscEngine::ensure_work(uint64_t n) {
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fz, finish_fn(maxj), 256, 0), "occupancy");
     fin_ctas_ = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)std::max(fz, 1) * prop.multiProcessorCount, (n + 7) / 8)));
-    sc_ctas_ = std::max({enum_ctas_, front_ctas_, fin_ctas_});
+    // finish fused with the ⟨S⟩ᵀ slicer (sliced path): 32-point sub-tiles while two CTAs fit an
+    // SM's shared memory beside each other or one does, else 16-point sub-tiles
+    fs_ctas_ = 0;
+    const char* fse = std::getenv("BSC_FUSED_FINISH");
+    if (oz_ && !(fse && fse[0] == '0')) {
+      fs_pt_ = finish_slice_smem(32, static_cast<int>(H_), Hp_) <= 200 * 1024 ? 32 : 16;
+      fs_smem_ = finish_slice_smem(fs_pt_, static_cast<int>(H_), Hp_);
+      ck(cudaFuncSetAttribute(finish_slice_fn(fs_pt_), cudaFuncAttributeMaxDynamicSharedMemorySize, fs_smem_),
+         "finish+slice smem attr");
+      int fo = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fo, finish_slice_fn(fs_pt_), 256, fs_smem_), "occupancy");
+      fs_ctas_ = std::max(fo, 1) * prop.multiProcessorCount;
+    }
+    sc_ctas_ = std::max({enum_ctas_, front_ctas_, fin_ctas_, fs_ctas_});
     const uint64_t tiles = (n + 31) / 32;
     d_rec_ = dalloc<double>(tiles * 32 * lane_rec_fields(static_cast<int>(hprime_)), "lane records");
     d_lout_ = dalloc<double>(tiles * 32 * lane_out_fields(static_cast<int>(hprime_)), "lane moments");
@@ -904,8 +918,23 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   fa.inv2s = a.inv2s;
   fa.dlp = a.dlp;
   fa.fx_scale = a.fx_scale;
-  void* fargs[] = {&fa};
-  ck(cudaLaunchKernel(finish_fn(maxj), dim3(fin_ctas_), dim3(256), fargs, 0, s), "finish launch");
+  es_sliced_ = false;
+  if (oz_ && fs_ctas_ > 0) {
+    // sliced path: the ⟨s⟩ rows go straight to the int8 operand of Yᵀ⟨S⟩ (finish_slice_kernels.cuh)
+    FinishSliceArgs fsa{};
+    fsa.f = fa;
+    fsa.ess = d_ess_;
+    fsa.slice_stride = static_cast<long long>(Hp_) * oz_npc_;
+    fsa.colsum = d_ozcs_ + (off / 128) * Hp_;
+    fsa.inv56 = 0x1.0p55;  // 2^56 / the ⟨S⟩ slice scale 2 (d_two_)
+    void* fsargs[] = {&fsa};
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(fs_ctas_, (rows + 127) / 128));
+    ck(cudaLaunchKernel(finish_slice_fn(fs_pt_), dim3(grid), dim3(256), fsargs, fs_smem_, s), "finish+slice launch");
+    es_sliced_ = true;
+  } else {
+    void* fargs[] = {&fa};
+    ck(cudaLaunchKernel(finish_fn(maxj), dim3(fin_ctas_), dim3(256), fargs, 0, s), "finish launch");
+  }
   ck(cudaGetLastError(), "lane path");
   launches_ += 4;
 }
@@ -951,11 +980,15 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     vpart_chunks_ = nchunks;
   }
   launches_ = 0;
+  NvtxRange nv_estep("bsc.estep");
   ev(0);
-  if (!gram_fresh_) refresh_gram();
+  if (!gram_fresh_) {
+    NvtxRange nv("bsc.gram");
+    refresh_gram();
+  }
   ev(1);
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
-  ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
+  ck(cudaMemsetAsync(d_err_, 0, 2 * sizeof(int), s), "zero err");
   ck(cudaMemsetAsync(d_warp_es_, 0, (size_t)nchunks * splits_ * Hp_ * 8, s), "zero colsums");
   // per-CTA scalar partials: [role: whole/front pass, lane finish, fallback][chunk][sc_ctas_]
   ck(cudaMemsetAsync(d_warp_sc_, 0, (size_t)3 * nchunks * sc_ctas_ * 2 * 8, s), "zero cta scalars");
@@ -1005,6 +1038,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     }
     if (oz_ && (host_y || nchunks > 1)) slice_y(off, rows, c, s);
     if (oz_ && c == 0 && !host_y && nchunks == 1 && !yts_whole_) slice_y(0, n, 0, s);  // after step_host
+    nvtxRangePushA("bsc.gemm_yw");
     if (oz_) {  // K1: B = Y·W, int8 slices on tcgen05
       const long long cap_rows = static_cast<long long>((cap_n_ + 1) & ~1ull);
       oz::Args g{};
@@ -1022,16 +1056,25 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
       ++launches_;
     }
+    nvtxRangePop();
     if (c == 0) ev(2);
-    launch_enumerate(temperature, want_candidates, false, off, rows, c);
+    {
+      NvtxRange nv("bsc.enumerate");
+      launch_enumerate(temperature, want_candidates, false, off, rows, c);
+    }
     if (c == 0) ev(3);
+    NvtxRange nv_k4("bsc.gemm_ytes");
     if (oz_) {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES — ⟨S⟩ᵀ slices (+ column sums = Σ⟨s⟩ partials), then tcgen05
-      const unsigned kb = static_cast<unsigned>((rows + 127) / 128);
-      oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, kb), 256, 0, s>>>(
-          d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_,
-          (static_cast<long long>(rows) + 127) / 128 * 128, d_two_, d_ess_, static_cast<long long>(Hp_) * oz_npc_,
-          d_ozcs_ + (off / 128) * Hp_, pscale_used_ ? d_pscale_ + off : nullptr);
-      ck(cudaGetLastError(), "slice ES");
+      if (!es_sliced_) {  // (the lane path's finish pass has written the slices already)
+        const unsigned kb = static_cast<unsigned>((rows + 127) / 128);
+        oz::oz_slice_cols_kernel<<<dim3((Hp_ + 31) / 32, kb), 256, 0, s>>>(
+            d_es_ + off * Hp_, Hp_, static_cast<long long>(rows), static_cast<int>(H_), Hp_,
+            (static_cast<long long>(rows) + 127) / 128 * 128, d_two_, d_ess_, static_cast<long long>(Hp_) * oz_npc_,
+            d_ozcs_ + (off / 128) * Hp_, pscale_used_ ? d_pscale_ + off : nullptr);
+        ck(cudaGetLastError(), "slice ES");
+        ++launches_;
+      }
+      es_sliced_ = false;
       oz::Args g{};
       g.sa = d_ytsa_ + (size_t)((host_y || nchunks > 1) ? c : 0) * Dp_;
       g.sb = d_two_;
@@ -1045,7 +1088,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
       ck(oz::launch_gemm(A, B, static_cast<int>(D_), static_cast<int>(H_), static_cast<int>(rows), g, oz_sms(device_),
                          s),
          "oz gemm Yt·ES");
-      launches_ += 2;
+      ++launches_;
     } else {  // K4: Σ y⟨s⟩ᵀ += Yᵀ·ES over this chunk (+ fused Σ⟨s⟩), split-K over its rows
       const int krows = static_cast<int>((rows + 1) & ~1ull);
       int kchunk = (krows + splits_ - 1) / splits_;
@@ -1067,6 +1110,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   }
   // the Yᵀ slices now carry one column scale per chunk (d_ytsa_[c]) unless one chunk ran
   if (oz_) yts_whole_ = nchunks == 1;
+  NvtxRange nv_fin("bsc.finalize_stats");
   const long long DH = (long long)D_ * H_;
   if (oz_)
   {
@@ -1107,6 +1151,7 @@ void BscEngine::check_err() {
 // The M-step is a fixed sequence of ~40 small launches for a given (D, H):
 // it runs eagerly once, is then captured into a CUDA graph and replayed.
 void BscEngine::mstep() {
+  NvtxRange nv("bsc.mstep");
   ck(cudaSetDevice(device_), "set device");
   auto s = static_cast<cudaStream_t>(stream_);
   auto* sc = static_cast<MstepScalars*>(d_msc_);
@@ -1317,7 +1362,7 @@ void BscEngine::inference(double* map_states, double* map_mass, double* expected
   GemmArgs g{static_cast<int>(n_), Hp_, Dp_, d_y_, Dp_, d_w_, Hp_, d_b_, Hp_, 1.0, 0.0, Dp_, 0};
   ck(launch_dgemm<GEMM1_CFG>(g, 1, s), "gemm Y·W");
   ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
-  ck(cudaMemsetAsync(d_err_, 0, sizeof(int), s), "zero err");
+  ck(cudaMemsetAsync(d_err_, 0, 2 * sizeof(int), s), "zero err");
   launch_enumerate(1.0, true, true, 0, n_, 0);
   std::vector<int> st(n_);
   std::vector<uint32_t> cand(n_ * hprime_);

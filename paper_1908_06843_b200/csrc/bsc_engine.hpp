@@ -40,6 +40,8 @@ int lane_smem(int gamma, int hprime);  // its dynamic shared memory per warp (by
 const void* select_fn(int hprime);     // thread-per-point selection pass (select_kernels.cuh)
 int select_smem(int latents);          // its dynamic shared memory per CTA (bytes)
 const void* finish_fn(int maxj);       // lane_finish_kernel<MAXJ>
+const void* finish_slice_fn(int pt);   // lane_finish_slice_kernel<PT> (finish_slice_kernels.cuh)
+int finish_slice_smem(int pt, int latents, int hp_padded);
 
 // The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
 const void* ldv_kernel_fn(int maxj, bool staged);
@@ -197,6 +199,8 @@ class BscEngine {
   // lane-per-point state pass (lane_kernels.cuh)
   bool lane_ok_ = false, front_stage_b_ = false;
   int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
+  int fs_ctas_ = 0, fs_pt_ = 32, fs_smem_ = 0;  // finish fused with the ⟨S⟩ᵀ slicer
+  bool es_sliced_ = false;                      // the finish pass of this chunk wrote the ⟨S⟩ᵀ slices
   int sc_ctas_ = 0, sc_chunks_ = 1;  // per-CTA scalar partial regions
   double *d_rec_ = nullptr, *d_lout_ = nullptr;
   int* d_pmode_ = nullptr;

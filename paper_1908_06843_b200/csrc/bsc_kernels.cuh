@@ -284,7 +284,7 @@ struct EnumArgs {
   uint32_t* cand_out;     // N × hprime or null
   double* map_mass;       // inference outputs or null
   int* map_state;         // N: index of the MAP state in reference order
-  int* err;
+  int* err;               // [0] error flags, [1] points marked kModeFallback (lane path)
   unsigned long long* prof;  // [8] cycles per phase (profiling mode) or null
   // [n_tab] offsets/8 (u16) {rel(parent), coup(sibling) | P[x][z], u[z]}; < hprime unused
   const uint2* sdesc;
@@ -483,6 +483,11 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
   const int wib = threadIdx.x >> 5;
   const int gwarp = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
+  if constexpr (PASS == kPassFallback) {
+    // the selection pass counts the points it leaves to this launch (err[1], zeroed with the
+    // error flag per E-step): none, the common case, and the CTA is gone before it stages a table
+    if (a.err[1] == 0) return;
+  }
   const EnumSmem L = PASS == kPassFront ? EnumSmem::make(a.hprime, 0, 0, 0, 0, a.H)
                                          : EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
   // The state descriptors and schedule entries are the same for every point:

@@ -1,6 +1,7 @@
 // Small host helpers shared by the engine translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <string>
@@ -21,6 +22,15 @@ T* dalloc(size_t count, const char* what) {
   ck(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), what);
   return static_cast<T*>(p);
 }
+
+// NVTX range over the host-side enqueue of one phase (header-only NVTX 3: a no-op
+// unless a tool injects itself; SURVEY.md §5 tracing).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 inline void dfree(void* p) {
   if (p) cudaFree(p);

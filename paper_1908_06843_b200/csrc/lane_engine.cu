@@ -5,6 +5,7 @@
 #include "bsc_engine.hpp"
 #include "lane_kernels.cuh"
 #include "select_kernels.cuh"
+#include "finish_slice_kernels.cuh"
 
 namespace bscgpu {
 
@@ -51,6 +52,11 @@ const void* finish_fn(int maxj) {
     default: return (const void*)lane_finish_kernel<32>;
   }
 }
+
+const void* finish_slice_fn(int pt) {
+  return pt == 32 ? (const void*)lane_finish_slice_kernel<32> : (const void*)lane_finish_slice_kernel<16>;
+}
+int finish_slice_smem(int pt, int latents, int hp_padded) { return finish_slice_smem_bytes(pt, latents, hp_padded); }
 
 int lane_smem(int gamma, int hprime) {
   if (gamma == 4 && hprime == 10) return LaneShape<10, 4>::SLOTS * 256;

@@ -215,6 +215,17 @@ struct LaneShape {
       return E[i * 32];
   }
   static constexpr int SLOTS = O_M + NM;
+  // The leaf-parent rows M[Z][·] with Z ≥ MR_ROW accumulate in registers over the whole walk
+  // (deep_child's indices are compile-time) and are added to the shared-memory triangle at the
+  // end: row Z is visited by the C(Z, γ−2) deepest nodes below it, so the last six rows
+  // (21 entries) take 85 % of the leaf updates at (12, 4) and 87 % at (14, 5), and a leaf
+  // there costs one shared-memory read (e^P) instead of two reads and a write.
+#ifndef LANE_MR_ROWS
+#define LANE_MR_ROWS 6
+#endif
+  static constexpr int MR_ROW = HP - 1 - (LANE_MR_ROWS < HP - 1 ? LANE_MR_ROWS : HP - 1);
+  static constexpr int MR_FIRST = MR_ROW * (2 * HP - MR_ROW - 1) / 2;
+  static constexpr int NMR = NP - MR_FIRST > 0 ? NP - MR_FIRST : 1;
   __host__ __device__ static constexpr int pidx(int p, int q) { return p * (2 * HP - p - 1) / 2 + (q - p - 1); }
   __host__ __device__ static constexpr int tri(int p, int q) { return p * (2 * HP - p + 1) / 2 + (q - p); }
 };
@@ -257,7 +268,8 @@ __device__ __forceinline__ void cv_dispatch(int z, double* S, const double* __re
 
 // Child A∪{Z} of the deepest node A and its leaves.
 template <int HP, int GM, int Z>
-__device__ __forceinline__ void deep_child(double* S, const double* __restrict__ E, double qA, const double (&ce)[HP], double (&R)[HP], double& ch) {
+__device__ __forceinline__ void deep_child(double* S, const double* __restrict__ E, double qA, const double (&ce)[HP], double (&R)[HP],
+                                           double (&MR)[LaneShape<HP, GM>::NMR], double& ch) {
   using F = LaneShape<HP, GM>;
   const double qz = qA * ce[Z];
   double s = qz;
@@ -268,12 +280,15 @@ __device__ __forceinline__ void deep_child(double* S, const double* __restrict__
     for (int j = 0; j < NW; ++j) {
       const int w = Z + 1 + j;
       q[j] = qz * ce[w] * F::ep(S, E, F::pidx(Z, w));
-      m[j] = LS(F::O_M + F::tri(Z, w));
+      if constexpr (Z < F::MR_ROW) m[j] = LS(F::O_M + F::tri(Z, w));
     }
 #pragma unroll
     for (int j = 0; j < NW; ++j) {
       const int w = Z + 1 + j;
-      LS(F::O_M + F::tri(Z, w)) = m[j] + q[j];
+      if constexpr (Z < F::MR_ROW)
+        LS(F::O_M + F::tri(Z, w)) = m[j] + q[j];
+      else
+        MR[F::pidx(Z, w) - F::MR_FIRST] += q[j];
       R[w] += q[j];
       s += q[j];
     }
@@ -284,9 +299,9 @@ __device__ __forceinline__ void deep_child(double* S, const double* __restrict__
 
 template <int HP, int GM, int Z>
 __device__ __forceinline__ void deep_pred(double* S, const double* __restrict__ E, double qA, int x, const double (&ce)[HP], double (&R)[HP],
-                                          double& ch) {
-  if (Z > x) deep_child<HP, GM, Z>(S, E, qA, ce, R, ch);
-  if constexpr (Z + 1 < HP) deep_pred<HP, GM, Z + 1>(S, E, qA, x, ce, R, ch);
+                                          double (&MR)[LaneShape<HP, GM>::NMR], double& ch) {
+  if (Z > x) deep_child<HP, GM, Z>(S, E, qA, ce, R, MR, ch);
+  if constexpr (Z + 1 < HP) deep_pred<HP, GM, Z + 1>(S, E, qA, x, ce, R, MR, ch);
 }
 
 // Duff-style dispatch on the node maximum x: case x falls through the
@@ -298,7 +313,8 @@ __device__ __forceinline__ void deep_pred(double* S, const double* __restrict__ 
 // Node A (|A| = K ≤ γ−2, max x, weight qA, members path[0..K)): walks its
 // children, returns Σ_children sub(child).
 template <int HP, int GM, int K>
-__device__ __forceinline__ double fnode(double* S, const double* __restrict__ E, double qA, int x, int (&path)[8]) {
+__device__ __forceinline__ double fnode(double* S, const double* __restrict__ E, double qA, int x, int (&path)[8],
+                                        double (&MR)[LaneShape<HP, GM>::NMR]) {
   using F = LaneShape<HP, GM>;
   int orow[K + 1];
 #pragma unroll
@@ -316,7 +332,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
         ce[w] = 0.0;
         if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(S, E, xrow + w) : LS(F::cvb(K - 2) + w));
       }
-      deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, ch);
+      deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, MR, ch);
 #pragma unroll
       for (int z = 0; z < HP; ++z) {
         if (z > x) {
@@ -347,7 +363,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
       switch (x) {
   #define LANE_DC(c_, Z_)                                                     \
     case c_:                                                                  \
-      if constexpr (Z_ < HP) deep_child<HP, GM, (Z_ < HP ? Z_ : 0)>(S, E, qA, ce, R, ch); \
+      if constexpr (Z_ < HP) deep_child<HP, GM, (Z_ < HP ? Z_ : 0)>(S, E, qA, ce, R, MR, ch); \
       [[fallthrough]];
         LANE_FT_CASES(LANE_DC)
   #undef LANE_DC
@@ -379,7 +395,7 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
       const double qz = qA * S[(F::O_EU + z) * 32] * c;
       cv_dispatch<HP, GM, K>(z, S, E, xrow);
       path[K] = z;
-      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, E, qz, z, path);
+      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, E, qz, z, path, MR);
       const int zz = F::O_M + mrow_(z, HP) + z;
       double m[K + 1];
       m[K] = S[zz * 32];
@@ -495,6 +511,9 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
   for (int i = 0; i < F::NM; ++i) S[(F::O_M + i) * 32] = 0.0;
   int path[8];
   double zm = 0.0;
+  double MR[F::NMR];
+#pragma unroll
+  for (int i = 0; i < F::NMR; ++i) MR[i] = 0.0;
 #pragma unroll 1
   for (int r = 0; r < HP; ++r) {
     double u = ur[0];
@@ -502,11 +521,16 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
     for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
     const double qr = live ? exp_nonpos(u - shift) : 0.0;
     path[0] = r;
-    const double ch = fnode<HP, GM, 1>(S, E, qr, r, path);
+    const double ch = fnode<HP, GM, 1>(S, E, qr, r, path, MR);
     const int rr = F::O_M + mrow_(r, HP) + r;
     S[rr * 32] += qr + ch;
     zm += ch;
   }
+  // the register-held leaf-parent rows join the triangle
+#pragma unroll
+  for (int p = F::MR_ROW; p < HP - 1; ++p)
+#pragma unroll
+    for (int q = p + 1; q < HP; ++q) S[(F::O_M + F::tri(p, q)) * 32] += MR[F::pidx(p, q) - F::MR_FIRST];
   if (live) {
     double* ot = a.out + tile * lane_out_fields(HP) * 32 + lane;
     ot[0] = shift;

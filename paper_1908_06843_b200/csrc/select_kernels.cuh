@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
         }
       }
       a.pmode[n] = mode;
+      if (mode == kModeFallback) atomicAdd(a.err + 1, 1);
     }
   }
   // per-CTA Σ‖y_n‖² in a fixed order (warp tree, then warps in index order)

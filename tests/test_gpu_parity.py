@@ -372,3 +372,35 @@ def test_sliced_gemm_path_matches_dmma_and_oracle(pkg, port, monkeypatch, d, h, 
     # amplifies the ~1e-13 statistic differences, so W′ is held to the north-star bar there
     assert rel(r0.params.W, r1.params.W) < (1e-11 if n >= 4 * h else TOL_STEP)
     assert abs(r0.free_energy - r1.free_energy) <= 1e-13 * abs(r1.free_energy)
+
+
+# ------------------------------------- finish pass fused with the ⟨S⟩ᵀ slicer
+@pytest.mark.parametrize("d,h,hp,g,n,s2", [(256, 300, 12, 4, 5003, 0.4), (576, 1000, 14, 5, 777, 0.4),
+                                          (100, 20, 10, 4, 130, 0.3), (64, 40, 8, 3, 1000, 1e-3)])
+def test_fused_finish_slice_matches_unfused(pkg, port, monkeypatch, d, h, hp, g, n, s2):
+    """lane_finish_slice_kernel (finish_slice_kernels.cuh: ⟨s⟩ rows cut into the
+    int8 operand of Yᵀ⟨S⟩ in shared memory, never written to HBM) against the
+    unfused finish + slicer launches (BSC_FUSED_FINISH=0): the slices, hence
+    Σ y⟨s⟩ᵀ, and Σ⟨ssᵀ⟩, Σ log Z are the same bits; Σ⟨s⟩ differs only in its
+    fixed summation order. Shapes: c2's and c3's (the latter takes the 16-point
+    sub-tiles), a ragged N below one 128-point block, and a small σ² that sends
+    points outside the range guard to the fallback launch (rows read back from ⟨S⟩)."""
+    wt = port.random_dictionary(d, h, 31, 5.0)
+    y = port.generate(wt, min(0.5, 4.0 / h), 0.25, n, 32)
+    p = pkg.BscParams(wt + 0.05 * np.cos(np.arange(d * h)).reshape(d, h), 1.0 / h, s2)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BSC_FUSED_FINISH", mode)
+        m = model_for(pkg, d, h, hp, g)
+        m.load(y)
+        out[mode] = (m.estep_stats(p), m.step(p))
+        m.close()
+    (s0, r0), (s1, r1) = out["1"], out["0"]
+    assert np.array_equal(s0.sum_y_sT, s1.sum_y_sT)
+    off = ~np.eye(h, dtype=bool)
+    assert np.array_equal(s0.sum_ssT[off], s1.sum_ssT[off])
+    assert s0.log_partition == s1.log_partition
+    assert rel(s0.sum_s, s1.sum_s) < 1e-14
+    check_stats(s0, port.estep_stats(p.W, p.pi, p.sigma2, y, hp, g))
+    assert rel(r0.params.W, r1.params.W) < (1e-11 if n >= 4 * h else TOL_STEP)
+    assert abs(r0.free_energy - r1.free_energy) <= 1e-13 * abs(r1.free_energy)
