@@ -198,6 +198,10 @@ void BscEngine::init(int device) {
   }
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
+  if (lane_ok_) {
+    d_pm_ = dalloc<double>((size_t)H_ * Hp_, "pair terms");
+    d_epm_ = dalloc<double>((size_t)H_ * Hp_, "pair factors");
+  }
   d_trace_part_ = dalloc<double>(2 * kTraceCtas, "trace partials");
   d_wnorm_ = dalloc<double>(H_, "wnorm");
   d_gdiag_ = dalloc<double>(H_, "gdiag");
@@ -235,7 +239,8 @@ BscEngine::~BscEngine() {
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
                   (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_,
                   (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
-                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_})
+                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_,
+                  (void*)d_pm_, (void*)d_epm_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -883,6 +888,14 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   // lane path: selection (thread per point) → lane-per-point states → fallback points → finish
   a.rec = d_rec_;
   a.pmode = d_pmode_;
+  a.Pm = d_pm_;
+  a.EPm = d_epm_;
+  if (chunk == 0) {  // once per E-step: the pairwise terms for this σ²
+    const long long cnt = static_cast<long long>(H_) * Hp_;
+    pair_terms_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(d_g_, static_cast<int>(H_), Hp_, a.inv2s,
+                                                                                 d_pm_, d_epm_);
+    ++launches_;
+  }
   a.cand_out = d_cand_ + off * hprime_;
   a.pscale = nullptr;
   pscale_used_ = false;

@@ -168,6 +168,7 @@ class BscEngine {
 
   uint64_t n_ = 0, cap_n_ = 0;
   double *d_y_ = nullptr, *d_w_ = nullptr, *d_g_ = nullptr, *d_wnorm_ = nullptr, *d_gdiag_ = nullptr;
+  double *d_pm_ = nullptr, *d_epm_ = nullptr;  // lane path: pairwise terms P = −2·inv2s·G and e^P (H × Hp)
   double* d_y2_ = nullptr;  // ‖y_n‖² per resident point
   double *d_b_ = nullptr, *d_es_ = nullptr;
   double *d_stats_ = nullptr, *d_smulti_ = nullptr;

@@ -237,15 +237,15 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
           int e = 0;
 #pragma unroll
           for (int p = 0; p < HP; ++p) {
-            const double* gr = a.G + static_cast<long long>(cand[p]) * Hp;
+            const long long go = static_cast<long long>(cand[p]) * Hp;
 #pragma unroll
             for (int q = p + 1; q < HP; ++q, ++e) {
-              const double v = -2.0 * inv2s * __ldg(gr + cand[q]);
+              const double v = __ldg(a.Pm + go + cand[q]);  // −2·inv2s·G_pq (pair_terms_kernel)
               fin = fin && isfinite(v);
               pmax = fmax(pmax, v);
               pabs = fmax(pabs, fabs(v));
               rt[(4 + 2 * HP + e) * 32] = v;
-              rt[(4 + 2 * HP + NP + e) * 32] = exp_nonpos(v);
+              rt[(4 + 2 * HP + NP + e) * 32] = __ldg(a.EPm + go + cand[q]);
             }
           }
           // q(S) = q(A)·e^{u_z}·e^{coup(S)} stays in fp64 range when |u| ≤ 300 and

@@ -5,6 +5,9 @@ timeout 300 python bench.py --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c
 BSC_FUSED_FINISH=0 timeout 300 python bench.py --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c2_unfused.log 2>&1
 timeout 600 python bench.py --config c3 --steps 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c3_fused.log 2>&1
 BSC_FUSED_FINISH=0 timeout 600 python bench.py --config c3 --steps 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c3_unfused.log 2>&1
+MR0=paper_1908_06843_b200/_lib_mr0/libprsp_bsc_b200.so
+PRSP_BSC_LIB=$MR0 timeout 300 python bench.py --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c2_mr0.log 2>&1
+PRSP_BSC_LIB=$MR0 timeout 600 python bench.py --config c3 --steps 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_c3_mr0.log 2>&1
 K='regex:select_kernel|lane_states|lane_finish|oz_gemm_kernel|enumerate_kernel'
 timeout 300 python tools/profile_case.py c2 200000 2 > gpurun_out/plain_c2.log 2>&1 &&
 timeout 1200 ncu --set full --clock-control none --import-source on -k "$K" -s 6 -c 6 -f -o gpurun_out/r02_c2 python tools/profile_case.py c2 200000 2 > gpurun_out/ncu_c2.log 2>&1
