@@ -240,7 +240,7 @@ BscEngine::~BscEngine() {
                   (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_,
                   (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
                   (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_,
-                  (void*)d_pm_, (void*)d_epm_})
+                  (void*)d_pm_, (void*)d_epm_, (void*)d_next_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -518,7 +518,8 @@ void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
   for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
                   (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_rec_,
-                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_, (void*)d_pscale_})
+                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_, (void*)d_pscale_,
+                  (void*)d_next_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
   if (oz_) {
@@ -631,6 +632,9 @@ void BscEngine::ensure_work(uint64_t n) {
     d_rec_ = dalloc<double>(tiles * 32 * lane_rec_fields(static_cast<int>(hprime_)), "lane records");
     d_lout_ = dalloc<double>(tiles * 32 * lane_out_fields(static_cast<int>(hprime_)), "lane moments");
     d_pmode_ = dalloc<int>(tiles * 32, "point modes");
+    d_next_ = dalloc<uint32_t>(tiles * 32, "selection runner-up");
+    const char* we = std::getenv("BSC_SELECT_WARM");
+    select_warm_ = !(we && we[0] == '0');
   }
   d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
   d_warp_sc_ = dalloc<double>((size_t)3 * sc_ctas_ * 2, "cta_scalars");
@@ -888,6 +892,7 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   // lane path: selection (thread per point) → lane-per-point states → fallback points → finish
   a.rec = d_rec_;
   a.pmode = d_pmode_;
+  a.next_idx = select_warm_ ? d_next_ + off : nullptr;
   a.Pm = d_pm_;
   a.EPm = d_epm_;
   if (chunk == 0) {  // once per E-step: the pairwise terms for this σ²

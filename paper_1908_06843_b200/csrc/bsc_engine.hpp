@@ -201,10 +201,12 @@ class BscEngine {
   bool lane_ok_ = false, front_stage_b_ = false;
   int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
   int fs_ctas_ = 0, fs_pt_ = 32, fs_smem_ = 0;  // finish fused with the ⟨S⟩ᵀ slicer
+  bool select_warm_ = true;                     // selection thresholds warm-started from the last candidates
   bool es_sliced_ = false;                      // the finish pass of this chunk wrote the ⟨S⟩ᵀ slices
   int sc_ctas_ = 0, sc_chunks_ = 1;  // per-CTA scalar partial regions
   double *d_rec_ = nullptr, *d_lout_ = nullptr;
   int* d_pmode_ = nullptr;
+  uint32_t* d_next_ = nullptr;  // per point: runner-up unit of the last selection (warm start)
   void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;

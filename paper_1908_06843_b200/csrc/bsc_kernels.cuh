@@ -323,6 +323,7 @@ struct EnumArgs {
   // lane path (lane_kernels.cuh): deferred-point records and per-point modes
   double* rec;
   int* pmode;
+  uint32_t* next_idx; // N: the (H'+1)-th ranked unit of the last selection (warm start of the next; select_kernels.cuh)
   const double* Pm;   // H × Hp: P_hk = −2·inv2s·G_hk, this E-step's σ² (pair_terms_kernel)
   const double* EPm;  // H × Hp: e^{P_hk}
   double* pscale;  // front pass: 1 per point (the finish may defer its ⟨s⟩-row scale here)

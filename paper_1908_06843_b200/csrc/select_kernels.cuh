@@ -36,9 +36,10 @@
 namespace bscgpu {
 
 constexpr int kSelWarps = 4;                  // points per CTA = 32 · kSelWarps
-constexpr int kSelCols = 16;                  // B columns per staged chunk (and per queue flush)
+constexpr int kSelCols = 16;                  // B columns per staged chunk
+constexpr int kSelQueue = 21;                 // key queue slots per lane (4 CTAs of 56.7 KB per SM at H = 300)
 constexpr int kSelStageBytes = 32 * kSelCols * 8;  // 32 rows × 16 columns fp64
-constexpr int kSelWarpBytes = 2 * kSelStageBytes + kSelCols * 256;  // 2 stages + the key queue
+constexpr int kSelWarpBytes = 2 * kSelStageBytes + kSelQueue * 256;  // 2 stages + the key queue
 
 __host__ __device__ inline int select_smem_bytes(int H) {
   return 8 * ((H + 1) & ~1) + 16 + kSelWarps * kSelWarpBytes;
@@ -65,7 +66,7 @@ __device__ __forceinline__ double key_score(double k) {  // the score with the c
 }
 
 template <int HP>
-__global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
+__global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
   constexpr int K = HP + 1;  // the H' best and the next one (gap test)
   constexpr int NP = HP * (HP - 1) / 2;
   extern __shared__ __align__(16) double ssm[];
@@ -121,43 +122,44 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
     issue(0, 0);
 
     // The best K keys so far, descending. A column's key is only queued when it
-    // beats the list's current K-th key (the threshold only rises: a valid lower
-    // bound of the final K-th), and the queue is merged into the list once per
-    // chunk, so the insertion network runs ~K·(1 + ln(H/16K)) times per point
-    // instead of at every column where any lane of the warp would insert.
+    // reaches the threshold tau, a lower bound of the final K-th key that only
+    // rises, and the queue is merged into the list (one insertion-network round
+    // per queued key of the fullest lane) only when it could overflow.
+    // Warm start: the point's previous candidates and runner-up (any K distinct
+    // units) give K current keys whose minimum bounds the K-th best from below,
+    // so from the second EM iteration on little more than the final K keys are
+    // ever queued — ~25 rounds per 32 points instead of ~140 with tau = −∞.
     double L[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) L[j] = -INFINITY;
     double tau = -INFINITY, probe = 0.0;
     const double log_pi = a.log_pi, inv2s = a.inv2s;
-    for (int c = 0; c < nch; ++c) {
-      if (c + 1 < nch) {
-        issue(c + 1, (c + 1) & 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      }
-      __syncwarp();
-      const char* row = stage + (c & 1) * kSelStageBytes + lane * 128;
-      const int h0 = c * kSelCols;
-      int cnt = 0;
+    if (HP < H && live && a.next_idx) {
+      const uint32_t* pc = a.cand_out + n * HP;
+      uint32_t ix[K];
 #pragma unroll
-      for (int j = 0; j < kSelCols / 2; ++j) {
-        const double2 v = *reinterpret_cast<const double2*>(row + ((j ^ (lane & 7)) << 4));
+      for (int j = 0; j < HP; ++j) ix[j] = pc[j];
+      ix[HP] = a.next_idx[n];
+      bool okw = ix[0] < static_cast<uint32_t>(H) && ix[HP] < static_cast<uint32_t>(H) && ix[HP] != ix[0];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int h = h0 + 2 * j + u;
-          if (h < H) {
-            const double t = __fma_rn(2.0, u ? v.y : v.x, -gd[h]);  // = 2b − G_hh (2b is exact)
-            const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));  // linear_discrete.cpp:248-249, unfused
-            probe = __fma_rn(f, 0.0, probe);                          // NaN once any score is not finite
-            const double k = sel_key(f, h);
-            if (k > tau) queue[(cnt++) * 32] = k;
-          }
+      for (int j = 1; j < HP; ++j)  // ascending and in range: K distinct units with the runner-up
+        okw = okw && ix[j] > ix[j - 1] && ix[j] < static_cast<uint32_t>(H) && ix[HP] != ix[j];
+      if (okw) {
+        const double* brow = a.B + n * Hp;
+        double lo = INFINITY;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int h = static_cast<int>(ix[j]);
+          const double t = __fma_rn(2.0, brow[h], -gd[h]);
+          const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));
+          lo = fmin(lo, sel_key(f, h));  // (a NaN key is ignored here and caught by the probe below)
         }
+        tau = lo;
       }
-      __syncwarp();
-      // merge the queue: L'[j] = c_j ? (c_{j−1} ? L[j−1] : k) : L[j], c_j = k > L[j]
+    }
+    int cnt = 0;
+    auto merge = [&]() {
+      // L'[j] = c_j ? (c_{j−1} ? L[j−1] : k) : L[j], c_j = k > L[j]
       const int rounds = __reduce_max_sync(0xffffffffu, cnt);
       for (int i = 0; i < rounds; ++i) {
         const double k = i < cnt ? queue[i * 32] : -INFINITY;
@@ -174,7 +176,37 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
           c_prev = cj;
         }
       }
-      tau = L[K - 1];
+      cnt = 0;
+      tau = fmax(tau, L[K - 1]);
+    };
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        issue(c + 1, (c + 1) & 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      const char* row = stage + (c & 1) * kSelStageBytes + lane * 128;
+      const int h0 = c * kSelCols;
+#pragma unroll
+      for (int j = 0; j < kSelCols / 2; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(row + ((j ^ (lane & 7)) << 4));
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int h = h0 + 2 * j + u;
+          if (h < H) {
+            const double t = __fma_rn(2.0, u ? v.y : v.x, -gd[h]);  // = 2b − G_hh (2b is exact)
+            const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));  // linear_discrete.cpp:248-249, unfused
+            probe = __fma_rn(f, 0.0, probe);                          // NaN once any score is not finite
+            const double k = sel_key(f, h);
+            if (k >= tau) queue[(cnt++) * 32] = k;  // (keys are distinct: ≥ only admits the warm bound itself)
+          }
+        }
+      }
+      __syncwarp();
+      // merge when the next chunk could overflow the fullest lane's queue
+      if (__reduce_max_sync(0xffffffffu, cnt) + kSelCols > kSelQueue || c + 1 == nch) merge();
       __syncwarp();
     }
 
@@ -216,6 +248,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(EnumArgs a) {
         uint32_t* co = a.cand_out + n * HP;
 #pragma unroll
         for (int j = 0; j < HP; ++j) co[j] = static_cast<uint32_t>(cand[j]);
+        if (HP < H && a.next_idx) a.next_idx[n] = static_cast<uint32_t>(key_index(L[HP]));  // the runner-up
         y2_acc += y2;
         mode = kModeFallback;
         if (exact) {
