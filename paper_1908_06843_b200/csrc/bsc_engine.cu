@@ -198,10 +198,6 @@ void BscEngine::init(int device) {
   }
   d_w_ = dalloc<double>((size_t)Dp_ * Hp_, "W");
   d_g_ = dalloc<double>((size_t)H_ * Hp_, "G");
-  if (lane_ok_) {
-    d_pm_ = dalloc<double>((size_t)H_ * Hp_, "pair terms");
-    d_epm_ = dalloc<double>((size_t)H_ * Hp_, "pair factors");
-  }
   d_trace_part_ = dalloc<double>(2 * kTraceCtas, "trace partials");
   d_wnorm_ = dalloc<double>(H_, "wnorm");
   d_gdiag_ = dalloc<double>(H_, "gdiag");
@@ -239,8 +235,7 @@ BscEngine::~BscEngine() {
                   (void*)d_map_state_, (void*)d_map_mass_, (void*)d_err_, (void*)d_bm_, (void*)d_x_, (void*)d_trace_part_, d_msc_,
                   (void*)d_vpart_, (void*)d_u_, d_chunk_, (void*)d_rec_, (void*)d_lout_, (void*)d_pmode_,
                   (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
-                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_,
-                  (void*)d_pm_, (void*)d_epm_, (void*)d_next_})
+                  (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_})
     dfree(p);
   for (void* p : {h_msc_, h_tail_, h_err_})
     if (p) cudaFreeHost(p);
@@ -518,8 +513,7 @@ void BscEngine::ensure_work(uint64_t n) {
   if (n <= cap_n_ && d_y_) return;
   for (void* p : {(void*)d_y_, (void*)d_y2_, (void*)d_b_, (void*)d_es_, (void*)d_cand_, (void*)d_map_state_,
                   (void*)d_map_mass_, (void*)d_part_, (void*)d_warp_es_, (void*)d_warp_sc_, (void*)d_rec_,
-                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_, (void*)d_pscale_,
-                  (void*)d_next_})
+                  (void*)d_lout_, (void*)d_pmode_, (void*)d_ys_, (void*)d_ysa_, (void*)d_yts_, (void*)d_ozcs_, (void*)d_pscale_})
     dfree(p);
   const uint64_t rows = (n + 1) & ~1ull;  // even: GEMM2 reads K in pairs
   if (oz_) {
@@ -632,9 +626,6 @@ void BscEngine::ensure_work(uint64_t n) {
     d_rec_ = dalloc<double>(tiles * 32 * lane_rec_fields(static_cast<int>(hprime_)), "lane records");
     d_lout_ = dalloc<double>(tiles * 32 * lane_out_fields(static_cast<int>(hprime_)), "lane moments");
     d_pmode_ = dalloc<int>(tiles * 32, "point modes");
-    d_next_ = dalloc<uint32_t>(tiles * 32, "selection runner-up");
-    const char* we = std::getenv("BSC_SELECT_WARM");
-    select_warm_ = !(we && we[0] == '0');
   }
   d_warp_es_ = dalloc<double>((size_t)splits_ * Hp_, "split-K column sums");
   d_warp_sc_ = dalloc<double>((size_t)3 * sc_ctas_ * 2, "cta_scalars");
@@ -892,15 +883,6 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   // lane path: selection (thread per point) → lane-per-point states → fallback points → finish
   a.rec = d_rec_;
   a.pmode = d_pmode_;
-  a.next_idx = select_warm_ ? d_next_ + off : nullptr;
-  a.Pm = d_pm_;
-  a.EPm = d_epm_;
-  if (chunk == 0) {  // once per E-step: the pairwise terms for this σ²
-    const long long cnt = static_cast<long long>(H_) * Hp_;
-    pair_terms_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, s>>>(d_g_, static_cast<int>(H_), Hp_, a.inv2s,
-                                                                                 d_pm_, d_epm_);
-    ++launches_;
-  }
   a.cand_out = d_cand_ + off * hprime_;
   a.pscale = nullptr;
   pscale_used_ = false;
@@ -911,7 +893,9 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
   if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[8]), s), "event");
   LaneArgs la{static_cast<int>(rows), static_cast<int>(hprime_), d_rec_, d_lout_, d_pmode_};
   void* largs[] = {&la};
-  ck(cudaLaunchKernel(lane_fn(gamma_, hprime_), dim3(static_cast<unsigned>((rows + 31) / 32)), dim3(32), largs, lane_smem_, s),
+  const unsigned wpc = static_cast<unsigned>(lane_wpc(gamma_, hprime_));
+  ck(cudaLaunchKernel(lane_fn(gamma_, hprime_), dim3(static_cast<unsigned>(((rows + 31) / 32 + wpc - 1) / wpc)),
+                      dim3(32 * wpc), largs, lane_smem_, s),
      "lane states launch");
   if (tm) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[9]), s), "event");
   a.warp_scalars = sc_fb;

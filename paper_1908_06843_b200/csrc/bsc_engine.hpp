@@ -36,7 +36,8 @@ enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
 
 // The lane-per-point state pass for (γ, H') (lane_engine.cu).
 const void* lane_fn(int gamma, int hprime);
-int lane_smem(int gamma, int hprime);  // its dynamic shared memory per warp (bytes)
+int lane_smem(int gamma, int hprime);  // its dynamic shared memory per CTA (bytes)
+int lane_wpc(int gamma, int hprime);   // its warps (32-point tiles) per CTA
 const void* select_fn(int hprime);     // thread-per-point selection pass (select_kernels.cuh)
 int select_smem(int latents);          // its dynamic shared memory per CTA (bytes)
 const void* finish_fn(int maxj);       // lane_finish_kernel<MAXJ>
@@ -168,7 +169,6 @@ class BscEngine {
 
   uint64_t n_ = 0, cap_n_ = 0;
   double *d_y_ = nullptr, *d_w_ = nullptr, *d_g_ = nullptr, *d_wnorm_ = nullptr, *d_gdiag_ = nullptr;
-  double *d_pm_ = nullptr, *d_epm_ = nullptr;  // lane path: pairwise terms P = −2·inv2s·G and e^P (H × Hp)
   double* d_y2_ = nullptr;  // ‖y_n‖² per resident point
   double *d_b_ = nullptr, *d_es_ = nullptr;
   double *d_stats_ = nullptr, *d_smulti_ = nullptr;
@@ -201,12 +201,10 @@ class BscEngine {
   bool lane_ok_ = false, front_stage_b_ = false;
   int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
   int fs_ctas_ = 0, fs_pt_ = 32, fs_smem_ = 0;  // finish fused with the ⟨S⟩ᵀ slicer
-  bool select_warm_ = true;                     // selection thresholds warm-started from the last candidates
   bool es_sliced_ = false;                      // the finish pass of this chunk wrote the ⟨S⟩ᵀ slices
   int sc_ctas_ = 0, sc_chunks_ = 1;  // per-CTA scalar partial regions
   double *d_rec_ = nullptr, *d_lout_ = nullptr;
   int* d_pmode_ = nullptr;
-  uint32_t* d_next_ = nullptr;  // per point: runner-up unit of the last selection (warm start)
   void* d_prof_ = nullptr;
   EngineTimings t_{};
   int launches_ = 0;

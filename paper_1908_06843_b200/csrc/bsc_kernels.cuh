@@ -145,18 +145,6 @@ __device__ __forceinline__ double exp_nonpos(double x) {
   return (p * s1) * s2;
 }
 
-// Pairwise log-joint terms of the lane path for this E-step's σ²: P = −2·inv2s·G
-// and e^P over the whole Gram matrix (H² exps once per E-step instead of
-// H'(H'−1)/2 per data point in the selection pass, which then only gathers).
-static __global__ void pair_terms_kernel(const double* __restrict__ G, int H, int ldg, double inv2s,
-                                         double* __restrict__ Pm, double* __restrict__ EPm) {
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= static_cast<long long>(H) * ldg) return;
-  const double v = -2.0 * inv2s * G[i];
-  Pm[i] = v;
-  EPm[i] = exp_nonpos(v);  // used only under the range guard (γ−1)|P| ≤ 300
-}
-
 // ‖y_n‖² per data point (linear_discrete.cpp:242), once per resident dataset:
 // one warp per row.
 static __global__ void row_sqnorm_kernel(const double* __restrict__ Y, long long N, int D, int ldy,
@@ -323,9 +311,6 @@ struct EnumArgs {
   // lane path (lane_kernels.cuh): deferred-point records and per-point modes
   double* rec;
   int* pmode;
-  uint32_t* next_idx; // N: the (H'+1)-th ranked unit of the last selection (warm start of the next; select_kernels.cuh)
-  const double* Pm;   // H × Hp: P_hk = −2·inv2s·G_hk, this E-step's σ² (pair_terms_kernel)
-  const double* EPm;  // H × Hp: e^{P_hk}
   double* pscale;  // front pass: 1 per point (the finish may defer its ⟨s⟩-row scale here)
   int stage_b;  // front pass: B rows double-buffered in shared memory by cp.async
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const

@@ -134,6 +134,14 @@ __global__ void __launch_bounds__(kFsThreads, 2) lane_finish_slice_kernel(Finish
         }
         const double* ot = f.out + (n >> 5) * lane_out_fields(hp) * 32 + (n & 31);
         const double shift = sh[i], zm = zmv[i];
+        // this lane's moment entries and candidates: in flight while the weights are formed
+        double mom[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) mom[t] = lane + 32 * t < nm ? ot[(2 + lane + 32 * t) * 32] : 0.0;
+        const uint32_t cmine = lane < hp ? f.cand[n * hp + lane] : 0u;
+        // (Dropping the weights below e^-48 of the point's largest and compacting the rest by
+        // ballot was measured slower — early EM iterations keep most units inside the window —
+        // profiles/r02_variants.txt.)
         double zs = 0.0;
 #pragma unroll 4
         for (int h = lane; h < H; h += 32) {
@@ -150,14 +158,19 @@ __global__ void __launch_bounds__(kFsThreads, 2) lane_finish_slice_kernel(Finish
           rs[r] = inv_z;
         }
         __syncwarp();
-        const uint32_t* cn = f.cand + n * hp;
-        for (int o = lane; o < nm; o += 32) {
-          const int p = pq[o] & 0xff, q = pq[o] >> 8;
-          const double v = ot[(2 + o) * 32];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const int o = lane + 32 * t;
+          if (32 * t >= nm) break;  // (warp-uniform)
+          const bool on = o < nm;
+          const int p = on ? pq[o] & 0xff : 0, q = on ? pq[o] >> 8 : 0;
+          const uint32_t cp = __shfl_sync(0xffffffffu, cmine, p), cq = __shfl_sync(0xffffffffu, cmine, q);
+          if (!on) continue;
+          const double v = mom[t];
           if (q == p)
-            row[cn[p]] = v;  // candidate marginal (unnormalised, as the singleton weights)
+            row[cp] = v;  // candidate marginal (unnormalised, as the singleton weights)
           else
-            pair_fx_add(f.ssT + static_cast<long long>(cn[p]) * H + cn[q], v * inv_z, f.fx_scale);
+            pair_fx_add(f.ssT + static_cast<long long>(cp) * H + cq, v * inv_z, f.fx_scale);
         }
       }
       __syncthreads();

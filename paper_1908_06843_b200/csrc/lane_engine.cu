@@ -10,9 +10,9 @@
 namespace bscgpu {
 
 const void* lane_fn(int gamma, int hprime) {
-  if (gamma == 4 && hprime == 10) return (const void*)lane_states_fixed_kernel<4, 10>;
-  if (gamma == 4 && hprime == 12) return (const void*)lane_states_fixed_kernel<4, 12>;
-  if (gamma == 5 && hprime == 14) return (const void*)lane_states_fixed_kernel<5, 14>;
+  if (gamma == 4 && hprime == 10) return (const void*)lane_states_fixed_kernel<4, 10, 2>;
+  if (gamma == 4 && hprime == 12) return (const void*)lane_states_fixed_kernel<4, 12, 2>;
+  if (gamma == 5 && hprime == 14) return (const void*)lane_states_fixed_kernel<5, 14, 1>;
   switch (gamma) {
     case 2: return (const void*)lane_states_kernel<2>;
     case 3: return (const void*)lane_states_kernel<3>;
@@ -58,10 +58,15 @@ const void* finish_slice_fn(int pt) {
 }
 int finish_slice_smem(int pt, int latents, int hp_padded) { return finish_slice_smem_bytes(pt, latents, hp_padded); }
 
+// warps (32-point tiles) per CTA of lane_fn's kernel
+int lane_wpc(int gamma, int hprime) { return gamma == 4 && (hprime == 10 || hprime == 12) ? 2 : 1; }
+
+// dynamic shared memory per CTA
 int lane_smem(int gamma, int hprime) {
-  if (gamma == 4 && hprime == 10) return LaneShape<10, 4>::SLOTS * 256;
-  if (gamma == 4 && hprime == 12) return LaneShape<12, 4>::SLOTS * 256;
-  if (gamma == 5 && hprime == 14) return LaneShape<14, 5>::SLOTS * 256;
+  const int w = lane_wpc(gamma, hprime);
+  if (gamma == 4 && hprime == 10) return w * LaneShape<10, 4>::SLOTS * 256;
+  if (gamma == 4 && hprime == 12) return w * LaneShape<12, 4>::SLOTS * 256;
+  if (gamma == 5 && hprime == 14) return w * LaneShape<14, 5>::SLOTS * 256;
   return lane_smem_bytes(hprime, gamma);
 }
 

@@ -185,7 +185,13 @@ template <int HP, int GM>
 struct LaneShape {
   static_assert(GM >= 3, "compile-time walk needs gamma >= 3");
   static constexpr int NP = HP * (HP - 1) / 2, NM = HP * (HP + 1) / 2;
-  static constexpr int CV_LEVELS = GM - 3;  // coupling rows of depths 2 .. γ−2
+  // γ = 4: the coupling row of a deepest node {r, z} is never stored. The part its entries share,
+  // e^{u_w}·e^{P_rw}, is held in registers per root r, and the node forms
+  // ce[w] = e^{u_w}·e^{P_rw}·e^{P_zw} in a block dispatched on z (compile-time e^P offsets), which
+  // saves the row's write, its read back and its H'−2 slots per lane: 121 -> 111 at (12, 4), 8
+  // resident warps per SM instead of 7 (two warps per CTA, lane_engine.cu).
+  static constexpr bool HOIST = GM == 4;
+  static constexpr int CV_LEVELS = HOIST ? 0 : GM - 3;  // stored coupling rows (depths 2 .. γ−2)
   // e^P staged in shared memory, or (EP_GLOBAL) read from the record tile ([pair][32 lanes])
   // through the read-only path, leaving the slots to e^u, the coupling rows and M. Measured:
   // (14, 5) 3 -> 5 warps/SM, state pass 20.0 -> 12.6 ms at c3; (12, 4) fully unstaged reached
@@ -266,6 +272,28 @@ __device__ __forceinline__ void cv_dispatch(int z, double* S, const double* __re
   }
 }
 
+// HOIST (γ = 4): ce[w] = pc[w]·e^{P_Zw}, w > Z, of the deepest node {r, Z} (pc = e^{u_w}·e^{P_rw}).
+template <int HP, int GM, int Z>
+__device__ __forceinline__ void ce_block(double* S, const double* __restrict__ E, const double (&pc)[HP], double (&ce)[HP]) {
+  using F = LaneShape<HP, GM>;
+#pragma unroll
+  for (int w = Z + 1; w < HP; ++w) ce[w] = pc[w] * F::ep(S, E, F::pidx(Z, w));
+}
+template <int HP, int GM>
+__device__ __forceinline__ void ce_dispatch(int z, double* S, const double* __restrict__ E, const double (&pc)[HP],
+                                            double (&ce)[HP]) {
+  switch (z) {
+#define LANE_CE_CASE(v)                                                         \
+  case v:                                                                       \
+    if constexpr (v < HP - 1) ce_block<HP, GM, (v < HP - 1 ? v : 0)>(S, E, pc, ce); \
+    break;
+    LANE_CASES(LANE_CE_CASE)
+#undef LANE_CE_CASE
+    default:
+      break;
+  }
+}
+
 // Child A∪{Z} of the deepest node A and its leaves.
 template <int HP, int GM, int Z>
 __device__ __forceinline__ void deep_child(double* S, const double* __restrict__ E, double qA, const double (&ce)[HP], double (&R)[HP],
@@ -314,7 +342,7 @@ __device__ __forceinline__ void deep_pred(double* S, const double* __restrict__ 
 // children, returns Σ_children sub(child).
 template <int HP, int GM, int K>
 __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E, double qA, int x, int (&path)[8],
-                                        double (&MR)[LaneShape<HP, GM>::NMR]) {
+                                        double (&MR)[LaneShape<HP, GM>::NMR], const double (&pc)[HP]) {
   using F = LaneShape<HP, GM>;
   int orow[K + 1];
 #pragma unroll
@@ -327,10 +355,16 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
     for (int w = 0; w < HP; ++w) R[w] = 0.0;
     if constexpr (GM < 5) {
       // predicated unrolled blocks (fewer, shorter nodes: cheaper than the indirect branch)
+      if constexpr (F::HOIST && K == 2) {
 #pragma unroll
-      for (int w = 0; w < HP; ++w) {
-        ce[w] = 0.0;
-        if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(S, E, xrow + w) : LS(F::cvb(K - 2) + w));
+        for (int w = 0; w < HP; ++w) ce[w] = 0.0;
+        ce_dispatch<HP, GM>(x, S, E, pc, ce);
+      } else {
+#pragma unroll
+        for (int w = 0; w < HP; ++w) {
+          ce[w] = 0.0;
+          if (w > x) ce[w] = LS(F::O_EU + w) * (K == 1 ? F::ep(S, E, xrow + w) : LS(F::cvb(K - 2) + w));
+        }
       }
       deep_pred<HP, GM, (K < HP ? K : 0)>(S, E, qA, x, ce, R, MR, ch);
 #pragma unroll
@@ -390,21 +424,36 @@ __device__ __forceinline__ double fnode(double* S, const double* __restrict__ E,
       }
     }
   } else {
-    for (int z = x + 1; z < HP; ++z) {
-      const double c = K == 1 ? F::ep(S, E, xrow + z) : S[(F::cvb(K - 2) + z) * 32];
-      const double qz = qA * S[(F::O_EU + z) * 32] * c;
-      cv_dispatch<HP, GM, K>(z, S, E, xrow);
-      path[K] = z;
-      const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, E, qz, z, path, MR);
-      const int zz = F::O_M + mrow_(z, HP) + z;
-      double m[K + 1];
-      m[K] = S[zz * 32];
+    // children at the deepest level form their own coupling factors; with HOIST (γ = 4, this
+    // node a root) the part they share, e^{u_w}·e^{P_xw}, stays in registers
+    auto children = [&](const double (&pcx)[HP]) {
+      for (int z = x + 1; z < HP; ++z) {
+        const double c = K == 1 ? F::ep(S, E, xrow + z) : S[(F::cvb(K - 2) + z) * 32];
+        const double qz = qA * S[(F::O_EU + z) * 32] * c;
+        if constexpr (!(F::HOIST && K + 1 == GM - 2)) cv_dispatch<HP, GM, K>(z, S, E, xrow);
+        path[K] = z;
+        const double s = qz + fnode<HP, GM, (K + 1 < GM - 1 ? K + 1 : K)>(S, E, qz, z, path, MR, pcx);
+        const int zz = F::O_M + mrow_(z, HP) + z;
+        double m[K + 1];
+        m[K] = S[zz * 32];
 #pragma unroll
-      for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
-      S[zz * 32] = m[K] + s;
+        for (int i = 0; i < K; ++i) m[i] = S[(orow[i] + z) * 32];
+        S[zz * 32] = m[K] + s;
 #pragma unroll
-      for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + s;
-      ch += s;
+        for (int i = 0; i < K; ++i) S[(orow[i] + z) * 32] = m[i] + s;
+        ch += s;
+      }
+    };
+    if constexpr (F::HOIST && K == 1) {
+      double pcn[HP];
+#pragma unroll
+      for (int w = 0; w < HP; ++w) {
+        pcn[w] = 0.0;
+        if (w > x + 1) pcn[w] = LS(F::O_EU + w) * F::ep(S, E, xrow + w);
+      }
+      children(pcn);
+    } else {
+      children(pc);
     }
   }
   return ch;
@@ -465,18 +514,20 @@ __global__ void __launch_bounds__(32) lane_states_kernel(LaneArgs a) {
 }
 
 // The compile-time walk for H' = HP, γ = GM (layout LaneShape<HP, GM>).
-template <int GM, int HP>
-__global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
+// WPC warps per CTA (independent tiles; no CTA-wide synchronisation): two where that lets one
+// more warp fit beside the 1 KB of shared memory the system reserves per CTA.
+template <int GM, int HP, int WPC>
+__global__ void __launch_bounds__(32 * WPC, 1) lane_states_fixed_kernel(LaneArgs a) {
   using F = LaneShape<HP, GM>;
   extern __shared__ __align__(16) double lsm[];
-  const int lane = threadIdx.x;
-  const long long tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long tile = static_cast<long long>(blockIdx.x) * WPC + wib;
   const long long n = tile * 32 + lane;
   const int mode = n < a.N ? a.pmode[n] : kModeDone;
   const bool live = mode == kModeShift || mode == kModeMax;
   if (!__any_sync(0xffffffffu, live)) return;
-  double* S = lsm + lane;
-  char* base = reinterpret_cast<char*>(lsm) + lane * 8;
+  double* S = lsm + wib * (F::SLOTS * 32) + lane;
+  char* base = reinterpret_cast<char*>(lsm) + wib * (F::SLOTS * 256) + lane * 8;
   const double* rt = a.rec + tile * lane_rec_fields(HP) * 32 + lane;
   constexpr int fu = 4, feu = 4 + HP, fP = 4 + 2 * HP, feP = 4 + 2 * HP + F::NP;
 
@@ -514,6 +565,9 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
   double MR[F::NMR];
 #pragma unroll
   for (int i = 0; i < F::NMR; ++i) MR[i] = 0.0;
+  double pc0[HP];  // (unused by the root level)
+#pragma unroll
+  for (int i = 0; i < HP; ++i) pc0[i] = 0.0;
 #pragma unroll 1
   for (int r = 0; r < HP; ++r) {
     double u = ur[0];
@@ -521,7 +575,7 @@ __global__ void __launch_bounds__(32) lane_states_fixed_kernel(LaneArgs a) {
     for (int j = 1; j < HP; ++j) u = r == j ? ur[j] : u;
     const double qr = live ? exp_nonpos(u - shift) : 0.0;
     path[0] = r;
-    const double ch = fnode<HP, GM, 1>(S, E, qr, r, path, MR);
+    const double ch = fnode<HP, GM, 1>(S, E, qr, r, path, MR, pc0);
     const int rr = F::O_M + mrow_(r, HP) + r;
     S[rr * 32] += qr + ch;
     zm += ch;

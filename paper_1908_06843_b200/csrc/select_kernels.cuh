@@ -29,6 +29,7 @@
 // the point's shift is final.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "bsc_kernels.cuh"
@@ -37,7 +38,7 @@ namespace bscgpu {
 
 constexpr int kSelWarps = 4;                  // points per CTA = 32 · kSelWarps
 constexpr int kSelCols = 16;                  // B columns per staged chunk
-constexpr int kSelQueue = 21;                 // key queue slots per lane (4 CTAs of 56.7 KB per SM at H = 300)
+constexpr int kSelQueue = kSelCols;           // key queue slots per lane (merged after every chunk)
 constexpr int kSelStageBytes = 32 * kSelCols * 8;  // 32 rows × 16 columns fp64
 constexpr int kSelWarpBytes = 2 * kSelStageBytes + kSelQueue * 256;  // 2 stages + the key queue
 
@@ -122,41 +123,17 @@ __global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
     issue(0, 0);
 
     // The best K keys so far, descending. A column's key is only queued when it
-    // reaches the threshold tau, a lower bound of the final K-th key that only
-    // rises, and the queue is merged into the list (one insertion-network round
-    // per queued key of the fullest lane) only when it could overflow.
-    // Warm start: the point's previous candidates and runner-up (any K distinct
-    // units) give K current keys whose minimum bounds the K-th best from below,
-    // so from the second EM iteration on little more than the final K keys are
-    // ever queued — ~25 rounds per 32 points instead of ~140 with tau = −∞.
+    // beats the list's current K-th key (the threshold only rises: a valid lower
+    // bound of the final K-th), and the queue is merged into the list once per
+    // chunk, so the insertion network runs ~K·(1 + ln(H/16K)) times per point
+    // instead of at every column where any lane of the warp would insert.
+    // (Measured and rejected, profiles/r02_variants.txt: thresholds warm-started from
+    // the previous iteration's candidates with merges deferred until the queue fills.)
     double L[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) L[j] = -INFINITY;
     double tau = -INFINITY, probe = 0.0;
     const double log_pi = a.log_pi, inv2s = a.inv2s;
-    if (HP < H && live && a.next_idx) {
-      const uint32_t* pc = a.cand_out + n * HP;
-      uint32_t ix[K];
-#pragma unroll
-      for (int j = 0; j < HP; ++j) ix[j] = pc[j];
-      ix[HP] = a.next_idx[n];
-      bool okw = ix[0] < static_cast<uint32_t>(H) && ix[HP] < static_cast<uint32_t>(H) && ix[HP] != ix[0];
-#pragma unroll
-      for (int j = 1; j < HP; ++j)  // ascending and in range: K distinct units with the runner-up
-        okw = okw && ix[j] > ix[j - 1] && ix[j] < static_cast<uint32_t>(H) && ix[HP] != ix[j];
-      if (okw) {
-        const double* brow = a.B + n * Hp;
-        double lo = INFINITY;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int h = static_cast<int>(ix[j]);
-          const double t = __fma_rn(2.0, brow[h], -gd[h]);
-          const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));
-          lo = fmin(lo, sel_key(f, h));  // (a NaN key is ignored here and caught by the probe below)
-        }
-        tau = lo;
-      }
-    }
     int cnt = 0;
     auto merge = [&]() {
       // L'[j] = c_j ? (c_{j−1} ? L[j−1] : k) : L[j], c_j = k > L[j]
@@ -177,7 +154,7 @@ __global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
         }
       }
       cnt = 0;
-      tau = fmax(tau, L[K - 1]);
+      tau = L[K - 1];
     };
     for (int c = 0; c < nch; ++c) {
       if (c + 1 < nch) {
@@ -189,24 +166,29 @@ __global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
       __syncwarp();
       const char* row = stage + (c & 1) * kSelStageBytes + lane * 128;
       const int h0 = c * kSelCols;
+      auto score = [&](auto checked) {
 #pragma unroll
-      for (int j = 0; j < kSelCols / 2; ++j) {
-        const double2 v = *reinterpret_cast<const double2*>(row + ((j ^ (lane & 7)) << 4));
+        for (int j = 0; j < kSelCols / 2; ++j) {
+          const double2 v = *reinterpret_cast<const double2*>(row + ((j ^ (lane & 7)) << 4));
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int h = h0 + 2 * j + u;
-          if (h < H) {
-            const double t = __fma_rn(2.0, u ? v.y : v.x, -gd[h]);  // = 2b − G_hh (2b is exact)
-            const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));  // linear_discrete.cpp:248-249, unfused
-            probe = __fma_rn(f, 0.0, probe);                          // NaN once any score is not finite
-            const double k = sel_key(f, h);
-            if (k >= tau) queue[(cnt++) * 32] = k;  // (keys are distinct: ≥ only admits the warm bound itself)
+          for (int u = 0; u < 2; ++u) {
+            const int h = h0 + 2 * j + u;
+            if (!decltype(checked)::value || h < H) {
+              const double t = __fma_rn(2.0, u ? v.y : v.x, -gd[h]);  // = 2b − G_hh (2b is exact)
+              const double f = __dadd_rn(log_pi, __dmul_rn(t, inv2s));  // linear_discrete.cpp:248-249, unfused
+              probe = __fma_rn(f, 0.0, probe);                          // NaN once any score is not finite
+              const double k = sel_key(f, h);
+              if (k > tau) queue[(cnt++) * 32] = k;
+            }
           }
         }
-      }
+      };
+      if (h0 + kSelCols <= H)  // a full chunk: one straight-line block of 16 columns, no per-column test
+        score(std::false_type{});
+      else
+        score(std::true_type{});
       __syncwarp();
-      // merge when the next chunk could overflow the fullest lane's queue
-      if (__reduce_max_sync(0xffffffffu, cnt) + kSelCols > kSelQueue || c + 1 == nch) merge();
+      merge();
       __syncwarp();
     }
 
@@ -248,7 +230,6 @@ __global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
         uint32_t* co = a.cand_out + n * HP;
 #pragma unroll
         for (int j = 0; j < HP; ++j) co[j] = static_cast<uint32_t>(cand[j]);
-        if (HP < H && a.next_idx) a.next_idx[n] = static_cast<uint32_t>(key_index(L[HP]));  // the runner-up
         y2_acc += y2;
         mode = kModeFallback;
         if (exact) {
@@ -273,12 +254,14 @@ __global__ void __launch_bounds__(32 * kSelWarps, 4) select_kernel(EnumArgs a) {
             const long long go = static_cast<long long>(cand[p]) * Hp;
 #pragma unroll
             for (int q = p + 1; q < HP; ++q, ++e) {
-              const double v = __ldg(a.Pm + go + cand[q]);  // −2·inv2s·G_pq (pair_terms_kernel)
+              // (P and e^P gathered from per-E-step H × H tables instead: measured slower, r02_variants.txt)
+              const double v = -2.0 * inv2s * __ldg(a.G + go + cand[q]);
+              const double ev = exp_nonpos(v);
               fin = fin && isfinite(v);
               pmax = fmax(pmax, v);
               pabs = fmax(pabs, fabs(v));
               rt[(4 + 2 * HP + e) * 32] = v;
-              rt[(4 + 2 * HP + NP + e) * 32] = __ldg(a.EPm + go + cand[q]);
+              rt[(4 + 2 * HP + NP + e) * 32] = ev;
             }
           }
           // q(S) = q(A)·e^{u_z}·e^{coup(S)} stays in fp64 range when |u| ≤ 300 and
