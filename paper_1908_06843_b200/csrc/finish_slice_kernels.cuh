@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kFsThreads, 2) lane_finish_slice_kernel(Finish
 #pragma unroll 4
         for (int h = lane; h < H; h += 32) {
           // rel = fma(inv2s, 2b − G_hh, dlp), the selection pass's rounding: shift ≥ rel
-          const double e = exp_nonpos(__fma_rn(f.inv2s, __fma_rn(2.0, row[h], -gd[h]), f.dlp) - shift);
+          const double e = exp_nonpos_ftz(__fma_rn(f.inv2s, __fma_rn(2.0, row[h], -gd[h]), f.dlp) - shift);
           row[h] = e;
           zs += e;
         }
