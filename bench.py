@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAKS = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
-TRAFFIC = os.path.join(ROOT, "profiles", "r01_traffic.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "r02_traffic.json")
 
 
 def measured_traffic(workload, kernel, points):
@@ -405,9 +405,11 @@ def main():
                      "algorithmic": "SURVEY.md §8(d): F_state=%d, F_dense=%d flops/point; int8 slice products "
                                     "36·2·D·H ops/point per product" % (state, dense)},
         "state_roofline": roof("enumerate"),
-        "step_roofline": {"flops_per_step": step_flops, "tflops": round(step_flops / (ms / 1e3) / 1e12 / world, 3),
-                          "frac_of_dmma_peak": round(step_flops / (ms / 1e3) / 1e12 / world / dmma_peak, 4),
-                          "note": "fp64-equivalent algorithmic flops (the products run on int8 slices)"},
+        "step_rate": {"flops_per_step": step_flops, "tflops_per_gpu": round(step_flops / (ms / 1e3) / 1e12 / world, 3),
+                      "note": "SURVEY.md §8(d) fp64-equivalent algorithmic flops of the whole step per second; not a "
+                              "fraction of any one peak: the two products run as int8 slice products on the tensor "
+                              "cores (kernels.gemm_*: int8 ops against the int8 peak), the state evaluation on the "
+                              "FP64 pipe (state_roofline)"},
         "kernels": kernels,
         "clocks": clk.summary(),
         "gpu_launches": int(launches_per_step * args.steps),

@@ -140,6 +140,11 @@ int prsp_bsc_gpu_timings(prsp_bsc_gpu* ctx, float* out6);
    fallback, finish; zeros when the single-kernel pass ran): the first min(n, 10) values. */
 int prsp_bsc_gpu_timings_ex(prsp_bsc_gpu* ctx, float* out, int n);
 int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out);
+/* Test hook (compute-sanitizer's memcheck is not available on every pool): with BSC_GUARD=1 in the
+ * environment every device buffer of the library carries 256 guard bytes on both sides;
+ * this call synchronises the device and returns PRSP_BSC_GPU_ERR_INTERNAL, naming the buffer in
+ * last_error, if a kernel has written into any guard. Without BSC_GUARD it returns OK. */
+int prsp_bsc_gpu_check_guards(void);
 /* Enumerator cycles per phase (summed over warps) of the last E-step when the
  * process runs with BSC_ENUM_PROFILE=1, else zeros: scores, selection, log-joint
  * terms, state log-joints, exp, MAP, subtree + moment sums, output + loop. */

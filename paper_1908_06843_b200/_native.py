@@ -54,6 +54,7 @@ SIGNATURES = {
     "prsp_bsc_gpu_timings": [_ptr, _ptr],
     "prsp_bsc_gpu_timings_ex": [_ptr, _ptr, C.c_int],
     "prsp_bsc_gpu_launches": [_ptr, C.POINTER(_int)],
+    "prsp_bsc_gpu_check_guards": [],
     "prsp_bsc_gpu_enum_phase_cycles": [_ptr, _ptr],
     "prsp_mca_gpu_create": [C.c_char_p, _dbl, _u32, _u32, _u32, _u32, _u64, _int, C.POINTER(_ptr)],
     "prsp_mca_gpu_free": [_ptr],

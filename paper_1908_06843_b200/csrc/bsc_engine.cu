@@ -150,6 +150,11 @@ BscEngine::BscEngine(int family, uint32_t dim, uint32_t latents, uint32_t hprime
   init(device);
 }
 
+void check_device_guards() {
+  const std::string bad = util::check_guards();
+  if (!bad.empty()) throw Error(kInternal, "guard: " + bad);
+}
+
 void BscEngine::init(int device) {
   if (D_ == 0 || H_ == 0) throw Error(kConfig, "linear model: dim and latents must be >= 1");
   // TruncationConfig::validate, truncation.cpp:23-30

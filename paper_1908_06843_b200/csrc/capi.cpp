@@ -381,6 +381,10 @@ int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out) {
   });
 }
 
+int prsp_bsc_gpu_check_guards(void) {
+  return guarded([&] { bscgpu::check_device_guards(); });
+}
+
 int prsp_bsc_gpu_enum_phase_cycles(prsp_bsc_gpu* ctx, uint64_t* out8) {
   return guarded([&] {
     need(ctx, "ctx");
