@@ -201,16 +201,22 @@ def test_posterior_weight_paths(pkg, port, s2):
     m.close()
 
 
-def test_temperature(pkg, port):
+@pytest.mark.parametrize("cfg,n", [("c1", 500), ("c2", 3000), ("c3", 400)])
+def test_temperature(pkg, port, cfg, n):
+    """Annealed posteriors (linear_discrete.cpp:277-286: q ∝ exp((lj − m)/T), log Z at T = 1) at the
+    bars shape and at the c2 / c3 shapes, statistics and the whole step."""
     from paper_1908_06843_b200 import configs
 
-    w = configs.CONFIGS["c1"]
-    y = configs.data(w, 500)
+    w = configs.CONFIGS[cfg]
+    y = configs.data(w, n)
     p = configs.init(w, y)
     m = model_for(pkg, w.D, w.H, w.hprime, w.gamma)
     m.load(y)
     for T in [1.0, 1.5, 4.0]:
-        check_stats(m.estep_stats(p, temperature=T), port.estep_stats(p.W, p.pi, p.sigma2, y, 10, 4, T))
+        check_stats(m.estep_stats(p, temperature=T),
+                    port.estep_stats(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma, T))
+    if n >= 4 * w.H:  # (fewer points than units leave Σ⟨ssᵀ⟩ to the ridge, which amplifies rounding differences)
+        check_step(m.step(p, temperature=2.0), *port.step(p.W, p.pi, p.sigma2, y, w.hprime, w.gamma, temperature=2.0))
     m.close()
 
 
