@@ -623,7 +623,8 @@ void BscEngine::ensure_work(uint64_t n) {
       ck(cudaFuncSetAttribute(finish_slice_fn(fs_pt_), cudaFuncAttributeMaxDynamicSharedMemorySize, fs_smem_),
          "finish+slice smem attr");
       int fo = 0;
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fo, finish_slice_fn(fs_pt_), 256, fs_smem_), "occupancy");
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fo, finish_slice_fn(fs_pt_), fs_threads(fs_pt_), fs_smem_),
+         "occupancy");
       fs_ctas_ = std::max(fo, 1) * prop.multiProcessorCount;
     }
     sc_ctas_ = std::max({enum_ctas_, front_ctas_, fin_ctas_, fs_ctas_});
@@ -936,7 +937,8 @@ void BscEngine::launch_enumerate(double temperature, bool cands, bool infer, uin
     fsa.inv56 = 0x1.0p55;  // 2^56 / the ⟨S⟩ slice scale 2 (d_two_)
     void* fsargs[] = {&fsa};
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(fs_ctas_, (rows + 127) / 128));
-    ck(cudaLaunchKernel(finish_slice_fn(fs_pt_), dim3(grid), dim3(256), fsargs, fs_smem_, s), "finish+slice launch");
+    ck(cudaLaunchKernel(finish_slice_fn(fs_pt_), dim3(grid), dim3(fs_threads(fs_pt_)), fsargs, fs_smem_, s),
+       "finish+slice launch");
     es_sliced_ = true;
   } else {
     void* fargs[] = {&fa};

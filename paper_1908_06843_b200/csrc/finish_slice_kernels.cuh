@@ -40,11 +40,15 @@ struct FinishSliceArgs {
   double inv56;            // 2⁵⁶ / slice scale (a power of two)
 };
 
-constexpr int kFsThreads = 256;
+
 constexpr int kFsBlock = 128;  // points per column-sum block (oz_colsum_reduce_kernel's rows)
 
+// threads per CTA: 256 with 32-point sub-tiles (two CTAs per SM), 512 with the 16-point sub-tiles of
+// H > 800 (one CTA per SM fits: 16 warps instead of 8)
+__host__ __device__ constexpr int fs_threads(int pt) { return pt == 32 ? 256 : 512; }
+
 __host__ __device__ inline int finish_slice_smem_bytes(int pt, int H, int Hp) {
-  return 8 * (pt * Hp + ((H + 1) & ~1) + pt) + 512 + 64;
+  return 8 * (pt * Hp + ((H + 1) & ~1) + pt) + 512 + 8 * (fs_threads(pt) / 32);  // tile, diag(G), row factors, pq, per-warp Σ log Z
 }
 
 // the four 7-bit digits of t (< 2²⁸) spread to the bytes of a word, digit k at byte k
@@ -53,7 +57,8 @@ __device__ __forceinline__ uint32_t spread7(uint32_t t) {
 }
 
 template <int PT>
-__global__ void __launch_bounds__(kFsThreads, 2) lane_finish_slice_kernel(FinishSliceArgs a) {
+__global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_slice_kernel(FinishSliceArgs a) {
+  constexpr int kFsThreads = fs_threads(PT);
   static_assert(PT == 32 || PT == 16, "sub-tile of 16 or 32 points");
   constexpr int NW = kFsThreads / 32, RPW = PT / NW;  // rows per warp and sub-tile
   constexpr int G = PT / 4;                           // words per slice and unit
