@@ -39,16 +39,23 @@ namespace oz {
 constexpr int S = 8;                    // slices
 constexpr int BM = 128, BN = 128, BK = 64;
 constexpr int GPP = 4, NPASS = 2;       // 4 group accumulators × 128 TMEM columns per pass
-constexpr int A_STAGES = 10, B_STAGES = 2;
+// A ring: 10 stages, or 8 beside the epilogue's staging tiles (the variant with TMA stores)
+__host__ __device__ constexpr int a_stages(bool tma_store) { return tma_store ? 8 : 10; }
+constexpr int B_STAGES = 2;
 constexpr int A_BYTES = BM * BK;        // 8 KB: one slice
 constexpr int B_BYTES = S * BN * BK;    // 64 KB: all slices
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);  // producer, MMA, 8 epilogue warps (2 per TMEM lane quadrant)
 constexpr int EPI_COLS = BN / 2;        // columns per epilogue thread
-constexpr int SMEM_BYTES = A_STAGES * A_BYTES + B_STAGES * B_BYTES + 1024 + 256;
+constexpr int C_COLS = 8;                         // output columns per staged epilogue piece (64-byte rows)
+constexpr int C_WARP_BYTES = 32 * C_COLS * 8;     // one warp's staging tile: 32 rows × 8 columns fp64
+constexpr int C_BYTES = EPI_WARPS * C_WARP_BYTES;
+__host__ __device__ constexpr int smem_bytes(bool tma_store) {
+  return a_stages(tma_store) * A_BYTES + B_STAGES * B_BYTES + (tma_store ? C_BYTES : 0) + 1024 + 256;
+}
 constexpr int MAX_KJOB = 16384;         // int32 headroom per job (see above)
 constexpr int MAX_KROW = 1024;          // longest row the row slicer holds in registers
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+static_assert(smem_bytes(true) <= 227 * 1024 && smem_bytes(false) <= 227 * 1024, "shared memory");
 static_assert(GPP * BN <= 512 && GPP * NPASS == S, "TMEM groups");
 
 struct Args {
@@ -64,6 +71,7 @@ struct Args {
   long long ldc;
   long long c_split_stride;  // partial slot stride per k-split
   int accumulate;            // C += result (else C = result)
+  int tma_store;             // the epilogue stores C through the tensor map tc (set by launch_gemm)
   int blk_a, blk_b;          // operand layout: 0 rows [S][rows][ld], 1 K-blocked [S][k/BK][rows][BK]
 };
 
@@ -175,14 +183,17 @@ __device__ __forceinline__ double i32_to_f64(int x) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------- the GEMM
+template <bool TMA_STORE>
 __global__ void __launch_bounds__(THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb8,
-                   const __grid_constant__ CUtensorMap tb4, Args a) {
+                   const __grid_constant__ CUtensorMap tb4, const __grid_constant__ CUtensorMap tc, Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
+  constexpr int A_STAGES = a_stages(TMA_STORE);
   uint8_t* sB = smem + A_STAGES * A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + B_STAGES * B_BYTES);
+  uint8_t* sC = sB + B_STAGES * B_BYTES;  // (1024-byte aligned: the stage sizes are multiples of 1024)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sC + (TMA_STORE ? C_BYTES : 0));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * A_STAGES + 2 * B_STAGES + 2);
   const uint32_t full_a = smem_u32(bars), empty_a = full_a + 8 * A_STAGES;
   const uint32_t full_b = empty_a + 8 * A_STAGES, empty_b = full_b + 8 * B_STAGES;
@@ -296,12 +307,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int gl = GPP - 1; gl >= 0; --gl) {  // smallest weights first
           const double w = ldexp(1.0, -7 * (gbase + gl + 2));
 #pragma unroll
-          for (int h = 0; h < EPI_COLS / 32; ++h) {
-            int v[32];
-            tmem_ld32(tbase + gl * BN + h * 32, v);
+          for (int h = 0; h < EPI_COLS / 16; ++h) {  // (16 columns per load: ptxas keeps several loads in flight)
+            int v[16];
+            tmem_ld16(tbase + gl * BN + h * 16, v);
             tmem_wait_ld();
 #pragma unroll
-            for (int x = 0; x < 32; ++x) acc[h * 32 + x] = fma(i32_to_f64(v[x]), w, acc[h * 32 + x]);
+            for (int x = 0; x < 16; ++x) acc[h * 16 + x] = fma(i32_to_f64(v[x]), w, acc[h * 16 + x]);
           }
         }
         tc_fence_before();
@@ -309,7 +320,49 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) mbar_arrive(tempty);
       }
       const int m = mt * BM + row;
-      if (m < a.M) {
+      if constexpr (TMA_STORE) {
+        // A thread owns one output row (its TMEM lane), so storing from the accumulators makes every
+        // warp store touch 32 rows: 8,192 L1 wavefronts per tile, on the path the tensor cores read
+        // their shared-memory operands through (probes: this block cost 0.19 ms of the c2 Y·W launch
+        // although it runs beside the next tile's MMAs). Instead the scaled values are staged 8 columns
+        // at a time in a swizzled 32 × 64-byte tile per warp and leave through the TMA unit, which
+        // also clips the ragged edges.
+        int ln = lane, wp = warp;
+        asm volatile("" : "+r"(ln), "+r"(wp));  // (derived addresses are formed here, not held across the drain loops)
+        const int c0 = nt * BN + ((wp - 2) >> 2) * EPI_COLS;
+        const double sam = m < a.M ? a.sa[ks * a.sa_stride + m] : 0.0;
+        const double* sb = a.sb + ks * a.sb_stride + c0;
+        uint8_t* wrow = sC + (wp - 2) * C_WARP_BYTES + ln * (C_COLS * 8);
+        const uint32_t wtile = smem_u32(sC + (wp - 2) * C_WARP_BYTES);
+        const int sw = (ln >> 1) & 3;  // SWIZZLE_64B: 16-byte piece j of row r at (j ^ ((r >> 1) & 3))
+#pragma unroll
+        for (int ch = 0; ch < EPI_COLS / C_COLS; ++ch) {
+          if (c0 + ch * C_COLS < a.N) {  // (warp-uniform)
+            if (ch > 0) {
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < C_COLS / 2; ++j) {
+              const int c = ch * C_COLS + 2 * j;
+              const double s0 = c0 + c < a.N ? sb[c] : 0.0, s1 = c0 + c + 1 < a.N ? sb[c + 1] : 0.0;
+              *reinterpret_cast<double2*>(wrow + ((j ^ sw) << 4)) =
+                  make_double2(acc[c] * sam * s0, acc[c + 1] * sam * s1);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (ln == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                  "cp.async.bulk.commit_group;" ::"l"(reinterpret_cast<uint64_t>(&tc)),
+                  "r"(c0 + ch * C_COLS), "r"(mt * BM + (wp & 3) * 32), "r"(ks), "r"(wtile)
+                  : "memory");
+            }
+          }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      } else if (m < a.M) {  // (the variant without the TMA store: accumulating launches, odd strides)
         const double sam = a.sa[ks * a.sa_stride + m];
         const int c0 = nt * BN + half * EPI_COLS;
         const double* sb = a.sb + ks * a.sb_stride + c0;
@@ -581,13 +634,38 @@ inline cudaError_t launch_gemm(const Operand& A, const Operand& B, int M, int N,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(oz_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(true));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(oz_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(false));
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
-  CUtensorMap ta, tb8, tb4;
+  CUtensorMap ta, tb8, tb4, tc;
   if (!make_map(&ta, A, K, BM, 1) || !make_map(&tb8, B, K, BN, S) || !make_map(&tb4, B, K, BN, S / 2))
     return cudaErrorInvalidValue;
+  {
+    // C as a 3-d fp64 tensor (columns, rows, k-splits) for the epilogue's TMA stores: boxes of
+    // C_COLS columns × 32 rows, 64-byte swizzle; used when C is overwritten and its strides
+    // are multiples of 16 bytes (else the kernel stores from registers)
+    const int splits = args.kchunk > 0 ? (K + args.kchunk - 1) / args.kchunk : 1;
+    const unsigned long long row_bytes = static_cast<unsigned long long>(args.ldc) * 8;
+    const unsigned long long split_bytes =
+        splits > 1 ? static_cast<unsigned long long>(args.c_split_stride) * 8 : row_bytes * static_cast<unsigned long long>(M);
+    // (split-K launches have long tiles and a small output: they keep the 10-stage A ring instead)
+    args.tma_store = splits == 1 && !args.accumulate && row_bytes % 16 == 0 && split_bytes % 16 == 0 &&
+                     (reinterpret_cast<uintptr_t>(args.C) & 15) == 0 && encode_fn() != nullptr;
+    if (args.tma_store) {
+      cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(splits)};
+      cuuint64_t strides[2] = {row_bytes, split_bytes};
+      cuuint32_t box[3] = {C_COLS, 32, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      if (encode_fn()(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, args.C, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        args.tma_store = 0;
+    }
+    if (!args.tma_store) tc = ta;  // (unused)
+  }
   args.blk_a = A.blocked;
   args.blk_b = B.blocked;
   args.M = M;
@@ -603,7 +681,10 @@ inline cudaError_t launch_gemm(const Operand& A, const Operand& B, int M, int N,
     grid = (num_sms / args.n_tiles) * args.n_tiles;
     if (grid <= 0) grid = num_sms;
   }
-  oz_gemm_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb8, tb4, args);
+  if (args.tma_store)
+    oz_gemm_kernel<true><<<grid, THREADS, smem_bytes(true), s>>>(ta, tb8, tb4, tc, args);
+  else
+    oz_gemm_kernel<false><<<grid, THREADS, smem_bytes(false), s>>>(ta, tb8, tb4, tc, args);
   return cudaGetLastError();
 }
 
