@@ -618,8 +618,8 @@ void BscEngine::ensure_work(uint64_t n) {
     fs_ctas_ = 0;
     const char* fse = std::getenv("BSC_FUSED_FINISH");
     if (oz_ && !(fse && fse[0] == '0')) {
-      fs_pt_ = finish_slice_smem(32, static_cast<int>(H_), Hp_) <= 200 * 1024 ? 32 : 16;
-      fs_smem_ = finish_slice_smem(fs_pt_, static_cast<int>(H_), Hp_);
+      fs_pt_ = finish_slice_smem(32, static_cast<int>(H_), Hp_, static_cast<int>(hprime_)) <= 200 * 1024 ? 32 : 16;
+      fs_smem_ = finish_slice_smem(fs_pt_, static_cast<int>(H_), Hp_, static_cast<int>(hprime_));
       ck(cudaFuncSetAttribute(finish_slice_fn(fs_pt_), cudaFuncAttributeMaxDynamicSharedMemorySize, fs_smem_),
          "finish+slice smem attr");
       int fo = 0;

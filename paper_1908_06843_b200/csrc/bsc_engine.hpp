@@ -44,7 +44,7 @@ const void* select_fn(int hprime);     // thread-per-point selection pass (selec
 int select_smem(int latents);          // its dynamic shared memory per CTA (bytes)
 const void* finish_fn(int maxj);       // lane_finish_kernel<MAXJ>
 const void* finish_slice_fn(int pt);   // lane_finish_slice_kernel<PT> (finish_slice_kernels.cuh)
-int finish_slice_smem(int pt, int latents, int hp_padded);
+int finish_slice_smem(int pt, int latents, int hp_padded, int hprime);
 
 // The multi-valued enumerator instantiation for (MAXJ, staged) (ldv_engine.cu).
 const void* ldv_kernel_fn(int maxj, bool staged);

@@ -47,8 +47,9 @@ constexpr int kFsBlock = 128;  // points per column-sum block (oz_colsum_reduce_
 // H > 800 (one CTA per SM fits: 16 warps instead of 8)
 __host__ __device__ constexpr int fs_threads(int pt) { return pt == 32 ? 256 : 512; }
 
-__host__ __device__ inline int finish_slice_smem_bytes(int pt, int H, int Hp) {
-  return 8 * (pt * Hp + ((H + 1) & ~1) + pt) + 512 + 8 * (fs_threads(pt) / 32);  // tile, diag(G), row factors, pq, per-warp Σ log Z
+__host__ __device__ inline int finish_slice_smem_bytes(int pt, int H, int Hp, int hp) {
+  // ⟨S⟩ tile, diag(G), row factors, pq, per-warp Σ log Z, and the sub-tile's lane outputs [field][pt + 2]
+  return 8 * (pt * Hp + ((H + 1) & ~1) + pt) + 512 + 8 * (fs_threads(pt) / 32) + 8 * lane_out_fields(hp) * (pt + 2);
 }
 
 // the four 7-bit digits of t (< 2²⁸) spread to the bytes of a word, digit k at byte k
@@ -71,6 +72,12 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
   double* rs = gd + ((H + 1) & ~1);            // per-row factor (1/Z, 1, or 0)
   uint16_t* pq = reinterpret_cast<uint16_t*>(rs + PT);  // moment entry o → (p, q)
   double* red = reinterpret_cast<double*>(pq + 256);
+  // the sub-tile's lane-pass outputs (shift, Σ multi-active weights, moments), staged [field][PT + 2]:
+  // a point's fields sit 256 bytes apart in the [field][32 points] tiles of the lane pass, so reading
+  // them per point from global memory cost 32 L1 wavefronts per load instruction
+  constexpr int MP = PT + 2;
+  double* momt = red + NW;
+  const int nf = lane_out_fields(hp);
   for (int i = threadIdx.x; i < H; i += kFsThreads) gd[i] = f.gdiag[i];
   for (int o = threadIdx.x; o < nm; o += kFsThreads) {
     int idx = o, p = 0;
@@ -90,13 +97,21 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
       const long long n0 = blk * kFsBlock + st * PT;
       // ---- phase A: this warp's rows r = wib + NW·i
       int mode[RPW];
-      double sh[RPW], zmv[RPW];
+      {
+        const double* src = f.out + (n0 >> 5) * nf * 32 + (n0 & 31);
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(momt));
+        for (int idx = threadIdx.x; idx < nf * (PT / 2); idx += kFsThreads) {
+          const int fld = idx / (PT / 2), pc = idx % (PT / 2);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + (fld * MP + 2 * pc) * 8),
+                       "l"(src + fld * 32 + 2 * pc)
+                       : "memory");
+        }
+      }
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
         const int r = wib + NW * i;
         const long long n = n0 + r;
         mode[i] = -1;
-        sh[i] = zmv[i] = 0.0;
         if (n < f.N) {
           mode[i] = f.pmode[n];
           const bool lanept = mode[i] == kModeShift || mode[i] == kModeMax;
@@ -104,11 +119,6 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
           const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(tile + r * Hp));
           for (int c = lane; c < row16; c += 32)
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + c * 16), "l"(src + 2 * c) : "memory");
-          if (lanept) {
-            const double* ot = f.out + (n >> 5) * lane_out_fields(hp) * 32 + (n & 31);
-            sh[i] = ot[0];
-            zmv[i] = ot[32];
-          }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -122,7 +132,7 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
             asm volatile("prefetch.global.L2 [%0];" ::"l"(f.B + n * Hp + l * 16));
       }
       asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
+      __syncthreads();  // (the lane outputs were fetched by all threads)
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {
         const int r = wib + NW * i;
@@ -137,12 +147,7 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
           if (lane == 0) rs[r] = 1.0;
           continue;
         }
-        const double* ot = f.out + (n >> 5) * lane_out_fields(hp) * 32 + (n & 31);
-        const double shift = sh[i], zm = zmv[i];
-        // this lane's moment entries and candidates: in flight while the weights are formed
-        double mom[5];
-#pragma unroll
-        for (int t = 0; t < 5; ++t) mom[t] = lane + 32 * t < nm ? ot[(2 + lane + 32 * t) * 32] : 0.0;
+        const double shift = momt[r], zm = momt[MP + r];
         const uint32_t cmine = lane < hp ? f.cand[n * hp + lane] : 0u;
         // (Dropping the weights below e^-48 of the point's largest and compacting the rest by
         // ballot was measured slower — early EM iterations keep most units inside the window —
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
           const int p = on ? pq[o] & 0xff : 0, q = on ? pq[o] >> 8 : 0;
           const uint32_t cp = __shfl_sync(0xffffffffu, cmine, p), cq = __shfl_sync(0xffffffffu, cmine, q);
           if (!on) continue;
-          const double v = mom[t];
+          const double v = momt[(2 + o) * MP + r];
           if (q == p)
             row[cp] = v;  // candidate marginal (unnormalised, as the singleton weights)
           else

@@ -56,7 +56,9 @@ const void* finish_fn(int maxj) {
 const void* finish_slice_fn(int pt) {
   return pt == 32 ? (const void*)lane_finish_slice_kernel<32> : (const void*)lane_finish_slice_kernel<16>;
 }
-int finish_slice_smem(int pt, int latents, int hp_padded) { return finish_slice_smem_bytes(pt, latents, hp_padded); }
+int finish_slice_smem(int pt, int latents, int hp_padded, int hprime) {
+  return finish_slice_smem_bytes(pt, latents, hp_padded, hprime);
+}
 
 // warps (32-point tiles) per CTA of lane_fn's kernel
 int lane_wpc(int gamma, int hprime) { return gamma == 4 && (hprime == 10 || hprime == 12) ? 2 : 1; }
