@@ -53,9 +53,9 @@ __host__ __device__ inline int select_smem_bytes(int H) {
 // fp64 min/max (DMNMX, the FP64 pipe) instead of 64-bit integer compare/select
 // chains on the ALU pipe.
 __device__ __forceinline__ double sel_key(double f, int h) {
-  const long long fb = __double_as_longlong(f);
-  const long long code = fb < 0 ? h : 1023 - h;
-  return __longlong_as_double((fb & ~1023LL) | code);
+  const int hi = __double2hiint(f);
+  const unsigned code = static_cast<unsigned>(hi < 0 ? h : 1023 - h);  // (only the low word changes)
+  return __hiloint2double(hi, static_cast<int>((static_cast<unsigned>(__double2loint(f)) & ~1023u) | code));
 }
 __device__ __forceinline__ int key_index(double k) {
   const long long kb = __double_as_longlong(k);
