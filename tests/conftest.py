@@ -58,3 +58,16 @@ def ref():
     if not O.Oracle.available("ref"):
         pytest.skip("reference build (oracle/_ref) not available")
     return O.Oracle("ref")
+
+
+@pytest.fixture(autouse=True)
+def _device_guards(request):
+    """With BSC_GUARD=1 in the environment (guarded device allocations,
+    csrc/engine_util.hpp) every GPU test ends with a check that no kernel wrote
+    outside a buffer: `BSC_GUARD=1 pytest tests -m gpu` is the whole suite as an
+    out-of-bounds check (compute-sanitizer is closed on this pool)."""
+    yield
+    if os.environ.get("BSC_GUARD") == "1" and request.node.get_closest_marker("gpu"):
+        from paper_1908_06843_b200 import _native as N
+
+        N.call("prsp_bsc_gpu_check_guards")
