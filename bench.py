@@ -292,10 +292,9 @@ def main():
         def one_step():
             model.step_allreduce()
     else:
-        stats_view = bdist.stats_tensor(model)
 
-        def one_step():
-            bdist.distributed_step(model, stats_view)
+        def one_step():  # E-step + M-step from the resident parameters: one C call (prsp_bsc_gpu_step)
+            model.step_resident()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:  # sampled over warm-up + timed steps (≥ 0.2 s of load)

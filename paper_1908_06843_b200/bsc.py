@@ -203,6 +203,14 @@ class LinearDiscreteGpuModel:
         N.call("prsp_bsc_gpu_step", self._h, float(temperature), C.byref(f))
         return StepResult(self.get_params(), f.value)
 
+    def step_resident(self, temperature: float = 1.0) -> float:
+        """One EM iteration from the parameters the engine holds (those of the last
+        set_params or the last step's result), nothing but F crossing the host
+        boundary: the inner loop of a training run (em.cpp:36-45). Returns F."""
+        f = _dbl()
+        N.call("prsp_bsc_gpu_step", self._h, float(temperature), C.byref(f))
+        return f.value
+
     def step_host(self, params: BscParams, y, temperature: float = 1.0) -> StepResult:
         """The reference call shape end to end: host Y and params in, host params and F out."""
         if self.model == "dsc":

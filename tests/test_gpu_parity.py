@@ -436,3 +436,26 @@ def test_dead_dictionary_element(pkg, port):
     assert so["sum_s"][dead] < 1e-30 and abs(sg.sum_s[dead] - so["sum_s"][dead]) <= 1e-9 * so["sum_s"][dead]
     check_step(m.step(p), *port.step(p.W, p.pi, p.sigma2, y, hp, g))
     m.close()
+
+
+def test_resident_steps_follow_the_stepwise_trajectory(pkg):
+    """step_resident (prsp_bsc_gpu_step from the parameters the engine holds: the bench's inner
+    loop) gives the same bits as step(params) fed with its own results."""
+    from paper_1908_06843_b200 import configs
+
+    w = configs.CONFIGS["c1"]
+    y = configs.data(w, 2000)
+    p = configs.init(w, y)
+    a, b = model_for(pkg, w.D, w.H, w.hprime, w.gamma), model_for(pkg, w.D, w.H, w.hprime, w.gamma)
+    a.load(y)
+    b.load(y)
+    b.set_params(p)
+    for _ in range(4):
+        r = a.step(p)
+        p = r.params
+        f = b.step_resident()
+        assert f == r.free_energy
+    q = b.get_params()
+    assert np.array_equal(q.W, p.W) and q.pi == p.pi and q.sigma2 == p.sigma2
+    a.close()
+    b.close()
