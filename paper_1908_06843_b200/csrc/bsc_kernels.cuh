@@ -146,27 +146,32 @@ __device__ __forceinline__ double exp_nonpos(double x) {
 }
 
 // exp_nonpos for bulk use (the H singleton weights per point): the same
-// reduction and polynomial, with round(x·log2e) taken from the low word of
+// reduction and Taylor polynomial (evaluated as two Horner chains instead of
+// Estrin's scheme), with round(x·log2e) taken from the low word of
 // x·log2e + 1.5·2⁵² and the power of two applied by one integer add to the
 // exponent field. Results below 2⁻¹⁰²¹ (x < −707) are returned as 0 instead of
 // as subnormals: they are weights of at most 1e-307 relative to Z.
+// Taylor coefficients 1/k!, k = 0..13, in constant memory: an FMA takes one of them straight from the
+// constant bank, where an immediate costs two moves per use (a quarter of the loop's instructions).
+static __constant__ double kExpTaylor[14] = {
+    1.0, 1.0, 0.5, 1.66666666666666657e-01, 4.16666666666666644e-02, 8.33333333333333322e-03,
+    1.38888888888888894e-03, 1.98412698412698413e-04, 2.48015873015873016e-05, 2.75573192239858907e-06,
+    2.75573192239858883e-07, 2.50521083854417188e-08, 2.08767569878680990e-09, 1.6059043836821613e-10};
 __device__ __forceinline__ double exp_nonpos_ftz(double x) {
   const double kd = fma(x, 1.4426950408889634, 6755399441055744.0);
   const int ki = __double2loint(kd);
   const double k = kd - 6755399441055744.0;
   double r = fma(k, -6.93147180559945286227e-01, x);
   r = fma(k, -2.319046813846299558e-17, r);
-  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-  const double q0 = fma(r, 1.0, 1.0);
-  const double q1 = fma(r, 1.66666666666666657e-01, 0.5);
-  const double q2 = fma(r, 8.33333333333333322e-03, 4.16666666666666644e-02);
-  const double q3 = fma(r, 1.98412698412698413e-04, 1.38888888888888894e-03);
-  const double q4 = fma(r, 2.75573192239858883e-06, 2.48015873015873016e-05);
-  const double q5 = fma(r, 2.50521083854417188e-08, 2.75573192239858907e-07);
-  const double q6 = fma(r, 1.6059043836821613e-10, 2.08767569878680990e-09);
-  const double v0 = fma(r2, q1, q0), v1 = fma(r2, q3, q2), v2 = fma(r2, q5, q4);
-  const double w0 = fma(r4, v1, v0), w1 = fma(r4, q6, v2);
-  const double p = fma(r8, w1, w0);
+  // even and odd parts by Horner in r² (two independent chains, one constant operand per FMA)
+  const double r2 = r * r;
+  double e = kExpTaylor[12], o = kExpTaylor[13];
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    e = fma(e, r2, kExpTaylor[2 * i]);
+    o = fma(o, r2, kExpTaylor[2 * i + 1]);
+  }
+  const double p = fma(o, r, e);
   const double y = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
   return x < -707.0 ? 0.0 : y;
 }

@@ -108,12 +108,18 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
         }
       }
 #pragma unroll
+      double y2v[RPW];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {  // (all of this warp's modes and ‖y‖² in flight before the first is used)
+        const long long n = n0 + wib + NW * i;
+        mode[i] = n < f.N ? f.pmode[n] : -1;
+        y2v[i] = n < f.N ? f.y2[n] : 0.0;
+      }
+#pragma unroll
       for (int i = 0; i < RPW; ++i) {
         const int r = wib + NW * i;
         const long long n = n0 + r;
-        mode[i] = -1;
         if (n < f.N) {
-          mode[i] = f.pmode[n];
           const bool lanept = mode[i] == kModeShift || mode[i] == kModeMax;
           const double* src = (lanept ? f.B : f.ES) + n * Hp;
           const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(tile + r * Hp));
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
         const double z1 = zs + zm;
         const double inv_z = 1.0 / z1;
         if (lane == 0) {
-          lse_acc += (f.base0 - f.y2[n] * f.inv2s) + (shift + log(z1));
+          lse_acc += (f.base0 - y2v[i] * f.inv2s) + (shift + log(z1));
           rs[r] = inv_z;
         }
         __syncwarp();
