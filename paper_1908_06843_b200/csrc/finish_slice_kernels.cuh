@@ -17,9 +17,9 @@
 //            candidate pairs go to Σ⟨ssᵀ⟩ in fixed point (pair_fx_add).
 //            Points the fallback launch handled arrive as finished ⟨s⟩ rows
 //            (factor 1); rows past N are zero.
-//   phase B  thread per unit h: the PT values of column h, scaled by their row
-//            factors, are cut into the 8 base-128 digits of ⌊x·2⁵⁶/scale⌋
-//            (x ≥ 0: no sign), transposed with byte permutes and stored as PT
+//   phase B  thread per (unit h, 16 points): the values of column h, scaled by their
+//            row factors, are cut into the 8 base-128 digits of ⌊x·2⁵⁶/scale⌋
+//            (x ≥ 0: no sign), transposed with byte permutes and stored as 16
 //            contiguous bytes per slice — the K-blocked operand layout
 //            [slice][point/64][h][64] of the Yᵀ⟨S⟩ GEMM — while the column sums
 //            Σ_n⟨s_nh⟩ of the 128-point block accumulate in a fixed order.
@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
   constexpr int kFsThreads = fs_threads(PT);
   static_assert(PT == 32 || PT == 16, "sub-tile of 16 or 32 points");
   constexpr int NW = kFsThreads / 32, RPW = PT / NW;  // rows per warp and sub-tile
-  constexpr int G = PT / 4;                           // words per slice and unit
+  constexpr int NH = PT / 16;                         // 16-point halves per unit and sub-tile (phase B items)
+  // phase B passes: the 32-point variant is only taken while its tile fits beside a second CTA's
+  // (Hp ≤ ~800), the 16-point variant covers Hp ≤ 1024
+  constexpr int ITS = PT == 32 ? 7 : 2;
   extern __shared__ __align__(16) double fsm[];
   const FinishArgs& f = a.f;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -92,7 +95,9 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
   const int row16 = Hp / 2;  // 16-byte pieces per row
   double lse_acc = 0.0;
   for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    double cs[4] = {0.0, 0.0, 0.0, 0.0};  // column sums of the units this thread owns (Hp ≤ 1024)
+    double cs[ITS];  // column sums of the items this thread owns
+#pragma unroll
+    for (int it = 0; it < ITS; ++it) cs[it] = 0.0;
     for (int st = 0; st < kFsBlock / PT; ++st) {
       const long long n0 = blk * kFsBlock + st * PT;
       // ---- phase A: this warp's rows r = wib + NW·i
@@ -190,65 +195,67 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
         }
       }
       __syncthreads();
-      // ---- phase B: unit h = threadIdx.x + 256·it
+      // ---- phase B: item t = threadIdx.x + threads·it is (unit h, 16-point half) = (t / NH, t % NH)
       const long long kpt = n0;  // first point of the sub-tile within the chunk
       const long long kb = kpt / 64;
       const int boff = static_cast<int>(kpt % 64);
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int h = threadIdx.x + kFsThreads * it;
+      for (int it = 0; it < ITS; ++it) {
+        const int t = threadIdx.x + kFsThreads * it;
+        const int h = t / NH, g0 = (t % NH) * 4;  // g0: first 4-point group of this half
         if (h >= Hp) break;
         double csum = cs[it];
-        int8_t* o = a.ess + (kb * Hp + h) * 64 + boff;
-        // 16 points (one 16-byte piece per slice) at a time
+        uint32_t w[8][4];
+        if (h < H) {
 #pragma unroll
-        for (int g0 = 0; g0 < G; g0 += 4) {
-          uint32_t w[8][4];
-          if (h < H) {
+          for (int g = 0; g < 4; ++g) {
+            uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              uint32_t hi[4], lo[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int p = 4 * (g0 + g) + e;
-                const double x = tile[p * Hp + h] * rs[p];
-                csum += x;
-                const unsigned long long m = static_cast<unsigned long long>(x * a.inv56);
-                hi[e] = spread7(static_cast<uint32_t>(m >> 28));         // digits 0-3: digit i at byte 3 − i
-                lo[e] = spread7(static_cast<uint32_t>(m) & 0xfffffffu);  // digits 4-7: digit i at byte 7 − i
-              }
-              // 4 × 4 byte transposes: word of slice i = that digit of points 4g … 4g+3
-              const uint32_t h01l = __byte_perm(hi[0], hi[1], 0x5140), h01h = __byte_perm(hi[0], hi[1], 0x7362);
-              const uint32_t h23l = __byte_perm(hi[2], hi[3], 0x5140), h23h = __byte_perm(hi[2], hi[3], 0x7362);
-              w[3][g] = __byte_perm(h01l, h23l, 0x5410);
-              w[2][g] = __byte_perm(h01l, h23l, 0x7632);
-              w[1][g] = __byte_perm(h01h, h23h, 0x5410);
-              w[0][g] = __byte_perm(h01h, h23h, 0x7632);
-              const uint32_t l01l = __byte_perm(lo[0], lo[1], 0x5140), l01h = __byte_perm(lo[0], lo[1], 0x7362);
-              const uint32_t l23l = __byte_perm(lo[2], lo[3], 0x5140), l23h = __byte_perm(lo[2], lo[3], 0x7362);
-              w[7][g] = __byte_perm(l01l, l23l, 0x5410);
-              w[6][g] = __byte_perm(l01l, l23l, 0x7632);
-              w[5][g] = __byte_perm(l01h, l23h, 0x5410);
-              w[4][g] = __byte_perm(l01h, l23h, 0x7632);
+            for (int e = 0; e < 4; ++e) {
+              const int p = 4 * (g0 + g) + e;
+              const double x = tile[p * Hp + h] * rs[p];
+              csum += x;
+              const unsigned long long m = static_cast<unsigned long long>(x * a.inv56);
+              hi[e] = spread7(static_cast<uint32_t>(m >> 28));         // digits 0-3: digit i at byte 3 − i
+              lo[e] = spread7(static_cast<uint32_t>(m) & 0xfffffffu);  // digits 4-7: digit i at byte 7 − i
             }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-              for (int g = 0; g < 4; ++g) w[i][g] = 0u;
+            // 4 × 4 byte transposes: word of slice i = that digit of points 4g … 4g+3
+            const uint32_t h01l = __byte_perm(hi[0], hi[1], 0x5140), h01h = __byte_perm(hi[0], hi[1], 0x7362);
+            const uint32_t h23l = __byte_perm(hi[2], hi[3], 0x5140), h23h = __byte_perm(hi[2], hi[3], 0x7362);
+            w[3][g] = __byte_perm(h01l, h23l, 0x5410);
+            w[2][g] = __byte_perm(h01l, h23l, 0x7632);
+            w[1][g] = __byte_perm(h01h, h23h, 0x5410);
+            w[0][g] = __byte_perm(h01h, h23h, 0x7632);
+            const uint32_t l01l = __byte_perm(lo[0], lo[1], 0x5140), l01h = __byte_perm(lo[0], lo[1], 0x7362);
+            const uint32_t l23l = __byte_perm(lo[2], lo[3], 0x5140), l23h = __byte_perm(lo[2], lo[3], 0x7362);
+            w[7][g] = __byte_perm(l01l, l23l, 0x5410);
+            w[6][g] = __byte_perm(l01l, l23l, 0x7632);
+            w[5][g] = __byte_perm(l01h, l23h, 0x5410);
+            w[4][g] = __byte_perm(l01h, l23h, 0x7632);
           }
+        } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            *reinterpret_cast<uint4*>(o + i * a.slice_stride + 4 * g0) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) w[i][g] = 0u;
         }
+        // (with two halves per unit, neighbouring lanes fill the two 16-byte halves of one 32-byte sector)
+        int8_t* o = a.ess + (kb * Hp + h) * 64 + boff + 4 * g0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<uint4*>(o + i * a.slice_stride) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
         cs[it] = csum;
       }
       __syncthreads();
     }
+    // Σ_n⟨s_nh⟩ of the block: the halves of a unit sit in neighbouring lanes
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int h = threadIdx.x + kFsThreads * it;
-      if (h < H) a.colsum[blk * Hp + h] = cs[it];
+    for (int it = 0; it < ITS; ++it) {
+      const int t = threadIdx.x + kFsThreads * it;
+      double v = cs[it];
+      if (NH == 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const int h = t / NH;
+      if (t % NH == 0 && h < H) a.colsum[blk * Hp + h] = v;
     }
   }
   if (lane == 0) red[wib] = lse_acc;
