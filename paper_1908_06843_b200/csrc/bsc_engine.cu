@@ -1031,9 +1031,13 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     ck(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(chunk_ev_[kMaxChunks]), 0), "wait");
     for (int c = 0; c < nchunks; ++c) {  // all copies queued up front; compute waits per chunk
       const uint64_t off = c * chunk, rows = std::min<uint64_t>(chunk, n - off);
-      ck(cudaMemcpy2DAsync(d_y_ + off * Dp_, (size_t)Dp_ * 8, host_y + off * D_, (size_t)D_ * 8, (size_t)D_ * 8, rows,
-                           cudaMemcpyHostToDevice, cs),
-         "upload Y chunk");
+      if (static_cast<int>(D_) == Dp_)  // unpadded rows: one contiguous copy
+        ck(cudaMemcpyAsync(d_y_ + off * Dp_, host_y + off * D_, rows * D_ * 8, cudaMemcpyHostToDevice, cs),
+           "upload Y chunk");
+      else
+        ck(cudaMemcpy2DAsync(d_y_ + off * Dp_, (size_t)Dp_ * 8, host_y + off * D_, (size_t)D_ * 8, (size_t)D_ * 8, rows,
+                             cudaMemcpyHostToDevice, cs),
+           "upload Y chunk");
       ck(cudaEventRecord(static_cast<cudaEvent_t>(chunk_ev_[c]), cs), "event");
     }
   }

@@ -7,20 +7,25 @@
 // common case; the rest keep the warp-per-point path of bsc_kernels.cuh).
 //
 // Split of the work (one E-step chunk):
-//   front   enumerate_kernel<…, kPassFront>: warp per point — scores, exact
-//           top-H', unary/pairwise terms u, P, singleton weights. A point that
+//   select  select_kernel<H'> (select_kernels.cuh): thread per point — scores,
+//           top-H' with a gap proof, unary/pairwise terms u, P. A point that
 //           passes the guard is *deferred*: its u, e^u, P, e^P and scalars go to
-//           a record tile, its ⟨s⟩ row gets the unnormalised singleton weights.
-//           Anything else is marked for the fallback launch (kPassFallback).
-//   states  lane_states_kernel<γ>: one LANE per deferred point, 32 points per
-//           warp walking the same depth-first state tree in lockstep, so every
-//           index, loop bound and table offset is warp-uniform and all that is
-//           left per state is the arithmetic: q(A∪{z}) = q(A)·e^{u_z}·c(A,z),
+//           a record tile. Anything else (near-ties, terms outside the range
+//           guard) is marked and counted for the fallback launch
+//           (enumerate_kernel<…, kPassFallback>, warp per point, bsc_kernels.cuh).
+//   states  lane_states_fixed_kernel<γ, H', W> for the BASELINE shapes (below),
+//           lane_states_kernel<γ> otherwise: one LANE per deferred point, 32
+//           points per warp walking the same depth-first state tree in lockstep,
+//           so every index, loop bound and table offset is warp-uniform and all
+//           that is left per state is the arithmetic: q(A∪{z}) = q(A)·e^{u_z}·c(A,z),
 //           c(A∪{z},w) = c(A,w)·e^{P_zw}, subtree sums, and the moment updates.
 //           Per-point arrays live in shared memory as [slot][32 lanes] (one
 //           conflict-free 256-byte row per slot).
-//   finish  lane_finish_kernel: warp per point — log Z, the ⟨s⟩ row (scaled
-//           singletons, candidate marginals) and the candidate-pair RED.ADDs.
+//   finish  lane_finish_slice_kernel<PT> (finish_slice_kernels.cuh) on the sliced
+//           path: log Z, the singleton weights of all H units, the candidate
+//           marginals and the candidate pairs of Σ⟨ssᵀ⟩, with the ⟨s⟩ rows cut into
+//           the int8 operand of Yᵀ⟨S⟩ in shared memory; lane_finish_kernel (below)
+//           writes fp64 ⟨s⟩ rows instead (BSC_GEMM=dmma, BSC_FUSED_FINISH=0).
 //
 // Moments by subtree sums (post-order): sub(A) = q(A) + Σ_children sub(child);
 // ⟨s_p⟩ = Σ_{A: max A = p} sub(A), ⟨s_p s_q⟩ = Σ_{A: max A = q, p∈A} sub(A).
