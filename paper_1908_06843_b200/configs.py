@@ -46,6 +46,10 @@ CONFIGS = {
                    sigma2_true=0.25, dict_seed=3),
     "c4": Workload("c4_strong_D576_H1000_N4M", 576, 1000, 14, 5, 4_000_000, 10, 4, "random", pi_true=8 / 1000,
                    sigma2_true=0.25, dict_seed=3, scaling="strong"),
+    # not a BASELINE config: a shape outside the compile-time lane walks ((10,4), (12,4), (14,5)), to time
+    # the run-time-H' state pass (lane_states_kernel<γ>) that every other (H', γ) takes
+    "g1": Workload("g1_random_D128_H200_generic", 128, 200, 8, 3, 200_000, 20, 5, "random", pi_true=4 / 200,
+                   sigma2_true=0.25, dict_seed=5),
 }
 
 

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
       const long long n0 = blk * kFsBlock + st * PT;
       // ---- phase A: this warp's rows r = wib + NW·i
       int mode[RPW];
-      {
+      if (n0 < f.N) {  // (a sub-tile wholly past the chunk only pads the slices: its lane tile does not exist)
         const double* src = f.out + (n0 >> 5) * nf * 32 + (n0 & 31);
         const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(momt));
         for (int idx = threadIdx.x; idx < nf * (PT / 2); idx += kFsThreads) {
@@ -112,7 +112,6 @@ __global__ void __launch_bounds__(fs_threads(PT), PT == 32 ? 2 : 1) lane_finish_
                        : "memory");
         }
       }
-#pragma unroll
       double y2v[RPW];
 #pragma unroll
       for (int i = 0; i < RPW; ++i) {  // (all of this warp's modes and ‖y‖² in flight before the first is used)
