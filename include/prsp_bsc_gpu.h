@@ -145,6 +145,12 @@ int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out);
  * this call synchronises the device and returns PRSP_BSC_GPU_ERR_INTERNAL, naming the buffer in
  * last_error, if a kernel has written into any guard. Without BSC_GUARD it returns OK. */
 int prsp_bsc_gpu_check_guards(void);
+/* BSC_GUARD=2 maps every device buffer so that it ends (to 16 bytes) at the end of its mapping with an
+ * unmapped page behind it: a device load or store past the end of a buffer is an immediate fault
+ * (overruns by reads included, which guard bytes cannot see). This probe reads byte `index` of a
+ * fresh `bytes`-byte buffer on the device; past the end it returns PRSP_BSC_GPU_ERR_INTERNAL and
+ * leaves the CUDA context unusable, so tests call it from a process of their own. */
+int prsp_bsc_gpu_guard_probe(int64_t bytes, int64_t index);
 /* Enumerator cycles per phase (summed over warps) of the last E-step when the
  * process runs with BSC_ENUM_PROFILE=1, else zeros: scores, selection, log-joint
  * terms, state log-joints, exp, MAP, subtree + moment sums, output + loop. */

@@ -55,6 +55,7 @@ SIGNATURES = {
     "prsp_bsc_gpu_timings_ex": [_ptr, _ptr, C.c_int],
     "prsp_bsc_gpu_launches": [_ptr, C.POINTER(_int)],
     "prsp_bsc_gpu_check_guards": [],
+    "prsp_bsc_gpu_guard_probe": [C.c_int64, C.c_int64],
     "prsp_bsc_gpu_enum_phase_cycles": [_ptr, _ptr],
     "prsp_mca_gpu_create": [C.c_char_p, _dbl, _u32, _u32, _u32, _u32, _u64, _int, C.POINTER(_ptr)],
     "prsp_mca_gpu_free": [_ptr],

@@ -150,6 +150,23 @@ BscEngine::BscEngine(int family, uint32_t dim, uint32_t latents, uint32_t hprime
   init(device);
 }
 
+namespace {
+__global__ void guard_probe_kernel(const unsigned char* p, long long i, unsigned char* out) { *out = p[i]; }
+}  // namespace
+
+// Test hook of the guarded allocations: one device read at byte `index` of a fresh `bytes`-byte
+// buffer (past its end under BSC_GUARD=2 that is a device fault, which leaves the context unusable:
+// call it from a process of its own).
+void guard_probe(long long bytes, long long index) {
+  auto* p = util::dalloc<unsigned char>(static_cast<size_t>(bytes), "guard probe");
+  auto* out = util::dalloc<unsigned char>(1, "guard probe out");
+  guard_probe_kernel<<<1, 1>>>(p, index, out);
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) throw Error(kInternal, std::string("guard probe: ") + cudaGetErrorString(e));
+  util::dfree(p);
+  util::dfree(out);
+}
+
 void check_device_guards() {
   const std::string bad = util::check_guards();
   if (!bad.empty()) throw Error(kInternal, "guard: " + bad);

@@ -37,6 +37,7 @@ enum Family : int { kBsc = 0, kTsc = 1, kDsc = 2 };
 // The lane-per-point state pass for (γ, H') (lane_engine.cu).
 // BSC_GUARD=1: throws Error(kInternal) naming the first device buffer with a damaged guard region
 void check_device_guards();
+void guard_probe(long long bytes, long long index);
 const void* lane_fn(int gamma, int hprime);
 int lane_smem(int gamma, int hprime);  // its dynamic shared memory per CTA (bytes)
 int lane_wpc(int gamma, int hprime);   // its warps (32-point tiles) per CTA

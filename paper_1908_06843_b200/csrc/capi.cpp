@@ -381,6 +381,10 @@ int prsp_bsc_gpu_launches(prsp_bsc_gpu* ctx, int* out) {
   });
 }
 
+int prsp_bsc_gpu_guard_probe(int64_t bytes, int64_t index) {
+  return guarded([&] { bscgpu::guard_probe(bytes, index); });
+}
+
 int prsp_bsc_gpu_check_guards(void) {
   return guarded([&] { bscgpu::check_device_guards(); });
 }

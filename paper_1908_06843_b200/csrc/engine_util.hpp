@@ -1,5 +1,6 @@
 // Small host helpers shared by the engine translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -22,30 +23,130 @@ inline void ck(cudaError_t e, const char* what) {
 // Guarded allocations (BSC_GUARD=1; the pool's compute-sanitizer is closed): every device buffer
 // gets 256 bytes of 0xA5 in front and behind, and check_guards() — prsp_bsc_gpu_check_guards in the
 // C ABI — reports the first buffer whose guards a kernel has written. Off by default.
+//
+// BSC_GUARD=2 catches overruns by READS as well: every buffer is mapped through the driver's
+// virtual-memory API so that it ENDS (to 16 bytes) at the end of its mapping, followed by an unmapped
+// page of address space — a load or store past the end of a buffer is an immediate device fault.
 struct GuardRegistry {
   struct Entry {
     size_t bytes;
     std::string what;
   };
+  struct Mapping {
+    CUdeviceptr va;
+    size_t reserved, mapped;
+    CUmemGenericAllocationHandle handle;
+  };
   std::mutex m;
   std::unordered_map<void*, Entry> live;
-  bool on = false;
+  std::unordered_map<void*, Mapping> mappings;
+  bool on = false;   // BSC_GUARD=1: guard bytes
+  bool vmm = false;  // BSC_GUARD=2: end-aligned mappings with an unmapped page behind
 };
 inline GuardRegistry& guard_registry() {
   static GuardRegistry g;
   static const bool init = [] {
     const char* e = std::getenv("BSC_GUARD");
     g.on = e && e[0] == '1';
+    g.vmm = e && e[0] == '2';
     return true;
   }();
   (void)init;
   return g;
+}
+
+// driver entry points of the virtual-memory API (the library links cudart statically, not libcuda)
+struct VmmApi {
+  CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*address_free)(CUdeviceptr, size_t) = nullptr;
+  bool ok = false;
+};
+inline VmmApi& vmm_api() {
+  static VmmApi a = [] {
+    VmmApi v;
+    auto get = [](const char* name) -> void* {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return p;
+    };
+    v.granularity = reinterpret_cast<decltype(v.granularity)>(get("cuMemGetAllocationGranularity"));
+    v.reserve = reinterpret_cast<decltype(v.reserve)>(get("cuMemAddressReserve"));
+    v.create = reinterpret_cast<decltype(v.create)>(get("cuMemCreate"));
+    v.map = reinterpret_cast<decltype(v.map)>(get("cuMemMap"));
+    v.set_access = reinterpret_cast<decltype(v.set_access)>(get("cuMemSetAccess"));
+    v.unmap = reinterpret_cast<decltype(v.unmap)>(get("cuMemUnmap"));
+    v.release = reinterpret_cast<decltype(v.release)>(get("cuMemRelease"));
+    v.address_free = reinterpret_cast<decltype(v.address_free)>(get("cuMemAddressFree"));
+    v.ok = v.granularity && v.reserve && v.create && v.map && v.set_access && v.unmap && v.release && v.address_free;
+    return v;
+  }();
+  return a;
+}
+
+inline void* vmm_alloc(size_t bytes, const char* what) {
+  VmmApi& v = vmm_api();
+  if (!v.ok) throw Error(kInternal, std::string("guard: virtual-memory API unavailable (") + what + ")");
+  auto cu = [&](CUresult r, const char* step) {
+    if (r != CUDA_SUCCESS) throw Error(kInternal, std::string("guard: ") + step + " failed for " + what);
+  };
+  int dev = 0;
+  ck(cudaGetDevice(&dev), what);
+  ck(cudaFree(nullptr), what);  // (a context on this device)
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  size_t gran = 0;
+  cu(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "granularity");
+  const size_t user = (bytes + 15) & ~size_t(15);
+  GuardRegistry::Mapping m{};
+  m.mapped = (user + gran - 1) / gran * gran;
+  m.reserved = m.mapped + gran;  // one granule of unmapped address space behind the mapping
+  cu(v.reserve(&m.va, m.reserved, gran, 0, 0), "address reserve");
+  cu(v.create(&m.handle, m.mapped, &prop, 0), "create");
+  cu(v.map(m.va, m.mapped, 0, m.handle, 0), "map");
+  CUmemAccessDesc acc{};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  cu(v.set_access(m.va, m.mapped, &acc, 1), "set access");
+  void* p = reinterpret_cast<void*>(m.va + m.mapped - user);  // the buffer ends where the mapping ends
+  ck(cudaMemset(reinterpret_cast<void*>(m.va), 0, m.mapped), what);
+  GuardRegistry& g = guard_registry();
+  std::lock_guard<std::mutex> lock(g.m);
+  g.mappings[p] = m;
+  return p;
+}
+inline bool vmm_free(void* p) {
+  GuardRegistry& g = guard_registry();
+  GuardRegistry::Mapping m{};
+  {
+    std::lock_guard<std::mutex> lock(g.m);
+    auto it = g.mappings.find(p);
+    if (it == g.mappings.end()) return false;
+    m = it->second;
+    g.mappings.erase(it);
+  }
+  cudaDeviceSynchronize();
+  VmmApi& v = vmm_api();
+  v.unmap(m.va, m.mapped);
+  v.release(m.handle);
+  v.address_free(m.va, m.reserved);
+  return true;
 }
 constexpr size_t kGuardBytes = 256;
 
 inline void* dalloc_bytes(size_t bytes, const char* what) {
   GuardRegistry& g = guard_registry();
   bytes = std::max<size_t>(bytes, 1);
+  if (g.vmm) return vmm_alloc(bytes, what);
   void* p = nullptr;
   if (!g.on) {
     ck(cudaMalloc(&p, bytes), what);
@@ -99,6 +200,7 @@ struct NvtxRange {
 inline void dfree(void* p) {
   if (!p) return;
   GuardRegistry& g = guard_registry();
+  if (g.vmm && vmm_free(p)) return;
   if (g.on) {
     std::lock_guard<std::mutex> lock(g.m);
     auto it = g.live.find(p);

@@ -80,3 +80,32 @@ def test_no_kernel_writes_outside_its_buffers():
     env = dict(os.environ, BSC_GUARD="1", PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ALL GUARDS INTACT" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
+
+
+PROBE = r"""
+import sys
+from paper_1908_06843_b200 import _native as N
+try:
+    N.call("prsp_bsc_gpu_guard_probe", 1000, int(sys.argv[1]))
+    print("PROBE OK")
+except N.PrspError as e:
+    print("PROBE FAULT", e)
+"""
+
+
+def test_vmm_guard_faults_on_a_read_past_the_end():
+    """BSC_GUARD=2 (buffers end-aligned in their mapping, unmapped page behind): a device read inside a
+    1000-byte buffer succeeds, one 16 bytes past its (16-byte rounded) end faults. The engine runs clean
+    under the same mode in the next test, so that silence means no overrun."""
+    env = dict(os.environ, BSC_GUARD="2", PYTHONPATH=ROOT)
+    ok = subprocess.run([sys.executable, "-c", PROBE, "999"], env=env, capture_output=True, text=True, timeout=300)
+    assert "PROBE OK" in ok.stdout, (ok.stdout, ok.stderr[-2000:])
+    bad = subprocess.run([sys.executable, "-c", PROBE, "1024"], env=env, capture_output=True, text=True, timeout=300)
+    assert "PROBE FAULT" in bad.stdout and "PROBE OK" not in bad.stdout, (bad.stdout, bad.stderr[-2000:])
+
+
+def test_no_kernel_reads_or_writes_past_a_buffer_end():
+    env = dict(os.environ, BSC_GUARD="2", PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.replace('N.call("prsp_bsc_gpu_check_guards")', "pass")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ALL GUARDS INTACT" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
