@@ -27,6 +27,7 @@ inline void ck(cudaError_t e, const char* what) {
 // BSC_GUARD=2 catches overruns by READS as well: every buffer is mapped through the driver's
 // virtual-memory API so that it ENDS (to 16 bytes) at the end of its mapping, followed by an unmapped
 // page of address space — a load or store past the end of a buffer is an immediate device fault.
+// BSC_GUARD=3 is the mirror image for underruns (the buffer starts its mapping, unmapped page in front).
 struct GuardRegistry {
   struct Entry {
     size_t bytes;
@@ -42,13 +43,15 @@ struct GuardRegistry {
   std::unordered_map<void*, Mapping> mappings;
   bool on = false;   // BSC_GUARD=1: guard bytes
   bool vmm = false;  // BSC_GUARD=2: end-aligned mappings with an unmapped page behind
+  bool vmm_front = false;  // BSC_GUARD=3: mappings that START at the buffer, with an unmapped page in front (underruns)
 };
 inline GuardRegistry& guard_registry() {
   static GuardRegistry g;
   static const bool init = [] {
     const char* e = std::getenv("BSC_GUARD");
     g.on = e && e[0] == '1';
-    g.vmm = e && e[0] == '2';
+    g.vmm = e && (e[0] == '2' || e[0] == '3');
+    g.vmm_front = e && e[0] == '3';
     return true;
   }();
   (void)init;
@@ -109,15 +112,19 @@ inline void* vmm_alloc(size_t bytes, const char* what) {
   const size_t user = (bytes + 15) & ~size_t(15);
   GuardRegistry::Mapping m{};
   m.mapped = (user + gran - 1) / gran * gran;
-  m.reserved = m.mapped + gran;  // one granule of unmapped address space behind the mapping
-  cu(v.reserve(&m.va, m.reserved, gran, 0, 0), "address reserve");
+  m.reserved = m.mapped + gran;  // one granule of unmapped address space behind (or in front of) the mapping
+  const bool front = guard_registry().vmm_front;
+  CUdeviceptr base = 0;
+  cu(v.reserve(&base, m.reserved, gran, 0, 0), "address reserve");
+  m.va = front ? base + gran : base;  // (Mapping::va is the mapped range; the reservation starts at va or va − gran)
   cu(v.create(&m.handle, m.mapped, &prop, 0), "create");
   cu(v.map(m.va, m.mapped, 0, m.handle, 0), "map");
   CUmemAccessDesc acc{};
   acc.location = prop.location;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   cu(v.set_access(m.va, m.mapped, &acc, 1), "set access");
-  void* p = reinterpret_cast<void*>(m.va + m.mapped - user);  // the buffer ends where the mapping ends
+  // the buffer ends where the mapping ends (overruns fault), or starts where it starts (underruns fault)
+  void* p = reinterpret_cast<void*>(front ? m.va : m.va + m.mapped - user);
   ck(cudaMemset(reinterpret_cast<void*>(m.va), 0, m.mapped), what);
   GuardRegistry& g = guard_registry();
   std::lock_guard<std::mutex> lock(g.m);
@@ -138,7 +145,7 @@ inline bool vmm_free(void* p) {
   VmmApi& v = vmm_api();
   v.unmap(m.va, m.mapped);
   v.release(m.handle);
-  v.address_free(m.va, m.reserved);
+  v.address_free(guard_registry().vmm_front ? m.va - (m.reserved - m.mapped) : m.va, m.reserved);
   return true;
 }
 constexpr size_t kGuardBytes = 256;

@@ -1,3 +1,3 @@
 set -x
-timeout 1200 python -m pytest tests/test_gpu_guards.py -m gpu -q > gpurun_out/t_guards.log 2>&1; echo rc=$? >> gpurun_out/t_guards.log
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/t_all.log 2>&1; echo rc=$? >> gpurun_out/t_all.log
+CUDA_LAUNCH_BLOCKING=1 BSC_GUARD=3 timeout 2400 python tools/shape_sweep.py > gpurun_out/sweep3.log 2>&1
+BSC_GUARD=3 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/t_guard3.log 2>&1; echo rc=$? >> gpurun_out/t_guard3.log
