@@ -201,7 +201,7 @@ class BscEngine {
   bool prof_on_ = false;
   int weight_mode_ = 0;
   // lane-per-point state pass (lane_kernels.cuh)
-  bool lane_ok_ = false, front_stage_b_ = false;
+  bool lane_ok_ = false;
   int front_ctas_ = 0, front_smem_ = 0, fin_ctas_ = 0, lane_smem_ = 0;
   int fs_ctas_ = 0, fs_pt_ = 32, fs_smem_ = 0;  // finish fused with the ⟨S⟩ᵀ slicer
   bool es_sliced_ = false;                      // the finish pass of this chunk wrote the ⟨S⟩ᵀ slices

@@ -342,8 +342,7 @@ struct EnumArgs {
   // lane path (lane_kernels.cuh): deferred-point records and per-point modes
   double* rec;
   int* pmode;
-  double* pscale;  // front pass: 1 per point (the finish may defer its ⟨s⟩-row scale here)
-  int stage_b;  // front pass: B rows double-buffered in shared memory by cp.async
+  double* pscale;  // optional per-point ⟨s⟩-row scale for the slicer (unused: null)
   double log_pi, dlp, inv2s, base0, inv_T;  // base0 = zero_prior + norm_const
   double eps_dot;                           // 2·(D+2)·2⁻⁵³: |b_fast − b_exact| ≤ eps_dot·‖W_h‖·‖y‖
   double fx_scale;                          // 2^k of the fixed-point Σ⟨ssᵀ⟩ pairs (pair_fx_add)
@@ -494,21 +493,15 @@ __device__ __forceinline__ void top_k(const double (&f)[MAXJ], uint32_t removed,
   }
 }
 
-// Launch roles of enumerate_kernel: the whole per-point pass; the front half
-// of the lane path (selection + terms; points passing the multiplicative range
-// guard are deferred to lane_kernels.cuh, the rest marked for the fallback);
-// the whole pass over the points marked for the fallback only.
-enum : int { kPassFull = 0, kPassFront = 1, kPassFallback = 2 };
+// Launch roles of enumerate_kernel: the whole per-point pass (inference, T ≠ 1, shapes outside the
+// lane path), or the same pass over only the points the lane path's selection pass
+// (select_kernels.cuh) marked for the fallback: near-ties, terms outside the range guard.
+enum : int { kPassFull = 0, kPassFallback = 2 };
 
 // STAGED: the state descriptors and schedule entries are staged in shared
 // memory (compile-time, so every table access is an LDS, not a generic load)
-#ifndef ENUM_FRONT_MINB
-// front pass CTAs per SM: 3 (80 registers) and 4 (64) were measured slower than 2 (c2 front
-// 0.95 -> 1.00 / 1.17 ms): the pass is issue-bound, not latency-bound
-#define ENUM_FRONT_MINB 2
-#endif
 template <int MAXJ, bool STAGED, int PASS = kPassFull>
-__global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2) enumerate_kernel(EnumArgs a) {
+__global__ void __launch_bounds__(256, 2) enumerate_kernel(EnumArgs a) {
   extern __shared__ __align__(16) double esm[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -519,8 +512,7 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
     // error flag per E-step): none, the common case, and the CTA is gone before it stages a table
     if (a.err[1] == 0) return;
   }
-  const EnumSmem L = PASS == kPassFront ? EnumSmem::make(a.hprime, 0, 0, 0, 0, a.H)
-                                         : EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
+  const EnumSmem L = EnumSmem::make(a.hprime, a.n_tab, a.n_coup, a.n_slots, a.n_out, a.H);
   // The state descriptors and schedule entries are the same for every point:
   // staged once per CTA in shared memory when they fit (else read from L1/L2).
   const uint2* sdesc = a.sdesc;
@@ -538,18 +530,8 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
     sdesc = reinterpret_cast<const uint2*>(cta);
     sent = reinterpret_cast<const uint32_t*>(cta + a.stage_desc_bytes);
   }
-  // front pass: diag(G) staged per CTA, and per warp two B-row buffers (when they fit)
   const double* gdiag = a.gdiag;
-  int gstage = 0, wstride = L.total;
-  if constexpr (PASS == kPassFront) {
-    gstage = (a.H + 1) & ~1;
-    for (int i = threadIdx.x; i < a.H; i += blockDim.x) esm[i] = a.gdiag[i];
-    __syncthreads();
-    gdiag = esm;
-    if (MAXJ <= 16 && a.stage_b) wstride += 2 * a.Hp;
-  }
-  double* sm = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + stage_bytes) + gstage + (long long)wib * wstride;
-  double* bbuf = sm + L.total;  // front pass with stage_b: [2][Hp]
+  double* sm = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + stage_bytes) + (long long)wib * L.total;
   double* su = sm + L.u;
   double* sP = sm + L.P;
   double* tab = sm + L.tab;
@@ -576,36 +558,15 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
     t_last = t_;                                                                        \
   }
 
-  // (compiled in for the register budget of MAXJ ≤ 16 only)
-  const bool stage_b = PASS == kPassFront && MAXJ <= 16 && a.stage_b;
-  if (stage_b && gwarp < a.N) {
-    cp_async_row(bbuf, a.B + (long long)gwarp * a.Hp, a.Hp / 2, lane);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
   int it = 0;
   for (int n = gwarp; n < a.N; n += nwarps, ++it) {
     if constexpr (PASS == kPassFallback) {
       if (a.pmode[n] != kModeFallback) continue;
     }
-    if constexpr (PASS == kPassFront) {
-      if (lane == 0) {
-        a.pmode[n] = kModeDone;  // stays so on an error (flagged in *err)
-        if (a.pscale) a.pscale[n] = 1.0;
-      }
-    }
     ENUM_PHASE(7);
     const double* y = a.Y + (long long)n * a.Dp;
     const double* brow = a.B + (long long)n * a.Hp;
-    if (stage_b) {
-      // the next point's row lands in the other buffer while this one is used
-      __syncwarp();
-      const long long nn = n + nwarps;
-      if (nn < a.N) cp_async_row(bbuf + ((it + 1) & 1) * a.Hp, a.B + nn * a.Hp, a.Hp / 2, lane);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-      __syncwarp();
-      brow = bbuf + (it & 1) * a.Hp;
-    } else {  // pull the B row two points ahead into L2 while this point is processed
+    {  // pull the B row two points ahead into L2 while this point is processed
       const long long nn = n + 2LL * nwarps;
       if (nn < a.N)
         for (int l = lane; l < row_lines; l += 32)
@@ -732,8 +693,8 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
       const int p = pair_row(e, HP), q = e - p * (2 * HP - p - 1) / 2 + p + 1;
       sP[e] = -2.0 * a.inv2s * a.G[(long long)scand[p] * a.Hp + scand[q]];
     }
-    // zero slot (the selection pool overlays the table); the front pass has no table
-    if (PASS != kPassFront && lane == 0) tab[a.n_tab] = 0.0;
+    // zero slot (the selection pool overlays the table)
+    if (lane == 0) tab[a.n_tab] = 0.0;
 
     ENUM_PHASE(2);
     // singletons over all H units and the zero state (rel = 0)
@@ -791,49 +752,13 @@ __global__ void __launch_bounds__(256, PASS == kPassFront ? ENUM_FRONT_MINB : 2)
     double* esrow = a.ES + (long long)n * a.Hp;
     double zs1 = lane == 0 ? exp_nonpos(-mxs) : 0.0;
     double zsT = lane == 0 && !t1 ? exp_nonpos(-mxs * a.inv_T) : 0.0;
-    const bool defer = PASS == kPassFront && mult_ok;
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const double x = rel1[j] - mxs;  // −inf beyond H: exp_nonpos gives 0
-      double e;
-      if (PASS == kPassFront && MAXJ <= 16 && x < -32.0)
-        e = small_exp(x);  // below e^-32 of the largest term: invisible in the fp64 sums
-      else
-        e = exp_nonpos(x);
-      zs1 += e;
+      zs1 += exp_nonpos(x);
       if (!t1) zsT += exp_nonpos(x * a.inv_T);
-      // deferred points: the unnormalised singleton weights (lane_finish_kernel scales them)
-      if (PASS == kPassFront && defer && lane + 32 * j < H) esrow[lane + 32 * j] = e;
     }
     if (t1) zsT = zs1;
-    if constexpr (PASS == kPassFront) {
-      if (defer) {
-        // record of the point for lane_states_kernel (layout: lane_kernels.cuh)
-        const int np = HP * (HP - 1) / 2;
-        double* rt = a.rec + (long long)(n >> 5) * lane_rec_fields(HP) * 32 + (n & 31);
-        zs1 = warp_sum(zs1);
-        if (lane == 0) {
-          rt[0] = fmax(mxs, ub);
-          rt[32] = zs1;
-          rt[64] = mxs;
-        }
-        for (int p = lane; p < HP; p += 32) {
-          const double u = su[p];
-          rt[(4 + p) * 32] = u;
-          rt[(4 + HP + p) * 32] = exp_nonpos(u);  // |u| ≤ 300: exact range of exp_nonpos
-        }
-        for (int e = lane; e < np; e += 32) {
-          const double v = sP[e];
-          rt[(4 + 2 * HP + e) * 32] = v;
-          rt[(4 + 2 * HP + np + e) * 32] = exp_nonpos(v);
-        }
-      }
-      if (lane == 0) {
-        a.pmode[n] = defer ? (skip_rel ? kModeShift : kModeMax) : kModeFallback;
-        y2_acc += y2;
-      }
-      continue;
-    }
     char* smb = reinterpret_cast<char*>(sm);
     const uint32_t zero_w = static_cast<uint32_t>(L.tab + a.n_tab);  // the zero slot, / 8
 

@@ -1,3 +1,4 @@
 set -x
-CUDA_LAUNCH_BLOCKING=1 BSC_GUARD=3 timeout 2400 python tools/shape_sweep.py > gpurun_out/sweep3.log 2>&1
-BSC_GUARD=3 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/t_guard3.log 2>&1; echo rc=$? >> gpurun_out/t_guard3.log
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/t_all.log 2>&1; echo rc=$? >> gpurun_out/t_all.log
+timeout 300 python bench.py --no-cpu-baseline --e2e-steps 0 > gpurun_out/k_c2.log 2>&1
+timeout 300 python bench.py --no-cpu-baseline --e2e-steps 0 --config c1 > gpurun_out/k_c1.log 2>&1
