@@ -236,6 +236,14 @@ void BscEngine::init(int device) {
   cudaStream_t cs;
   ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
   copy_stream_ = cs;
+  ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "side stream");
+  side_stream_ = cs;
+  for (void** e : {&ev_fork_, &ev_join_}) {
+    cudaEvent_t ev;
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    *e = ev;
+  }
+  if (const char* v = std::getenv("BSC_MSTEP_OVERLAP")) overlap_enabled_ = std::atoi(v) != 0;
   for (auto& e : chunk_ev_) {
     cudaEvent_t ev;
     ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
@@ -263,7 +271,11 @@ BscEngine::~BscEngine() {
     if (p) cudaFreeHost(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
-  if (mstep_exec_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(mstep_exec_));
+  for (GraphPart* g : {&factor_part_, &update_part_})
+    if (g->exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g->exec));
+  for (void* e : {ev_fork_, ev_join_})
+    if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  if (side_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(side_stream_));
   for (auto& e : chunk_ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (copy_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(copy_stream_));
@@ -734,7 +746,14 @@ double BscEngine::step_streamed(const double* y_host, uint64_t n, double tempera
     ck(cudaMemsetAsync(d_y_ + n * Dp_, 0, (cap_n_ - n) * Dp_ * sizeof(double), static_cast<cudaStream_t>(stream_)),
        "clear Y");
   n_ = n;
-  estep_chunked(temperature, false, y_host, chunk);
+  overlap_factor_ = overlap_enabled_;
+  try {
+    estep_chunked(temperature, false, y_host, chunk);
+  } catch (...) {
+    overlap_factor_ = false;
+    throw;
+  }
+  overlap_factor_ = false;
   mstep();
   return last_F_;
 }
@@ -1006,6 +1025,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     vpart_chunks_ = nchunks;
   }
   launches_ = 0;
+  factored_ = false;
   NvtxRange nv_estep("bsc.estep");
   ev(0);
   if (!gram_fresh_) {
@@ -1105,6 +1125,7 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
         ++launches_;
       }
       es_sliced_ = false;
+      if (c == nchunks - 1 && overlap_factor_ && !vpath()) fork_factor(nchunks, n);
       oz::Args g{};
       g.sa = d_ytsa_ + (size_t)((host_y || nchunks > 1) ? c : 0) * Dp_;
       g.sb = d_two_;
@@ -1142,28 +1163,27 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
   if (oz_) yts_whole_ = nchunks == 1;
   NvtxRange nv_fin("bsc.finalize_stats");
   const long long DH = (long long)D_ * H_;
-  if (oz_)
-  {
+  if (oz_)  // Σ⟨s⟩ and the Σ⟨ssᵀ⟩ diagonal come from the slicer's column sums (finalize_moments)
     reduce_ysT_kernel<<<(DH + 255) / 256, 256, 0, s>>>(d_ozpart_, d_ozcs_, oz_splits0, 0, part_stride_, D_, H_, Hp_,
                                                         d_stats_, lay_.off_s(), lay_.off_ssT());
-    oz::oz_colsum_reduce_kernel<<<(H_ + 7) / 8, 256, 0, s>>>(d_ozcs_, static_cast<int>((n + 127) / 128), Hp_,
-                                                             static_cast<int>(H_), d_stats_ + lay_.off_s(),
-                                                             d_stats_ + lay_.off_ssT(), static_cast<int>(H_));
-    ++launches_;
-  }
   else
     reduce_ysT_kernel<<<(DH + H_ + 255) / 256, 256, 0, s>>>(d_part_, d_warp_es_, splits_, nchunks * splits_,
                                                              part_stride_, D_, H_, Hp_, d_stats_, lay_.off_s(),
                                                              vpath() ? -1 : lay_.off_ssT());
+  ++launches_;
   if (vpath()) {
     finalize_v(nchunks * enum_ctas_, n);
-    launches_ += 2;
+    ++launches_;
+  } else if (factored_) {  // the side stream has finalised the moments and factored Σ⟨ssᵀ⟩
+    ck(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_join_), 0), "join wait");
+  } else if (oz_) {
+    finalize_moments(s, nchunks, n);
   } else {
     finalize_stats_kernel<<<std::max(1u, std::min(1024u, (H_ * H_ + 255) / 256)), 256, 0, s>>>(
         3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail(),
         1.0 / fx_scale_);
     counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
-    launches_ += 3;
+    launches_ += 2;
   }
   ck(cudaGetLastError(), "finalize");
   ev(5);
@@ -1178,46 +1198,79 @@ void BscEngine::check_err() {
   if (err & kErrNonFiniteLogJoint) throw Error(kNumeric, "log_sum_exp: empty support");
 }
 
-// The M-step is a fixed sequence of ~40 small launches for a given (D, H):
-// it runs eagerly once, is then captured into a CUDA graph and replayed.
-void BscEngine::mstep() {
-  NvtxRange nv("bsc.mstep");
-  ck(cudaSetDevice(device_), "set device");
-  auto s = static_cast<cudaStream_t>(stream_);
-  auto* sc = static_cast<MstepScalars*>(d_msc_);
-  if (mstep_exec_) {
-    ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(mstep_exec_), s), "mstep graph");
-    launches_ += mstep_nodes_;
-  } else if (mstep_calls_++ == 0) {
+// The M-step is a fixed sequence of ~40 small launches for a given (D, H), in two
+// parts: each runs eagerly once, is then captured into a CUDA graph and replayed.
+void BscEngine::run_part(GraphPart& part, void (BscEngine::*enqueue)(void*), void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  if (!part.exec) {
     const int before = launches_;
-    enqueue_mstep(s);
-    mstep_nodes_ = launches_ - before;
-  } else {
+    if (part.calls++ == 0) {
+      (this->*enqueue)(s);
+      part.nodes = launches_ - before;
+      return;
+    }
     cudaStream_t cap;
     ck(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
     ck(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
-    const int before = launches_;
-    enqueue_mstep(cap);
+    (this->*enqueue)(cap);
     cudaGraph_t graph;
     ck(cudaStreamEndCapture(cap, &graph), "end capture");
     cudaGraphExec_t exec;
     ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
     cudaGraphDestroy(graph);
     cudaStreamDestroy(cap);
-    mstep_exec_ = exec;
-    mstep_nodes_ = launches_ - before;
+    part.exec = exec;
+    part.nodes = launches_ - before;
     launches_ = before;
-    ck(cudaGraphLaunch(exec, s), "mstep graph");
-    launches_ += mstep_nodes_;
   }
+  ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(part.exec), s), "mstep graph");
+  launches_ += part.nodes;
+}
+
+void BscEngine::mstep() {
+  NvtxRange nv("bsc.mstep");
+  ck(cudaSetDevice(device_), "set device");
+  if (!factored_) run_part(factor_part_, &BscEngine::enqueue_factor, stream_);
+  factored_ = false;
+  run_part(update_part_, &BscEngine::enqueue_update, stream_);
   finish_mstep();
 }
 
-void BscEngine::enqueue_mstep(void* stream) {
+// Inside a step(), before the last chunk's Yᵀ⟨S⟩ product: every moment sum the factor needs
+// is complete (pair sums, ⟨S⟩ column sums, per-CTA scalars), so the statistics' Σ⟨s⟩ / Σ⟨ssᵀ⟩ /
+// scalar entries are finalised and Σ⟨ssᵀ⟩ + ridge·I factored on the side stream while the
+// product runs. The same kernels in the same order as the serial path: identical bits.
+void BscEngine::fork_factor(int nchunks, uint64_t n) {
+  auto s = static_cast<cudaStream_t>(stream_);
+  auto side = static_cast<cudaStream_t>(side_stream_);
+  ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_fork_), s), "fork");
+  ck(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(ev_fork_), 0), "fork wait");
+  finalize_moments(side, nchunks, n);
+  run_part(factor_part_, &BscEngine::enqueue_factor, side);
+  ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_join_), side), "join");
+  factored_ = true;
+}
+
+// Σ⟨s⟩ and the Σ⟨ssᵀ⟩ diagonal from the ⟨S⟩ column sums, the off-diagonals from the
+// fixed-point pair sums, the scalars (BSC on the tensor-core product path).
+void BscEngine::finalize_moments(void* stream, int nchunks, uint64_t n) {
+  auto s = static_cast<cudaStream_t>(stream);
+  oz::oz_colsum_reduce_kernel<<<(H_ + 7) / 8, 256, 0, s>>>(d_ozcs_, static_cast<int>((n + 127) / 128), Hp_,
+                                                           static_cast<int>(H_), d_stats_ + lay_.off_s(),
+                                                           d_stats_ + lay_.off_ssT(), static_cast<int>(H_));
+  finalize_stats_kernel<<<std::max(1u, std::min(1024u, (H_ * H_ + 255) / 256)), 256, 0, s>>>(
+      3 * nchunks * sc_ctas_, d_warp_sc_, H_, static_cast<long long>(n), d_stats_, lay_.off_ssT(), lay_.off_tail(),
+      1.0 / fx_scale_);
+  counts_kernel<<<1, 32, 0, s>>>(d_stats_, lay_.off_s(), H_, lay_.off_tail());
+  ck(cudaGetLastError(), "finalize");
+  launches_ += 3;
+}
+
+void BscEngine::enqueue_factor(void* stream) {
   auto s = static_cast<cudaStream_t>(stream);
   auto* sc = static_cast<MstepScalars*>(d_msc_);
   const int H = static_cast<int>(H_), D = static_cast<int>(D_);
-  mstep_prepare_kernel<<<64, 256, 0, s>>>(d_stats_, lay_.off_ssT(), D, H, Hp_, d_bm_, d_x_, Hp_, sc);
+  mstep_prepare_kernel<<<64, 256, 0, s>>>(d_stats_, lay_.off_ssT(), D, H, Hp_, d_bm_, d_x_, Hp_, sc, kPrepareFactor);
   ck(cudaGetLastError(), "mstep prepare");
   ++launches_;
   // blocked right-looking Cholesky, lower: L overwrites Bm
@@ -1234,10 +1287,20 @@ void BscEngine::enqueue_mstep(void* stream) {
       launches_ += 2;
     }
   }
+  // U = Lᵀ for the forward solve
+  transpose_lower_kernel<<<dim3((H + 31) / 32, (Hp_ + 31) / 32), dim3(32, 8), 0, s>>>(d_bm_, Hp_, H, d_u_);
   ck(cudaGetLastError(), "cholesky");
+  ++launches_;
+}
+
+void BscEngine::enqueue_update(void* stream) {
+  auto s = static_cast<cudaStream_t>(stream);
+  auto* sc = static_cast<MstepScalars*>(d_msc_);
+  const int H = static_cast<int>(H_), D = static_cast<int>(D_);
+  mstep_prepare_kernel<<<64, 256, 0, s>>>(d_stats_, lay_.off_ssT(), D, H, Hp_, d_bm_, d_x_, Hp_, sc, kPrepareRhs);
+  ++launches_;
   // X·L·Lᵀ = Σy⟨s⟩ᵀ: forward (Z·Lᵀ = R, against U = Lᵀ) then backward (X·L = Z),
   // one warp per row of X over the full width
-  transpose_lower_kernel<<<dim3((H + 31) / 32, (Hp_ + 31) / 32), dim3(32, 8), 0, s>>>(d_bm_, Hp_, H, d_u_);
   {
     // 4 rows per CTA; pivot rows staged in blocks of rb (double-buffered)
     const unsigned blocks = static_cast<unsigned>((D + 3) / 4);
@@ -1251,7 +1314,7 @@ void BscEngine::enqueue_mstep(void* stream) {
       fn<<<blocks, 128, smem, s>>>(fwd ? d_u_ : d_bm_, Hp_, H, d_x_, Hp_, D, rb);
     }
   }
-  launches_ += 3;
+  launches_ += 2;
   ck(cudaGetLastError(), "solve");
   commit_w_kernel<<<64, 256, 0, s>>>(d_x_, Hp_, d_w_, Hp_, D, H, sc);
   // Gram of W' (the next E-step's G; exact diagonal) also feeds t3
@@ -1335,7 +1398,14 @@ void BscEngine::finish_mstep() {
 }
 
 double BscEngine::step(double temperature) {
-  estep(temperature);
+  overlap_factor_ = overlap_enabled_;
+  try {
+    estep(temperature);
+  } catch (...) {
+    overlap_factor_ = false;
+    throw;
+  }
+  overlap_factor_ = false;
   mstep();
   return last_F_;
 }

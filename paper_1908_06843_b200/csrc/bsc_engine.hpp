@@ -133,7 +133,17 @@ class BscEngine {
   void launch_enumerate(double temperature, bool cands, bool infer, uint64_t off, uint64_t rows, int chunk);
   void estep_chunked(double temperature, bool want_candidates, const double* host_y, uint64_t chunk);
   void check_err();
-  void enqueue_mstep(void* stream);
+  // The M-step in two graph-captured parts: the factor (Bm, Cholesky, Lᵀ) needs only the
+  // E-step's moment sums; the update (right-hand side, solves, W', Gram, σ²/π) needs Yᵀ⟨S⟩.
+  struct GraphPart {
+    void* exec = nullptr;  // cudaGraphExec_t
+    int calls = 0, nodes = 0;
+  };
+  void run_part(GraphPart& part, void (BscEngine::*enqueue)(void*), void* stream);
+  void enqueue_factor(void* stream);
+  void enqueue_update(void* stream);
+  void fork_factor(int nchunks, uint64_t n);
+  void finalize_moments(void* stream, int nchunks, uint64_t n);
   void enqueue_gram(void* stream);
   void finish_mstep();
 
@@ -188,8 +198,14 @@ class BscEngine {
   void* d_msc_ = nullptr;
   void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // pinned
   double last_F_ = 0.0;
-  void* mstep_exec_ = nullptr;  // cudaGraphExec_t of the captured M-step
-  int mstep_calls_ = 0, mstep_nodes_ = 0;
+  GraphPart factor_part_, update_part_;
+  // step(): the factor runs on a side stream beside the Yᵀ⟨S⟩ product, which leaves SMs idle
+  // (its grid is a multiple of the output tiles: 144 of 148 CTAs at c2, 120 at c3)
+  void* side_stream_ = nullptr;
+  void *ev_fork_ = nullptr, *ev_join_ = nullptr;
+  bool overlap_enabled_ = true;  // BSC_MSTEP_OVERLAP=0 turns it off
+  bool overlap_factor_ = false;  // this E-step belongs to a step(): fork the factor
+  bool factored_ = false;        // the factor of the current statistics is in Bm / U
 
   int enum_ctas_ = 0, enum_warps_total_ = 0, enum_block_ = 256, enum_smem_ = 0;
   // host-streamed E-step: copy stream + per-chunk events

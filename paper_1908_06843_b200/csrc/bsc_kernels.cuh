@@ -1074,7 +1074,7 @@ static __global__ void reduce_ysT_kernel(const double* __restrict__ part, const 
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += part[z * split_stride + (long long)d * ldp + h];
     stats[idx] = s;
-  } else if (idx < DH + H) {
+  } else if (idx < DH + H && colsum_rows > 0) {  // (0: the column sums are reduced elsewhere)
     const int h = static_cast<int>(idx - DH);
     double s = 0.0;
     for (int z = 0; z < colsum_rows; ++z) s += colsum[(long long)z * ldp + h];

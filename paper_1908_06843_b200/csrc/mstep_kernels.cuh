@@ -22,9 +22,21 @@ struct MstepScalars {
 };
 
 // Bm = Σ⟨ssᵀ⟩ + ridge·I with ridge = 1e-9·trace/H (:349-353); Xr = Σ y⟨s⟩ᵀ.
+// Two launches (`parts`): the factor's input, which needs only the E-step's
+// moment sums, and the right-hand side, which needs the Yᵀ⟨S⟩ product.
+constexpr int kPrepareFactor = 1, kPrepareRhs = 2;
 __global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long off_ssT, int D, int H,
                                      int ldb, double* __restrict__ Bm, double* __restrict__ X, int ldx,
-                                     MstepScalars* sc) {
+                                     MstepScalars* sc, int parts) {
+  if (parts & kPrepareRhs) {
+    const long long DH = (long long)D * H;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < DH;
+         e += (long long)gridDim.x * blockDim.x) {
+      const int d = static_cast<int>(e / H), h = static_cast<int>(e % H);
+      X[(long long)d * ldx + h] = stats[e];
+    }
+  }
+  if (!(parts & kPrepareFactor)) return;
   __shared__ double tr;
   if (threadIdx.x < 32) {
     double acc = 0.0;
@@ -47,11 +59,6 @@ __global__ void mstep_prepare_kernel(const double* __restrict__ stats, long long
     double v = stats[off_ssT + e];
     if (i == j) v += ridge;
     Bm[(long long)i * ldb + j] = v;
-  }
-  const long long DH = (long long)D * H;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < DH; e += (long long)gridDim.x * blockDim.x) {
-    const int d = static_cast<int>(e / H), h = static_cast<int>(e % H);
-    X[(long long)d * ldx + h] = stats[e];
   }
 }
 

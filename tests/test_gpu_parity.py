@@ -411,6 +411,40 @@ def test_fused_finish_slice_matches_unfused(pkg, port, monkeypatch, d, h, hp, g,
     assert abs(r0.free_energy - r1.free_energy) <= 1e-13 * abs(r1.free_energy)
 
 
+@pytest.mark.parametrize("d,h,hp,g,n", [(256, 300, 12, 4, 20011), (100, 20, 10, 4, 1300), (64, 40, 8, 3, 257)])
+def test_factor_overlap_is_bitwise_the_serial_mstep(pkg, port, monkeypatch, d, h, hp, g, n):
+    """step() finalises the moment sums and factors Σ⟨ssᵀ⟩ + ridge·I on a side
+    stream while the Yᵀ⟨S⟩ product runs (BscEngine::fork_factor); estep_stats +
+    mstep, and BSC_MSTEP_OVERLAP=0, run the same launches on one stream. Same
+    kernels, same order per buffer: W′, π′, σ²′ and F are identical bits over a
+    few iterations, and the chunked host-data step (the fork sits before its
+    last chunk's product) lands on the same parameters within rounding."""
+    wt = port.random_dictionary(d, h, 61, 5.0)
+    y = port.generate(wt, min(0.5, 4.0 / h), 0.25, n, 62)
+    p0 = pkg.BscParams(wt + 0.05 * np.cos(np.arange(d * h)).reshape(d, h), 1.0 / h, 0.4)
+    runs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BSC_MSTEP_OVERLAP", mode)
+        m = model_for(pkg, d, h, hp, g)
+        m.load(y)
+        p, traj = p0, []
+        for _ in range(4):
+            r = m.step(p)
+            p = r.params
+            traj.append((p.W.copy(), p.pi, p.sigma2, r.free_energy))
+        runs[mode] = traj
+        if mode == "1":  # the two-call path never forks
+            m.estep_stats(p0)
+            r2 = m.mstep(None, p0)
+            assert np.array_equal(r2.W, traj[0][0]) and r2.pi == traj[0][1] and r2.sigma2 == traj[0][2]
+            rh = m.step_host(p0, y)
+            assert rel(rh.params.W, traj[0][0]) < 1e-9 and abs(rh.free_energy - traj[0][3]) <= 1e-12 * abs(traj[0][3])
+        m.close()
+    for a, b in zip(runs["1"], runs["0"]):
+        assert np.array_equal(a[0], b[0])
+        assert a[1:] == b[1:]
+
+
 def test_dead_dictionary_element(pkg, port):
     """A unit no data point ever selects (its column points away from all the
     data): its statistics are made of singleton weights ~e^-100 and smaller. The
