@@ -238,7 +238,7 @@ void BscEngine::init(int device) {
   copy_stream_ = cs;
   ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "side stream");
   side_stream_ = cs;
-  for (void** e : {&ev_fork_, &ev_join_}) {
+  for (void** e : {&ev_fork_, &ev_join_, &ev_branch_[0], &ev_branch_[1]}) {
     cudaEvent_t ev;
     ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     *e = ev;
@@ -273,7 +273,7 @@ BscEngine::~BscEngine() {
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (GraphPart* g : {&factor_part_, &update_part_})
     if (g->exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g->exec));
-  for (void* e : {ev_fork_, ev_join_})
+  for (void* e : {ev_fork_, ev_join_, ev_branch_[0], ev_branch_[1]})
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   if (side_stream_) cudaStreamDestroy(static_cast<cudaStream_t>(side_stream_));
   for (auto& e : chunk_ev_)
@@ -813,7 +813,7 @@ void BscEngine::refresh_gram() {
 
 // G = WᵀW on the DMMA GEMM, then the diagonal (selection scores) recomputed in
 // the oracle's left-to-right order.
-void BscEngine::enqueue_gram(void* stream) {
+void BscEngine::enqueue_gram(void* stream, bool with_slices) {
   auto s = static_cast<cudaStream_t>(stream);
   const int H = static_cast<int>(H_);
   GemmArgs g{H, H, Dp_, d_w_, Hp_, d_w_, Hp_, d_g_, Hp_, 1.0, 0.0, Dp_, 0};
@@ -821,7 +821,7 @@ void BscEngine::enqueue_gram(void* stream) {
   gram_diag_exact_kernel<<<(H_ + 31) / 32, 32, 0, s>>>(d_w_, D_, H_, Hp_, d_g_, Hp_, d_wnorm_, d_gdiag_);
   ck(cudaGetLastError(), "gram");
   launches_ += 2;
-  if (oz_) slice_w(stream);
+  if (oz_ && with_slices) slice_w(stream);
 }
 
 // The fields both enumerators share (EnumArgs, bsc_kernels.cuh): shapes, the
@@ -1317,12 +1317,22 @@ void BscEngine::enqueue_update(void* stream) {
   launches_ += 2;
   ck(cudaGetLastError(), "solve");
   commit_w_kernel<<<64, 256, 0, s>>>(d_x_, Hp_, d_w_, Hp_, D, H, sc);
-  // Gram of W' (the next E-step's G; exact diagonal) also feeds t3
-  enqueue_gram(s);
+  // two branches from W': the next E-step's int8 operand slices on the side stream, and the
+  // Gram (the next E-step's G; exact diagonal) that also feeds t3, σ² and π here
+  auto side = static_cast<cudaStream_t>(side_stream_);
+  const bool branch = oz_ && overlap_enabled_ && s != side;
+  if (branch) {
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_branch_[0]), s), "branch");
+    ck(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(ev_branch_[0]), 0), "branch wait");
+    slice_w(side);
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_branch_[1]), side), "branch join");
+  }
+  enqueue_gram(s, !branch);
   mstep_traces_kernel<<<kTraceCtas, 256, 0, s>>>(d_w_, Hp_, d_g_, Hp_, d_stats_, lay_.off_ssT(), D, H,
                                                   d_trace_part_);
   mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, static_cast<int>(values_.size()),
                                        d_trace_part_, sc);
+  if (branch) ck(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_branch_[1]), 0), "branch join wait");
   ck(cudaGetLastError(), "mstep scalars");
   launches_ += 3;
 }

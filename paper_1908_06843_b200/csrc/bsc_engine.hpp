@@ -144,7 +144,7 @@ class BscEngine {
   void enqueue_update(void* stream);
   void fork_factor(int nchunks, uint64_t n);
   void finalize_moments(void* stream, int nchunks, uint64_t n);
-  void enqueue_gram(void* stream);
+  void enqueue_gram(void* stream, bool with_slices = true);
   void finish_mstep();
 
   int family_ = kBsc;
@@ -202,7 +202,7 @@ class BscEngine {
   // step(): the factor runs on a side stream beside the Yᵀ⟨S⟩ product, which leaves SMs idle
   // (its grid is a multiple of the output tiles: 144 of 148 CTAs at c2, 120 at c3)
   void* side_stream_ = nullptr;
-  void *ev_fork_ = nullptr, *ev_join_ = nullptr;
+  void *ev_fork_ = nullptr, *ev_join_ = nullptr, *ev_branch_[2] = {};
   bool overlap_enabled_ = true;  // BSC_MSTEP_OVERLAP=0 turns it off
   bool overlap_factor_ = false;  // this E-step belongs to a step(): fork the factor
   bool factored_ = false;        // the factor of the current statistics is in Bm / U

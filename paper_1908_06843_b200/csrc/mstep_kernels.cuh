@@ -3,6 +3,7 @@
 // updates on the DMMA GEMM), and the σ²/π updates.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "dgemm.cuh"
@@ -177,6 +178,14 @@ __global__ void transpose_lower_kernel(const double* __restrict__ Bm, int ldb, i
 // order by every warp of the CTA: blocks of `rb` rows are staged in shared
 // memory with cp.async, double-buffered, so each step reads the pivot row at
 // shared-memory latency. Shared layout: rinv[n (padded)] | buf[2][rb·ldt].
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {  // f(integral_constant<I>) … f(<N-1>), unrolled by construction
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
 template <int S, bool FWD>
 __global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restrict__ T, int ldt, int n,
                                                          double* __restrict__ X, int ldx, int nrows, int rb) {
@@ -224,37 +233,62 @@ __global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restric
     blk_end = FWD ? cur_r0 + rb : cur_r0 - 1;
     ++blk;
   };
+  // Columns are taken in segments (the run of one 32-column slot inside the staged row
+  // block): first the dependent chain alone — pivot, broadcast, the update of the slot's own
+  // remaining lanes — then the segment's updates of every other slot, which nothing in the
+  // segment waits on. Each entry still receives its column updates in ascending (descending)
+  // column order, so the result is the bits of the column-at-a-time loop.
   if (FWD) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
+    static_for<0, S>([&](auto si) {
+      constexpr int s = decltype(si)::value;
       const int cend = n - 32 * s < 32 ? n - 32 * s : 32;
-      for (int cc = 0; cc < cend; ++cc) {
-        const int c = 32 * s + cc;
-        if (c >= blk_end) advance(c);
-        const double* tr = cur + (size_t)(c - cur_r0) * ldt;
-        if (lane == cc) x[s] *= rinv[c];
-        const double xc = __shfl_sync(0xffffffffu, x[s], cc);
-        if (lane > cc && lane < cend) x[s] -= xc * tr[lane + 32 * s];
+      int cc = 0;
+      while (cc < cend) {
+        if (32 * s + cc >= blk_end) advance(32 * s + cc);
+        const int seg_end = blk_end - 32 * s < cend ? blk_end - 32 * s : cend;
+        const double* tb = cur + ((ptrdiff_t)32 * s - cur_r0) * ldt;  // row of column 32·s
+        for (int q = cc; q < seg_end; ++q) {
+          const double* tr = tb + (ptrdiff_t)q * ldt;
+          if (lane == q) x[s] *= rinv[32 * s + q];
+          const double xc = __shfl_sync(0xffffffffu, x[s], q);
+          if (lane > q && lane < cend) x[s] -= xc * tr[lane + 32 * s];
+        }
+        if (s + 1 < S)
+          for (int q = cc; q < seg_end; ++q) {
+            const double* tr = tb + (ptrdiff_t)q * ldt;
+            const double xc = __shfl_sync(0xffffffffu, x[s], q);
 #pragma unroll
-        for (int s2 = s + 1; s2 < S; ++s2)
-          if (lane + 32 * s2 < n) x[s2] -= xc * tr[lane + 32 * s2];
+            for (int s2 = s + 1; s2 < S; ++s2)
+              if (lane + 32 * s2 < n) x[s2] -= xc * tr[lane + 32 * s2];
+          }
+        cc = seg_end;
       }
-    }
+    });
   } else {
-#pragma unroll
-    for (int s = S - 1; s >= 0; --s) {
+    static_for<0, S>([&](auto si) {
+      constexpr int s = S - 1 - decltype(si)::value;
       const int cend = n - 32 * s < 32 ? n - 32 * s : 32;
-      for (int cc = cend - 1; cc >= 0; --cc) {
-        const int c = 32 * s + cc;
-        if (c <= blk_end) advance(c);
-        const double* tr = cur + (size_t)(c - cur_r0) * ldt;
-        if (lane == cc) x[s] *= rinv[c];
-        const double xc = __shfl_sync(0xffffffffu, x[s], cc);
-        if (lane < cc) x[s] -= xc * tr[lane + 32 * s];
+      int cc = cend - 1;
+      while (cc >= 0) {
+        if (32 * s + cc <= blk_end) advance(32 * s + cc);
+        const int seg_lo = cur_r0 - 32 * s > 0 ? cur_r0 - 32 * s : 0;
+        const double* tb = cur + ((ptrdiff_t)32 * s - cur_r0) * ldt;
+        for (int q = cc; q >= seg_lo; --q) {
+          const double* tr = tb + (ptrdiff_t)q * ldt;
+          if (lane == q) x[s] *= rinv[32 * s + q];
+          const double xc = __shfl_sync(0xffffffffu, x[s], q);
+          if (lane < q) x[s] -= xc * tr[lane + 32 * s];
+        }
+        if (s > 0)
+          for (int q = cc; q >= seg_lo; --q) {
+            const double* tr = tb + (ptrdiff_t)q * ldt;
+            const double xc = __shfl_sync(0xffffffffu, x[s], q);
 #pragma unroll
-        for (int s2 = 0; s2 < s; ++s2) x[s2] -= xc * tr[lane + 32 * s2];
+            for (int s2 = 0; s2 < s; ++s2) x[s2] -= xc * tr[lane + 32 * s2];
+          }
+        cc = seg_lo - 1;
       }
-    }
+    });
   }
   if (active) {
 #pragma unroll
