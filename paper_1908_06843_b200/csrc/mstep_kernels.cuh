@@ -199,11 +199,10 @@ __global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restric
   auto stage = [&](int blk, double* dst) {  // rows of block blk (in consumption order)
     const int b = FWD ? blk : nblk - 1 - blk;
     const int r0 = b * rb, rows = (r0 + rb <= n ? rb : n - r0);
-    const int vec = ldt / 2;  // 16-byte chunks per row
-    for (int e = threadIdx.x; e < rows * vec; e += blockDim.x) {
-      const int r = e / vec, q = e - r * vec;
-      cp_async16(dst + (size_t)r * ldt + 2 * q, T + (long long)(r0 + r) * ldt + 2 * q, true);
-    }
+    // whole rows, same stride on both sides: one contiguous range of 16-byte chunks
+    const double* src = T + (long long)r0 * ldt;
+    const int chunks = rows * (ldt / 2);
+    for (int e = threadIdx.x; e < chunks; e += blockDim.x) cp_async16(dst + 2 * e, src + 2 * e, true);
     cp_async_commit();
   };
   stage(0, buf0);
