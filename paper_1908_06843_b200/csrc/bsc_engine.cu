@@ -230,9 +230,13 @@ void BscEngine::init(int device) {
   d_u_ = dalloc<double>((size_t)H_ * Hp_, "U");
   d_x_ = dalloc<double>((size_t)Dp_ * Hp_, "X");
   d_msc_ = dalloc<MstepScalars>(1, "mstep scalars");
-  ck(cudaMallocHost(&h_msc_, sizeof(MstepScalars)), "pinned");
-  ck(cudaMallocHost(&h_tail_, (values_.size() + 3) * sizeof(double)), "pinned");
-  ck(cudaMallocHost(&h_err_, sizeof(int)), "pinned");
+  // one pinned, device-mapped block: the last M-step kernel writes the iteration's result into it
+  ck(cudaHostAlloc(&h_result_, kHostResultTail + (values_.size() + 3) * sizeof(double), cudaHostAllocMapped),
+     "pinned");
+  ck(cudaHostGetDevicePointer(&d_result_, h_result_, 0), "mapped pointer");
+  h_msc_ = h_result_;
+  h_err_ = static_cast<char*>(h_result_) + kHostResultErr;
+  h_tail_ = static_cast<char*>(h_result_) + kHostResultTail;
   cudaStream_t cs;
   ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
   copy_stream_ = cs;
@@ -267,8 +271,7 @@ BscEngine::~BscEngine() {
                   (void*)d_ys_, (void*)d_yts_, (void*)d_ws_, (void*)d_ess_, (void*)d_ysa_, (void*)d_ytsa_,
                   (void*)d_wsb_, (void*)d_two_, (void*)d_ozpart_, (void*)d_ozcs_, (void*)d_ozmax_, (void*)d_pscale_})
     dfree(p);
-  for (void* p : {h_msc_, h_tail_, h_err_})
-    if (p) cudaFreeHost(p);
+  if (h_result_) cudaFreeHost(h_result_);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (GraphPart* g : {&factor_part_, &update_part_})
@@ -1033,11 +1036,12 @@ void BscEngine::estep_chunked(double temperature, bool want_candidates, const do
     refresh_gram();
   }
   ev(1);
-  ck(cudaMemsetAsync(d_stats_ + lay_.off_ssT(), 0, (size_t)H_ * H_ * 8, s), "zero ssT");
-  ck(cudaMemsetAsync(d_err_, 0, 2 * sizeof(int), s), "zero err");
-  ck(cudaMemsetAsync(d_warp_es_, 0, (size_t)nchunks * splits_ * Hp_ * 8, s), "zero colsums");
   // per-CTA scalar partials: [role: whole/front pass, lane finish, fallback][chunk][sc_ctas_]
-  ck(cudaMemsetAsync(d_warp_sc_, 0, (size_t)3 * nchunks * sc_ctas_ * 2 * 8, s), "zero cta scalars");
+  estep_clear_kernel<<<64, 256, 0, s>>>(d_stats_ + lay_.off_ssT(), (long long)H_ * H_, d_err_, d_warp_es_,
+                                        (long long)nchunks * splits_ * Hp_, d_warp_sc_,
+                                        (long long)3 * nchunks * sc_ctas_ * 2);
+  ck(cudaGetLastError(), "clear accumulators");
+  ++launches_;
   sc_chunks_ = nchunks;
   // Yᵀ⟨S⟩ on the integer tensor cores: k-splits sized on the first (largest) chunk
   int oz_kchunk = 0, oz_splits0 = 0;
@@ -1331,7 +1335,7 @@ void BscEngine::enqueue_update(void* stream) {
   mstep_traces_kernel<<<kTraceCtas, 256, 0, s>>>(d_w_, Hp_, d_g_, Hp_, d_stats_, lay_.off_ssT(), D, H,
                                                   d_trace_part_);
   mstep_scalars_kernel<<<1, 1, 0, s>>>(d_stats_, lay_.off_tail(), D, H, static_cast<int>(values_.size()),
-                                       d_trace_part_, sc);
+                                       d_trace_part_, sc, d_err_, static_cast<char*>(d_result_));
   if (branch) ck(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_branch_[1]), 0), "branch join wait");
   ck(cudaGetLastError(), "mstep scalars");
   launches_ += 3;
@@ -1339,16 +1343,11 @@ void BscEngine::enqueue_update(void* stream) {
 
 void BscEngine::finish_mstep() {
   auto s = static_cast<cudaStream_t>(stream_);
-  auto* sc = static_cast<MstepScalars*>(d_msc_);
   gram_fresh_ = true;
   if (timing_) ck(cudaEventRecord(static_cast<cudaEvent_t>(ev_[6]), s), "event");
-  // one synchronisation per iteration: new π, σ², the (all-reduced) F and the
-  // E-step error flag come back together
-  ck(cudaMemcpyAsync(h_msc_, sc, sizeof(MstepScalars), cudaMemcpyDeviceToHost, s), "mstep scalars D2H");
+  // one synchronisation per iteration: new π, σ², the (all-reduced) F and the E-step error
+  // flag are in the mapped host block when the last M-step kernel (mstep_scalars_kernel) ends
   const size_t V = values_.size();
-  ck(cudaMemcpyAsync(h_tail_, d_stats_ + lay_.off_tail(), (V + 3) * sizeof(double), cudaMemcpyDeviceToHost, s),
-     "F D2H");
-  ck(cudaMemcpyAsync(h_err_, d_err_, sizeof(int), cudaMemcpyDeviceToHost, s), "err D2H");
   sync();
   const int err = *static_cast<int*>(h_err_);
   if (err & kErrNonFiniteScore) throw Error(kConfig, "select_candidates: scores must be finite");

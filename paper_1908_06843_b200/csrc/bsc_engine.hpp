@@ -196,7 +196,8 @@ class BscEngine {
   // M-step workspace
   double *d_bm_ = nullptr, *d_x_ = nullptr, *d_trace_part_ = nullptr, *d_u_ = nullptr;
   void* d_msc_ = nullptr;
-  void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // pinned
+  void *h_result_ = nullptr, *d_result_ = nullptr;                // pinned + mapped: the iteration's result
+  void *h_msc_ = nullptr, *h_tail_ = nullptr, *h_err_ = nullptr;  // views into h_result_
   double last_F_ = 0.0;
   GraphPart factor_part_, update_part_;
   // step(): the factor runs on a side stream beside the Yᵀ⟨S⟩ product, which leaves SMs idle

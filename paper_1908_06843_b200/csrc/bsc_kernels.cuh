@@ -1115,6 +1115,18 @@ static __global__ void finalize_stats_kernel(int nctas, const double* __restrict
   }
 }
 
+// Start of an E-step: the accumulators every launch adds into, cleared in one launch
+// (Σ⟨ssᵀ⟩ fixed-point triangle, error flags, split-K column sums, per-CTA scalars).
+static __global__ void estep_clear_kernel(double* __restrict__ ssT, long long n_ssT, int* __restrict__ err,
+                                          double* __restrict__ colsums, long long n_colsums,
+                                          double* __restrict__ cta_scalars, long long n_scalars) {
+  const long long stride = (long long)gridDim.x * blockDim.x, t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long e = t0; e < n_ssT; e += stride) ssT[e] = 0.0;
+  for (long long e = t0; e < n_colsums; e += stride) colsums[e] = 0.0;
+  for (long long e = t0; e < n_scalars; e += stride) cta_scalars[e] = 0.0;
+  if (t0 < 2) err[t0] = 0;
+}
+
 // value_counts = Σ_h Σ⟨s⟩_h (every active unit carries value 1)
 static __global__ void counts_kernel(double* stats, long long off_s, int H, long long off_tail) {
   double acc = 0.0;

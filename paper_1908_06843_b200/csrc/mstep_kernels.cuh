@@ -346,8 +346,14 @@ __global__ void mstep_traces_kernel(const double* __restrict__ W, int ldw, const
 // π' = clip(Σ_v counts_v/(N·H), 1e-6, 1−1e-6) (linear_discrete.cpp:369-381:
 // bsc counts(0,0), tsc counts(0,0) + counts(0,1)); dsc probabilities are
 // finished on the host from the counts. Tail layout: counts[V], y2, logZ, N.
+// The iteration's host-visible result goes straight into one pinned, device-mapped block
+// (kHostResult* offsets): the scalars, the E-step error flags and the statistics tail (F among
+// them), so the host needs a stream synchronisation and no copy.
+constexpr int kHostResultErr = 64, kHostResultTail = 72;
+static_assert(sizeof(MstepScalars) <= kHostResultErr, "host result layout");
 __global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long off_tail, int D, int H, int V,
-                                     const double* __restrict__ partial, MstepScalars* sc) {
+                                     const double* __restrict__ partial, MstepScalars* sc,
+                                     const int* __restrict__ err, char* __restrict__ host_result) {
   double t2 = 0.0, t3 = 0.0;
   for (int c = 0; c < kTraceCtas; ++c) {
     t2 += partial[2 * c];
@@ -365,6 +371,11 @@ __global__ void mstep_scalars_kernel(const double* __restrict__ stats, long long
   p = p < 1e-6 ? 1e-6 : p;
   p = (1.0 - 1e-6) < p ? (1.0 - 1e-6) : p;
   sc->pi = p;
+  *reinterpret_cast<MstepScalars*>(host_result) = *sc;
+  *reinterpret_cast<int*>(host_result + kHostResultErr) = *err;
+  double* tail = reinterpret_cast<double*>(host_result + kHostResultTail);
+  for (int k = 0; k < V + 3; ++k) tail[k] = stats[off_tail + k];
+  __threadfence_system();
 }
 
 }  // namespace bscgpu
