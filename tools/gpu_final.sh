@@ -10,4 +10,5 @@ timeout 300 python bench.py --config c1 > gpurun_out/bench_c1.json 2> gpurun_out
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_reference_c2.json 2> gpurun_out/bench_reference_c2.err
 bash tools/gpu_r02_prof.sh
 BSC_GUARD=1 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/t_guard_suite.log 2>&1; echo rc=$? >> gpurun_out/t_guard_suite.log
+BSC_GUARD=2 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/t_guard2.log 2>&1; echo rc=$? >> gpurun_out/t_guard2.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
