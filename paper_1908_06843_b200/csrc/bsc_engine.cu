@@ -753,7 +753,7 @@ double BscEngine::step_streamed(const double* y_host, uint64_t n, double tempera
   try {
     estep_chunked(temperature, false, y_host, chunk);
   } catch (...) {
-    overlap_factor_ = false;
+    overlap_factor_ = factored_ = false;
     throw;
   }
   overlap_factor_ = false;
@@ -1411,7 +1411,7 @@ double BscEngine::step(double temperature) {
   try {
     estep(temperature);
   } catch (...) {
-    overlap_factor_ = false;
+    overlap_factor_ = factored_ = false;
     throw;
   }
   overlap_factor_ = false;

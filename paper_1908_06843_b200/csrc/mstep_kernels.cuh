@@ -11,6 +11,10 @@
 namespace bscgpu {
 
 constexpr int kCholNb = 64;
+#ifndef SOLVE_CHAIN_UNROLL
+#define SOLVE_CHAIN_UNROLL 4  // unroll of the solves' dependent chain loop (1 / 4 / 8 measured: profiles/r02_variants.txt)
+#endif
+constexpr int kSolveChainUnroll = SOLVE_CHAIN_UNROLL;
 
 // Device-side scalars of one EM iteration (kept resident; the host reads
 // back only what the StepResult API needs).
@@ -246,6 +250,7 @@ __global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restric
         if (32 * s + cc >= blk_end) advance(32 * s + cc);
         const int seg_end = blk_end - 32 * s < cend ? blk_end - 32 * s : cend;
         const double* tb = cur + ((ptrdiff_t)32 * s - cur_r0) * ldt;  // row of column 32·s
+#pragma unroll kSolveChainUnroll
         for (int q = cc; q < seg_end; ++q) {
           const double* tr = tb + (ptrdiff_t)q * ldt;
           if (lane == q) x[s] *= rinv[32 * s + q];
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(128) solve_rows_kernel(const double* __restric
         if (32 * s + cc <= blk_end) advance(32 * s + cc);
         const int seg_lo = cur_r0 - 32 * s > 0 ? cur_r0 - 32 * s : 0;
         const double* tb = cur + ((ptrdiff_t)32 * s - cur_r0) * ldt;
+#pragma unroll kSolveChainUnroll
         for (int q = cc; q >= seg_lo; --q) {
           const double* tr = tb + (ptrdiff_t)q * ldt;
           if (lane == q) x[s] *= rinv[32 * s + q];
